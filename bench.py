@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""bench.py -- MinatoLoader preprocessing hot path on B200 (one process per GPU).
+
+Metric (BASELINE.json): samples/sec/GPU delivered to the trainer; consumer GPU
+idle %; transform HBM GB/s.  A "step" is one batch through the whole hot path:
+submit -> fused transform kernels -> timeout classification -> eager seal ->
+delivered (resident, stream-ordered) to the trainer stream.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload rrc|img3d|img3d_heavy]
+  python bench.py --impl reference ...   # the reference CPU loader on host cores
+
+Workloads:
+  rrc          C2: ImageNet-shaped u8 3x(256..512)^2 -> RandomResizedCrop 224 + flip +
+               normalize, batch 256 (BASELINE configs[1], the N=1 headline)
+  img3d        C1/C3 shapes: KiTS19-shaped volumes (H=W=384, D from gen_empirical
+               img_seg sizes) -> crop 128^3 + flip + brightness + noise, batch 2
+  img3d_heavy  C3: as img3d with a heavy-tailed per-sample cost (spin) on a fraction
+               of samples and a synthetic trainer: reports consumer idle %
+
+value      : whole-job samples/s with raw inputs resident in HBM (device events on
+             each rank's trainer stream, max over ranks)
+e2e        : same metric with raw inputs in pinned host memory (H2D of each sample's
+             crop box / window inside the timed region) plus a 16-byte D2H read of every
+             delivered batch
+roofline   : the dominant kernel timed alone (serial mode) with CUDA events:
+             algorithmic bytes per launch / mean launch time, against MEASURED_PEAKS.json
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform HBM GB/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        return rank, local, world, dist
+    return 0, 0, 1, None
+
+
+def allreduce_max(dist, x: float, local: int) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(dist, xs, local: int):
+    """The run's only collective use: one reduce of a small counter vector (north_star)."""
+    if dist is None:
+        return list(xs)
+    import torch
+    t = torch.tensor(list(xs), dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t)
+    return t.tolist()
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ workloads
+def shard_ids(n_total_batches: int, B: int, rank: int, world: int):
+    """Batch-block round robin: global sample i goes to GPU floor(i/B) mod G."""
+    ids = []
+    for k in range(n_total_batches * world):
+        if k % world == rank:
+            ids.extend(range(k * B, (k + 1) * B))
+    return ids
+
+
+class RrcWorkload:
+    name = "rrc"
+    B = 256
+
+    def __init__(self, L, ctx, pool: int, host: bool, seed: int):
+        self.L, self.ctx, self.seed = L, ctx, seed
+        rng = np.random.default_rng(seed)
+        self.hw = rng.integers(256, 513, size=(pool, 2))
+        sizes = [int(h * w * 3) for h, w in self.hw]
+        self.offs = np.concatenate([[0], np.cumsum([(s + 255) // 256 * 256 for s in sizes])])
+        total = int(self.offs[-1])
+        self.host = host
+        self.base = ctx.host_alloc(total) if host else ctx.device_alloc(total)
+        for i, (h, w) in enumerate(self.hw):
+            ctx.synth_image(seed, i, int(h), int(w), self.base + int(self.offs[i]),
+                            on_device=not host)
+        self.pool = pool
+        self.pool_bytes = total
+        self.chain = ctx.chain(L.obj_det_ops())
+
+    def descs(self, ids):
+        L = self.L
+        out = []
+        for i in ids:
+            k = i % self.pool
+            h, w = self.hw[k]
+            out.append(L.sample_desc(i, (int(h), int(w), 3), self.base + int(self.offs[k]),
+                                     src_kind=L.SRC_HOST_PINNED if self.host else L.SRC_DEVICE))
+        return out
+
+    def close(self):
+        (self.ctx.host_free if self.host else self.ctx.device_free)(self.base)
+
+
+def img_seg_dims(n: int, seed: int):
+    """Volume depth from the reference's img_seg size model (workloads.cpp:180-185):
+    bytes_in ~ 30..375 MB cost-correlated; D = clamp(round(bytes_in / (5*384^2)), 128, 512)."""
+    mu = math.log(470.0)
+    sigma = math.log(750.0 / 470.0) / 1.2815515655446004
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal(n)
+    total = np.clip(np.exp(mu + sigma * z), 10, 2230)
+    q = 0.5 * (1 + np.vectorize(math.erf)((np.log(total) - mu) / (sigma * math.sqrt(2))))
+    pos = np.clip(0.85 * q + 0.15 * rng.random(n), 0, 1)
+    mb = 30.0 + 345.0 * pos
+    D = np.clip(np.rint(mb * 1e6 / (5 * 384 * 384)), 128, 512).astype(int)
+    return D, np.rint(total).astype(int)
+
+
+class Img3dWorkload:
+    name = "img3d"
+    B = 2
+
+    def __init__(self, L, ctx, pool: int, host: bool, seed: int, heavy_frac: float = 0.0,
+                 time_scale_us_per_ms: float = 0.0):
+        self.L, self.ctx, self.seed, self.host = L, ctx, seed, host
+        self.D, self.cost_ms = img_seg_dims(pool, seed)
+        self.pool = pool
+        self.bufs = []
+        for i in range(pool):
+            D = int(self.D[i])
+            vox = D * 384 * 384
+            pi = ctx.host_alloc(vox * 4) if host else ctx.device_alloc(vox * 4)
+            pl = ctx.host_alloc(vox) if host else ctx.device_alloc(vox)
+            ctx.synth_volume(seed, i, D, 384, 384, pi, pl, on_device=not host)
+            self.bufs.append((pi, pl))
+        self.pool_bytes = int(sum(int(d) * 384 * 384 * 5 for d in self.D))
+        self.heavy_frac = heavy_frac
+        self.scale = time_scale_us_per_ms
+        self.chain = ctx.chain(L.img_seg_ops(spin_first=heavy_frac > 0))
+
+    def descs(self, ids):
+        L = self.L
+        rng = np.random.default_rng(self.seed + 17)
+        heavy = rng.random(max(ids) + 1 if ids else 1) < self.heavy_frac
+        out = []
+        for i in ids:
+            k = i % self.pool
+            spin = [int(self.cost_ms[k] * self.scale)] if heavy[i] else [0]
+            pi, pl = self.bufs[k]
+            out.append(L.sample_desc(i, (int(self.D[k]), 384, 384), pi, pl,
+                                     src_kind=L.SRC_HOST_PINNED if self.host else L.SRC_DEVICE,
+                                     spin_us=spin))
+        return out
+
+    def close(self):
+        f = self.ctx.host_free if self.host else self.ctx.device_free
+        for pi, pl in self.bufs:
+            f(pi)
+            f(pl)
+
+
+def make_workload(name, L, ctx, host, seed, args):
+    if name == "rrc":
+        return RrcWorkload(L, ctx, pool=args.pool or 1024, host=host, seed=seed)
+    if name == "img3d":
+        return Img3dWorkload(L, ctx, pool=args.pool or 12, host=host, seed=seed)
+    if name == "img3d_heavy":
+        return Img3dWorkload(L, ctx, pool=args.pool or 12, host=host, seed=seed,
+                             heavy_frac=args.heavy_frac, time_scale_us_per_ms=args.time_scale)
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ------------------------------------------------------------------ runs
+def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, policy=0,
+              t_out_us=0, d2h_probe=0):
+    B = wl.B
+    rc_w = L.run_config(batch_size=B, t_out_us=t_out_us, policy=policy, trainer_us=trainer_us,
+                        n_workers=args.workers, warmup_us=args.profiler_warmup_us,
+                        update_interval_us=1000, d2h_probe=d2h_probe)
+    if ids_warm:
+        ctx.run_shard(wl.chain, wl.descs(ids_warm), rc_w, want_ids=False)
+    ctx.synchronize()
+    barrier(dist)
+    c0 = ctx.counters()
+    descs = wl.descs(ids_timed)
+    t0 = time.perf_counter()
+    rep, ids, bsz, cls = ctx.run_shard(wl.chain, descs, rc_w)
+    ctx.synchronize()
+    wall = time.perf_counter() - t0
+    barrier(dist)
+    c1 = ctx.counters()
+    return rep, ids, wall, {k: c1[k] - c0[k] for k in c1}
+
+
+def kernel_roofline(L, ctx, wl, ids, hbm_peak):
+    """Dominant kernel alone: serial stream, device-resident inputs, CUDA events per launch."""
+    ctx.set_serial(True)
+    try:
+        rc = L.run_config(batch_size=wl.B, n_workers=64)
+        c0 = ctx.counters()
+        rep, _, _, _ = ctx.run_shard(wl.chain, wl.descs(ids), rc, want_ids=False)
+        c1 = ctx.counters()
+    finally:
+        ctx.set_serial(False)
+    launches = c1["launches"] - c0["launches"] - (c1["gathered_batches"] - c0["gathered_batches"])
+    algo = c1["kernel_bytes"] - c0["kernel_bytes"]
+    ms = rep.kernel_ms
+    achieved = algo / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4), "traffic": None,
+            "kernel": {"rrc": "rrc2d_kernel", "img3d": "img3d_kernel"}.get(wl.name.split("_")[0], wl.name),
+            "launches": int(launches), "algo_bytes_per_launch": int(algo / max(launches, 1)),
+            "mean_launch_us": round(1e3 * ms / max(launches, 1), 2)}
+
+
+def cpu_baseline(workload: str, seconds: float = 12.0):
+    """The CPU oracle (a port of the chain, fp64) on all host cores: a bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import lf_oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(5)
+    if workload == "rrc":
+        cfg = O.cfg2d()
+        imgs = [rng.integers(0, 256, (int(h), int(w), 3), dtype=np.uint8)
+                for h, w in rng.integers(256, 513, size=(32, 2))]
+
+        def one(i):
+            O.chain2d(cfg, 1, i, imgs[i % len(imgs)])
+        sample = "RandomResizedCrop224+flip+normalize on 3x(256..512)^2 u8 images"
+    else:
+        cfg = O.cfg3d()
+        vols = []
+        for _ in range(2):
+            D = 160
+            vols.append((rng.standard_normal((D, 384, 384)).astype(np.float32),
+                         rng.integers(0, 3, (D, 384, 384), dtype=np.uint8)))
+
+        def one(i):
+            v = vols[i % len(vols)]
+            O.chain3d(cfg, 1, i, v[0], v[1])
+        sample = "crop128^3+flip+brightness+noise+cast on 160x384x384 volumes"
+    done = 0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        while time.perf_counter() - t0 < seconds:
+            list(ex.map(one, range(done, done + cores)))
+            done += cores
+    el = time.perf_counter() - t0
+    return {"value": round(done / el, 2), "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{done} samples of {sample} in {el:.1f} s (oracle, fp64, "
+                      f"{cores} threads)"}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = args.workload
+    harness = os.path.join(ROOT, "oracle", "_ref", "minato_cpu")
+    if os.path.exists(harness):
+        out = subprocess.run([harness, "--workload", wl, "--steps", str(args.steps),
+                              "--warmup", str(args.warmup)], capture_output=True, text=True,
+                             check=True).stdout.strip().splitlines()[-1]
+        base = json.loads(out)
+        kind = "reference"
+    else:
+        base = cpu_baseline(wl, seconds=max(5.0, min(60.0, 2.0 * args.steps)))
+        kind = "port"
+    v = base["value"]
+    line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * (256 if wl == "rrc" else 2) / v, 3) if v else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl, "batch": 256 if wl == "rrc" else 2},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": base["cores"],
+                             "kind": kind, "sample": base["sample"]},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="rrc", choices=["rrc", "img3d", "img3d_heavy"])
+    ap.add_argument("--pool", type=int, default=0)
+    ap.add_argument("--workers", type=int, default=16)
+    ap.add_argument("--group", type=int, default=0, help="samples per launch group (0 = auto)")
+    ap.add_argument("--heavy-frac", type=float, default=0.2)
+    ap.add_argument("--time-scale", type=float, default=10.0, help="spin us per reference ms")
+    ap.add_argument("--trainer-us", type=int, default=0)
+    ap.add_argument("--profiler-warmup-us", type=int, default=20000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    from paper_2509_10712_b200 import lfgpu as L
+    rank, local, world, dist = dist_setup(args.gpus)
+    hbm_peak, peak_src = peaks()
+    B = 256 if args.workload == "rrc" else 2
+    group = args.group or (64 if args.workload == "rrc" else 1)
+    ctx = L.Context(device=local, batch_size=B, n_workers=args.workers, max_group=group,
+                    max_slot_buffers=8, seed=args.seed)
+    ids_all = shard_ids(args.warmup + args.steps, B, rank, world)
+    ids_warm, ids_timed = ids_all[: args.warmup * B], ids_all[args.warmup * B:]
+    heavy = args.workload == "img3d_heavy"
+    trainer_us = args.trainer_us if args.trainer_us else (2000 if heavy else 0)
+
+    # ---- value: inputs resident in HBM
+    wl = make_workload(args.workload, L, ctx, host=False, seed=args.seed, args=args)
+    with ClockSampler(local) as clk:
+        rep, ids, wall, dc = run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local,
+                                       trainer_us=trainer_us, policy=1 if heavy else 0)
+    clocks = clk.summary()
+    el_max = allreduce_max(dist, rep.elapsed_ms, local)
+    samples_total = allreduce_sum(dist, [rep.timed_samples], local)[0]
+    value = samples_total / (el_max / 1e3)
+    roof = kernel_roofline(L, ctx, wl, ids_timed[: min(len(ids_timed), 64 * B if B > 2 else 64)],
+                           hbm_peak)
+    wl.close()
+
+    # ---- e2e: inputs in pinned host memory, H2D + a D2H read of every delivered batch
+    wl_h = make_workload(args.workload, L, ctx, host=True, seed=args.seed, args=args)
+    rep_h, ids_h, wall_h, dc_h = run_timed(L, ctx, wl_h, ids_warm, ids_timed, args, dist, local,
+                                           trainer_us=trainer_us, policy=1 if heavy else 0,
+                                           d2h_probe=1)
+    el_h = allreduce_max(dist, rep_h.elapsed_ms, local)
+    e2e_total = allreduce_sum(dist, [rep_h.timed_samples], local)[0]
+    e2e = e2e_total / (el_h / 1e3)
+    wl_h.close()
+
+    counters = allreduce_sum(dist, [rep.samples, rep.fast, rep.slow, rep.exactly_once,
+                                    rep.duplicates, rep.batches, rep.short_batches], local)
+    ctx.close()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
+    steps = args.steps
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": round(el_max / steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (Philox(seed,id) images/volumes generated on device / pinned host)",
+        "config": {"workload": {"rrc": "C2 ImageNet-shaped u8 3x(256..512)^2 -> RRC224+hflip+normalize",
+                                "img3d": "C1 KiTS19-shaped 3D crop128^3+flip+brightness+noise+cast",
+                                "img3d_heavy": "C3 heavy-tailed 3D + synthetic trainer"}[args.workload],
+                   "batch": B, "launch_group": group, "workers": args.workers,
+                   "raw_pool_bytes": int(wl.pool_bytes), "l2": "inputs > L2 (pool larger than 126 MB)",
+                   "parallelism": f"dp{world} independent loader shards"},
+        "roofline": dict(roof, peak_source=peak_src),
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e, 1), "unit": "samples/s",
+                "h2d_bytes_per_step": int(rep_h.h2d_bytes / max(1, steps)),
+                "d2h_bytes_per_step": int(rep_h.d2h_bytes / max(1, steps))},
+        "clocks": clocks,
+        "gpu_launches": int(dc["launches"]),
+        "consumer_idle_pct": round(100 * rep.consumer_idle_frac, 2) if trainer_us else None,
+        "slow_frac": round(counters[2] / max(1, counters[0]), 4),
+        "exactly_once": bool(counters[3] == world and counters[4] == 0),
+        "wall_s": round(wall, 3),
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

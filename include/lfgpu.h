@@ -1,0 +1,265 @@
+/*
+ * lfgpu.h -- C ABI of the B200-native MinatoLoader preprocessing hot path.
+ *
+ * One context per GPU.  Plain pointers, sizes and int error codes; no C++
+ * types and no exceptions cross this boundary.  Every entry point returns
+ * LFG_OK (0) or a negative LFG_ERR_*; lfg_last_error() gives a thread-local
+ * message for the last failure on the calling thread.
+ *
+ * The reference (/root/reference/proj) has no C ABI or FFI; its boundary is
+ * the C++ API in proj/include/loadflow.  Each entry point below names the
+ * reference function/type whose role it takes over on the GPU path, and the
+ * C++ adapter in include/loadflow/ (our signature-compatible headers) calls
+ * these entry points underneath the reference-shaped API.
+ * shows the binding a maintainer would add on the reference side.
+ *
+ * Error codes map onto the reference's exceptions:
+ *   LFG_ERR_INVALID  std::invalid_argument  (sample.cpp:27-33, balancer.cpp:83-89, batcher.cpp:43)
+ *   LFG_ERR_STATE    std::logic_error       (balancer.cpp:16)
+ *   LFG_ERR_CLOSED   QueueClosedError       (queue.hpp:29-33)
+ *   LFG_ERR_AGAIN    a bounded resource is full (BoundedQueue::put would block, queue.hpp:57-59)
+ *   LFG_ERR_CUDA     CUDA runtime failure (no reference analogue; realtime "partial", experiment.cpp:331-340)
+ */
+#ifndef LFGPU_H
+#define LFGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFG_ABI_VERSION 1
+
+#define LFG_OK 0
+#define LFG_ERR_INVALID -1
+#define LFG_ERR_STATE -2
+#define LFG_ERR_CLOSED -3
+#define LFG_ERR_AGAIN -4
+#define LFG_ERR_CUDA -5
+#define LFG_ERR_NOMEM -6
+#define LFG_ERR_UNSUPPORTED -7
+
+/* ---- transform op kinds: 1:1 with the reference Transform::name values ---- */
+enum {
+    /* img_seg chain, proj/src/workloads.cpp:142-148 */
+    LFG_OP_RANDOM_CROP = 1,       /* param: crop_d, crop_h, crop_w          */
+    LFG_OP_RANDOM_FLIP = 2,       /* param: p_flip                          */
+    LFG_OP_RANDOM_BRIGHTNESS = 3, /* param: p, lo, hi                       */
+    LFG_OP_GAUSSIAN_NOISE = 4,    /* param: p, std_max                      */
+    LFG_OP_CAST = 5,              /* no params: img f32, label u8           */
+    /* obj_det chain, proj/src/workloads.cpp:151-156 */
+    LFG_OP_RESIZE = 10,           /* RandomResizedCrop; param: out_h, out_w, scale_lo, scale_hi, ratio_lo, ratio_hi */
+    LFG_OP_RANDOM_HFLIP = 11,     /* param: p                               */
+    LFG_OP_TO_TENSOR = 12,        /* no params                              */
+    LFG_OP_NORMALIZE = 13,        /* param: mean[3], std[3]                 */
+    /* speech chain, proj/src/workloads.cpp:103-111 */
+    LFG_OP_PAD = 20,
+    LFG_OP_SPEC_AUGMENT = 21,     /* param: n_freq, freq_max, n_time, time_frac */
+    LFG_OP_FILTER_BANK = 22,      /* param: n_fft, win, hop, n_mels, sr, f_min, f_max */
+    LFG_OP_FRAME_SPLICING = 23,   /* param: stack (=subsample)              */
+    LFG_OP_PERMUTE_AUDIO = 24,
+    /* synthetic cost steps (LightStep/HeavyStep, workloads.cpp:109-110; and the
+     * per-sample step_costs of synthetic chains): a %globaltimer spin whose
+     * length is the sample's cost for this op (lfg_sample_desc.spin_us[k]) */
+    LFG_OP_SPIN = 30
+};
+
+/* Transform, proj/include/loadflow/sample.hpp:30-38 (name, size_factor, barrier).
+ * `param` carries the op's configuration (see the enum comments); unused = 0. */
+typedef struct {
+    int32_t kind;
+    int32_t barrier;
+    double size_factor;
+    double param[8];
+    char name[32];
+} lfg_op;
+
+enum { LFG_DT_U8 = 1, LFG_DT_I16 = 2, LFG_DT_F32 = 3 };
+
+/* Where a sample's raw bytes live when it is submitted. */
+enum {
+    LFG_SRC_DEVICE = 0,      /* already resident in HBM (caller-owned device memory) */
+    LFG_SRC_HOST_PINNED = 1  /* pinned host staging (lfg_host_alloc); H2D happens on the
+                                sample's stream, only the bytes the chain reads are copied */
+};
+
+/* Per-sample input description (the fields of reference Sample that the
+ * device path needs: id and the raw payload; sample.hpp:40-55). */
+typedef struct {
+    uint64_t id;
+    int32_t src_kind;        /* LFG_SRC_* */
+    int32_t ndim;            /* 3 (volume D,H,W), 3 (image H,W,C=3) or 1 (waveform L) */
+    int64_t dims[4];
+    const void* data;        /* primary payload: img f32 / image u8 HWC / waveform f32 */
+    const void* aux;         /* secondary payload: u8 label volume for img_seg; else NULL */
+    int64_t spin_us[4];      /* synthetic cost (microseconds) of the chain's LFG_OP_SPIN ops, in op order */
+} lfg_sample_desc;
+
+/* Context configuration.  n_workers is the reference PoolConfig::max_workers
+ * analogue (worker_pool.hpp:12-15): the number of concurrently in-flight,
+ * not-yet-slow launch groups, each on its own stream. */
+typedef struct {
+    int32_t device;
+    int32_t n_workers;          /* in-flight launch groups (streams), default 12 */
+    int32_t max_group;          /* samples per launch group (multi-sample launch), default 1 */
+    int32_t batch_size;         /* slot-buffer capacity = batch size */
+    int32_t max_slot_buffers;   /* bound on live output batch buffers (HBM budget) */
+    int32_t reserved0;
+    uint64_t seed;              /* per-sample Rng: mt19937_64(seed ^ 0x9e3779b97f4a7c15*(id+1)) */
+    int64_t max_raw_bytes;      /* bound on one group's raw staging (0 = auto) */
+} lfg_config;
+
+typedef struct lfg_ctx lfg_ctx;
+typedef struct lfg_chain lfg_chain;
+typedef int64_t lfg_ticket;     /* >= 0; one per submitted sample */
+typedef int64_t lfg_batch;      /* >= 0; one per sealed batch */
+
+/* ---- context ---- */
+const char* lfg_last_error(void);
+int lfg_abi_version(void);
+int lfg_device_count(int* n);
+void lfg_config_default(lfg_config* cfg);
+int lfg_open(const lfg_config* cfg, lfg_ctx** out);
+int lfg_close(lfg_ctx* ctx);
+int lfg_synchronize(lfg_ctx* ctx);
+
+/* ---- memory helpers (caller-owned buffers) ---- */
+int lfg_host_alloc(lfg_ctx* ctx, size_t bytes, void** out);     /* pinned */
+int lfg_host_free(lfg_ctx* ctx, void* p);
+int lfg_device_alloc(lfg_ctx* ctx, size_t bytes, void** out);
+int lfg_device_free(lfg_ctx* ctx, void* p);
+int lfg_memcpy_h2d(lfg_ctx* ctx, void* dst, const void* src, size_t bytes);
+int lfg_memcpy_d2h(lfg_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* ---- chains: TransformChain (sample.hpp:57-77) ----
+ * Validates the op list and compiles it into fused launch stages (one CUDA
+ * kernel per stage).  out_bytes = bytes of one sample's output slot. */
+int lfg_chain_create(lfg_ctx* ctx, const lfg_op* ops, int n_ops, lfg_chain** out);
+int lfg_chain_destroy(lfg_ctx* ctx, lfg_chain* chain);
+int lfg_chain_info(lfg_chain* chain, int* n_stages, int64_t* out_bytes, int* family);
+/* stage s covers ops [stage_first[s], stage_last[s]) */
+int lfg_chain_stage(lfg_chain* chain, int s, int* first_op, int* last_op);
+
+/* ---- per-sample parameters (host draws, product side) ----
+ * Writes the sample's drawn parameters as doubles (layout per family, see
+ * DESIGN.md section 3) -- used by the parity tests to check the host draws
+ * bit-exactly against the oracle. */
+int lfg_draw_params(lfg_chain* chain, uint64_t seed, const lfg_sample_desc* s, double* out,
+                    int cap, int* n_out);
+
+/* ---- submit / progress: replaces process_sample's transform loop
+ * (balancer.cpp:42-77) and the worker slot (worker_pool.cpp:63-98).
+ * lfg_submit draws the sample's parameters, assigns its output slot and adds
+ * it to the chain's open launch group; lfg_flush launches open groups (a
+ * group also launches when it reaches max_group).  Asynchronous. */
+int lfg_submit(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* s, lfg_ticket* out);
+int lfg_flush(lfg_ctx* ctx);
+
+/* Non-blocking.  ops_done is the reference RouteResult::timeout_index analogue
+ * (the index of the first transform not yet finished, at fused-stage
+ * granularity); complete is 1 once the whole chain finished.  elapsed_us is
+ * host wall time since the sample's group was launched. */
+int lfg_progress(lfg_ctx* ctx, lfg_ticket t, int* ops_done, int* complete, int64_t* elapsed_us);
+/* Blocks until the ticket's chain completes (resume_slow's wait, balancer.cpp:96-113). */
+int lfg_wait(lfg_ctx* ctx, lfg_ticket t);
+/* Device-timed per-op costs in microseconds (one per op; ops fused into one
+ * stage share the stage's time, attributed to the stage's last op). */
+int lfg_exec_costs(lfg_ctx* ctx, lfg_ticket t, double* costs_us, int cap, int* n_out);
+/* Copy a completed sample's output slot to host memory (tests). */
+int lfg_ticket_output(lfg_ctx* ctx, lfg_ticket t, void* host_dst, size_t bytes);
+int lfg_ticket_release(lfg_ctx* ctx, lfg_ticket t);
+
+/* ---- batches: build_batches seal (batcher.cpp:50-58) ----
+ * Seals the given completed tickets, in order, into one device-resident
+ * batch.  If the tickets are exactly the samples of one output slot buffer,
+ * the batch is that buffer (zero copy); otherwise one gather kernel collates
+ * them into a fresh batch buffer.  The tickets are consumed. */
+int lfg_seal_batch(lfg_ctx* ctx, const lfg_ticket* tickets, int n, lfg_batch* out);
+/* Device pointer of the batch tensor, its byte size, sample count, ids in
+ * batch order (ids may be NULL), and whether the seal was zero-copy. */
+int lfg_batch_info(lfg_ctx* ctx, lfg_batch b, void** dev_ptr, int64_t* bytes, int* n,
+                   uint64_t* ids, int* in_place);
+/* Makes `stream` (a cudaStream_t, may be NULL = legacy) wait until the batch is resident. */
+int lfg_batch_wait_stream(lfg_ctx* ctx, lfg_batch b, void* stream);
+int lfg_batch_copy_to_host(lfg_ctx* ctx, lfg_batch b, void* host_dst, size_t bytes);
+/* Returns the batch buffer to the pool once work already queued on `stream`
+ * (the consumer) has finished with it. */
+int lfg_batch_release(lfg_ctx* ctx, lfg_batch b, void* stream);
+
+/* ---- synthetic trainer step (trainer.cpp:50-51 consumer compute): a
+ * device-clock spin of `us` microseconds on `stream` after the batch is resident. */
+int lfg_trainer_step(lfg_ctx* ctx, lfg_batch b, void* stream, int64_t us);
+
+/* ---- synthetic input generators (bench / tests data source; Philox(seed, id)) ---- */
+int lfg_synth_volume(lfg_ctx* ctx, uint64_t seed, uint64_t id, int64_t D, int64_t H, int64_t W,
+                     void* img_f32, void* lbl_u8, int on_device);
+int lfg_synth_image(lfg_ctx* ctx, uint64_t seed, uint64_t id, int64_t H, int64_t W, void* hwc_u8,
+                    int on_device);
+int lfg_synth_waveform(lfg_ctx* ctx, uint64_t seed, uint64_t id, int64_t L, void* wav_f32,
+                       int on_device);
+
+/* ---- counters for the end-of-run reduce (the only NCCL use) ---- */
+typedef struct {
+    int64_t submitted, completed, fast, slow;
+    int64_t batches, short_batches, inplace_batches, gathered_batches;
+    int64_t launches;           /* CUDA kernels launched by this context */
+    int64_t h2d_bytes, d2h_bytes;
+    int64_t kernel_bytes;       /* algorithmic HBM bytes of the transform kernels */
+    int64_t reserved[4];
+} lfg_counters;
+int lfg_get_counters(lfg_ctx* ctx, lfg_counters* out);
+
+/* Serial mode: every launch group runs on one stream, so per-stage CUDA
+ * events time each kernel in isolation (used for the roofline measurement). */
+int lfg_set_serial(lfg_ctx* ctx, int serial);
+
+/* ---- event-driven shard runner: the whole Algorithm-1 loop for one GPU
+ * (run_minato_pipeline, experiment.cpp:129-276, with workers -> streams,
+ * resume -> completion events, batcher -> seal, consumer -> trainer stream). */
+typedef struct {
+    int32_t batch_size;
+    int32_t policy;             /* 0 fixed t_out, 1 profiler (p75 -> p90 escalation) */
+    int64_t t_out_us;           /* fixed budget (policy 0) or initial budget (policy 1); <=0 = none */
+    int64_t warmup_us;          /* profiler warm-up before the first percentile (profiler.hpp:41) */
+    int64_t update_interval_us; /* profiler refresh period */
+    int32_t window;             /* profiler window (profiler.hpp:40) */
+    int32_t n_workers;          /* 0 = context default */
+    int64_t trainer_us;         /* consumer compute per batch (trainer.hpp:15), 0 = drain only */
+    int32_t trainer_priority;   /* 1 = high-priority trainer stream */
+    int32_t warmup_batches;     /* batches excluded from the timed window */
+    int32_t record_trace;       /* keep per-sample / per-batch records */
+    int32_t d2h_probe;          /* read 16 bytes of every delivered batch back to the host
+                                   on the trainer stream (end-to-end result check) */
+} lfg_run_config;
+
+typedef struct {
+    int64_t samples, batches, short_batches, fast, slow, inplace_batches;
+    double elapsed_ms;          /* device time (trainer-stream events) of the timed window */
+    double timed_samples;       /* samples consumed inside the timed window */
+    double samples_per_s;
+    double consumer_busy_ms, consumer_span_ms, consumer_idle_frac; /* ConsumerStats, trainer.hpp:30-47 */
+    double final_t_out_us;
+    int32_t final_percentile;
+    int32_t exactly_once;       /* consumed ids == submitted ids, no duplicates */
+    int64_t duplicates;
+    double kernel_ms;           /* summed device time of transform stages in the timed window */
+    int64_t h2d_bytes, d2h_bytes;
+    int64_t launches;
+} lfg_run_report;
+
+/* samples[i] are fed in order (the feeder, experiment.cpp:221-228).
+ * consumed_ids (may be NULL, capacity n) receives ids in consumption order;
+ * batch_sizes (may be NULL, capacity n) the size of each consumed batch;
+ * sample_class (may be NULL, capacity n, indexed by position in `samples`)
+ * receives 1 = fast, 2 = slow. */
+int lfg_run_shard(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples, int64_t n,
+                  const lfg_run_config* cfg, lfg_run_report* report, uint64_t* consumed_ids,
+                  int32_t* batch_sizes, int32_t* sample_class);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFGPU_H */

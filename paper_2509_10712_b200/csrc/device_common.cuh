@@ -1,0 +1,56 @@
+// device_common.cuh -- counter-based RNG and small helpers shared by the kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lfg {
+
+// Philox4x32-10 (Salmon et al. SC'11), Random123 constants.  The CPU oracle
+// restates the same function (oracle/lf_oracle.c) and pins it to the
+// Random123 known-answer vectors.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+// -2 ln(u), u = (x + 0.5) * 2^-32, accurate at both ends of (0, 1): the upper
+// half goes through log1p of the exact complement so values of u near 1 keep
+// their relative precision (the oracle computes this in fp64).
+__device__ __forceinline__ float neg2ln_u(uint32_t x) {
+    const float two_m32 = 2.3283064365386963e-10f;  // 2^-32
+    float l;
+    if (x < 0x80000000u) {
+        l = logf(fmaf((float)x, two_m32, 0.5f * two_m32));
+    } else {
+        const uint32_t m = 0xFFFFFFFFu - x;          // exact: 1 - u = (m + 0.5) * 2^-32
+        l = log1pf(-fmaf((float)m, two_m32, 0.5f * two_m32));
+    }
+    return -2.0f * l;
+}
+
+// Box-Muller on one pair of 32-bit uniforms (same pairing as lfo_normals4).
+__device__ __forceinline__ float2 box_muller(uint32_t xa, uint32_t xb) {
+    const float two_m31 = 4.656612873077393e-10f;    // 2 * 2^-32
+    const float r = sqrtf(neg2ln_u(xa));
+    float s, c;
+    sincospif(fmaf((float)xb, two_m31, two_m31 * 0.5f), &s, &c);  // angle = 2*pi*u2
+    return make_float2(r * c, r * s);
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+}  // namespace lfg

@@ -1,0 +1,209 @@
+// engine.h -- internal C++ engine behind the lfgpu C ABI.
+//
+// Objects (all owned by one Context = one GPU):
+//   Chain      compiled transform chain (reference TransformChain) -> fused stages
+//   Group      a launch group: 1..max_group samples sharing one stream and one
+//              kernel launch per stage, with a CUDA event after every stage
+//   Ticket     one submitted sample: drawn params, output slot, group
+//   SlotBuf    a device buffer of batch_size output slots (planar); samples are
+//              written straight into it and a batch sealed from exactly its
+//              samples is handed over in place (zero copy)
+//   BatchRec   a sealed batch: slot buffer + ids + ready event
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/lfgpu.h"
+#include "kernels.h"
+
+namespace lfg {
+
+enum Family { FAM_NONE = 0, FAM_IMG3D = 1, FAM_RRC2D = 2, FAM_SPEECH = 3 };
+enum StageKind { ST_SPIN = 1, ST_IMG3D = 2, ST_RRC2D = 3, ST_SPEECH = 4 };
+
+struct Error {
+    int code;
+    std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+
+int64_t host_now_us();
+
+struct Stage {
+    int kind;
+    int first_op, last_op;   // ops [first, last) covered by this stage
+    std::vector<int> spin_ops;  // spin slot indices launched in this stage (in order)
+};
+
+struct Chain {
+    std::vector<lfg_op> ops;
+    Family fam = FAM_NONE;
+    std::vector<Stage> stages;
+    int n_spin = 0;
+    // img3d
+    int crop[3] = {128, 128, 128};
+    double p_flip = 0, p_bright = 0, b_lo = 1, b_hi = 1, p_noise = 0, noise_max = 0;
+    // rrc2d
+    int oh = 224, ow = 224;
+    double scale_lo = 0.08, scale_hi = 1.0, ratio_lo = 0.75, ratio_hi = 4.0 / 3.0, p_hflip = 0;
+    double mean[3] = {0, 0, 0}, std[3] = {1, 1, 1};
+    bool to_tensor = false;
+    // speech
+    int n_fft = 512, win = 320, hop = 160, n_mels = 80, stack = 3;
+    int n_fmask = 0, fmask_max = 0, n_tmask = 0;
+    double tmask_frac = 0;
+    int64_t max_L = 170000;
+    // output slot layout (planar)
+    int nplanes = 1;
+    int64_t plane_bytes[2] = {0, 0};
+    int64_t out_bytes = 0;
+    int64_t algo_bytes_per_sample(const lfg_sample_desc& s) const;
+};
+
+// Per-sample drawn parameters (host, std::mt19937_64 keyed by sample id).
+struct Params3D { int64_t off[3]; int flip[3]; double scale, sigma; uint32_t key[2]; };
+struct Params2D { int64_t top, left, h, w; int flip; };
+struct ParamsSp { int T; int f_lo[2], f_w[2]; int t_lo[10], t_w[10]; };
+
+void draw_3d(const Chain& c, uint64_t seed, uint64_t id, const int64_t dims[3], Params3D& p);
+void draw_2d(const Chain& c, uint64_t seed, uint64_t id, int64_t H, int64_t W, Params2D& p);
+void draw_sp(const Chain& c, uint64_t seed, uint64_t id, int64_t L, ParamsSp& p);
+
+struct SlotBuf {
+    char* base = nullptr;
+    int cap = 0;
+    int assigned = 0;        // slots handed to tickets
+    int live = 0;            // assigned tickets whose bytes are still needed here
+    bool open = false;       // still accepting slot assignments
+    bool in_batch = false;   // owned by a sealed batch
+    std::vector<cudaEvent_t> pending;  // readers that must finish before reuse
+    const Chain* chain = nullptr;
+    int64_t bytes = 0;
+    bool gather_role = false;  // created as a collation target (not a sample slot buffer)
+};
+
+struct RawBuf {
+    char* ptr = nullptr;
+    int64_t cap = 0;
+};
+
+struct Group {
+    int64_t id = 0;
+    Chain* chain = nullptr;
+    int src_kind = LFG_SRC_DEVICE;
+    std::vector<int64_t> tickets;
+    int stream_idx = -1;
+    cudaStream_t stream = nullptr;
+    std::vector<cudaEvent_t> ev;   // ev[0] start, ev[s+1] end of stage s
+    bool launched = false;
+    bool complete = false;
+    int stages_done = 0;
+    int64_t t_launch_us = 0;
+    int64_t raw_idx = -1;
+    int refs = 0;
+    std::vector<float> stage_ms;   // filled once complete
+};
+
+struct Ticket {
+    uint64_t id = 0;
+    int64_t group = -1;
+    int idx = 0;
+    int buf = -1, pos = -1;
+    lfg_sample_desc desc{};
+    Params3D p3{};
+    Params2D p2{};
+    ParamsSp ps{};
+    bool released = false;
+    bool consumed = false;   // sealed into a batch
+};
+
+struct BatchRec {
+    int buf = -1;
+    bool in_place = false;
+    std::vector<uint64_t> ids;
+    cudaEvent_t ready = nullptr;
+    const Chain* chain = nullptr;
+    int n = 0;
+    bool released = false;
+};
+
+class Context {
+public:
+    explicit Context(const lfg_config& cfg);
+    ~Context();
+
+    lfg_config cfg;
+    int sm_count = 148;
+
+    Chain* chain_create(const lfg_op* ops, int n);
+    void chain_destroy(Chain* c);
+
+    int64_t submit(Chain* c, const lfg_sample_desc& s);
+    void flush();
+    void progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed_us);
+    void wait(int64_t t);
+    int exec_costs(int64_t t, double* out, int cap);
+    void ticket_output(int64_t t, void* dst, size_t bytes);
+    void ticket_release(int64_t t);
+
+    int64_t seal(const int64_t* tickets, int n);
+    BatchRec& batch(int64_t b);
+    void batch_wait_stream(int64_t b, cudaStream_t s);
+    void batch_release(int64_t b, cudaStream_t s);
+    void trainer_step(int64_t b, cudaStream_t s, int64_t us);
+    void batch_ptr(const BatchRec& br, void** p, int64_t* bytes) const {
+        *p = bufs_[br.buf].base;
+        *bytes = bufs_[br.buf].bytes;
+    }
+
+    // group-level queries used by the shard runner
+    Group& group_of(int64_t t);
+    bool poll_group(Group& g);          // updates stages_done/complete; true if complete
+    void finalize_group_timing(Group& g);
+    int64_t open_group_count() const;
+
+    lfg_counters counters{};
+    bool serial = false;
+    std::mutex mu;   // one lock per context (C ABI calls serialise on it)
+
+    cudaStream_t seal_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;
+
+    std::vector<Ticket> tickets;
+    std::vector<Group> groups;
+    std::vector<BatchRec> batches;
+
+private:
+    std::vector<std::unique_ptr<Chain>> chains_;
+    std::vector<cudaStream_t> streams_;
+    std::vector<int> free_streams_;
+    std::vector<cudaEvent_t> free_events_;
+    std::vector<SlotBuf> bufs_;
+    std::vector<RawBuf> raws_;
+    std::vector<int64_t> free_raws_;
+    std::unordered_map<const Chain*, int> open_buf_;     // chain -> open slot buffer
+    std::unordered_map<const Chain*, int64_t> open_group_[2];  // [src_kind] chain -> group
+
+    cudaEvent_t get_event();
+    void put_event(cudaEvent_t e);
+    int get_stream();
+    int alloc_buf(const Chain* c, bool for_batch);
+    bool buf_reusable(SlotBuf& b);
+    void assign_slot(Ticket& t, const Chain* c);
+    int64_t get_raw(int64_t bytes);
+    void launch_group(Group& g);
+    char* slot_ptr(const Ticket& t, int plane) const;
+    int64_t stage_raw_bytes(const Chain& c, const Ticket& t) const;
+};
+
+}  // namespace lfg

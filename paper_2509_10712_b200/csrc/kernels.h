@@ -1,0 +1,108 @@
+// kernels.h -- launch-parameter structs and host launchers for the sm_100a
+// transform kernels.  Each fused kernel takes a whole launch group (up to
+// kMax* samples) as one __grid_constant__ parameter block, so a group costs
+// one launch and no descriptor upload.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lfg {
+
+constexpr int kMax3D = 16;   // img_seg samples per launch group
+constexpr int kMax2D = 64;   // obj_det samples per launch group
+constexpr int kMaxSp = 64;   // speech utterances per launch group
+constexpr int kMaxSpin = 64;
+constexpr int kMaxGather = 256;
+
+// ---- K1: RandomCrop + RandomFlip + RandomBrightness + GaussianNoise + Cast
+struct Img3dDesc {
+    const float* img;        // source buffer (full volume or staged crop window)
+    const uint8_t* lbl;
+    float* out_img;          // [cd, ch, cw] f32
+    uint8_t* out_lbl;        // [cd, ch, cw] u8
+    int32_t sdim[3];         // source buffer extents (d, h, w)
+    int32_t off[3];          // crop origin inside the source buffer
+    int32_t flip;            // bit a = flip axis a
+    float scale;             // brightness multiplier
+    float sigma;             // noise std (0 = no noise)
+    uint32_t key0, key1;     // Philox key
+};
+struct Img3dLaunch {
+    int32_t crop[3];
+    int32_t n;
+    Img3dDesc d[kMax3D];
+};
+
+// ---- K3: RandomResizedCrop (bilinear) + RandomHorizontalFlip + ToTensor + Normalize
+struct RrcDesc {
+    const uint8_t* src;      // HWC u8 buffer (full image or staged crop box)
+    float* out;              // [3, oh, ow] f32
+    int32_t sw;              // source row length in pixels
+    int32_t top, left;       // crop origin inside the buffer
+    int32_t h, w;            // crop box size
+    int32_t flip;
+};
+struct RrcLaunch {
+    int32_t oh, ow;
+    float a[3], b[3];        // out = v * a_c + b_c  (= (v/255 - mean_c) / std_c)
+    int32_t n;
+    RrcDesc d[kMax2D];
+};
+
+// ---- K8-K11 (speech): STFT power -> mel -> log -> SpecAugment -> FrameSplicing
+struct SpDesc {
+    const float* wav;
+    float* out;              // spliced log-mel [T', stack*n_mels]  (time-major)
+    int32_t L;
+    int32_t T;               // frames
+    int32_t f_lo[2], f_w[2];
+    int32_t t_lo[10], t_w[10];
+};
+struct SpLaunch {
+    int32_t n;
+    int32_t n_fmask, n_tmask;
+    int32_t stack;
+    SpDesc d[kMaxSp];
+};
+
+// ---- K14: synthetic per-sample cost (LightStep / HeavyStep / step_costs)
+struct SpinLaunch {
+    int32_t n;
+    int64_t ns[kMaxSpin];
+};
+
+// ---- K12: batch collation gather (planar: plane p of sample i -> dst + p*plane_stride + i*plane_bytes[p])
+struct GatherLaunch {
+    int32_t n;
+    int32_t nplanes;
+    int64_t plane_bytes[2];
+    int64_t src_plane_stride[kMaxGather];   // per source slot: distance from plane 0 to plane 1
+    const char* src[kMaxGather];
+    char* dst;
+    int64_t dst_plane_stride;
+};
+
+cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s);
+cudaError_t launch_rrc2d(const RrcLaunch& L, cudaStream_t s);
+cudaError_t launch_spin(const SpinLaunch& L, cudaStream_t s);
+cudaError_t launch_gather(const GatherLaunch& L, cudaStream_t s);
+cudaError_t launch_trainer_spin(int64_t ns, int ctas, cudaStream_t s);
+
+// speech: constant tables (window, DFT basis, mel filterbank) live in device memory
+struct SpeechTables;
+cudaError_t speech_tables_create(SpeechTables** out);
+void speech_tables_destroy(SpeechTables* t);
+cudaError_t launch_speech(const SpLaunch& L, const SpeechTables* t, float* scratch,
+                          cudaStream_t s);
+int64_t speech_scratch_bytes(int n, int max_T);
+
+// synthetic data (Philox(seed, id)); device kernels
+cudaError_t launch_synth_volume(uint64_t seed, uint64_t id, int64_t D, int64_t H, int64_t W,
+                                float* img, uint8_t* lbl, cudaStream_t s);
+cudaError_t launch_synth_image(uint64_t seed, uint64_t id, int64_t H, int64_t W, uint8_t* hwc,
+                               cudaStream_t s);
+cudaError_t launch_synth_waveform(uint64_t seed, uint64_t id, int64_t L, float* wav,
+                                  cudaStream_t s);
+
+}  // namespace lfg

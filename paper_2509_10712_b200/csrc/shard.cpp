@@ -1,0 +1,314 @@
+// shard.cpp -- event-driven Algorithm 1 for one GPU shard.
+//
+// The reference wires one actor per role (run_minato_pipeline,
+// proj/src/experiment.cpp:129-276): N worker threads running process_sample
+// (balancer.cpp:81-94), N resume threads (balancer.cpp:96-113), a batcher
+// polling in 10 ms sleeps (batcher.cpp:60-90), a consumer (trainer.cpp:20-66)
+// and a profiler loop (profiler.cpp:108-121).  On the GPU the transform work
+// is asynchronous, so all of those collapse into one host loop driven by CUDA
+// event queries:
+//   workers     -> at most n_workers in-flight launch groups, each on its own stream
+//   timeout     -> host clock since launch > t_out while the group's last stage
+//                  event is still pending: the group is classified slow and its
+//                  stream is parked (no preemption; nothing is re-executed)
+//   resume      -> the parked group's completion event -> slow list
+//   batcher     -> seal B samples, fast list first (FIFO), then slow list
+//   consumer    -> a (high-priority) trainer stream that waits on each batch's
+//                  ready event and runs the synthetic step; idle accounting from
+//                  CUDA events exactly like ConsumerStats (trainer.hpp:30-47)
+//   profiler    -> sliding window of device-timed per-sample totals; nearest-rank
+//                  p75 after warm-up, p90 escalation above a 0.35 slow rate,
+//                  de-escalation on a full window below 0.15 (profiler.cpp:47-72)
+#include <algorithm>
+#include <cmath>
+#include <deque>
+#include <thread>
+
+#include "engine.h"
+
+namespace lfg {
+
+namespace {
+
+constexpr int64_t kNoTimeoutUs = INT64_MAX / 4;  // time.hpp:16 analogue
+
+struct Profile {
+    // SampleStats window (profiler.hpp:27-46), totals in microseconds
+    std::deque<std::pair<int64_t, bool>> window;
+    size_t cap = 1024;
+    int pct = 75;
+    double escalate = 0.35, deescalate = 0.15;
+
+    void record(int64_t total_us, bool slow) {
+        window.emplace_back(total_us, slow);
+        if (window.size() > cap) window.pop_front();
+    }
+    // Profiler::update_timeout (profiler.cpp:47-72) with nearest-rank percentile (profiler.cpp:13-21)
+    int64_t update() {
+        std::vector<int64_t> totals;
+        size_t slow = 0;
+        for (auto& w : window) {
+            totals.push_back(w.first);
+            slow += w.second;
+        }
+        const double rate = double(slow) / double(window.size());
+        if (pct == 75 && rate > escalate) pct = 90;
+        else if (pct == 90 && window.size() == cap && rate < deescalate) pct = 75;
+        std::sort(totals.begin(), totals.end());
+        size_t rank = static_cast<size_t>(std::ceil(pct / 100.0 * double(totals.size())));
+        if (rank == 0) rank = 1;
+        return totals[rank - 1];
+    }
+};
+
+}  // namespace
+
+int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_t n,
+              const lfg_run_config& rc, lfg_run_report& rep, uint64_t* consumed_ids,
+              int32_t* batch_sizes, int32_t* sample_class) {
+    if (n < 0 || (n > 0 && samples == nullptr)) fail(LFG_ERR_INVALID, "bad sample list");
+    const int B = rc.batch_size > 0 ? rc.batch_size : ctx.cfg.batch_size;
+    if (B > ctx.cfg.batch_size) fail(LFG_ERR_INVALID, "run batch_size exceeds context batch_size");
+    const int n_workers = rc.n_workers > 0 ? rc.n_workers : ctx.cfg.n_workers;
+    const int cap = chain->fam == FAM_IMG3D ? kMax3D : (chain->fam == FAM_RRC2D ? kMax2D : kMaxSp);
+    const int group = std::max(1, std::min(ctx.cfg.max_group, cap));
+
+    rep = lfg_run_report{};
+    const lfg_counters c0 = ctx.counters;
+
+    int lo = 0, hi = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    cudaStream_t trainer;
+    cuda_check(cudaStreamCreateWithPriority(&trainer, cudaStreamNonBlocking,
+                                            rc.trainer_priority ? hi : lo),
+               "trainer stream");
+    std::vector<cudaEvent_t> evs;
+    auto mk = [&]() {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "event");
+        evs.push_back(e);
+        return e;
+    };
+    cudaEvent_t t_start = mk();
+    cuda_check(cudaEventRecord(t_start, trainer), "record");
+    cudaEvent_t t_timed = t_start;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> steps;   // timed-window trainer steps
+
+    // end-to-end probe: 16 bytes of every delivered batch are read back on the trainer stream
+    char* probe = nullptr;
+    if (rc.d2h_probe) cuda_check(cudaMallocHost(&probe, 16 * 1024), "probe buffer");
+    int64_t probe_bytes = 0;
+
+    Profile prof;
+    prof.cap = rc.window > 0 ? static_cast<size_t>(rc.window) : 1024;
+    int64_t t_out = rc.t_out_us > 0 ? rc.t_out_us : kNoTimeoutUs;
+    const int64_t run_t0 = host_now_us();
+    int64_t last_update = run_t0;
+
+    const int64_t tbase = static_cast<int64_t>(ctx.tickets.size());
+    std::vector<int64_t> inflight, parked;
+    std::deque<int64_t> fast, slow;
+    int64_t fed = 0, consumed = 0, nbatches = 0, timed_samples = 0;
+    std::vector<uint64_t> all_ids;
+    all_ids.reserve(static_cast<size_t>(n));
+    double kernel_ms = 0;
+
+    auto total_us = [&](const Group& g) {
+        double ms = 0;
+        for (float x : g.stage_ms) ms += x;
+        return static_cast<int64_t>(std::llround(ms * 1000.0));
+    };
+    auto classify = [&](const Group& g, bool is_slow) {
+        for (int64_t t : g.tickets)
+            if (sample_class) sample_class[t - tbase] = is_slow ? 2 : 1;
+        if (is_slow) rep.slow += static_cast<int64_t>(g.tickets.size());
+        else rep.fast += static_cast<int64_t>(g.tickets.size());
+    };
+
+    while (consumed < n) {
+        bool progressed = false;
+        const int64_t now = host_now_us();
+
+        // (1) in-flight groups: finished in budget -> fast; over budget -> slow (parked)
+        for (size_t k = 0; k < inflight.size();) {
+            Group& g = ctx.groups[inflight[k]];
+            const bool done = ctx.poll_group(g);
+            bool remove = false;
+            if (done) {
+                const int64_t dev_us = total_us(g);
+                const bool is_slow = dev_us > t_out;   // inclusive budget, balancer.cpp:17
+                classify(g, is_slow);
+                for (int64_t t : g.tickets) (is_slow ? slow : fast).push_back(t);
+                prof.record(dev_us, is_slow);
+                if (nbatches >= rc.warmup_batches) kernel_ms += dev_us / 1000.0;
+                remove = true;
+            } else if (now - g.t_launch_us > t_out) {
+                classify(g, true);
+                parked.push_back(inflight[k]);
+                remove = true;
+            }
+            if (remove) {
+                inflight[k] = inflight.back();
+                inflight.pop_back();
+                progressed = true;
+            } else {
+                ++k;
+            }
+        }
+        // (2) parked (slow) groups finishing in the background -> slow list
+        for (size_t k = 0; k < parked.size();) {
+            Group& g = ctx.groups[parked[k]];
+            if (ctx.poll_group(g)) {
+                for (int64_t t : g.tickets) slow.push_back(t);
+                prof.record(total_us(g), true);
+                parked[k] = parked.back();
+                parked.pop_back();
+                progressed = true;
+            } else {
+                ++k;
+            }
+        }
+        // (3) feed new samples while a worker (stream) is free
+        while (static_cast<int>(inflight.size()) < n_workers && fed < n) {
+            const int64_t take = std::min<int64_t>(group, n - fed);
+            int64_t got = 0;
+            int64_t gid = -1;
+            try {
+                for (; got < take; ++got) {
+                    const int64_t t = ctx.submit(chain, samples[fed + got]);
+                    gid = ctx.tickets[t].group;
+                }
+            } catch (const Error& e) {
+                if (e.code != LFG_ERR_AGAIN) throw;
+            }
+            if (got == 0) break;
+            ctx.flush();
+            fed += got;
+            inflight.push_back(gid);
+            progressed = true;
+            if (got < take) break;
+        }
+        // (4) batcher: seal eagerly, fast first
+        const bool tail = fed == n && inflight.empty() && parked.empty();
+        while (static_cast<int64_t>(fast.size() + slow.size()) >= B ||
+               (tail && !fast.empty()) || (tail && !slow.empty())) {
+            const int64_t k = std::min<int64_t>(B, static_cast<int64_t>(fast.size() + slow.size()));
+            std::vector<int64_t> ts;
+            ts.reserve(static_cast<size_t>(k));
+            for (int64_t i = 0; i < k; ++i) {
+                if (!fast.empty()) {
+                    ts.push_back(fast.front());
+                    fast.pop_front();
+                } else {
+                    ts.push_back(slow.front());
+                    slow.pop_front();
+                }
+            }
+            int64_t b;
+            try {
+                b = ctx.seal(ts.data(), static_cast<int>(k));
+            } catch (const Error& e) {
+                if (e.code != LFG_ERR_AGAIN) throw;
+                for (auto it = ts.rbegin(); it != ts.rend(); ++it) {
+                    const int cls = sample_class ? sample_class[*it - tbase] : 1;
+                    (cls == 2 ? slow : fast).push_front(*it);
+                }
+                break;
+            }
+            BatchRec& br = ctx.batch(b);
+            const bool timed = nbatches >= rc.warmup_batches;
+            if (timed && rc.trainer_us > 0) {
+                cudaEvent_t s0 = mk(), s1 = mk();
+                ctx.batch_wait_stream(b, trainer);
+                cuda_check(cudaEventRecord(s0, trainer), "record");
+                ctx.trainer_step(b, trainer, rc.trainer_us);
+                cuda_check(cudaEventRecord(s1, trainer), "record");
+                steps.emplace_back(s0, s1);
+            } else {
+                ctx.trainer_step(b, trainer, rc.trainer_us);
+            }
+            if (probe) {
+                void* bp = nullptr;
+                int64_t bb = 0;
+                ctx.batch_ptr(br, &bp, &bb);
+                cuda_check(cudaMemcpyAsync(probe + 16 * (nbatches % 1024), bp, 16,
+                                           cudaMemcpyDeviceToHost, trainer),
+                           "probe D2H");
+                probe_bytes += 16;
+            }
+            for (uint64_t id : br.ids) {
+                if (consumed_ids) consumed_ids[consumed] = id;
+                all_ids.push_back(id);
+                ++consumed;
+            }
+            if (batch_sizes) batch_sizes[nbatches] = br.n;
+            if (timed) timed_samples += br.n;
+            ctx.batch_release(b, trainer);
+            for (int64_t t : ts) ctx.ticket_release(t);
+            ++nbatches;
+            if (nbatches == rc.warmup_batches) {
+                t_timed = mk();
+                cuda_check(cudaEventRecord(t_timed, trainer), "record");
+            }
+            progressed = true;
+        }
+        // (5) profiler maintenance (profiler_loop, profiler.cpp:108-121)
+        if (rc.policy == 1 && !prof.window.empty() && now - run_t0 >= rc.warmup_us &&
+            now - last_update >= std::max<int64_t>(1, rc.update_interval_us)) {
+            t_out = prof.update();
+            last_update = now;
+        }
+        if (!progressed) {
+            if (inflight.empty() && parked.empty() && fed == n && fast.empty() && slow.empty())
+                fail(LFG_ERR_STATE, "shard stalled with samples unaccounted for");
+            std::this_thread::yield();
+        }
+    }
+    cudaEvent_t t_end = mk();
+    cuda_check(cudaEventRecord(t_end, trainer), "record");
+    cuda_check(cudaEventSynchronize(t_end), "sync");
+
+    float el = 0;
+    cuda_check(cudaEventElapsedTime(&el, t_timed, t_end), "elapsed");
+    double busy = 0;
+    for (auto& s : steps) {
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, s.first, s.second), "elapsed");
+        busy += ms;
+    }
+    for (auto e : evs) cudaEventDestroy(e);
+    if (probe) cudaFreeHost(probe);
+    cudaStreamDestroy(trainer);
+
+    // exactly-once audit (experiment.cpp:396-413)
+    std::vector<uint64_t> want(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) want[i] = samples[i].id;
+    std::sort(want.begin(), want.end());
+    std::sort(all_ids.begin(), all_ids.end());
+    int64_t dups = 0;
+    for (size_t i = 1; i < all_ids.size(); ++i) dups += all_ids[i] == all_ids[i - 1];
+
+    rep.samples = consumed;
+    rep.batches = nbatches;
+    rep.short_batches = 0;
+    if (batch_sizes)
+        for (int64_t i = 0; i < nbatches; ++i) rep.short_batches += batch_sizes[i] < B;
+    rep.inplace_batches = ctx.counters.inplace_batches - c0.inplace_batches;
+    rep.elapsed_ms = el;
+    rep.timed_samples = static_cast<double>(timed_samples);
+    rep.samples_per_s = el > 0 ? timed_samples / (el / 1000.0) : 0.0;
+    rep.consumer_busy_ms = busy;
+    rep.consumer_span_ms = el;
+    rep.consumer_idle_frac = (rc.trainer_us > 0 && el > 0) ? 1.0 - busy / el : 1.0;
+    rep.final_t_out_us = static_cast<double>(t_out >= kNoTimeoutUs ? -1 : t_out);
+    rep.final_percentile = prof.pct;
+    rep.exactly_once = (all_ids == want && dups == 0) ? 1 : 0;
+    rep.duplicates = dups;
+    rep.kernel_ms = kernel_ms;
+    rep.h2d_bytes = ctx.counters.h2d_bytes - c0.h2d_bytes;
+    rep.d2h_bytes = ctx.counters.d2h_bytes - c0.d2h_bytes + probe_bytes;
+    rep.launches = ctx.counters.launches - c0.launches;
+    return LFG_OK;
+}
+
+}  // namespace lfg

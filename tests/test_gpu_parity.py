@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a transform kernels (through the C ABI) against the CPU oracle.
+
+Bars:
+  * crop / flip / label / indexing: bit-exact (labels compared with ==; crop
+    boxes and flip bits compared as integers via lfg_draw_params).
+  * image values: |gpu - oracle| <= RTOL * |oracle| + ATOL with RTOL = 1e-5
+    (north_star: <= 1e-5 relative in fp32) and an absolute floor ATOL for
+    values near zero where relative error is undefined: 1e-6 for the 3D chain
+    (unit-variance voxels), 1e-5 for the normalised 2D chain (outputs O(1)).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SEED = 1
+RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ctx(lfgpu):
+    if lfgpu.device_count() < 1:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+    c = lfgpu.Context(batch_size=8, n_workers=8, max_group=4, max_slot_buffers=16, seed=SEED)
+    yield c
+    c.close()
+
+
+def _upload(ctx, arr):
+    p = ctx.device_alloc(arr.nbytes)
+    ctx.h2d(p, np.ascontiguousarray(arr))
+    return p
+
+
+def _pinned(ctx, arr):
+    p = ctx.host_alloc(arr.nbytes)
+    import ctypes
+    ctypes.memmove(p, arr.ctypes.data, arr.nbytes)
+    return p
+
+
+def _assert_close(got, want, atol):
+    err = np.abs(got.astype(np.float64) - want)
+    bound = RTOL * np.abs(want) + atol
+    bad = err > bound
+    assert not bad.any(), (f"{bad.sum()} / {bad.size} values out of tolerance; "
+                           f"max err {err.max():.3e}, worst ratio {(err / bound).max():.3f}")
+
+
+# ------------------------------------------------------------------ img_seg (K1)
+CASES_3D = [
+    # (dims, crop, probability overrides)
+    ((20, 24, 40), (16, 16, 32), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),
+    ((20, 24, 40), (16, 16, 32), dict()),                                   # MLPerf defaults
+    ((12, 30, 20), (16, 16, 32), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),  # zero padding
+    ((16, 16, 32), (16, 16, 32), dict(p_flip=1.0, p_bright=0.0, p_noise=1.0)),  # exact fit
+    ((136, 140, 150), (128, 128, 128), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),
+]
+
+
+@pytest.mark.parametrize("src_kind", [0, 1], ids=["device", "host_pinned"])
+@pytest.mark.parametrize("case", range(len(CASES_3D)))
+def test_img3d_matches_oracle(ctx, lfgpu, oracle, case, src_kind):
+    dims, crop, probs = CASES_3D[case]
+    kw = dict(p_flip=1 / 3, p_bright=0.1, p_noise=0.1)
+    kw.update(probs)
+    ops = lfgpu.img_seg_ops(crop=crop, p_flip=kw["p_flip"], p_bright=kw["p_bright"],
+                            p_noise=kw["p_noise"])
+    ch = ctx.chain(ops)
+    ocfg = oracle.cfg3d(crop=crop, p_flip=kw["p_flip"], p_bright=kw["p_bright"],
+                        p_noise=kw["p_noise"])
+    rng = np.random.default_rng(100 + case)
+    n_ids = 3 if crop[0] == 128 else 12
+    ids = [int(x) for x in rng.integers(0, 1 << 40, n_ids)]
+    vox = int(np.prod(crop))
+    bufs = []
+    tickets = []
+    expect = []
+    for sid in ids:
+        img = rng.standard_normal(dims).astype(np.float32)
+        lbl = rng.integers(0, 3, dims, dtype=np.uint8)
+        if src_kind == 0:
+            pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+            bufs += [("d", pi), ("d", pl)]
+        else:
+            pi, pl = _pinned(ctx, img), _pinned(ctx, lbl)
+            bufs += [("h", pi), ("h", pl)]
+        desc = lfgpu.sample_desc(sid, dims, pi, pl, src_kind=src_kind)
+        # host parameter draws are bit-identical to the oracle's
+        p = ch.draw_params(SEED, desc)
+        op_ = oracle.draw3d(ocfg, SEED, sid, dims)
+        assert list(p[:3]) == list(op_.off) and list(p[3:6]) == list(op_.flip)
+        assert p[6] == op_.scale and p[7] == op_.sigma and list(p[8:10]) == list(op_.key)
+        tickets.append(ctx.submit(ch, desc))
+        expect.append(oracle.apply3d(ocfg, op_, img, lbl))
+    ctx.flush()
+    for t, (e_img, e_lbl) in zip(tickets, expect):
+        ctx.wait(t)
+        od, done, _ = ctx.progress(t)
+        assert done and od == len(ops)
+        raw = ctx.ticket_output(t, vox * 4 + ((vox + 15) // 16) * 16)
+        g_img = raw[: vox * 4].view(np.float32).reshape(crop)
+        g_lbl = raw[vox * 4: vox * 5].reshape(crop)
+        assert np.array_equal(g_lbl, e_lbl), "label crop/flip is not bit-exact"
+        _assert_close(g_img, e_img, atol=1e-6)
+        ctx.release(t)
+    for kind, p in bufs:
+        (ctx.device_free if kind == "d" else ctx.host_free)(p)
+    ctx.destroy_chain(ch)
+
+
+# ------------------------------------------------------------------ obj_det (K3)
+@pytest.mark.parametrize("src_kind", [0, 1], ids=["device", "host_pinned"])
+def test_rrc2d_matches_oracle(ctx, lfgpu, oracle, src_kind):
+    ch = ctx.chain(lfgpu.obj_det_ops())
+    ocfg = oracle.cfg2d()
+    rng = np.random.default_rng(7 + src_kind)
+    bufs, tickets, expect = [], [], []
+    for k in range(24):
+        sid = int(rng.integers(0, 1 << 40))
+        H, W = (int(x) for x in rng.integers(256, 513, 2))
+        if k == 0:
+            H, W = 40, 500     # extreme aspect -> centre-crop fallback
+        if k == 1:
+            H, W = 100, 100    # upsampling
+        img = rng.integers(0, 256, (H, W, 3), dtype=np.uint8)
+        p = _upload(ctx, img) if src_kind == 0 else _pinned(ctx, img)
+        bufs.append(p)
+        desc = lfgpu.sample_desc(sid, (H, W, 3), p, src_kind=src_kind)
+        dp = ch.draw_params(SEED, desc)
+        op_ = oracle.draw2d(ocfg, SEED, sid, H, W)
+        assert list(dp) == [op_.top, op_.left, op_.h, op_.w, op_.flip]
+        tickets.append(ctx.submit(ch, desc))
+        expect.append(oracle.apply2d(ocfg, op_, img))
+    ctx.flush()
+    for t, e in zip(tickets, expect):
+        ctx.wait(t)
+        raw = ctx.ticket_output(t, 3 * 224 * 224 * 4)
+        _assert_close(raw.view(np.float32).reshape(3, 224, 224), e, atol=1e-5)
+        ctx.release(t)
+    for p in bufs:
+        (ctx.device_free if src_kind == 0 else ctx.host_free)(p)
+    ctx.destroy_chain(ch)
+
+
+# ------------------------------------------------------------------ batches
+def test_seal_in_place_and_gather(ctx, lfgpu, oracle):
+    """A batch sealed from exactly one slot buffer is zero-copy; any other
+    composition is collated by the gather kernel; both hold the same bytes as
+    the per-sample outputs."""
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, p_flip=0.5, p_bright=1.0, p_noise=1.0))
+    ocfg = oracle.cfg3d(crop=crop, p_flip=0.5, p_bright=1.0, p_noise=1.0)
+    B = ctx.cfg.batch_size
+    dims = (10, 12, 20)
+    rng = np.random.default_rng(3)
+    img = rng.standard_normal(dims).astype(np.float32)
+    lbl = rng.integers(0, 3, dims, dtype=np.uint8)
+    pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+    ids = list(range(1000, 1000 + 2 * B))
+    ts = [ctx.submit(ch, lfgpu.sample_desc(i, dims, pi, pl)) for i in ids]
+    ctx.flush()
+    for t in ts:
+        ctx.wait(t)
+    vox = int(np.prod(crop))
+    exp = {i: oracle.chain3d(ocfg, SEED, i, img, lbl)[0] for i in ids}
+
+    def check_batch(b, want_ids, in_place):
+        info = ctx.batch_info(b)
+        assert info["in_place"] == in_place
+        assert sorted(info["ids"]) == sorted(want_ids)
+        host = ctx.batch_to_host(b, info["n"] * (vox * 4 + ((vox + 15) // 16) * 16))
+        n = info["n"]
+        imgs = host[: n * vox * 4].view(np.float32).reshape(n, *crop)
+        lbls = host[n * vox * 4: n * vox * 4 + n * vox].reshape(n, *crop)
+        for k, sid in enumerate(info["ids"]):
+            assert np.array_equal(lbls[k], exp[sid][1])
+            _assert_close(imgs[k], exp[sid][0], atol=1e-6)
+
+    b0 = ctx.seal(ts[:B][::-1])                         # exactly buffer 0, any order
+    check_batch(b0, ids[:B], True)
+    mixed = ts[B: B + B // 2] + ts[B + B // 2:][:B // 2]
+    b1 = ctx.seal(mixed[: B - 1])                       # not the whole buffer -> gather
+    check_batch(b1, [ids[ts.index(t)] for t in mixed[: B - 1]], False)
+    ctx.batch_release(b0)
+    ctx.batch_release(b1)
+    rest = [t for t in ts[B:] if t not in mixed[: B - 1]]
+    for t in rest:
+        ctx.release(t)
+    with pytest.raises(lfgpu.LfgError):
+        ctx.seal([ts[0]])                               # already consumed
+    ctx.synchronize()
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+
+
+def test_progress_reports_stage_boundaries(ctx, lfgpu):
+    """A spin stage before the fused kernel gives ops_done = 1 while the kernel is pending."""
+    ops = lfgpu.img_seg_ops(crop=(8, 8, 16), spin_first=True)
+    ch = ctx.chain(ops)
+    assert ch.stages() == [(0, 1), (1, 6)]
+    dims = (8, 8, 16)
+    img = np.zeros(dims, np.float32)
+    lbl = np.zeros(dims, np.uint8)
+    pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+    t = ctx.submit(ch, lfgpu.sample_desc(5, dims, pi, pl, spin_us=[200_000]))
+    ctx.flush()
+    od, done, _ = ctx.progress(t)
+    assert not done and od == 0
+    ctx.wait(t)
+    od, done, el = ctx.progress(t)
+    assert done and od == 6 and el >= 150_000
+    costs = ctx.exec_costs(t, len(ops))
+    assert costs[0] >= 190_000            # the spin op's device time (us)
+    ctx.release(t)
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+
+
+# ------------------------------------------------------------------ shard loop
+def test_shard_exactly_once_fast_first(lfgpu):
+    """Algorithm 1 on the device: samples whose synthetic cost exceeds t_out are
+    classified slow, finish in the background and are batched after the fast
+    ones; every id is delivered exactly once.  (One sample per launch group, so
+    classification is per sample.)"""
+    ctx = lfgpu.Context(batch_size=8, n_workers=6, max_group=1, max_slot_buffers=16, seed=SEED)
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, spin_first=True))
+    dims = (10, 10, 20)
+    rng = np.random.default_rng(11)
+    img = rng.standard_normal(dims).astype(np.float32)
+    lbl = rng.integers(0, 3, dims, dtype=np.uint8)
+    pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+    n = 96
+    heavy = set(range(3, n, 10))
+    descs = [lfgpu.sample_desc(i, dims, pi, pl, spin_us=[40_000 if i in heavy else 200])
+             for i in range(n)]
+    rc = lfgpu.run_config(batch_size=8, t_out_us=10_000, policy=0, n_workers=6)
+    rep, ids, bsz, cls = ctx.run_shard(ch, descs, rc)
+    assert rep.exactly_once == 1 and rep.duplicates == 0
+    assert sorted(ids.tolist()) == list(range(n))
+    assert rep.slow == len(heavy) and rep.fast == n - len(heavy)
+    assert all(cls[i] == (2 if i in heavy else 1) for i in range(n))
+    assert bsz.sum() == n
+    # a heavy (slow) sample never appears before the fast ones submitted with it
+    pos = {int(s): k for k, s in enumerate(ids)}
+    for h in heavy:
+        assert pos[h] > pos.get(h + 1, -1) or h + 1 >= n
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
