@@ -29,6 +29,8 @@ int64_t host_now_us() {
     return duration_cast<microseconds>(steady_clock::now().time_since_epoch()).count();
 }
 
+static int64_t rows_touched(int64_t h, int oh);
+
 // ------------------------------------------------------------------ params
 // Per-sample generator: the reference's Rng (std::mt19937_64, sample.hpp:25)
 // seeded with experiment.cpp:163's mixing constant keyed by sample id.
@@ -99,6 +101,7 @@ void draw_2d(const Chain& c, uint64_t seed, uint64_t id, int64_t H, int64_t W, P
         p.w = w;
     }
     p.flip = r.unif01() < c.p_hflip;
+    p.rows_touched = rows_touched(p.h, c.oh);
 }
 
 void draw_sp(const Chain& c, uint64_t seed, uint64_t id, int64_t L, ParamsSp& p) {
@@ -117,6 +120,29 @@ void draw_sp(const Chain& c, uint64_t seed, uint64_t id, int64_t L, ParamsSp& p)
         const int room = p.T - w;
         p.t_lo[i] = static_cast<int>(r.randint(0, room > 0 ? room : 0));
     }
+}
+
+// Algorithmic HBM bytes of K3 for one sample: the distinct source rows the
+// bilinear taps touch (exact, from the same index formula the kernel uses)
+// times the crop-box row bytes, plus the f32 output.
+int64_t rrc_algo_bytes(const Chain& c, const Params2D& p) {
+    return p.rows_touched * p.w * 3 + c.out_bytes;
+}
+
+static int64_t rows_touched(int64_t h, int oh) {
+    int64_t rows = 0, last = -1;
+    const double scale = static_cast<double>(h) / oh;
+    for (int y = 0; y < oh; ++y) {
+        double src = (y + 0.5) * scale - 0.5;
+        if (src < 0) src = 0;
+        int64_t a = static_cast<int64_t>(std::floor(src));
+        if (a > h - 1) a = h - 1;
+        const int64_t b = a < h - 1 ? a + 1 : a;
+        if (a > last) ++rows;
+        if (b > a && b > last) ++rows;
+        last = std::max(last, b);
+    }
+    return rows;
 }
 
 int64_t Chain::algo_bytes_per_sample(const lfg_sample_desc& s) const {
@@ -150,6 +176,28 @@ Context::Context(const lfg_config& c) : cfg(c) {
     cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     cuda_check(cudaStreamCreateWithPriority(&seal_stream, cudaStreamNonBlocking, hi), "seal stream");
     cuda_check(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking), "aux stream");
+    // Nothing that can implicitly synchronise the device (stream / event /
+    // buffer creation) may run inside the shard loop: a blocked host loop
+    // would push in-flight samples past t_out.  Pools are created up front.
+    // Stream pool = the hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS = 32,
+    // set when the library loads) minus the seal / aux / trainer streams, so no
+    // two launch groups ever share a queue: a parked (slow) group must not
+    // create a false dependency for the fast groups behind it.
+    for (int i = 0; i < kStreamPool; ++i) {
+        cudaStream_t s;
+        cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        streams_.push_back(s);
+        if (i > 0) free_streams_.push_back(static_cast<int>(streams_.size()) - 1);
+    }
+    cuda_check(warm_stage(), "load stage kernel");
+    cuda_check(warm_img3d(), "load img3d kernel");
+    cuda_check(warm_rrc2d(), "load rrc2d kernel");
+    cuda_check(warm_misc(), "load misc kernels");
+    for (int i = 0; i < 512; ++i) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        free_events_.push_back(e);
+    }
 }
 
 Context::~Context() {
@@ -182,14 +230,7 @@ cudaEvent_t Context::get_event() {
 void Context::put_event(cudaEvent_t e) { free_events_.push_back(e); }
 
 int Context::get_stream() {
-    if (serial) {
-        if (streams_.empty()) {
-            cudaStream_t s;
-            cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-            streams_.push_back(s);
-        }
-        return 0;
-    }
+    if (serial) return 0;   // stream 0 is reserved for serial (roofline) mode
     if (!free_streams_.empty()) {
         int i = free_streams_.back();
         free_streams_.pop_back();
@@ -351,6 +392,7 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
         }
     }
     chains_.push_back(std::move(c));
+    reserve_bufs(chains_.back().get());
     return chains_.back().get();
 }
 
@@ -362,6 +404,14 @@ void Context::chain_destroy(Chain* c) {
             open_buf_.erase(c);
             open_group_[0].erase(c);
             open_group_[1].erase(c);
+            // orphan the chain's buffers: a later chain may be allocated at the
+            // same address, so buffers must never be matched by a stale pointer
+            for (auto& b : bufs_) {
+                if (b.chain != c) continue;
+                b.chain = nullptr;
+                b.open = false;
+                b.assigned = b.live = 0;
+            }
             chains_.erase(chains_.begin() + static_cast<long>(i));
             return;
         }
@@ -382,26 +432,48 @@ bool Context::buf_reusable(SlotBuf& b) {
     return true;
 }
 
-int Context::alloc_buf(const Chain* c, bool for_batch) {
-    // Slot buffers (samples are written into them) and gather buffers (targets
-    // of a collating seal) are bounded separately so stragglers pinning slot
-    // buffers can never starve the seal of a destination.
-    int count = 0;
+bool Context::chain_alive(const Chain* c) const {
+    for (auto& ch : chains_)
+        if (ch.get() == c) return true;
+    return false;
+}
+
+// All output buffers of a chain are created when the chain is (the shard loop
+// never allocates): max_slot_buffers sample-slot buffers plus max_slot_buffers
+// gather (collation target) buffers, bounded separately so stragglers pinning
+// slot buffers can never starve a seal of its destination.  Idle buffers of
+// destroyed chains are recycled first.
+void Context::reserve_bufs(const Chain* c) {
     const int64_t need = static_cast<int64_t>(cfg.batch_size) * c->out_bytes;
-    for (size_t i = 0; i < bufs_.size(); ++i) {
-        SlotBuf& b = bufs_[i];
-        if (b.gather_role != for_batch) continue;
-        bool alive = b.chain == c;
-        if (!alive) {
-            bool chain_live = false;
-            for (auto& ch : chains_) chain_live |= ch.get() == b.chain;
-            if (chain_live) continue;          // belongs to another live chain
-            if (b.bytes < need) continue;      // dead chain's buffer, too small to recycle
-        }
-        ++count;
-        if (buf_reusable(b)) {
+    for (int role = 0; role < 2; ++role) {
+        int have = 0;
+        for (auto& b : bufs_) {
+            if (have >= cfg.max_slot_buffers) break;
+            if (b.gather_role != (role == 1) || chain_alive(b.chain)) continue;
+            if (b.bytes < need || !buf_reusable(b)) continue;
             b.chain = c;
             b.cap = cfg.batch_size;
+            b.assigned = b.live = 0;
+            b.open = b.in_batch = false;
+            ++have;
+        }
+        for (; have < cfg.max_slot_buffers; ++have) {
+            SlotBuf b;
+            cuda_check(cudaMalloc(&b.base, static_cast<size_t>(need)), "cudaMalloc(output buffer)");
+            b.cap = cfg.batch_size;
+            b.chain = c;
+            b.bytes = need;
+            b.gather_role = role == 1;
+            bufs_.push_back(b);
+        }
+    }
+}
+
+int Context::alloc_buf(const Chain* c, bool for_batch) {
+    for (size_t i = 0; i < bufs_.size(); ++i) {
+        SlotBuf& b = bufs_[i];
+        if (b.gather_role != for_batch || b.chain != c) continue;
+        if (buf_reusable(b)) {
             b.assigned = 0;
             b.live = 0;
             b.open = !for_batch;
@@ -409,19 +481,7 @@ int Context::alloc_buf(const Chain* c, bool for_batch) {
             return static_cast<int>(i);
         }
     }
-    if (count >= cfg.max_slot_buffers) {
-        fail(LFG_ERR_AGAIN, "all output buffers are in use (consume or release batches)");
-    }
-    SlotBuf b;
-    cuda_check(cudaMalloc(&b.base, static_cast<size_t>(need)), "cudaMalloc(slot buffer)");
-    b.cap = cfg.batch_size;
-    b.chain = c;
-    b.bytes = need;
-    b.gather_role = for_batch;
-    b.open = !for_batch;
-    b.in_batch = for_batch;
-    bufs_.push_back(b);
-    return static_cast<int>(bufs_.size()) - 1;
+    fail(LFG_ERR_AGAIN, "all output buffers are in use (consume or release batches)");
 }
 
 void Context::assign_slot(Ticket& t, const Chain* c) {
@@ -469,18 +529,57 @@ int64_t Context::get_raw(int64_t bytes) {
 
 static int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
-int64_t Context::stage_raw_bytes(const Chain& c, const Ticket& t) const {
+// Geometry of the bytes a sample's chain reads, as strided boxes (K0 copies
+// them from pinned host memory; see kernels.h for the row-skew convention).
+struct Box {
+    const char* src;
+    int64_t src_py, src_pz;
+    int32_t row_bytes, ny, nz;
+    int64_t dst_py() const { return 16 * ((static_cast<int64_t>(row_bytes) + 30) / 16); }
+    int64_t bytes() const { return dst_py() * ny * nz; }
+};
+
+static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) {
+    const lfg_sample_desc& s = t.desc;
+    wd[0] = wd[1] = wd[2] = 0;
     if (c.fam == FAM_IMG3D) {
-        int64_t vox = 1;
-        for (int a = 0; a < 3; ++a) vox *= std::min<int64_t>(c.crop[a], t.desc.dims[a] - t.p3.off[a]);
-        return align256(vox * 4) + align256(vox);
+        const int64_t H = s.dims[1], W = s.dims[2];
+        for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(c.crop[a], s.dims[a] - t.p3.off[a]);
+        const int64_t first = (t.p3.off[0] * H + t.p3.off[1]) * W + t.p3.off[2];
+        out[0] = Box{static_cast<const char*>(s.data) + first * 4, W * 4, H * W * 4,
+                     static_cast<int32_t>(wd[2] * 4), static_cast<int32_t>(wd[1]),
+                     static_cast<int32_t>(wd[0])};
+        out[1] = Box{static_cast<const char*>(s.aux) + first, W, H * W, static_cast<int32_t>(wd[2]),
+                     static_cast<int32_t>(wd[1]), static_cast<int32_t>(wd[0])};
+        return 2;
     }
-    if (c.fam == FAM_RRC2D) return align256(t.p2.h * t.p2.w * 3);
-    return align256(t.desc.dims[0] * 4);
+    if (c.fam == FAM_RRC2D) {
+        const int64_t W = s.dims[1];
+        out[0] = Box{static_cast<const char*>(s.data) + (t.p2.top * W + t.p2.left) * 3, W * 3, 0,
+                     static_cast<int32_t>(t.p2.w * 3), static_cast<int32_t>(t.p2.h), 1};
+        return 1;
+    }
+    out[0] = Box{static_cast<const char*>(s.data), 0, 0, static_cast<int32_t>(s.dims[0] * 4), 1, 1};
+    return 1;
+}
+
+int64_t Context::stage_raw_bytes(const Chain& c, const Ticket& t) const {
+    Box b[2];
+    int64_t wd[3];
+    const int nb = boxes_of(c, t, b, wd);
+    int64_t total = 0;
+    for (int i = 0; i < nb; ++i) total += align256(b[i].bytes());
+    return total;
 }
 
 // ------------------------------------------------------------------ submit
-int64_t Context::submit(Chain* c, const lfg_sample_desc& s) {
+void draw_params(const Chain& c, uint64_t seed, const lfg_sample_desc& s, PreDraw& out) {
+    if (c.fam == FAM_IMG3D) draw_3d(c, seed, s.id, s.dims, out.p3);
+    else if (c.fam == FAM_RRC2D) draw_2d(c, seed, s.id, s.dims[0], s.dims[1], out.p2);
+    else draw_sp(c, seed, s.id, s.dims[0], out.ps);
+}
+
+int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) {
     if (c == nullptr) fail(LFG_ERR_INVALID, "null chain");
     if (s.data == nullptr) fail(LFG_ERR_INVALID, "sample has no payload");
     if (s.src_kind != LFG_SRC_DEVICE && s.src_kind != LFG_SRC_HOST_PINNED)
@@ -492,16 +591,32 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s) {
         if (s.ndim != 3 || s.aux == nullptr) fail(LFG_ERR_INVALID, "img_seg sample needs a D,H,W volume and a label");
         for (int a = 0; a < 3; ++a)
             if (s.dims[a] < 1 || s.dims[a] > (1 << 20)) fail(LFG_ERR_INVALID, "volume dims out of range");
-        draw_3d(*c, cfg.seed, s.id, s.dims, t.p3);
     } else if (c->fam == FAM_RRC2D) {
         if (s.ndim != 3 || s.dims[2] != 3 || s.dims[0] < 1 || s.dims[1] < 1)
             fail(LFG_ERR_INVALID, "obj_det sample needs an H,W,3 image");
-        draw_2d(*c, cfg.seed, s.id, s.dims[0], s.dims[1], t.p2);
     } else {
         if (s.ndim != 1 || s.dims[0] < 2 || s.dims[0] > c->max_L)
             fail(LFG_ERR_INVALID, "speech sample needs a waveform of length in [2, max_L]");
-        draw_sp(*c, cfg.seed, s.id, s.dims[0], t.ps);
     }
+    if (s.src_kind == LFG_SRC_HOST_PINNED) {
+        // K0 reads the payload over PCIe through its UVA mapping: it must be pinned
+        for (const void* p : {s.data, s.aux}) {
+            if (p == nullptr) continue;
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+                cudaGetLastError();
+                fail(LFG_ERR_INVALID, "LFG_SRC_HOST_PINNED payload is not pinned host memory");
+            }
+        }
+    }
+    PreDraw local;
+    if (pre == nullptr) {
+        draw_params(*c, cfg.seed, s, local);
+        pre = &local;
+    }
+    t.p3 = pre->p3;
+    t.p2 = pre->p2;
+    t.ps = pre->ps;
     for (int k = 0; k < c->n_spin; ++k)
         if (s.spin_us[k] < 0) fail(LFG_ERR_STATE, "negative transform cost");  // balancer.cpp:16
     assign_slot(t, c);
@@ -556,66 +671,81 @@ void Context::launch_group(Group& g) {
     cudaStream_t st = g.stream;
     cuda_check(cudaEventRecord(g.ev[0], st), "record start");
     const int n = static_cast<int>(g.tickets.size());
+    const bool staged = g.src_kind == LFG_SRC_HOST_PINNED;
 
-    // host-pinned payloads: copy only the bytes the chain reads (crop window /
-    // crop box / waveform) into one device staging buffer
-    std::vector<const char*> src0(n), src1(n);
-    std::vector<int64_t> sdim(3 * n);
-    if (g.src_kind == LFG_SRC_HOST_PINNED) {
+    // Host-pinned payloads: K0 pulls exactly the boxes the chain reads over
+    // PCIe into one staging buffer (part of the group's first stage).
+    struct View {
+        const char* p[2];
+        int64_t py[2], pz[2];
+        int32_t sk0[2], sky[2], skz[2];
+        int64_t sdim[3], off[3];
+    };
+    std::vector<View> views(n);
+    if (staged) {
         int64_t total = 0;
         for (int i = 0; i < n; ++i) total += stage_raw_bytes(c, tickets[g.tickets[i]]);
         g.raw_idx = get_raw(total);
         char* dst = raws_[g.raw_idx].ptr;
+        StageLaunch SL{};
         for (int i = 0; i < n; ++i) {
             Ticket& t = tickets[g.tickets[i]];
-            if (c.fam == FAM_IMG3D) {
-                int64_t wd[3];
-                for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(c.crop[a], t.desc.dims[a] - t.p3.off[a]);
-                const int64_t vox = wd[0] * wd[1] * wd[2];
-                for (int plane = 0; plane < 2; ++plane) {
-                    const int64_t esz = plane == 0 ? 4 : 1;
-                    cudaMemcpy3DParms p{};
-                    p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(plane == 0 ? t.desc.data : t.desc.aux),
-                                                   t.desc.dims[2] * esz, t.desc.dims[2], t.desc.dims[1]);
-                    p.srcPos = make_cudaPos(t.p3.off[2] * esz, t.p3.off[1], t.p3.off[0]);
-                    p.dstPtr = make_cudaPitchedPtr(dst, wd[2] * esz, wd[2], wd[1]);
-                    p.extent = make_cudaExtent(wd[2] * esz, wd[1], wd[0]);
-                    p.kind = cudaMemcpyHostToDevice;
-                    cuda_check(cudaMemcpy3DAsync(&p, st), "H2D crop window");
-                    (plane == 0 ? src0 : src1)[i] = dst;
-                    dst += align256(vox * esz);
-                    counters.h2d_bytes += vox * esz;
-                }
-                for (int a = 0; a < 3; ++a) sdim[3 * i + a] = wd[a];
-            } else if (c.fam == FAM_RRC2D) {
-                const int64_t W = t.desc.dims[1];
-                const char* s = static_cast<const char*>(t.desc.data) + (t.p2.top * W + t.p2.left) * 3;
-                cuda_check(cudaMemcpy2DAsync(dst, t.p2.w * 3, s, W * 3, t.p2.w * 3, t.p2.h,
-                                             cudaMemcpyHostToDevice, st),
-                           "H2D crop box");
-                src0[i] = dst;
-                sdim[3 * i] = t.p2.w;
-                counters.h2d_bytes += t.p2.h * t.p2.w * 3;
-                dst += align256(t.p2.h * t.p2.w * 3);
-            } else {
-                cuda_check(cudaMemcpyAsync(dst, t.desc.data, t.desc.dims[0] * 4,
-                                           cudaMemcpyHostToDevice, st),
-                           "H2D waveform");
-                src0[i] = dst;
-                counters.h2d_bytes += t.desc.dims[0] * 4;
-                dst += align256(t.desc.dims[0] * 4);
+            Box b[2];
+            int64_t wd[3];
+            const int nb = boxes_of(c, t, b, wd);
+            View& v = views[i];
+            for (int k = 0; k < nb; ++k) {
+                StageDesc& d = SL.d[SL.n++];
+                d.src = b[k].src;
+                d.dst = dst;
+                d.src_py = b[k].src_py;
+                d.src_pz = b[k].src_pz;
+                d.dst_py = b[k].dst_py();
+                d.dst_pz = b[k].dst_py() * b[k].ny;
+                d.row_bytes = b[k].row_bytes;
+                d.ny = b[k].ny;
+                d.nz = b[k].nz;
+                const uintptr_t sa = reinterpret_cast<uintptr_t>(b[k].src);
+                const int esz = (c.fam == FAM_IMG3D && k == 0) ? 4 : 1;  // skew unit
+                v.p[k] = dst;
+                v.py[k] = d.dst_py / esz;
+                v.pz[k] = d.dst_pz / esz;
+                v.sk0[k] = static_cast<int32_t>((sa & 15) / esz);
+                v.sky[k] = static_cast<int32_t>((b[k].src_py & 15) / esz);
+                v.skz[k] = static_cast<int32_t>((b[k].src_pz & 15) / esz);
+                counters.h2d_bytes += static_cast<int64_t>(b[k].row_bytes) * b[k].ny * b[k].nz;
+                dst += align256(b[k].bytes());
+            }
+            for (int a = 0; a < 3; ++a) {
+                v.sdim[a] = wd[a];
+                v.off[a] = 0;
             }
         }
+        cuda_check(launch_stage(SL, st), "stage launch");
+        counters.launches++;
     } else {
         for (int i = 0; i < n; ++i) {
             Ticket& t = tickets[g.tickets[i]];
-            src0[i] = static_cast<const char*>(t.desc.data);
-            src1[i] = static_cast<const char*>(t.desc.aux);
-            if (c.fam == FAM_IMG3D) for (int a = 0; a < 3; ++a) sdim[3 * i + a] = t.desc.dims[a];
-            else if (c.fam == FAM_RRC2D) sdim[3 * i] = t.desc.dims[1];
+            View& v = views[i];
+            std::memset(&v, 0, sizeof(v));
+            const lfg_sample_desc& s = t.desc;
+            if (c.fam == FAM_IMG3D) {
+                v.p[0] = static_cast<const char*>(s.data);
+                v.p[1] = static_cast<const char*>(s.aux);
+                v.py[0] = v.py[1] = s.dims[2];
+                v.pz[0] = v.pz[1] = s.dims[1] * s.dims[2];
+                for (int a = 0; a < 3; ++a) {
+                    v.sdim[a] = s.dims[a];
+                    v.off[a] = t.p3.off[a];
+                }
+            } else if (c.fam == FAM_RRC2D) {
+                v.p[0] = static_cast<const char*>(s.data) + (t.p2.top * s.dims[1] + t.p2.left) * 3;
+                v.py[0] = s.dims[1] * 3;
+            } else {
+                v.p[0] = static_cast<const char*>(s.data);
+            }
         }
     }
-    const bool staged = g.src_kind == LFG_SRC_HOST_PINNED;
 
     auto launch_spins = [&](int slot) {
         SpinLaunch L{};
@@ -635,14 +765,25 @@ void Context::launch_group(Group& g) {
             L.n = n;
             for (int i = 0; i < n; ++i) {
                 Ticket& t = tickets[g.tickets[i]];
+                const View& v = views[i];
                 Img3dDesc& d = L.d[i];
-                d.img = reinterpret_cast<const float*>(src0[i]);
-                d.lbl = reinterpret_cast<const uint8_t*>(src1[i]);
+                d.img = reinterpret_cast<const float*>(v.p[0]);
+                d.lbl = reinterpret_cast<const uint8_t*>(v.p[1]);
                 d.out_img = reinterpret_cast<float*>(slot_ptr(t, 0));
                 d.out_lbl = reinterpret_cast<uint8_t*>(slot_ptr(t, 1));
+                d.img_py = v.py[0];
+                d.img_pz = v.pz[0];
+                d.lbl_py = v.py[1];
+                d.lbl_pz = v.pz[1];
+                d.img_sk0 = v.sk0[0];
+                d.img_sky = v.sky[0];
+                d.img_skz = v.skz[0];
+                d.lbl_sk0 = v.sk0[1];
+                d.lbl_sky = v.sky[1];
+                d.lbl_skz = v.skz[1];
                 for (int a = 0; a < 3; ++a) {
-                    d.sdim[a] = static_cast<int32_t>(sdim[3 * i + a]);
-                    d.off[a] = staged ? 0 : static_cast<int32_t>(t.p3.off[a]);
+                    d.sdim[a] = static_cast<int32_t>(v.sdim[a]);
+                    d.off[a] = static_cast<int32_t>(v.off[a]);
                 }
                 d.flip = t.p3.flip[0] | (t.p3.flip[1] << 1) | (t.p3.flip[2] << 2);
                 d.scale = static_cast<float>(t.p3.scale);
@@ -665,18 +806,17 @@ void Context::launch_group(Group& g) {
             L.n = n;
             for (int i = 0; i < n; ++i) {
                 Ticket& t = tickets[g.tickets[i]];
+                const View& v = views[i];
                 RrcDesc& d = L.d[i];
-                d.src = reinterpret_cast<const uint8_t*>(src0[i]);
+                d.src = reinterpret_cast<const uint8_t*>(v.p[0]);
                 d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
-                d.sw = static_cast<int32_t>(sdim[3 * i]);
-                d.top = staged ? 0 : static_cast<int32_t>(t.p2.top);
-                d.left = staged ? 0 : static_cast<int32_t>(t.p2.left);
+                d.pitch = v.py[0];
+                d.sk0 = v.sk0[0];
+                d.sky = v.sky[0];
                 d.h = static_cast<int32_t>(t.p2.h);
                 d.w = static_cast<int32_t>(t.p2.w);
                 d.flip = t.p2.flip;
-                const int64_t rows = std::min<int64_t>(t.p2.h, 2 * c.oh);
-                const int64_t cols = std::min<int64_t>(t.p2.w, 2 * c.ow);
-                counters.kernel_bytes += c.out_bytes + rows * cols * 3;
+                counters.kernel_bytes += rrc_algo_bytes(c, t.p2);
             }
             cuda_check(launch_rrc2d(L, st), "rrc2d launch");
             counters.launches++;
@@ -710,7 +850,7 @@ bool Context::poll_group(Group& g) {
     g.complete = true;
     finalize_group_timing(g);
     counters.completed += static_cast<int64_t>(g.tickets.size());
-    if (!serial || g.stream_idx != 0) free_streams_.push_back(g.stream_idx);
+    if (g.stream_idx != 0) free_streams_.push_back(g.stream_idx);
     if (g.raw_idx >= 0) {
         free_raws_.push_back(g.raw_idx);
         g.raw_idx = -1;
@@ -860,7 +1000,7 @@ int64_t Context::seal(const int64_t* ts, int n) {
         }
         cuda_check(launch_gather(L, seal_stream), "gather launch");
         counters.launches++;
-        counters.kernel_bytes += 2 * static_cast<int64_t>(n) * c->out_bytes;
+        counters.reserved[0] += 2 * static_cast<int64_t>(n) * c->out_bytes;  // gather bytes
         std::sort(src_bufs.begin(), src_bufs.end());
         src_bufs.erase(std::unique(src_bufs.begin(), src_bufs.end()), src_bufs.end());
         for (int sb : src_bufs) {

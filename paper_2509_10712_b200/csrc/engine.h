@@ -72,12 +72,19 @@ struct Chain {
 
 // Per-sample drawn parameters (host, std::mt19937_64 keyed by sample id).
 struct Params3D { int64_t off[3]; int flip[3]; double scale, sigma; uint32_t key[2]; };
-struct Params2D { int64_t top, left, h, w; int flip; };
+struct Params2D { int64_t top, left, h, w; int flip; int64_t rows_touched; };
 struct ParamsSp { int T; int f_lo[2], f_w[2]; int t_lo[10], t_w[10]; };
 
 void draw_3d(const Chain& c, uint64_t seed, uint64_t id, const int64_t dims[3], Params3D& p);
 void draw_2d(const Chain& c, uint64_t seed, uint64_t id, int64_t H, int64_t W, Params2D& p);
 void draw_sp(const Chain& c, uint64_t seed, uint64_t id, int64_t L, ParamsSp& p);
+
+// One sample's drawn parameters (whichever family applies); pure function of
+// (chain, seed, sample id, dims), so the shard runner draws them ahead of time
+// on a host thread pool.
+struct PreDraw { Params3D p3{}; Params2D p2{}; ParamsSp ps{}; };
+void draw_params(const Chain& c, uint64_t seed, const lfg_sample_desc& s, PreDraw& out);
+int64_t rrc_algo_bytes(const Chain& c, const Params2D& p);
 
 struct SlotBuf {
     char* base = nullptr;
@@ -148,7 +155,7 @@ public:
     Chain* chain_create(const lfg_op* ops, int n);
     void chain_destroy(Chain* c);
 
-    int64_t submit(Chain* c, const lfg_sample_desc& s);
+    int64_t submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre = nullptr);
     void flush();
     void progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed_us);
     void wait(int64_t t);
@@ -161,6 +168,11 @@ public:
     void batch_wait_stream(int64_t b, cudaStream_t s);
     void batch_release(int64_t b, cudaStream_t s);
     void trainer_step(int64_t b, cudaStream_t s, int64_t us);
+    // samples assigned to slot buffer bi once it stopped accepting new ones; -1 otherwise
+    int buf_closed_count(int bi) const {
+        const SlotBuf& b = bufs_[bi];
+        return (b.open || b.in_batch) ? -1 : b.assigned;
+    }
     void batch_ptr(const BatchRec& br, void** p, int64_t* bytes) const {
         *p = bufs_[br.buf].base;
         *bytes = bufs_[br.buf].bytes;
@@ -172,6 +184,8 @@ public:
     void finalize_group_timing(Group& g);
     int64_t open_group_count() const;
 
+    static constexpr int kStreamPool = 28;
+    int free_stream_count() const { return static_cast<int>(free_streams_.size()); }
     lfg_counters counters{};
     bool serial = false;
     std::mutex mu;   // one lock per context (C ABI calls serialise on it)
@@ -198,6 +212,8 @@ private:
     void put_event(cudaEvent_t e);
     int get_stream();
     int alloc_buf(const Chain* c, bool for_batch);
+    void reserve_bufs(const Chain* c);
+    bool chain_alive(const Chain* c) const;
     bool buf_reusable(SlotBuf& b);
     void assign_slot(Ticket& t, const Chain* c);
     int64_t get_raw(int64_t bytes);

@@ -31,7 +31,6 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
     const int fz = (d.flip & 1) ? cd - 1 - z : z;
     const int sz = d.off[0] + fz;
     const bool z_ok = sz < d.sdim[0];
-    const int64_t plane = (int64_t)d.sdim[1] * d.sdim[2];
     const bool noise = d.sigma != 0.0f;
 
     for (int qx = threadIdx.x; qx < cw4; qx += 32) {
@@ -45,15 +44,19 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
             const int fy = (d.flip & 2) ? ch - 1 - y : y;
             const int sy = d.off[1] + fy;
             const bool row_ok = z_ok && y < ch && sy < d.sdim[1];
-            const int64_t row = (int64_t)sz * plane + (int64_t)sy * d.sdim[2];
+            // row start (see kernels.h): pitch + alignment-phase skew
+            const float* irow = d.img + sz * d.img_pz + sy * d.img_py +
+                                ((d.img_sk0 + sz * d.img_skz + sy * d.img_sky) & 3);
+            const uint8_t* lrow = d.lbl + sz * d.lbl_pz + sy * d.lbl_py +
+                                  ((d.lbl_sk0 + sz * d.lbl_skz + sy * d.lbl_sky) & 15);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int x = 4 * qx + j;
                 const int fx = (d.flip & 4) ? cw - 1 - x : x;
                 const int sx = d.off[2] + fx;
                 const bool ok = row_ok && sx < d.sdim[2];
-                v[r][j] = ok ? __ldg(d.img + row + sx) : 0.0f;
-                l[r][j] = ok ? __ldg(d.lbl + row + sx) : (uint8_t)0;
+                v[r][j] = ok ? __ldg(irow + sx) : 0.0f;
+                l[r][j] = ok ? __ldg(lrow + sx) : (uint8_t)0;
             }
         }
 #pragma unroll
@@ -93,4 +96,11 @@ cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+}  // namespace lfg
+
+namespace lfg {
+cudaError_t warm_img3d() {
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, img3d_kernel);
+}
 }  // namespace lfg

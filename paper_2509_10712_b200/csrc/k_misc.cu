@@ -161,3 +161,13 @@ cudaError_t launch_synth_waveform(uint64_t seed, uint64_t id, int64_t L, float* 
 }
 
 }  // namespace lfg
+
+namespace lfg {
+cudaError_t warm_misc() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, spin_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, trainer_spin_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gather_kernel);
+    return e;
+}
+}  // namespace lfg

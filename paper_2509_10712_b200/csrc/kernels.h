@@ -15,14 +15,38 @@ constexpr int kMaxSp = 64;   // speech utterances per launch group
 constexpr int kMaxSpin = 64;
 constexpr int kMaxGather = 256;
 
+// Row addressing shared by K1/K3: a source row (z, y) starts at
+//   base + z*pitch_z + y*pitch_y + ((skew0 + z*skew_z + y*skew_y) & mask)
+// For HBM-resident payloads the skews are 0.  For payloads staged from pinned
+// host memory by K0 the skews re-create the source's 16-byte alignment phase,
+// which lets K0 move every row with aligned 16-byte loads and stores.
+
+// ---- K0: strided-box gather from pinned host memory (PCIe) into HBM staging
+struct StageDesc {
+    const char* src;         // first byte of the box in host memory (UVA pointer)
+    char* dst;               // 16-B aligned staging base
+    int64_t src_py, src_pz;  // host row / plane pitch (bytes)
+    int64_t dst_py, dst_pz;  // staging row / plane pitch (bytes, multiples of 16)
+    int32_t row_bytes, ny, nz;
+    int32_t pad;
+};
+struct StageLaunch {
+    int32_t n;
+    StageDesc d[2 * 64];
+};
+
 // ---- K1: RandomCrop + RandomFlip + RandomBrightness + GaussianNoise + Cast
 struct Img3dDesc {
-    const float* img;        // source buffer (full volume or staged crop window)
+    const float* img;        // source: full volume (HBM) or staged crop window
     const uint8_t* lbl;
     float* out_img;          // [cd, ch, cw] f32
     uint8_t* out_lbl;        // [cd, ch, cw] u8
-    int32_t sdim[3];         // source buffer extents (d, h, w)
-    int32_t off[3];          // crop origin inside the source buffer
+    int64_t img_py, img_pz;  // row / plane pitch in elements
+    int64_t lbl_py, lbl_pz;  // row / plane pitch in bytes
+    int32_t img_sk0, img_sky, img_skz;  // skew in floats (mask 3)
+    int32_t lbl_sk0, lbl_sky, lbl_skz;  // skew in bytes (mask 15)
+    int32_t sdim[3];         // valid extents of the source (d, h, w)
+    int32_t off[3];          // crop origin inside the source
     int32_t flip;            // bit a = flip axis a
     float scale;             // brightness multiplier
     float sigma;             // noise std (0 = no noise)
@@ -36,12 +60,13 @@ struct Img3dLaunch {
 
 // ---- K3: RandomResizedCrop (bilinear) + RandomHorizontalFlip + ToTensor + Normalize
 struct RrcDesc {
-    const uint8_t* src;      // HWC u8 buffer (full image or staged crop box)
+    const uint8_t* src;      // crop-box origin (row 0, column 0) of an HWC u8 image
     float* out;              // [3, oh, ow] f32
-    int32_t sw;              // source row length in pixels
-    int32_t top, left;       // crop origin inside the buffer
+    int64_t pitch;           // bytes per source row
+    int32_t sk0, sky;        // row skew (mask 15), see above
     int32_t h, w;            // crop box size
     int32_t flip;
+    int32_t pad;
 };
 struct RrcLaunch {
     int32_t oh, ow;
@@ -83,11 +108,20 @@ struct GatherLaunch {
     int64_t dst_plane_stride;
 };
 
+cudaError_t launch_stage(const StageLaunch& L, cudaStream_t s);
 cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s);
 cudaError_t launch_rrc2d(const RrcLaunch& L, cudaStream_t s);
 cudaError_t launch_spin(const SpinLaunch& L, cudaStream_t s);
 cudaError_t launch_gather(const GatherLaunch& L, cudaStream_t s);
 cudaError_t launch_trainer_spin(int64_t ns, int ctas, cudaStream_t s);
+int rrc2d_smem_bytes(const RrcLaunch& L);
+
+// Force module loading at context creation: with lazy loading the first launch
+// of a kernel loads its module, which can stall the shard loop mid-run.
+cudaError_t warm_stage();
+cudaError_t warm_img3d();
+cudaError_t warm_rrc2d();
+cudaError_t warm_misc();
 
 // speech: constant tables (window, DFT basis, mel filterbank) live in device memory
 struct SpeechTables;

@@ -20,9 +20,12 @@
 //                  p75 after warm-up, p90 escalation above a 0.35 slow rate,
 //                  de-escalation on a full window below 0.15 (profiler.cpp:47-72)
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <memory>
 #include <deque>
 #include <thread>
+#include <unordered_map>
 
 #include "engine.h"
 
@@ -125,6 +128,39 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         else rep.fast += static_cast<int64_t>(g.tickets.size());
     };
 
+    // Parameter prefetch: the per-sample draws (std::mt19937_64 seeding + twist,
+    // ~2 us each) are a pure function of (seed, id, dims), so a host thread pool
+    // draws them ahead of the submit loop, chunk by chunk.
+    constexpr int64_t kChunk = 64;
+    const int64_t n_chunks = (n + kChunk - 1) / kChunk;
+    std::vector<PreDraw> pre(static_cast<size_t>(n));
+    std::unique_ptr<std::atomic<uint8_t>[]> ready(new std::atomic<uint8_t>[std::max<int64_t>(n_chunks, 1)]);
+    for (int64_t i = 0; i < n_chunks; ++i) ready[i].store(0, std::memory_order_relaxed);
+    std::atomic<int64_t> next_chunk{0};
+    std::atomic<bool> stop_draw{false};
+    const int n_threads = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({8, std::max(1u, std::thread::hardware_concurrency()) / 2, n_chunks})));
+    std::vector<std::thread> drawers;
+    for (int t = 0; t < n_threads; ++t) {
+        drawers.emplace_back([&] {
+            for (;;) {
+                const int64_t ck = next_chunk.fetch_add(1);
+                if (ck >= n_chunks || stop_draw.load(std::memory_order_relaxed)) return;
+                for (int64_t i = ck * kChunk; i < std::min(n, (ck + 1) * kChunk); ++i)
+                    draw_params(*chain, ctx.cfg.seed, samples[i], pre[i]);
+                ready[ck].store(1, std::memory_order_release);
+            }
+        });
+    }
+    struct Joiner {
+        std::vector<std::thread>& th;
+        std::atomic<bool>& stop;
+        ~Joiner() {
+            stop.store(true);
+            for (auto& t : th) t.join();
+        }
+    } joiner{drawers, stop_draw};
+
     while (consumed < n) {
         bool progressed = false;
         const int64_t now = host_now_us();
@@ -148,8 +184,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 remove = true;
             }
             if (remove) {
-                inflight[k] = inflight.back();
-                inflight.pop_back();
+                inflight.erase(inflight.begin() + static_cast<long>(k));  // keep launch order
                 progressed = true;
             } else {
                 ++k;
@@ -161,21 +196,23 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             if (ctx.poll_group(g)) {
                 for (int64_t t : g.tickets) slow.push_back(t);
                 prof.record(total_us(g), true);
-                parked[k] = parked.back();
-                parked.pop_back();
+                parked.erase(parked.begin() + static_cast<long>(k));
                 progressed = true;
             } else {
                 ++k;
             }
         }
         // (3) feed new samples while a worker (stream) is free
-        while (static_cast<int>(inflight.size()) < n_workers && fed < n) {
+        while (static_cast<int>(inflight.size()) < n_workers && fed < n &&
+               (ctx.serial || ctx.free_stream_count() > 0)) {
             const int64_t take = std::min<int64_t>(group, n - fed);
             int64_t got = 0;
             int64_t gid = -1;
             try {
                 for (; got < take; ++got) {
-                    const int64_t t = ctx.submit(chain, samples[fed + got]);
+                    const int64_t i = fed + got;
+                    while (!ready[i / kChunk].load(std::memory_order_acquire)) std::this_thread::yield();
+                    const int64_t t = ctx.submit(chain, samples[i], &pre[i]);
                     gid = ctx.tickets[t].group;
                 }
             } catch (const Error& e) {
@@ -195,7 +232,31 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             const int64_t k = std::min<int64_t>(B, static_cast<int64_t>(fast.size() + slow.size()));
             std::vector<int64_t> ts;
             ts.reserve(static_cast<size_t>(k));
-            for (int64_t i = 0; i < k; ++i) {
+            // Zero-copy preference: if every sample of some closed slot buffer is
+            // in the fast list, seal exactly those (the buffer becomes the batch).
+            // Eagerness is unchanged -- a batch is sealed whenever B samples are
+            // ready -- only its membership is chosen to avoid the gather copy.
+            if (k == B && static_cast<int64_t>(fast.size()) >= B) {
+                std::unordered_map<int, int> per_buf;
+                for (int64_t t : fast) per_buf[ctx.tickets[t].buf]++;
+                int pick = -1;
+                for (auto& kv : per_buf)
+                    if (kv.second == B && ctx.buf_closed_count(kv.first) == B) {
+                        pick = kv.first;
+                        break;
+                    }
+                if (pick >= 0) {
+                    for (auto it = fast.begin(); it != fast.end();) {
+                        if (ctx.tickets[*it].buf == pick) {
+                            ts.push_back(*it);
+                            it = fast.erase(it);
+                        } else {
+                            ++it;
+                        }
+                    }
+                }
+            }
+            for (int64_t i = static_cast<int64_t>(ts.size()); i < k; ++i) {
                 if (!fast.empty()) {
                     ts.push_back(fast.front());
                     fast.pop_front();
