@@ -119,11 +119,15 @@ def dist_setup(n_gpus: int):
     return 0, 0, 1, None
 
 
+def _coll_device(dist, local: int) -> str:
+    return f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+
+
 def allreduce_max(dist, x: float, local: int) -> float:
     if dist is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device(dist, local))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -133,7 +137,7 @@ def allreduce_sum(dist, xs, local: int):
     if dist is None:
         return list(xs)
     import torch
-    t = torch.tensor(list(xs), dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor(list(xs), dtype=torch.float64, device=_coll_device(dist, local))
     dist.all_reduce(t)
     return t.tolist()
 
@@ -299,33 +303,47 @@ def kernel_roofline(L, ctx, wl, ids, hbm_peak):
             "mean_launch_us": round(1e3 * ms / max(launches, 1), 2)}
 
 
-def cpu_baseline(workload: str, seconds: float = 12.0):
-    """The CPU oracle (a port of the chain, fp64) on all host cores: a bounded sample."""
+def ref_harness():
+    p = os.path.join(ROOT, "oracle", "_ref", "minato_cpu")
+    return p if os.path.exists(p) else None
+
+
+def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: int = 2):
+    """Reported CPU baseline on this host's cores: the reference CPU loader
+    (oracle/_ref/minato_cpu: reference libloadflow + oracle transforms) when it
+    was built, else the oracle port alone on a thread pool.  Bounded sample."""
+    cores = os.cpu_count() or 1
+    h = ref_harness()
+    wl = "rrc" if workload == "rrc" else "img3d"
+    if h:
+        k = steps or (8 if wl == "rrc" else 10)
+        out = subprocess.run([h, "--workload", wl, "--steps", str(k), "--warmup", str(warmup),
+                              "--workers", str(cores), "--max-seconds", "150"],
+                             capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
+        b = json.loads(out)
+        return {"value": b["value"], "unit": "samples/s", "cores": b["cores"], "kind": "reference",
+                "sample": b["sample"] + f"; timed {b['samples']:.0f} samples over {b['span_ms']:.0f} ms"}
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import lf_oracle as O
     from concurrent.futures import ThreadPoolExecutor
-    cores = os.cpu_count() or 1
     rng = np.random.default_rng(5)
-    if workload == "rrc":
+    if wl == "rrc":
         cfg = O.cfg2d()
-        imgs = [rng.integers(0, 256, (int(h), int(w), 3), dtype=np.uint8)
-                for h, w in rng.integers(256, 513, size=(32, 2))]
+        imgs = [rng.integers(0, 256, (int(h_), int(w_), 3), dtype=np.uint8)
+                for h_, w_ in rng.integers(256, 513, size=(32, 2))]
 
         def one(i):
             O.chain2d(cfg, 1, i, imgs[i % len(imgs)])
         sample = "RandomResizedCrop224+flip+normalize on 3x(256..512)^2 u8 images"
     else:
         cfg = O.cfg3d()
-        vols = []
-        for _ in range(2):
-            D = 160
-            vols.append((rng.standard_normal((D, 384, 384)).astype(np.float32),
-                         rng.integers(0, 3, (D, 384, 384), dtype=np.uint8)))
+        vols = [(rng.standard_normal((128, 384, 384)).astype(np.float32),
+                 rng.integers(0, 3, (128, 384, 384), dtype=np.uint8)) for _ in range(2)]
 
         def one(i):
             v = vols[i % len(vols)]
             O.chain3d(cfg, 1, i, v[0], v[1])
-        sample = "crop128^3+flip+brightness+noise+cast on 160x384x384 volumes"
+        sample = "crop128^3+flip+brightness+noise+cast on 128x384x384 volumes"
     done = 0
     t0 = time.perf_counter()
     with ThreadPoolExecutor(cores) as ex:
@@ -334,34 +352,27 @@ def cpu_baseline(workload: str, seconds: float = 12.0):
             done += cores
     el = time.perf_counter() - t0
     return {"value": round(done / el, 2), "unit": "samples/s", "cores": cores, "kind": "port",
-            "sample": f"{done} samples of {sample} in {el:.1f} s (oracle, fp64, "
-                      f"{cores} threads)"}
+            "sample": f"{done} samples of {sample} in {el:.1f} s (oracle, fp64, {cores} threads)"}
 
 
 def reference_arm(args):
+    """--impl reference: the reference's own CPU loader on all host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     wl = args.workload
-    harness = os.path.join(ROOT, "oracle", "_ref", "minato_cpu")
-    if os.path.exists(harness):
-        out = subprocess.run([harness, "--workload", wl, "--steps", str(args.steps),
-                              "--warmup", str(args.warmup)], capture_output=True, text=True,
-                             check=True).stdout.strip().splitlines()[-1]
-        base = json.loads(out)
-        kind = "reference"
-    else:
-        base = cpu_baseline(wl, seconds=max(5.0, min(60.0, 2.0 * args.steps)))
-        kind = "port"
+    B = 256 if wl == "rrc" else 2
+    base = cpu_baseline(wl, seconds=max(5.0, min(60.0, 2.0 * args.steps)), steps=args.steps,
+                        warmup=args.warmup)
     v = base["value"]
     line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 * (256 if wl == "rrc" else 2) / v, 3) if v else None,
+            "ms_per_step": round(1e3 * B / v, 3) if v else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": wl, "batch": 256 if wl == "rrc" else 2},
+            "config": {"workload": wl, "batch": B},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": base["cores"],
-                             "kind": kind, "sample": base["sample"]},
+                             "kind": base["kind"], "sample": base["sample"]},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

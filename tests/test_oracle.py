@@ -1,0 +1,188 @@
+"""CPU tests of the oracle (test infrastructure) -- pinning it before trusting it.
+
+1. Generators: mt19937_64 against libstdc++'s std::mt19937_64 (the reference's
+   Rng, sample.hpp:25) and Philox4x32-10 against the Random123 known-answer
+   vectors.
+2. Formulas: bilinear resize against torch F.interpolate(antialias=False);
+   STFT power against torch.stft; the slaney mel filterbank against
+   torchaudio.functional.melscale_fbanks; normalize against torchvision.
+3. Regression: the committed golden fixtures (tests/golden, made by
+   make_golden.py) are reproduced exactly.
+4. Semantics: parameter draws stay in range; crop/flip/label movement is a
+   pure permutation; noise statistics."""
+import os
+
+import numpy as np
+import pytest
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SEED = 1
+
+
+def test_mt19937_64_matches_libstdcxx(oracle):
+    kat = np.load(os.path.join(GOLD, "mt19937_64_kat.npy"))
+    seeds = [5489, 42, 1 ^ ((0x9e3779b97f4a7c15 * 8) & (2**64 - 1))]
+    got = np.concatenate([oracle.mt64(s, 8) for s in seeds])
+    assert np.array_equal(got, kat[:24])
+    assert oracle.mt64(5489, 10000)[-1] == kat[24] == 9981545732273789042  # C++ standard KAT
+
+
+@pytest.mark.parametrize("ctr,key,want", [
+    ([0, 0, 0, 0], [0, 0], [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]),
+    ([0xffffffff] * 4, [0xffffffff] * 2, [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]),
+    ([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0],
+     [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]),
+])
+def test_philox4x32_10_random123_kat(oracle, ctr, key, want):
+    assert list(oracle.philox(ctr, key)) == want
+
+
+def test_box_muller_normals_are_standard(oracle):
+    z = np.concatenate([oracle.normals4(g, 12345, 678) for g in range(20000)])
+    assert abs(z.mean()) < 0.02 and abs(z.std() - 1.0) < 0.02
+    assert abs(np.mean(z ** 3)) < 0.05 and abs(np.mean(z ** 4) - 3.0) < 0.15
+
+
+# ------------------------------------------------------------ formulas vs torch
+def test_bilinear_matches_torch_interpolate(oracle):
+    torch = pytest.importorskip("torch")
+    import torch.nn.functional as F
+    rng = np.random.default_rng(0)
+    for (H, W), (oh, ow) in [((37, 53), (16, 16)), ((37, 53), (224, 224)), ((300, 420), (224, 224)),
+                             ((512, 130), (224, 224))]:
+        src = (rng.random((3, H, W)) * 255).astype(np.float32)
+        a = oracle.bilinear_chw(src, oh, ow)
+        b = F.interpolate(torch.from_numpy(src)[None].double(), size=(oh, ow), mode="bilinear",
+                          align_corners=False, antialias=False)[0].numpy()
+        assert np.abs(a - b).max() < 1e-9
+
+
+def test_rrc_chain_matches_torchvision_ops(oracle):
+    torch = pytest.importorskip("torch")
+    tvf = pytest.importorskip("torchvision.transforms.v2.functional")
+    import torch.nn.functional as F
+    cfg = oracle.cfg2d()
+    rng = np.random.default_rng(1)
+    for sid in range(6):
+        H, W = (int(x) for x in rng.integers(256, 513, 2))
+        img = rng.integers(0, 256, (H, W, 3), dtype=np.uint8)
+        out, p = oracle.chain2d(cfg, SEED, sid, img)
+        crop = torch.from_numpy(img).permute(2, 0, 1)[:, p.top:p.top + p.h, p.left:p.left + p.w]
+        r = F.interpolate(crop[None].double(), size=(224, 224), mode="bilinear",
+                          align_corners=False, antialias=False)[0]
+        if p.flip:
+            r = torch.flip(r, dims=[2])
+        r = tvf.normalize(r / 255.0, list(cfg.mean), list(cfg.std))
+        assert np.abs(out - r.numpy()).max() < 1e-9
+
+
+def test_rrc_params_follow_torchvision_rules(oracle):
+    cfg = oracle.cfg2d()
+    rng = np.random.default_rng(2)
+    n_fallback = 0
+    for sid in range(2000):
+        H, W = (int(x) for x in rng.integers(16, 700, 2))
+        p = oracle.draw2d(cfg, SEED, sid, H, W)
+        assert 0 <= p.top <= H - p.h and 0 <= p.left <= W - p.w
+        assert 0 < p.h <= H and 0 < p.w <= W
+        area = p.h * p.w / (H * W)
+        if not (0.08 * 0.9 <= area <= 1.0 + 1e-9):
+            n_fallback += 1   # centre-crop fallback after 10 rejected tries
+    assert n_fallback < 200
+
+
+def test_stft_power_and_mel_match_torch(oracle):
+    torch = pytest.importorskip("torch")
+    ta = pytest.importorskip("torchaudio")
+    cfg = oracle.cfgsp(freq_masks=0, time_masks=0)
+    rng = np.random.default_rng(3)
+    wav = rng.standard_normal(4000).astype(np.float32)
+    (lm, pw), p = oracle.chainsp(cfg, SEED, 9, wav, want_power=True)
+    X = torch.stft(torch.from_numpy(wav).double(), 512, hop_length=160, win_length=320,
+                   window=torch.hann_window(320, dtype=torch.float64), center=True,
+                   pad_mode="reflect", return_complex=True)
+    P = (X.abs() ** 2).numpy()
+    assert pw.shape == P.shape and np.abs(pw - P).max() / P.max() < 1e-12
+    fb = ta.functional.melscale_fbanks(257, 0.0, 8000.0, 80, 16000, norm="slaney",
+                                       mel_scale="slaney").T.double().numpy()
+    ofb = oracle.mel_fbank(cfg)
+    assert np.abs(ofb - fb).max() < 1e-6 * np.abs(fb).max() * 10   # torchaudio builds it in fp32
+    lm2 = np.log(ofb @ P + 2.0 ** -24)
+    assert np.abs(lm - lm2).max() < 1e-9
+
+
+# ------------------------------------------------------------ golden fixtures
+def _cases(path):
+    z = np.load(path)
+    n = 1 + max(int(k.split("_")[0]) for k in z.files)
+    return [{k.split("_", 1)[1]: z[k] for k in z.files if k.startswith(f"{i}_")} for i in range(n)]
+
+
+def test_golden_img3d(oracle):
+    for c in _cases(os.path.join(GOLD, "img3d.npz")):
+        kw = dict(crop=(8, 8, 16))
+        if int(c["forced"]):
+            kw.update(p_flip=0.5, p_bright=1.0, p_noise=1.0)
+        cfg = oracle.cfg3d(**kw)
+        (o_img, o_lbl), p = oracle.chain3d(cfg, SEED, int(c["sid"]), c["img"], c["lbl"])
+        assert list(p.off) == list(c["off"]) and list(p.flip) == list(c["flip"])
+        assert p.scale == float(c["scale"]) and p.sigma == float(c["sigma"])
+        assert np.array_equal(o_lbl, c["out_lbl"]) and np.array_equal(o_img, c["out_img"])
+
+
+def test_golden_rrc2d(oracle):
+    cfg = oracle.cfg2d(out_h=32, out_w=32)
+    for c in _cases(os.path.join(GOLD, "rrc2d.npz")):
+        out, p = oracle.chain2d(cfg, SEED, int(c["sid"]), c["img"])
+        assert [p.top, p.left, p.h, p.w, p.flip] == list(c["box"])
+        assert np.array_equal(out, c["out"])
+
+
+def test_golden_speech(oracle):
+    cfg = oracle.cfgsp()
+    for c in _cases(os.path.join(GOLD, "speech.npz")):
+        (lm, _), p = oracle.chainsp(cfg, SEED, int(c["sid"]), c["wav"])
+        assert p.n_frames == int(c["masks"][0])
+        assert np.array_equal(lm, c["logmel"])
+
+
+# ------------------------------------------------------------ semantics
+def test_img3d_crop_flip_is_a_permutation(oracle):
+    """With brightness/noise off, the image output is an exact re-indexing of the
+    input (crop + flips), and labels move identically (bit-exact movement)."""
+    cfg = oracle.cfg3d(crop=(8, 8, 16), p_flip=0.5, p_bright=0.0, p_noise=0.0)
+    dims = (10, 12, 20)
+    n = int(np.prod(dims))
+    img = np.arange(n, dtype=np.float32).reshape(dims)
+    lbl = (np.arange(n) % 251).astype(np.uint8).reshape(dims)
+    for sid in range(50):
+        (o_img, o_lbl), p = oracle.chain3d(cfg, SEED, sid, img, lbl)
+        sl = tuple(slice(p.off[a], p.off[a] + (8, 8, 16)[a]) for a in range(3))
+        want = img[sl]
+        for a in range(3):
+            if p.flip[a]:
+                want = np.flip(want, axis=a)
+        assert np.array_equal(o_img, want.astype(np.float64))
+        assert np.array_equal(o_lbl, (want.astype(np.int64) % 251).astype(np.uint8))
+
+
+def test_img3d_zero_pads_small_volumes(oracle):
+    cfg = oracle.cfg3d(crop=(16, 16, 32), p_flip=0.0, p_bright=0.0, p_noise=0.0)
+    img = np.ones((5, 6, 7), np.float32)
+    lbl = np.ones((5, 6, 7), np.uint8)
+    (o_img, o_lbl), p = oracle.chain3d(cfg, SEED, 3, img, lbl)
+    assert list(p.off) == [0, 0, 0]
+    assert o_img.sum() == 5 * 6 * 7 and o_img[5:].sum() == 0 and o_lbl[:, 6:].sum() == 0
+
+
+def test_specaugment_masks_in_range(oracle):
+    cfg = oracle.cfgsp()
+    for sid in range(300):
+        L = 30000 + 467 * sid
+        p = oracle.drawsp(cfg, SEED, sid, L)
+        T = p.n_frames
+        assert T == 1 + L // 160
+        for i in range(2):
+            assert 0 <= p.f_w[i] <= 27 and 0 <= p.f_lo[i] and p.f_lo[i] + p.f_w[i] <= 80
+        for i in range(10):
+            assert 0 <= p.t_w[i] <= int(0.05 * T) and p.t_lo[i] + p.t_w[i] <= T
