@@ -505,6 +505,10 @@ void unbind_all();
 TransformChain img_seg_chain(int crop = 128);
 TransformChain obj_det_chain(int out = 224);
 
+// Compiles a device chain for a shard ahead of the run (allocates its output
+// pools); otherwise the first process_sample compiles it on the clock.
+void prepare_chain(const TransformChain& chain, int shard);
+
 // Seals a batch of completed device samples into a device-resident batch
 // (lfg_seal_batch); fills Batch::device_batch.
 void seal_device_batch(Batch& batch);

@@ -1,6 +1,7 @@
 // api.cpp -- extern "C" entry points (include/lfgpu.h).  Every call takes the
 // context lock, converts engine exceptions into LFG_ERR_* codes and records a
 // thread-local message for lfg_last_error().
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -302,10 +303,23 @@ int lfg_progress(lfg_ctx* ctx, lfg_ticket t, int* ops_done, int* complete, int64
 }
 
 int lfg_wait(lfg_ctx* ctx, lfg_ticket t) {
+    // Never block while holding the context lock: a slow sample's wait (the
+    // resume path) would stall every other thread's progress polls and push
+    // their fast samples past t_out.  Launch under the lock, then poll.
     return guarded([&] {
         Context& c = C(ctx);
-        std::lock_guard<std::mutex> g(c.mu);
-        c.wait(t);
+        {
+            std::lock_guard<std::mutex> g(c.mu);
+            if (c.launch_if_pending(t)) return;
+        }
+        for (int spins = 0;; ++spins) {
+            {
+                std::lock_guard<std::mutex> g(c.mu);
+                if (c.poll_group(c.group_of(t))) return;
+            }
+            if (spins < 64) std::this_thread::yield();
+            else std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
     });
 }
 

@@ -880,7 +880,7 @@ void Context::progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed
     if (elapsed_us) *elapsed_us = g.launched ? host_now_us() - g.t_launch_us : 0;
 }
 
-void Context::wait(int64_t t) {
+bool Context::launch_if_pending(int64_t t) {
     Group& g = group_of(t);
     if (!g.launched) {
         for (auto& og : open_group_)
@@ -888,7 +888,12 @@ void Context::wait(int64_t t) {
                 if (it->second == g.id) { og.erase(it); break; }
         launch_group(g);
     }
-    if (!g.complete) {
+    return poll_group(g);
+}
+
+void Context::wait(int64_t t) {
+    Group& g = group_of(t);
+    if (!launch_if_pending(t)) {
         cuda_check(cudaEventSynchronize(g.ev.back()), "wait");
         poll_group(g);
     }

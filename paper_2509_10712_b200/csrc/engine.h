@@ -158,7 +158,8 @@ public:
     int64_t submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre = nullptr);
     void flush();
     void progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed_us);
-    void wait(int64_t t);
+    void wait(int64_t t);                 // blocking; callers must not hold `mu` (see lfg_wait)
+    bool launch_if_pending(int64_t t);    // launches t's open group if needed; true if complete
     int exec_costs(int64_t t, double* out, int cap);
     void ticket_output(int64_t t, void* dst, size_t bytes);
     void ticket_release(int64_t t);

@@ -134,6 +134,12 @@ TransformChain obj_det_chain(int out) {
          dev("Normalize", 1.0, LFG_OP_NORMALIZE, {0.485, 0.456, 0.406, 0.229, 0.224, 0.225})});
 }
 
+void prepare_chain(const TransformChain& chain, int shard) {
+    lfg_ctx* c = shard_context(shard);
+    if (c == nullptr) throw std::logic_error("prepare_chain: no GPU shard bound");
+    compiled(c, chain);
+}
+
 void seal_device_batch(Batch& b) {
     if (b.samples.empty() || b.samples.front().device.ticket < 0) return;
     lfg_ctx* ctx = ctx_of(b.samples.front());
