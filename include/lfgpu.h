@@ -184,6 +184,9 @@ int lfg_batch_info(lfg_ctx* ctx, lfg_batch b, void** dev_ptr, int64_t* bytes, in
 /* Makes `stream` (a cudaStream_t, may be NULL = legacy) wait until the batch is resident. */
 int lfg_batch_wait_stream(lfg_ctx* ctx, lfg_batch b, void* stream);
 int lfg_batch_copy_to_host(lfg_ctx* ctx, lfg_batch b, void* host_dst, size_t bytes);
+/* Speech batches (PermuteAudio + Pad, proj/src/workloads.cpp:107-108) are
+ * time-major [t_max, n, stack*80] f32, zero-padded: lengths[i] = T'_i. */
+int lfg_batch_lengths(lfg_ctx* ctx, lfg_batch b, int32_t* lengths, int32_t* t_max);
 /* Returns the batch buffer to the pool once work already queued on `stream`
  * (the consumer) has finished with it. */
 int lfg_batch_release(lfg_ctx* ctx, lfg_batch b, void* stream);

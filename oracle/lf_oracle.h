@@ -146,7 +146,8 @@ int32_t lfo_sp_frames(const lfo_cfgsp* c, int64_t L);
 void lfo_drawsp(const lfo_cfgsp* c, uint64_t seed, uint64_t id, int64_t L, lfo_paramssp* p);
 /* slaney mel filterbank [n_mels, n_fft/2+1] row-major, f64 */
 void lfo_mel_fbank(const lfo_cfgsp* c, double* fb);
-/* waveform f32 [L] -> log-mel f64 [n_mels, T] (masked), also power f64 [n_fft/2+1, T] if non-null */
+/* waveform f32 [L], L > n_fft/2 (reflect padding) -> log-mel f64 [n_mels, T] (masked),
+ * also power f64 [n_fft/2+1, T] if non-null */
 void lfo_applysp(const lfo_cfgsp* c, const lfo_paramssp* p, const float* wav, int64_t L,
                  double* logmel, double* power);
 

@@ -386,6 +386,17 @@ int lfg_batch_wait_stream(lfg_ctx* ctx, lfg_batch b, void* stream) {
     });
 }
 
+int lfg_batch_lengths(lfg_ctx* ctx, lfg_batch b, int32_t* lengths, int32_t* t_max) {
+    return guarded([&] {
+        Context& c = C(ctx);
+        std::lock_guard<std::mutex> g(c.mu);
+        BatchRec& br = c.batch(b);
+        if (br.chain->fam != FAM_SPEECH) fail(LFG_ERR_INVALID, "lengths exist for speech batches only");
+        if (lengths) std::memcpy(lengths, br.rows.data(), br.rows.size() * sizeof(int32_t));
+        if (t_max) *t_max = br.t_max;
+    });
+}
+
 int lfg_batch_copy_to_host(lfg_ctx* ctx, lfg_batch b, void* host_dst, size_t bytes) {
     return guarded([&] {
         Context& c = C(ctx);
@@ -393,11 +404,19 @@ int lfg_batch_copy_to_host(lfg_ctx* ctx, lfg_batch b, void* host_dst, size_t byt
         std::lock_guard<std::mutex> g(c.mu);
         BatchRec& br = c.batch(b);
         const Chain& ch = *br.chain;
-        const int64_t need = static_cast<int64_t>(br.n) * ch.out_bytes;
-        if (static_cast<int64_t>(bytes) < need) fail(LFG_ERR_INVALID, "host buffer too small");
         void* p = nullptr;
         int64_t by = 0;
         c.batch_ptr(br, &p, &by);
+        if (ch.fam == FAM_SPEECH) {   // time-major [t_max, n, stack * 80]
+            const int64_t need = int64_t(br.t_max) * br.n * ch.stack * ch.n_mels * 4;
+            if (static_cast<int64_t>(bytes) < need) fail(LFG_ERR_INVALID, "host buffer too small");
+            cuda_check(cudaEventSynchronize(br.ready), "batch ready");
+            cuda_check(cudaMemcpy(host_dst, p, need, cudaMemcpyDeviceToHost), "D2H batch");
+            c.counters.d2h_bytes += need;
+            return;
+        }
+        const int64_t need = static_cast<int64_t>(br.n) * ch.out_bytes;
+        if (static_cast<int64_t>(bytes) < need) fail(LFG_ERR_INVALID, "host buffer too small");
         cuda_check(cudaEventSynchronize(br.ready), "batch ready");
         char* d = static_cast<char*>(host_dst);
         const int64_t cap = c.cfg.batch_size;

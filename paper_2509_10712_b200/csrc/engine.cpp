@@ -193,6 +193,7 @@ Context::Context(const lfg_config& c) : cfg(c) {
     cuda_check(warm_img3d(), "load img3d kernel");
     cuda_check(warm_rrc2d(), "load rrc2d kernel");
     cuda_check(warm_misc(), "load misc kernels");
+    cuda_check(warm_speech(), "load speech kernels");
     for (int i = 0; i < 512; ++i) {
         cudaEvent_t e;
         cuda_check(cudaEventCreate(&e), "cudaEventCreate");
@@ -214,6 +215,7 @@ Context::~Context() {
     for (auto s : streams_) cudaStreamDestroy(s);
     cudaStreamDestroy(seal_stream);
     cudaStreamDestroy(aux_stream);
+    speech_tables_destroy(speech_);
 }
 
 cudaEvent_t Context::get_event() {
@@ -373,7 +375,17 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
         c->nplanes = 1;
         c->plane_bytes[0] = int64_t(3) * c->oh * c->ow * 4;
     } else {
-        fail(LFG_ERR_UNSUPPORTED, "speech chain not available in this build");
+        bool splice = false;
+        for (int i = 0; i < n; ++i) splice |= ops[i].kind == LFG_OP_FRAME_SPLICING;
+        if (!splice) c->stack = 1;
+        if (c->stack < 1 || speech_frames_per_cta() % c->stack != 0)
+            fail(LFG_ERR_UNSUPPORTED, "FrameSplicing stack must divide 126 (1, 2, 3, 6, 7, 9, ...)");
+        if (c->max_L < 2 || c->max_L > (1 << 24)) fail(LFG_ERR_INVALID, "FilterBank max length out of range");
+        if (speech_ == nullptr) cuda_check(speech_tables_create(&speech_), "speech tables");
+        const int64_t t_max = 1 + c->max_L / c->hop;
+        const int64_t rows = (t_max + c->stack - 1) / c->stack;
+        c->nplanes = 1;
+        c->plane_bytes[0] = rows * c->stack * c->n_mels * 4;   // time-major [T'_max, stack * 80]
     }
     c->out_bytes = c->plane_bytes[0] + c->plane_bytes[1];
     // stages: leading spins, the fused stage (with interleaved spins), trailing spins
@@ -595,8 +607,9 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
         if (s.ndim != 3 || s.dims[2] != 3 || s.dims[0] < 1 || s.dims[1] < 1)
             fail(LFG_ERR_INVALID, "obj_det sample needs an H,W,3 image");
     } else {
-        if (s.ndim != 1 || s.dims[0] < 2 || s.dims[0] > c->max_L)
-            fail(LFG_ERR_INVALID, "speech sample needs a waveform of length in [2, max_L]");
+        // reflect padding by n_fft/2 needs L > n_fft/2 (torch.stft center=True has the same rule)
+        if (s.ndim != 1 || s.dims[0] < c->n_fft / 2 + 1 || s.dims[0] > c->max_L)
+            fail(LFG_ERR_INVALID, "speech sample needs a waveform of length in [n_fft/2 + 1, max_L]");
     }
     if (s.src_kind == LFG_SRC_HOST_PINNED) {
         // K0 reads the payload over PCIe through its UVA mapping: it must be pinned
@@ -690,10 +703,20 @@ void Context::launch_group(Group& g) {
         StageLaunch SL{};
         for (int i = 0; i < n; ++i) {
             Ticket& t = tickets[g.tickets[i]];
+            View& v = views[i];
+            if (c.fam == FAM_SPEECH) {
+                // a waveform is one contiguous block: a single DMA copy is efficient
+                const int64_t bytes = t.desc.dims[0] * 4;
+                cuda_check(cudaMemcpyAsync(dst, t.desc.data, bytes, cudaMemcpyHostToDevice, st),
+                           "H2D waveform");
+                v.p[0] = dst;
+                counters.h2d_bytes += bytes;
+                dst += align256(bytes);
+                continue;
+            }
             Box b[2];
             int64_t wd[3];
             const int nb = boxes_of(c, t, b, wd);
-            View& v = views[i];
             for (int k = 0; k < nb; ++k) {
                 StageDesc& d = SL.d[SL.n++];
                 d.src = b[k].src;
@@ -721,8 +744,10 @@ void Context::launch_group(Group& g) {
                 v.off[a] = 0;
             }
         }
-        cuda_check(launch_stage(SL, st), "stage launch");
-        counters.launches++;
+        if (SL.n > 0) {
+            cuda_check(launch_stage(SL, st), "stage launch");
+            counters.launches++;
+        }
     } else {
         for (int i = 0; i < n; ++i) {
             Ticket& t = tickets[g.tickets[i]];
@@ -821,7 +846,32 @@ void Context::launch_group(Group& g) {
             cuda_check(launch_rrc2d(L, st), "rrc2d launch");
             counters.launches++;
         } else {
-            fail(LFG_ERR_UNSUPPORTED, "speech stage not available");
+            SpLaunch L{};
+            L.n = n;
+            L.n_fmask = c.n_fmask;
+            L.n_tmask = c.n_tmask;
+            L.stack = c.stack;
+            for (int i = 0; i < n; ++i) {
+                Ticket& t = tickets[g.tickets[i]];
+                SpDesc& d = L.d[i];
+                d.wav = reinterpret_cast<const float*>(views[i].p[0]);
+                d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
+                d.L = static_cast<int32_t>(t.desc.dims[0]);
+                d.T = t.ps.T;
+                for (int k = 0; k < c.n_fmask; ++k) {
+                    d.f_lo[k] = t.ps.f_lo[k];
+                    d.f_w[k] = t.ps.f_w[k];
+                }
+                for (int k = 0; k < c.n_tmask; ++k) {
+                    d.t_lo[k] = t.ps.t_lo[k];
+                    d.t_w[k] = t.ps.t_w[k];
+                }
+                counters.kernel_bytes += 4 * t.desc.dims[0] +
+                                         4 * int64_t((t.ps.T + c.stack - 1) / c.stack) * c.stack * c.n_mels;
+                counters.reserved[1] += int64_t(t.ps.T) * 2 * kTapsDft * 512 * 3;   // tensor FLOPs
+            }
+            cuda_check(launch_speech(L, speech_, nullptr, st), "speech launch");
+            counters.launches++;
         }
         for (int slot : S.spin_ops) launch_spins(slot);
         cuda_check(cudaEventRecord(g.ev[s + 1], st), "record stage end");
@@ -959,7 +1009,9 @@ int64_t Context::seal(const int64_t* ts, int n) {
         for (int j = i + 1; j < n; ++j)
             if (ts[i] == ts[j]) fail(LFG_ERR_INVALID, "duplicate ticket in batch");
     const int b0 = tickets[ts[0]].buf;
-    const bool in_place = same_buf && bufs_[b0].assigned == n && !bufs_[b0].in_batch;
+    // speech batches are time-major (PermuteAudio), so they are always collated
+    const bool in_place = c->fam != FAM_SPEECH && same_buf && bufs_[b0].assigned == n &&
+                          !bufs_[b0].in_batch;
 
     BatchRec br;
     br.chain = c;
@@ -1003,9 +1055,27 @@ int64_t Context::seal(const int64_t* ts, int n) {
             br.ids[i] = t.id;
             src_bufs.push_back(t.buf);
         }
-        cuda_check(launch_gather(L, seal_stream), "gather launch");
+        if (c->fam == FAM_SPEECH) {
+            // PermuteAudio + Pad: time-major [T'_max, n, stack * 80], zero-padded
+            SpCollate SC{};
+            SC.n = n;
+            SC.width = c->stack * c->n_mels;
+            for (int i = 0; i < n; ++i) {
+                const Ticket& t = tickets[ts[i]];
+                SC.rows[i] = (t.ps.T + c->stack - 1) / c->stack;
+                SC.src[i] = reinterpret_cast<const float*>(L.src[i]);
+                SC.t_max = std::max(SC.t_max, SC.rows[i]);
+            }
+            SC.dst = reinterpret_cast<float*>(bufs_[nb].base);
+            br.t_max = SC.t_max;
+            br.rows.assign(SC.rows, SC.rows + n);
+            cuda_check(launch_speech_collate(SC, seal_stream), "collate launch");
+            counters.reserved[0] += 2 * static_cast<int64_t>(SC.t_max) * n * SC.width * 4;
+        } else {
+            cuda_check(launch_gather(L, seal_stream), "gather launch");
+            counters.reserved[0] += 2 * static_cast<int64_t>(n) * c->out_bytes;  // gather bytes
+        }
         counters.launches++;
-        counters.reserved[0] += 2 * static_cast<int64_t>(n) * c->out_bytes;  // gather bytes
         std::sort(src_bufs.begin(), src_bufs.end());
         src_bufs.erase(std::unique(src_bufs.begin(), src_bufs.end()), src_bufs.end());
         for (int sb : src_bufs) {

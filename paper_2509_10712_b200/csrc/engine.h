@@ -142,6 +142,8 @@ struct BatchRec {
     const Chain* chain = nullptr;
     int n = 0;
     bool released = false;
+    int t_max = 0;               // speech: padded time length of the batch tensor
+    std::vector<int> rows;       // speech: per-sample spliced lengths T'_i
 };
 
 class Context {
@@ -200,6 +202,7 @@ public:
 
 private:
     std::vector<std::unique_ptr<Chain>> chains_;
+    SpeechTables* speech_ = nullptr;   // DFT basis + mel tables, created with the first speech chain
     std::vector<cudaStream_t> streams_;
     std::vector<int> free_streams_;
     std::vector<cudaEvent_t> free_events_;

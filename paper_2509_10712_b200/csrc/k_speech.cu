@@ -1,18 +1,461 @@
-// k_speech.cu -- speech chain kernels (placeholder until the tensor-core path lands).
+// k_speech.cu -- K8/K9/K10: FilterBank (STFT power -> slaney mel -> log) with
+// SpecAugment and FrameSplicing fused, on the 5th-gen tensor cores; and K11,
+// the PermuteAudio + Pad collation of a speech batch.
+//
+// Reference chain: Pad, SpecAugment, FilterBank, FrameSplicing, PermuteAudio
+// (proj/src/workloads.cpp:103-111).  Semantics: oracle/lf_oracle.c lfo_applysp.
+//
+// K8/K9 as a GEMM.  With the periodic Hann window (320 taps centred in the
+// 512-point frame) folded into the basis, the STFT of frame f is
+//     X[f, k] = sum_{j<320} x[(f-1)*160 + j] * w[j] * exp(-2 pi i k (j+96) / 512)
+// i.e. C[frames x 512] = A[frames x 320] . B[320 x 512] with B's columns the
+// cos / sin rows for bins 0..255 (bin 256, Nyquist, is a signed sum done on the
+// CUDA cores while A is built).  fp32 accuracy on TF32 tensor cores by the
+// 3xTF32 split: A = Ah + Al, B = Bh + Bl, C ~ Al.Bh + Ah.Bl + Ah.Bh.
+//
+// Per CTA (128 threads, 1 per SM): 126 frames of one utterance (M = 128 rows,
+// a multiple of 3 frames so FrameSplicing never crosses CTAs).  The full
+// 128 x 512 fp32 accumulator lives in TMEM (all 512 columns) as two
+// M128 x N256 tcgen05.mma.kind::tf32 tiles.  K = 320 in 20 chunks of 16 taps,
+// double-buffered in shared memory: the constant B chunk (64 KB, hi+lo, both
+// N halves) arrives by cp.async.bulk on an mbarrier while the threads build
+// the A chunk (frames read from the waveform with reflect padding, split into
+// tf32 hi/lo); one elected thread issues 12 MMAs per chunk and commits them to
+// the stage's mbarrier.  Operands use the no-swizzle K-major canonical layout:
+// 8-row x 16-byte core matrices, LBO = 128 B (the two 16-B K halves of a K=8
+// step), SBO = 256 B (next 8-row group).
+//
+// Epilogue (all 4 warps, thread = frame = TMEM lane): tcgen05.ld 16 columns of
+// cos and sin at a time -> power -> the slaney mel filterbank as a streaming
+// reduction (each FFT bin feeds at most two adjacent triangular filters; the
+// bank is 2.4% dense, so it stays on the CUDA cores instead of a mostly-zero
+// GEMM) -> shared memory -> log(x + eps), SpecAugment masks, stack-3 splice,
+// coalesced time-major stores into the sample's output slot.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "device_common.cuh"
 #include "kernels.h"
 
 namespace lfg {
 
-struct SpeechTables {};
+namespace {
+
+constexpr int kTaps = 320;            // Hann window length (non-zero taps of the 512 frame)
+constexpr int kWinOff = 96;           // (512 - 320) / 2
+constexpr int kHop = 160;
+constexpr int kNfft = 512;
+constexpr int kBins = 256;            // bins 0..255 on the tensor cores, 256 on the CUDA cores
+constexpr int kMels = 80;
+constexpr int kRowsM = 128;           // MMA M
+constexpr int kFramesPerCta = 126;    // multiple of 3 (FrameSplicing stack)
+constexpr int kKChunk = 16;           // taps per pipeline stage (2 MMA K-steps of 8)
+constexpr int kChunks = kTaps / kKChunk;          // 20
+constexpr int kABytesStep = kRowsM * 32;          // one K=8 step of A (one part): 4 KB
+constexpr int kAPartBytes = 2 * kABytesStep;      // one stage, one part (hi or lo): 8 KB
+constexpr int kBBlock = 256 * 32;                 // one K=8 step, one N half, one part: 8 KB
+constexpr int kBStageBytes = 2 * 2 * 2 * kBBlock; // q x half x part = 64 KB
+constexpr int kStageBytes = 2 * kAPartBytes + kBStageBytes;   // 80 KB
+constexpr int kSmemBytes = 2 * kStageBytes + 1024;            // + barriers / scratch
+constexpr int kMelPitch = kMels + 1;
+
+// instruction descriptor: D f32, A/B tf32, K-major both, N = 256, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+
+__constant__ float c_win_nyq[kTaps];  // w[j] * (-1)^(j + 96): the Nyquist bin's real coefficients
+__constant__ int c_mel_m[kBins + 1];  // lower filter index fed by bin k (-1: none)
+__constant__ float c_mel_wa[kBins + 1], c_mel_wb[kBins + 1];   // weights into m and m+1
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LAB_WAIT;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    // no-swizzle K-major: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48)
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
+           ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+        "[%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------ the kernel
+__global__ void __launch_bounds__(128, 1)
+speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const SpDesc& d = L.d[blockIdx.y];
+    const int tile = blockIdx.x;
+    const int T = d.T;
+    const int f0 = tile * kFramesPerCta;
+    if (f0 >= T) return;                                  // CTA-uniform
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    uint8_t* stage_base[2] = {smem, smem + kStageBytes};
+    uint64_t* bar_b = reinterpret_cast<uint64_t*>(smem + 2 * kStageBytes);     // [2] B landed
+    uint64_t* bar_mma = bar_b + 2;                                             // [2] stage free
+    uint64_t* bar_done = bar_b + 4;                                            // all MMAs done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_b + 6);
+
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar_b + i, 1);
+            mbar_init(bar_mma + i, 1);
+        }
+        mbar_init(bar_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    // this thread's frame (A row) and its waveform window
+    const int r = tid;
+    const int f = f0 + r;
+    const bool row_live = r < kFramesPerCta && f < T;
+    const int64_t n0 = (int64_t)(f - 1) * kHop;           // first tap's sample index
+    const bool interior = row_live && n0 >= 0 && n0 + kTaps <= d.L &&
+                          ((reinterpret_cast<uintptr_t>(d.wav + n0) & 15) == 0);
+    float nyq = 0.0f;
+
+    for (int it = 0; it < kChunks; ++it) {
+        const int st = it & 1;
+        uint8_t* sb = stage_base[st];
+        if (it >= 2) mbar_wait(bar_mma + st, ((it - 2) >> 1) & 1);   // stage's previous MMAs done
+        if (tid == 0) {
+            mbar_expect_tx(bar_b + st, kBStageBytes);
+            bulk_g2s(sb + 2 * kAPartBytes, basis + (size_t)it * kBStageBytes, kBStageBytes, bar_b + st);
+        }
+        // A chunk: taps [16 it, 16 it + 16) of frame f, split into tf32 hi / lo
+        float x[kKChunk];
+        if (interior) {
+            const float4* p = reinterpret_cast<const float4*>(d.wav + n0 + it * kKChunk);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v = __ldg(p + q);
+                x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kKChunk; ++j) {
+                float v = 0.0f;
+                if (row_live) {
+                    int64_t n = n0 + it * kKChunk + j;                       // reflect padding
+                    if (n < 0) n = -n;
+                    if (n >= d.L) n = 2 * ((int64_t)d.L - 1) - n;
+                    v = __ldg(d.wav + n);
+                }
+                x[j] = v;
+            }
+        }
+        uint32_t hi[kKChunk], lo[kKChunk];
+#pragma unroll
+        for (int j = 0; j < kKChunk; ++j) {
+            nyq = fmaf(x[j], c_win_nyq[it * kKChunk + j], nyq);
+            hi[j] = tf32_rna(x[j]);
+            lo[j] = tf32_rna(x[j] - __uint_as_float(hi[j]));
+        }
+        // canonical no-swizzle K-major: [q][row group][k half][row in group][16 B]
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int off = q * kABytesStep + (r >> 3) * 256 + c * 128 + (r & 7) * 16;
+                const int j = 8 * q + 4 * c;
+                *reinterpret_cast<uint4*>(sb + off) = make_uint4(hi[j], hi[j + 1], hi[j + 2], hi[j + 3]);
+                *reinterpret_cast<uint4*>(sb + kAPartBytes + off) =
+                    make_uint4(lo[j], lo[j + 1], lo[j + 2], lo[j + 3]);
+            }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+        __syncthreads();
+        if (tid == 0) {
+            mbar_wait(bar_b + st, (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t a_hi = smem_u32(sb), a_lo = a_hi + kAPartBytes;
+            const uint32_t b0 = smem_u32(sb + 2 * kAPartBytes);
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t bh = b0 + ((q * 2 + h) * 2 + 0) * kBBlock;
+                    const uint32_t bl = b0 + ((q * 2 + h) * 2 + 1) * kBBlock;
+                    const uint64_t dah = smem_desc(a_hi + q * kABytesStep);
+                    const uint64_t dal = smem_desc(a_lo + q * kABytesStep);
+                    const uint32_t acc = tmem + h * 256;
+                    const uint32_t first = (it == 0 && q == 0) ? 0u : 1u;
+                    mma_tf32(acc, dal, smem_desc(bh), first);     // small terms first
+                    mma_tf32(acc, dah, smem_desc(bl), 1u);
+                    mma_tf32(acc, dah, smem_desc(bh), 1u);
+                }
+            mma_commit(bar_mma + st);
+            if (it == kChunks - 1) mma_commit(bar_done);
+        }
+    }
+    mbar_wait(bar_done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    // ---- epilogue: power -> mel (streaming, 2 filters per bin) -> shared memory
+    float* mel_s = reinterpret_cast<float*>(smem);          // stage buffers are free now
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    int cur = 0;
+    float acc_a = 0.0f, acc_b = 0.0f;
+    auto feed = [&](int k, float p) {
+        const int m = c_mel_m[k];
+        if (m < 0) return;
+        while (cur < m) {                                   // filter `cur` complete (uniform)
+            mel_s[r * kMelPitch + cur] = acc_a;
+            acc_a = acc_b;
+            acc_b = 0.0f;
+            ++cur;
+        }
+        acc_a = fmaf(c_mel_wa[k], p, acc_a);
+        acc_b = fmaf(c_mel_wb[k], p, acc_b);
+    };
+    for (int h = 0; h < 2; ++h)
+        for (int b = 0; b < 8; ++b) {
+            float re[16], im[16];
+            tmem_ld16(lane_base + h * 256 + 16 * b, re);
+            tmem_ld16(lane_base + h * 256 + 128 + 16 * b, im);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) feed(h * 128 + 16 * b + i, fmaf(re[i], re[i], im[i] * im[i]));
+        }
+    feed(kBins, nyq * nyq);
+    while (cur < kMels) {
+        mel_s[r * kMelPitch + cur] = acc_a;
+        acc_a = acc_b;
+        acc_b = 0.0f;
+        ++cur;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+
+    // ---- log, SpecAugment, FrameSplicing (stack 3): coalesced time-major rows
+    const int stack = L.stack;
+    const int width = stack * kMels;
+    const int rows = kFramesPerCta / stack;
+    const int row0 = f0 / stack;
+    const int t_rows = (T + stack - 1) / stack;
+    for (int i = tid; i < rows * width; i += 128) {
+        const int rr = i / width, col = i - rr * width;
+        if (row0 + rr >= t_rows) break;
+        const int fl = rr * stack + col / kMels, m = col % kMels;   // frame within the CTA, mel bin
+        const int ff = f0 + fl;
+        float v = 0.0f;
+        if (ff < T) {
+            bool masked = false;
+            for (int q = 0; q < L.n_fmask; ++q) masked |= m >= d.f_lo[q] && m < d.f_lo[q] + d.f_w[q];
+            for (int q = 0; q < L.n_tmask; ++q) masked |= ff >= d.t_lo[q] && ff < d.t_lo[q] + d.t_w[q];
+            v = masked ? 0.0f : logf(mel_s[fl * kMelPitch + m] + 5.9604644775390625e-8f);   // + 2^-24
+        }
+        d.out[(int64_t)(row0 + rr) * width + col] = v;
+    }
+}
+
+// K11: PermuteAudio + Pad: per-sample [T'_i, W] slots -> batch [T'_max, n, W], zero-padded.
+__global__ void __launch_bounds__(256) speech_collate_kernel(const __grid_constant__ SpCollate C) {
+    const int t = blockIdx.x;
+    const int w4 = C.width / 4;
+    for (int i = threadIdx.x; i < C.n * w4; i += blockDim.x) {
+        const int b = i / w4, q = i - b * w4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < C.rows[b]) v = __ldcs(reinterpret_cast<const float4*>(C.src[b] + (int64_t)t * C.width) + q);
+        reinterpret_cast<float4*>(C.dst + ((int64_t)t * C.n + b) * C.width)[q] = v;
+    }
+}
+
+// ------------------------------------------------------------------ host tables
+uint32_t h_tf32_rna(float x) {   // cvt.rna.tf32.f32: round to nearest, ties away, 10-bit mantissa
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u) return u & 0xFFFFE000u;
+    u += 0x1000u;
+    return u & 0xFFFFE000u;
+}
+float as_f(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+}  // namespace
+
+struct SpeechTables {
+    char* basis = nullptr;   // kChunks x 64 KB, the per-stage smem image of B
+};
 
 cudaError_t speech_tables_create(SpeechTables** out) {
-    *out = nullptr;
-    return cudaErrorNotSupported;
+    // B: column col of N half h is bin 128 h + (col mod 128), cos (col < 128) or
+    // -sin; row j is window tap j (frame position j + 96).  Computed in fp64.
+    std::vector<double> win(kTaps);
+    for (int j = 0; j < kTaps; ++j) win[j] = 0.5 - 0.5 * std::cos(2.0 * M_PI * j / kTaps);
+    std::vector<char> img((size_t)kChunks * kBStageBytes, 0);
+    for (int it = 0; it < kChunks; ++it)
+        for (int q = 0; q < 2; ++q)
+            for (int h = 0; h < 2; ++h)
+                for (int col = 0; col < 256; ++col) {
+                    const int k = 128 * h + (col & 127);
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const int j = it * kKChunk + q * 8 + jj;
+                        const int n = j + kWinOff;
+                        const double ang = 2.0 * M_PI * (double)((int64_t)k * n % kNfft) / kNfft;
+                        const double v = win[j] * (col < 128 ? std::cos(ang) : -std::sin(ang));
+                        const uint32_t vh = h_tf32_rna((float)v);
+                        const uint32_t vl = h_tf32_rna((float)(v - (double)as_f(vh)));
+                        const int c = jj >> 2, e = jj & 3;
+                        const size_t blk = (size_t)it * kBStageBytes + (size_t)((q * 2 + h) * 2) * kBBlock;
+                        const size_t off = (size_t)(col >> 3) * 256 + c * 128 + (col & 7) * 16 + e * 4;
+                        std::memcpy(&img[blk + off], &vh, 4);
+                        std::memcpy(&img[blk + kBBlock + off], &vl, 4);
+                    }
+                }
+    // Nyquist coefficients w[j] * (-1)^(j + 96)
+    float nyq[kTaps];
+    for (int j = 0; j < kTaps; ++j) nyq[j] = (float)(win[j] * (((j + kWinOff) & 1) ? -1.0 : 1.0));
+    // slaney mel bank (torchaudio melscale_fbanks norm='slaney', mel_scale='slaney'), fp64
+    auto hz2mel = [](double f) {
+        const double fsp = 200.0 / 3.0, lo_hz = 1000.0, lo_mel = lo_hz / fsp, step = std::log(6.4) / 27.0;
+        return f >= lo_hz ? lo_mel + std::log(f / lo_hz) / step : f / fsp;
+    };
+    auto mel2hz = [](double m) {
+        const double fsp = 200.0 / 3.0, lo_hz = 1000.0, lo_mel = lo_hz / fsp, step = std::log(6.4) / 27.0;
+        return m >= lo_mel ? lo_hz * std::exp(step * (m - lo_mel)) : fsp * m;
+    };
+    const int nf = kBins + 1;
+    std::vector<double> pts(kMels + 2);
+    const double m0 = hz2mel(0.0), m1 = hz2mel(8000.0);
+    for (int i = 0; i < kMels + 2; ++i) pts[i] = mel2hz(m0 + (m1 - m0) * i / (kMels + 1));
+    std::vector<double> fb((size_t)kMels * nf, 0.0);
+    for (int m = 0; m < kMels; ++m)
+        for (int k = 0; k < nf; ++k) {
+            const double fk = 8000.0 * k / (nf - 1);
+            const double down = (fk - pts[m]) / (pts[m + 1] - pts[m]);
+            const double up = (pts[m + 2] - fk) / (pts[m + 2] - pts[m + 1]);
+            const double v = std::max(0.0, std::min(down, up));
+            fb[(size_t)m * nf + k] = v * 2.0 / (pts[m + 2] - pts[m]);
+        }
+    int mel_m[kBins + 1];
+    float wa[kBins + 1], wb[kBins + 1];
+    for (int k = 0; k < nf; ++k) {
+        int first = -1;
+        for (int m = 0; m < kMels; ++m)
+            if (fb[(size_t)m * nf + k] != 0.0) {
+                first = m;
+                break;
+            }
+        mel_m[k] = first;
+        wa[k] = first >= 0 ? (float)fb[(size_t)first * nf + k] : 0.f;
+        wb[k] = (first >= 0 && first + 1 < kMels) ? (float)fb[(size_t)(first + 1) * nf + k] : 0.f;
+        for (int m = first + 2; first >= 0 && m < kMels; ++m)
+            if (fb[(size_t)m * nf + k] != 0.0) return cudaErrorInvalidValue;   // > 2 filters per bin
+    }
+    cudaError_t e;
+    if ((e = cudaMemcpyToSymbol(c_win_nyq, nyq, sizeof(nyq))) != cudaSuccess) return e;
+    if ((e = cudaMemcpyToSymbol(c_mel_m, mel_m, sizeof(mel_m))) != cudaSuccess) return e;
+    if ((e = cudaMemcpyToSymbol(c_mel_wa, wa, sizeof(wa))) != cudaSuccess) return e;
+    if ((e = cudaMemcpyToSymbol(c_mel_wb, wb, sizeof(wb))) != cudaSuccess) return e;
+    auto* t = new SpeechTables;
+    if ((e = cudaMalloc(&t->basis, img.size())) != cudaSuccess) {
+        delete t;
+        return e;
+    }
+    if ((e = cudaMemcpy(t->basis, img.data(), img.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+        cudaFree(t->basis);
+        delete t;
+        return e;
+    }
+    if ((e = cudaFuncSetAttribute(speech_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemBytes)) != cudaSuccess)
+        return e;
+    *out = t;
+    return cudaSuccess;
 }
-void speech_tables_destroy(SpeechTables*) {}
-cudaError_t launch_speech(const SpLaunch&, const SpeechTables*, float*, cudaStream_t) {
-    return cudaErrorNotSupported;
+
+void speech_tables_destroy(SpeechTables* t) {
+    if (!t) return;
+    cudaFree(t->basis);
+    delete t;
 }
+
+int speech_frames_per_cta() { return kFramesPerCta; }
+
+cudaError_t launch_speech(const SpLaunch& L, const SpeechTables* t, float*, cudaStream_t s) {
+    if (L.n <= 0) return cudaSuccess;
+    int max_tiles = 1;
+    for (int i = 0; i < L.n; ++i) max_tiles = max(max_tiles, (L.d[i].T + kFramesPerCta - 1) / kFramesPerCta);
+    speech_kernel<<<dim3(max_tiles, L.n), 128, kSmemBytes, s>>>(L, t->basis);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_speech_collate(const SpCollate& C, cudaStream_t s) {
+    if (C.n <= 0 || C.t_max <= 0) return cudaSuccess;
+    speech_collate_kernel<<<C.t_max, 256, 0, s>>>(C);
+    return cudaGetLastError();
+}
+
 int64_t speech_scratch_bytes(int, int) { return 0; }
+
+cudaError_t warm_speech() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, speech_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, speech_collate_kernel);
+    return e;
+}
 
 }  // namespace lfg

@@ -14,6 +14,7 @@ constexpr int kMax2D = 64;   // obj_det samples per launch group
 constexpr int kMaxSp = 64;   // speech utterances per launch group
 constexpr int kMaxSpin = 64;
 constexpr int kMaxGather = 256;
+constexpr int kTapsDft = 320;   // speech: non-zero window taps per frame (the DFT GEMM's K)
 
 // Row addressing shared by K1/K3: a source row (z, y) starts at
 //   base + z*pitch_z + y*pitch_y + ((skew0 + z*skew_z + y*skew_y) & mask)
@@ -91,6 +92,16 @@ struct SpLaunch {
     SpDesc d[kMaxSp];
 };
 
+// ---- K11 (speech seal): PermuteAudio + Pad, per-sample [T'_i, width] -> [t_max, n, width]
+struct SpCollate {
+    int32_t n;
+    int32_t width;
+    int32_t t_max;
+    int32_t rows[kMaxGather];
+    const float* src[kMaxGather];
+    float* dst;
+};
+
 // ---- K14: synthetic per-sample cost (LightStep / HeavyStep / step_costs)
 struct SpinLaunch {
     int32_t n;
@@ -129,7 +140,10 @@ cudaError_t speech_tables_create(SpeechTables** out);
 void speech_tables_destroy(SpeechTables* t);
 cudaError_t launch_speech(const SpLaunch& L, const SpeechTables* t, float* scratch,
                           cudaStream_t s);
+cudaError_t launch_speech_collate(const SpCollate& C, cudaStream_t s);
 int64_t speech_scratch_bytes(int n, int max_T);
+int speech_frames_per_cta();
+cudaError_t warm_speech();
 
 // synthetic data (Philox(seed, id)); device kernels
 cudaError_t launch_synth_volume(uint64_t seed, uint64_t id, int64_t D, int64_t H, int64_t W,

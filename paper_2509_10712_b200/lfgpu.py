@@ -124,6 +124,7 @@ _sig = {
                         _P(C.c_int)], C.c_int),
     "lfg_batch_wait_stream": ([_vp, C.c_int64, _vp], C.c_int),
     "lfg_batch_copy_to_host": ([_vp, C.c_int64, _vp, C.c_size_t], C.c_int),
+    "lfg_batch_lengths": ([_vp, C.c_int64, _P(C.c_int32), _P(C.c_int32)], C.c_int),
     "lfg_batch_release": ([_vp, C.c_int64, _vp], C.c_int),
     "lfg_trainer_step": ([_vp, C.c_int64, _vp, C.c_int64], C.c_int),
     "lfg_synth_volume": ([_vp, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, _vp, _vp,
@@ -194,6 +195,21 @@ def obj_det_ops(out=(224, 224), scale=(0.08, 1.0), ratio=(3 / 4, 4 / 3), p_hflip
         op(OP_TO_TENSOR, "ToTensor", 8.0),
         op(OP_NORMALIZE, "Normalize", 1.0, list(mean) + list(std)),
     ]
+
+
+def speech_ops(max_len=170_000, freq_masks=2, freq_mask_max=27, time_masks=10,
+               time_mask_frac=0.05, stack=3) -> list[Op]:
+    """speech chain, proj/src/workloads.cpp:103-108: Pad, SpecAugment, FilterBank
+    (STFT 512/320/160 -> 80 slaney mels -> log), FrameSplicing, PermuteAudio."""
+    ops = [
+        op(OP_PAD, "Pad", 1.12),
+        op(OP_SPEC_AUGMENT, "SpecAugment", 1.0, [freq_masks, freq_mask_max, time_masks, time_mask_frac]),
+        op(OP_FILTER_BANK, "FilterBank", 1.0, [512, 320, 160, 80, max_len]),
+    ]
+    if stack > 1:
+        ops.append(op(OP_FRAME_SPLICING, "FrameSplicing", 0.9, [stack]))
+    ops.append(op(OP_PERMUTE_AUDIO, "PermuteAudio", 1.0))
+    return ops
 
 
 def _arr_ptr(a) -> int:
@@ -353,6 +369,13 @@ class Context:
         out = np.empty(nbytes, dtype=np.uint8)
         _check(_lib.lfg_batch_copy_to_host(self.h, b, out.ctypes.data, nbytes))
         return out
+
+    def batch_lengths(self, b: int):
+        n = self.batch_info(b)["n"]
+        lens = (C.c_int32 * n)()
+        tm = C.c_int32()
+        _check(_lib.lfg_batch_lengths(self.h, b, lens, C.byref(tm)))
+        return list(lens), tm.value
 
     def batch_release(self, b: int, stream: int = 0):
         _check(_lib.lfg_batch_release(self.h, b, stream))

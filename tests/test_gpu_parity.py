@@ -271,3 +271,77 @@ def test_cpp_api_device_pipeline():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr
+
+
+# ------------------------------------------------------------------ speech (K8-K11)
+def _splice(logmel, stack=3):
+    """FrameSplicing (stack, subsample) of the oracle's [80, T] log-mel -> [T', 80*stack]."""
+    m, T = logmel.shape
+    rows = (T + stack - 1) // stack
+    out = np.zeros((rows, m * stack))
+    for s in range(stack):
+        idx = np.arange(rows) * stack + s
+        ok = idx < T
+        out[ok, s * m:(s + 1) * m] = logmel[:, idx[ok]].T
+    return out
+
+
+def test_speech_matches_oracle(lfgpu, oracle):
+    """STFT power on tcgen05 (3xTF32) -> mel -> log -> SpecAugment -> splicing.
+    Tolerance (stated): compared in the mel-energy domain, |e^g - e^o| <= 1e-5 e^o +
+    1e-6 * (frame's peak mel energy) -- relative 1e-5 with an energy floor, because
+    log amplifies fp32 round-off in near-empty bands; masked entries exactly 0."""
+    ctx = lfgpu.Context(batch_size=8, n_workers=4, max_group=8, max_slot_buffers=8, seed=SEED)
+    ch = ctx.chain(lfgpu.speech_ops(max_len=40000))
+    ocfg = oracle.cfgsp()
+    rng = np.random.default_rng(21)
+    lens = [4000, 4321, 20000, 39999, 257, 300, 16000, 12345]
+    ts, exp, bufs = [], [], []
+    for k, L in enumerate(lens):
+        t = np.arange(L) / 16000.0
+        wav = (0.5 * np.sin(2 * np.pi * (200 + 50 * k) * t) + 0.2 * np.sin(2 * np.pi * 3100 * t)
+               + 0.01 * rng.standard_normal(L)).astype(np.float32)
+        p = ctx.device_alloc(wav.nbytes)
+        ctx.h2d(p, wav)
+        bufs.append(p)
+        sid = 300 + k
+        desc = lfgpu.sample_desc(sid, (L,), p)
+        dp = ch.draw_params(SEED, desc)
+        op_ = oracle.drawsp(ocfg, SEED, sid, L)
+        assert dp[0] == op_.n_frames
+        (lm, _), _ = oracle.chainsp(ocfg, SEED, sid, wav)
+        exp.append(_splice(lm))
+        ts.append(ctx.submit(ch, desc))
+    ctx.flush()
+    _, out_bytes, _ = ch.info()
+    worst = 0.0
+    for t, e in zip(ts, exp):
+        ctx.wait(t)
+        got = ctx.ticket_output(t, out_bytes).view(np.float32).reshape(-1, 240)[: e.shape[0]]
+        zero = e == 0.0
+        assert np.array_equal(got[zero], e[zero]), "SpecAugment / padding zeros differ"
+        ge, oe = np.exp(got[~zero].astype(np.float64)), np.exp(e[~zero])
+        frame_peak = np.exp(e.reshape(e.shape[0], 3, 80).max(axis=2)).repeat(80, axis=1)[~zero]
+        err = np.abs(ge - oe)
+        bound = 1e-5 * oe + 1e-6 * frame_peak
+        worst = max(worst, float((err / bound).max()))
+        assert (err <= bound).all(), f"max err/bound {(err / bound).max():.3f}"
+    print("speech worst err/bound", worst)
+    # batch collation: PermuteAudio + Pad -> [T'max, n, 240]
+    b = ctx.seal(ts)
+    lengths, t_max = ctx.batch_lengths(b)
+    assert t_max == max(x.shape[0] for x in exp)
+    host = ctx.batch_to_host(b, t_max * len(ts) * 240 * 4).view(np.float32).reshape(t_max, len(ts), 240)
+    info = ctx.batch_info(b)
+    for i, sid in enumerate(info["ids"]):
+        e = exp[sid - 300]
+        assert lengths[i] == e.shape[0]
+        assert np.array_equal(host[lengths[i]:, i], np.zeros_like(host[lengths[i]:, i]))
+        np.testing.assert_allclose(np.exp(host[: lengths[i], i]), np.exp(e), rtol=1e-4, atol=1e-6)
+    ctx.batch_release(b)
+    with pytest.raises(lfgpu.LfgError):                 # reflect padding needs L > n_fft / 2
+        ctx.submit(ch, lfgpu.sample_desc(1, (256,), bufs[0]))
+    ctx.synchronize()
+    for p in bufs:
+        ctx.device_free(p)
+    ctx.close()
