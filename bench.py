@@ -44,14 +44,22 @@ sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform HBM GB/s"
 
+# workload -> (batch size, samples per launch group, default timed steps)
+BATCH = {"rrc": (256, 64, 200), "img3d": (2, 1, 400), "img3d_heavy": (2, 1, 400),
+         "speech": (64, 64, 100)}
+
 
 def peaks():
+    """(HBM GB/s, dense TF32 TFLOP/s, source).  TF32 is half the dense bf16 rate on
+    B200 (1.1 vs 2.25 PFLOP/s nominal), so the tensor denominator is the measured
+    cuBLAS bf16 burst figure / 2."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        return (float(p["hbm_gbs"]), float(p["bf16_tflops"]) / 2.0,
+                "measured (MEASURED_PEAKS.json; tf32 = bf16_tflops / 2)")
     except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md)"
+        return 6650.0, 1590.0 / 2.0, "fallback (B200_PROFILING.md; tf32 = bf16 / 2)"
 
 
 # ------------------------------------------------------------------ clocks
@@ -227,6 +235,7 @@ class Img3dWorkload:
         self.heavy_frac = heavy_frac
         self.scale = time_scale_us_per_ms
         self.chain = ctx.chain(L.img_seg_ops(spin_first=heavy_frac > 0))
+        self.roof_chain = ctx.chain(L.img_seg_ops()) if heavy_frac > 0 else self.chain
 
     def descs(self, ids):
         L = self.L
@@ -249,7 +258,38 @@ class Img3dWorkload:
             f(pl)
 
 
+class SpeechWorkload:
+    """C4: 16 kHz utterances, L ~ U{30000..170000} (the reference's speech bytes_in of
+    60k-340k B as int16, workloads.cpp:115); three sines + N(0, 0.01) noise."""
+    name = "speech"
+    B = 64
+
+    def __init__(self, L, ctx, pool: int, host: bool, seed: int):
+        self.L, self.ctx, self.host = L, ctx, host
+        rng = np.random.default_rng(seed)
+        self.lens = rng.integers(30000, 170001, size=pool)
+        offs = np.concatenate([[0], np.cumsum([(int(n) * 4 + 255) // 256 * 256 for n in self.lens])])
+        self.offs = offs
+        total = int(offs[-1])
+        self.base = ctx.host_alloc(total) if host else ctx.device_alloc(total)
+        for i, n in enumerate(self.lens):
+            ctx.synth_waveform(seed, i, int(n), self.base + int(offs[i]), on_device=not host)
+        self.pool = pool
+        self.pool_bytes = total
+        self.chain = ctx.chain(L.speech_ops())
+
+    def descs(self, ids):
+        L = self.L
+        return [L.sample_desc(i, (int(self.lens[i % self.pool]),), self.base + int(self.offs[i % self.pool]),
+                              src_kind=L.SRC_HOST_PINNED if self.host else L.SRC_DEVICE) for i in ids]
+
+    def close(self):
+        (self.ctx.host_free if self.host else self.ctx.device_free)(self.base)
+
+
 def make_workload(name, L, ctx, host, seed, args):
+    if name == "speech":
+        return SpeechWorkload(L, ctx, pool=args.pool or 512, host=host, seed=seed)
     if name == "rrc":
         return RrcWorkload(L, ctx, pool=args.pool or 1024, host=host, seed=seed)
     if name == "img3d":
@@ -282,25 +322,37 @@ def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, 
     return rep, ids, wall, {k: c1[k] - c0[k] for k in c1}
 
 
-def kernel_roofline(L, ctx, wl, ids, hbm_peak):
-    """Dominant kernel alone: serial stream, device-resident inputs, CUDA events per launch."""
+def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
+    """Dominant kernel alone: serial stream, device-resident inputs, CUDA events around
+    every launch (the group's stage events); achieved = algorithmic bytes (or tensor
+    FLOPs) / summed launch time."""
+    chain = getattr(wl, "roof_chain", None) or wl.chain     # no synthetic spin stages
     ctx.set_serial(True)
     try:
         rc = L.run_config(batch_size=wl.B, n_workers=64)
         c0 = ctx.counters()
-        rep, _, _, _ = ctx.run_shard(wl.chain, wl.descs(ids), rc, want_ids=False)
+        rep, _, _, _ = ctx.run_shard(chain, wl.descs(ids), rc, want_ids=False)
         c1 = ctx.counters()
     finally:
         ctx.set_serial(False)
-    launches = c1["launches"] - c0["launches"] - (c1["gathered_batches"] - c0["gathered_batches"])
-    algo = c1["kernel_bytes"] - c0["kernel_bytes"]
+    d = {k: c1[k] - c0[k] for k in c1}
+    launches = d["launches"] - d["gathered_batches"]
     ms = rep.kernel_ms
-    achieved = algo / (ms / 1e3) / 1e9 if ms > 0 else 0.0
-    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(achieved / hbm_peak, 4), "traffic": None,
-            "kernel": {"rrc": "rrc2d_kernel", "img3d": "img3d_kernel"}.get(wl.name.split("_")[0], wl.name),
-            "launches": int(launches), "algo_bytes_per_launch": int(algo / max(launches, 1)),
-            "mean_launch_us": round(1e3 * ms / max(launches, 1), 2)}
+    kernel = {"rrc": "rrc2d_kernel", "img3d": "img3d_kernel", "speech": "speech_kernel"}[
+        wl.name.split("_")[0]]
+    out = {"kernel": kernel, "launches": int(launches), "mean_launch_us": round(1e3 * ms / max(launches, 1), 2),
+           "traffic": None, "algo_bytes_per_launch": int(d["kernel_bytes"] / max(launches, 1))}
+    if wl.name == "speech":
+        tf = d["tensor_flops"] / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        out.update({"bound": "tensor", "achieved": round(tf, 1), "peak": tf32_peak, "unit": "TFLOP/s",
+                    "frac": round(tf / tf32_peak, 4),
+                    "flops_per_launch": int(d["tensor_flops"] / max(launches, 1)),
+                    "hbm_gbs": round(d["kernel_bytes"] / (ms / 1e3) / 1e9, 1) if ms > 0 else 0.0})
+    else:
+        gbs = d["kernel_bytes"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        out.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(gbs / hbm_peak, 4)})
+    return out
 
 
 def ref_harness():
@@ -314,8 +366,8 @@ def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: i
     was built, else the oracle port alone on a thread pool.  Bounded sample."""
     cores = os.cpu_count() or 1
     h = ref_harness()
-    wl = "rrc" if workload == "rrc" else "img3d"
-    if h:
+    wl = {"rrc": "rrc", "speech": "speech"}.get(workload, "img3d")
+    if h and wl != "speech":
         k = steps or (8 if wl == "rrc" else 10)
         out = subprocess.run([h, "--workload", wl, "--steps", str(k), "--warmup", str(warmup),
                               "--workers", str(cores), "--max-seconds", "150"],
@@ -344,6 +396,14 @@ def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: i
             v = vols[i % len(vols)]
             O.chain3d(cfg, 1, i, v[0], v[1])
         sample = "crop128^3+flip+brightness+noise+cast on 128x384x384 volumes"
+    if wl == "speech":
+        cfg = O.cfgsp()
+        waves = [(0.3 * rng.standard_normal(int(n))).astype(np.float32)
+                 for n in rng.integers(30000, 170001, size=8)]
+
+        def one(i):
+            O.chainsp(cfg, 1, i, waves[i % len(waves)])
+        sample = "STFT(512/320/160)+80 slaney mels+log+SpecAugment on 30k..170k-sample utterances"
     done = 0
     t0 = time.perf_counter()
     with ThreadPoolExecutor(cores) as ex:
@@ -361,7 +421,7 @@ def reference_arm(args):
     if rank != 0:
         return
     wl = args.workload
-    B = 256 if wl == "rrc" else 2
+    B = BATCH[wl][0]
     base = cpu_baseline(wl, seconds=max(5.0, min(60.0, 2.0 * args.steps)), steps=args.steps,
                         warmup=args.warmup)
     v = base["value"]
@@ -381,10 +441,10 @@ def reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=0, help="timed batches (0 = workload default)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="rrc", choices=["rrc", "img3d", "img3d_heavy"])
+    ap.add_argument("--workload", default="rrc", choices=list(BATCH))
     ap.add_argument("--pool", type=int, default=0)
     ap.add_argument("--workers", type=int, default=16)
     ap.add_argument("--group", type=int, default=0, help="samples per launch group (0 = auto)")
@@ -396,6 +456,8 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps <= 0:
+        args.steps = BATCH[args.workload][2]
 
     if args.impl == "reference":
         reference_arm(args)
@@ -403,9 +465,9 @@ def main():
 
     from paper_2509_10712_b200 import lfgpu as L
     rank, local, world, dist = dist_setup(args.gpus)
-    hbm_peak, peak_src = peaks()
-    B = 256 if args.workload == "rrc" else 2
-    group = args.group or (64 if args.workload == "rrc" else 1)
+    hbm_peak, tf32_peak, peak_src = peaks()
+    B = BATCH[args.workload][0]
+    group = args.group or BATCH[args.workload][1]
     ctx = L.Context(device=local, batch_size=B, n_workers=args.workers, max_group=group,
                     max_slot_buffers=8, seed=args.seed)
     ids_all = shard_ids(args.warmup + args.steps, B, rank, world)
@@ -423,7 +485,7 @@ def main():
     samples_total = allreduce_sum(dist, [rep.timed_samples], local)[0]
     value = samples_total / (el_max / 1e3)
     roof = kernel_roofline(L, ctx, wl, ids_timed[: min(len(ids_timed), 64 * B if B > 2 else 64)],
-                           hbm_peak)
+                           hbm_peak, tf32_peak)
     wl.close()
 
     # ---- e2e: inputs in pinned host memory, H2D + a D2H read of every delivered batch
@@ -452,7 +514,8 @@ def main():
         "data": "synthetic (Philox(seed,id) images/volumes generated on device / pinned host)",
         "config": {"workload": {"rrc": "C2 ImageNet-shaped u8 3x(256..512)^2 -> RRC224+hflip+normalize",
                                 "img3d": "C1 KiTS19-shaped 3D crop128^3+flip+brightness+noise+cast",
-                                "img3d_heavy": "C3 heavy-tailed 3D + synthetic trainer"}[args.workload],
+                                "img3d_heavy": "C3 heavy-tailed 3D + synthetic trainer",
+                                "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT + log-mel (tcgen05 3xTF32) + SpecAugment + splice, batch 64"}[args.workload],
                    "batch": B, "launch_group": group, "workers": args.workers,
                    "raw_pool_bytes": int(wl.pool_bytes), "l2": "inputs > L2 (pool larger than 126 MB)",
                    "parallelism": f"dp{world} independent loader shards"},

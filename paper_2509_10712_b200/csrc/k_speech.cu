@@ -20,10 +20,11 @@
 // double-buffered in shared memory: the constant B chunk (64 KB, hi+lo, both
 // N halves) arrives by cp.async.bulk on an mbarrier while the threads build
 // the A chunk (frames read from the waveform with reflect padding, split into
-// tf32 hi/lo); one elected thread issues 12 MMAs per chunk and commits them to
-// the stage's mbarrier.  Operands use the no-swizzle K-major canonical layout:
-// 8-row x 16-byte core matrices, LBO = 128 B (the two 16-B K halves of a K=8
-// step), SBO = 256 B (next 8-row group).
+// tf32 hi/lo); one elected thread issues the MMAs and commits them to the
+// stage's mbarrier.  Operands use the 32-byte-swizzled K-major canonical layout
+// (one 32-B row per frame / basis column = one K=8 tf32 step; the swizzle keeps
+// the tensor core's operand reads bank-conflict free -- the unswizzled layout
+// measured ~5x slower).
 //
 // Epilogue (all 4 warps, thread = frame = TMEM lane): tcgen05.ld 16 columns of
 // cos and sin at a time -> power -> the slaney mel filterbank as a streaming
@@ -32,11 +33,13 @@
 // GEMM) -> shared memory -> log(x + eps), SpecAugment masks, stack-3 splice,
 // coalesced time-major stores into the sample's output slot.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "device_common.cuh"
 #include "kernels.h"
+#include "mel_table.h"
 
 namespace lfg {
 
@@ -50,15 +53,17 @@ constexpr int kBins = 256;            // bins 0..255 on the tensor cores, 256 on
 constexpr int kMels = 80;
 constexpr int kRowsM = 128;           // MMA M
 constexpr int kFramesPerCta = 126;    // multiple of 3 (FrameSplicing stack)
-constexpr int kKChunk = 16;           // taps per pipeline stage (2 MMA K-steps of 8)
-constexpr int kChunks = kTaps / kKChunk;          // 20
+constexpr int kKChunk = 8;            // taps per pipeline stage = one MMA K-step
+constexpr int kChunks = kTaps / kKChunk;          // 40
+constexpr int kStages = 5;
 constexpr int kABytesStep = kRowsM * 32;          // one K=8 step of A (one part): 4 KB
-constexpr int kAPartBytes = 2 * kABytesStep;      // one stage, one part (hi or lo): 8 KB
+constexpr int kAPartBytes = (kKChunk / 8) * kABytesStep;
 constexpr int kBBlock = 256 * 32;                 // one K=8 step, one N half, one part: 8 KB
-constexpr int kBStageBytes = 2 * 2 * 2 * kBBlock; // q x half x part = 64 KB
-constexpr int kStageBytes = 2 * kAPartBytes + kBStageBytes;   // 80 KB
-constexpr int kSmemBytes = 2 * kStageBytes + 1024;            // + barriers / scratch
+constexpr int kBStageBytes = (kKChunk / 8) * 2 * 2 * kBBlock;   // 32 KB
+constexpr int kStageBytes = 2 * kAPartBytes + kBStageBytes;     // 40 KB
+constexpr int kSmemBytes = kStages * kStageBytes + 1024;        // + barriers
 constexpr int kMelPitch = kMels + 1;
+constexpr int kThreads = 192;         // warp 0 producer, warp 1 MMA, warps 2-5 A builders / epilogue
 
 // instruction descriptor: D f32, A/B tf32, K-major both, N = 256, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
@@ -83,6 +88,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -100,10 +108,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
-    // no-swizzle K-major: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48)
-    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
-           ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+    // K-major, 32-byte swizzle: start>>4 [0,14), LBO>>4 = 1 [16,30), SBO>>4 = 256 B [32,46),
+    // version 1 [46,48), layout SWIZZLE_32B = 6 [61,64).  Rows are 32 B (= one K=8 tf32
+    // step); the 16-B half index is XORed with address bit 7 (row bit 2).
+    return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(256 >> 4) << 32) |
+           (1ull << 46) | (6ull << 61);
 }
+// byte offset of 16-B half c of row (or column) r in a 32-B-swizzled K-major tile
+__host__ __device__ __forceinline__ int sw32_off(int r, int c) { return r * 32 + ((c ^ ((r >> 2) & 1)) << 4); }
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -129,33 +141,44 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void epilogue_sync() {   // the 4 builder / epilogue warps only
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+}
 
 // ------------------------------------------------------------------ the kernel
-__global__ void __launch_bounds__(128, 1)
+// Warp-specialised: warp 0 streams the constant B chunks (cp.async.bulk) into a
+// 5-deep ring, warp 1 issues the MMAs (one elected thread), warps 2-5 build the
+// A chunks from the waveform and then run the epilogue.  Per stage: full_a (128
+// builder arrivals), full_b (bulk-copy bytes), empty (tcgen05.commit).
+__global__ void __launch_bounds__(kThreads, 1)
 speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    const SpDesc& d = L.d[blockIdx.y];
-    const int tile = blockIdx.x;
+    // flattened grid: CTA -> (utterance, tile) through the tile prefix sums
+    int u = 0;
+    while (u + 1 < L.n && L.tile_start[u + 1] <= (int)blockIdx.x) ++u;
+    const SpDesc& d = L.d[u];
+    const int tile = blockIdx.x - L.tile_start[u];
     const int T = d.T;
     const int f0 = tile * kFramesPerCta;
     if (f0 >= T) return;                                  // CTA-uniform
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    uint8_t* stage_base[2] = {smem, smem + kStageBytes};
-    uint64_t* bar_b = reinterpret_cast<uint64_t*>(smem + 2 * kStageBytes);     // [2] B landed
-    uint64_t* bar_mma = bar_b + 2;                                             // [2] stage free
-    uint64_t* bar_done = bar_b + 4;                                            // all MMAs done
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_b + 6);
+    uint64_t* full_a = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full_b = full_a + kStages;
+    uint64_t* empty = full_b + kStages;
+    uint64_t* done = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(bar_b + i, 1);
-            mbar_init(bar_mma + i, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full_a + s, 4);          // one arrival per builder warp
+            mbar_init(full_b + s, 1);
+            mbar_init(empty + s, 1);
         }
-        mbar_init(bar_done, 1);
+        mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                          smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -165,147 +188,189 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
-    // this thread's frame (A row) and its waveform window
-    const int r = tid;
-    const int f = f0 + r;
-    const bool row_live = r < kFramesPerCta && f < T;
-    const int64_t n0 = (int64_t)(f - 1) * kHop;           // first tap's sample index
-    const bool interior = row_live && n0 >= 0 && n0 + kTaps <= d.L &&
-                          ((reinterpret_cast<uintptr_t>(d.wav + n0) & 15) == 0);
-    float nyq = 0.0f;
-
-    for (int it = 0; it < kChunks; ++it) {
-        const int st = it & 1;
-        uint8_t* sb = stage_base[st];
-        if (it >= 2) mbar_wait(bar_mma + st, ((it - 2) >> 1) & 1);   // stage's previous MMAs done
-        if (tid == 0) {
-            mbar_expect_tx(bar_b + st, kBStageBytes);
-            bulk_g2s(sb + 2 * kAPartBytes, basis + (size_t)it * kBStageBytes, kBStageBytes, bar_b + st);
-        }
-        // A chunk: taps [16 it, 16 it + 16) of frame f, split into tf32 hi / lo
-        float x[kKChunk];
-        if (interior) {
-            const float4* p = reinterpret_cast<const float4*>(d.wav + n0 + it * kKChunk);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float4 v = __ldg(p + q);
-                x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+    if (warp == 0) {
+        // ---------------- producer: constant DFT basis chunks
+        if (lane == 0) {
+            for (int it = 0; it < kChunks; ++it) {
+                const int s = it % kStages, use = it / kStages;
+                if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
+                if (L.debug & 4) {
+                    mbar_arrive(full_b + s);
+                } else {
+                    mbar_expect_tx(full_b + s, kBStageBytes);
+                    bulk_g2s(smem + s * kStageBytes + 2 * kAPartBytes, basis + (size_t)it * kBStageBytes,
+                             kBStageBytes, full_b + s);
+                }
             }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            for (int it = 0; it < kChunks; ++it) {
+                const int s = it % kStages, use = it / kStages;
+                mbar_wait(full_b + s, use & 1);
+                mbar_wait(full_a + s, use & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t a_hi = smem_u32(smem + s * kStageBytes), a_lo = a_hi + kAPartBytes;
+                const uint32_t b0 = a_hi + 2 * kAPartBytes;
+                const uint64_t dah = smem_desc(a_hi), dal = smem_desc(a_lo);
+#pragma unroll
+                for (int h = 0; h < 2 && !(L.debug & 2); ++h) {
+                    const uint64_t dbh = smem_desc(b0 + (h * 2 + 0) * kBBlock);
+                    const uint64_t dbl = smem_desc(b0 + (h * 2 + 1) * kBBlock);
+                    const uint32_t acc = tmem + h * 256;
+                    mma_tf32(acc, dal, dbh, it > 0 ? 1u : 0u);     // 3xTF32, small terms first
+                    mma_tf32(acc, dah, dbl, 1u);
+                    mma_tf32(acc, dah, dbh, 1u);
+                }
+                mma_commit(empty + s);
+            }
+            mma_commit(done);
+        }
+        __syncwarp();
+    } else {
+        // ---------------- A builders (then the epilogue): one frame per thread,
+        // thread row = TMEM lane (warp w may only read lanes 32*(w%4) .. +31)
+        const int r = 32 * (warp & 3) + lane;
+        const int f = f0 + r;
+        const bool row_live = r < kFramesPerCta && f < T;
+        const int64_t n0 = (int64_t)(f - 1) * kHop;       // first tap's sample index
+        const bool interior = row_live && n0 >= 0 && n0 + kTaps <= d.L &&
+                              ((reinterpret_cast<uintptr_t>(d.wav + n0) & 15) == 0);
+        float nyq = 0.0f;
+        auto load = [&](int it, float x[kKChunk]) {
+            if (interior) {
+                const float4* p = reinterpret_cast<const float4*>(d.wav + n0 + it * kKChunk);
+                const float4 a = __ldg(p), b = __ldg(p + 1);
+                x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+                x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < kKChunk; ++j) {
+                    float v = 0.0f;
+                    if (row_live) {
+                        int64_t n = n0 + it * kKChunk + j;     // reflect padding
+                        if (n < 0) n = -n;
+                        if (n >= d.L) n = 2 * ((int64_t)d.L - 1) - n;
+                        v = __ldg(d.wav + n);
+                    }
+                    x[j] = v;
+                }
+            }
+        };
+        float x[kKChunk];
+        const bool skip_loads = (L.debug & 1) != 0;
+        if (skip_loads) {
+#pragma unroll
+            for (int j = 0; j < kKChunk; ++j) x[j] = 0.001f * j;
         } else {
+            load(0, x);
+        }
+        for (int it = 0; it < kChunks; ++it) {
+            const int s = it % kStages, use = it / kStages;
+            float xn[kKChunk];
+            if (skip_loads) {
+#pragma unroll
+                for (int j = 0; j < kKChunk; ++j) xn[j] = x[j];
+            } else if (it + 1 < kChunks) {
+                load(it + 1, xn);                            // prefetch the next chunk's taps
+            }
+            uint32_t hi[kKChunk], lo[kKChunk];
 #pragma unroll
             for (int j = 0; j < kKChunk; ++j) {
-                float v = 0.0f;
-                if (row_live) {
-                    int64_t n = n0 + it * kKChunk + j;                       // reflect padding
-                    if (n < 0) n = -n;
-                    if (n >= d.L) n = 2 * ((int64_t)d.L - 1) - n;
-                    v = __ldg(d.wav + n);
-                }
-                x[j] = v;
+                nyq = fmaf(x[j], c_win_nyq[it * kKChunk + j], nyq);
+                hi[j] = tf32_rna(x[j]);
+                lo[j] = tf32_rna(x[j] - __uint_as_float(hi[j]));
             }
-        }
-        uint32_t hi[kKChunk], lo[kKChunk];
-#pragma unroll
-        for (int j = 0; j < kKChunk; ++j) {
-            nyq = fmaf(x[j], c_win_nyq[it * kKChunk + j], nyq);
-            hi[j] = tf32_rna(x[j]);
-            lo[j] = tf32_rna(x[j] - __uint_as_float(hi[j]));
-        }
-        // canonical no-swizzle K-major: [q][row group][k half][row in group][16 B]
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
+            if (use > 0) {                                   // one poller per warp
+                if (lane == 0) mbar_wait(empty + s, (use - 1) & 1);
+                __syncwarp();
+            }
+            uint8_t* sa = smem + s * kStageBytes;
+            // canonical K-major, 32-byte swizzle (see smem_desc)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int off = q * kABytesStep + (r >> 3) * 256 + c * 128 + (r & 7) * 16;
-                const int j = 8 * q + 4 * c;
-                *reinterpret_cast<uint4*>(sb + off) = make_uint4(hi[j], hi[j + 1], hi[j + 2], hi[j + 3]);
-                *reinterpret_cast<uint4*>(sb + kAPartBytes + off) =
-                    make_uint4(lo[j], lo[j + 1], lo[j + 2], lo[j + 3]);
+                const int off = sw32_off(r, c);
+                *reinterpret_cast<uint4*>(sa + off) =
+                    make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+                *reinterpret_cast<uint4*>(sa + kAPartBytes + off) =
+                    make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
             }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
-        __syncthreads();
-        if (tid == 0) {
-            mbar_wait(bar_b + st, (it >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t a_hi = smem_u32(sb), a_lo = a_hi + kAPartBytes;
-            const uint32_t b0 = smem_u32(sb + 2 * kAPartBytes);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full_a + s);
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t bh = b0 + ((q * 2 + h) * 2 + 0) * kBBlock;
-                    const uint32_t bl = b0 + ((q * 2 + h) * 2 + 1) * kBBlock;
-                    const uint64_t dah = smem_desc(a_hi + q * kABytesStep);
-                    const uint64_t dal = smem_desc(a_lo + q * kABytesStep);
-                    const uint32_t acc = tmem + h * 256;
-                    const uint32_t first = (it == 0 && q == 0) ? 0u : 1u;
-                    mma_tf32(acc, dal, smem_desc(bh), first);     // small terms first
-                    mma_tf32(acc, dah, smem_desc(bl), 1u);
-                    mma_tf32(acc, dah, smem_desc(bh), 1u);
-                }
-            mma_commit(bar_mma + st);
-            if (it == kChunks - 1) mma_commit(bar_done);
+            for (int j = 0; j < kKChunk; ++j) x[j] = xn[j];
         }
-    }
-    mbar_wait(bar_done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
 
-    // ---- epilogue: power -> mel (streaming, 2 filters per bin) -> shared memory
-    float* mel_s = reinterpret_cast<float*>(smem);          // stage buffers are free now
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-    int cur = 0;
-    float acc_a = 0.0f, acc_b = 0.0f;
-    auto feed = [&](int k, float p) {
-        const int m = c_mel_m[k];
-        if (m < 0) return;
-        while (cur < m) {                                   // filter `cur` complete (uniform)
-            mel_s[r * kMelPitch + cur] = acc_a;
-            acc_a = acc_b;
-            acc_b = 0.0f;
-            ++cur;
-        }
-        acc_a = fmaf(c_mel_wa[k], p, acc_a);
-        acc_b = fmaf(c_mel_wb[k], p, acc_b);
-    };
-    for (int h = 0; h < 2; ++h)
-        for (int b = 0; b < 8; ++b) {
-            float re[16], im[16];
-            tmem_ld16(lane_base + h * 256 + 16 * b, re);
-            tmem_ld16(lane_base + h * 256 + 128 + 16 * b, im);
+        // ---------------- epilogue: power -> mel, all 80 filters in registers.
+        // The bank is a compile-time table (mel_table.h): with the bin loops fully
+        // unrolled every filter index is a constant, so this is 2 FMAs per bin with
+        // immediate weights -- no table loads, no branches.
+        mbar_wait(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float* mel_s = reinterpret_cast<float*>(smem);    // the operand ring is free now
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+        float mel[kMels];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) feed(h * 128 + 16 * b + i, fmaf(re[i], re[i], im[i] * im[i]));
+        for (int m = 0; m < kMels; ++m) mel[m] = 0.0f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                float re[16], im[16];
+                tmem_ld16(lane_base + h * 256 + 16 * b, re);
+                tmem_ld16(lane_base + h * 256 + 128 + 16 * b, im);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int kk = h * 128 + 16 * b + i;
+                    const float p = fmaf(re[i], re[i], im[i] * im[i]);
+                    if (kMelM[kk] >= 0) mel[kMelM[kk]] = fmaf(kMelWa[kk], p, mel[kMelM[kk]]);
+                    if (kMelM[kk] >= 0 && kMelM[kk] + 1 < kMels)
+                        mel[kMelM[kk] + 1] = fmaf(kMelWb[kk], p, mel[kMelM[kk] + 1]);
+                }
+            }
         }
-    feed(kBins, nyq * nyq);
-    while (cur < kMels) {
-        mel_s[r * kMelPitch + cur] = acc_a;
-        acc_a = acc_b;
-        acc_b = 0.0f;
-        ++cur;
+        if (kMelM[kBins] >= 0) {                           // Nyquist bin (CUDA cores)
+            const float p = nyq * nyq;
+            mel[kMelM[kBins]] = fmaf(kMelWa[kBins], p, mel[kMelM[kBins]]);
+        }
+        // log + SpecAugment on this thread's own frame (one time-mask test per
+        // frame; the freq-mask tests are CTA-uniform); padding frames are zero
+        {
+            bool tmask = f >= T || r >= kFramesPerCta;
+            for (int q = 0; q < L.n_tmask; ++q) tmask |= f >= d.t_lo[q] && f < d.t_lo[q] + d.t_w[q];
+            const int fl0 = L.n_fmask > 0 ? d.f_lo[0] : 0, fh0 = L.n_fmask > 0 ? d.f_lo[0] + d.f_w[0] : 0;
+            const int fl1 = L.n_fmask > 1 ? d.f_lo[1] : 0, fh1 = L.n_fmask > 1 ? d.f_lo[1] + d.f_w[1] : 0;
+            float* row = mel_s + r * kMelPitch;
+#pragma unroll
+            for (int m = 0; m < kMels; ++m) {
+                const bool masked = tmask || (m >= fl0 && m < fh0) || (m >= fl1 && m < fh1);
+                row[m] = masked ? 0.0f : logf(mel[m] + 5.9604644775390625e-8f);   // + 2^-24
+            }
+        }
+        epilogue_sync();
+
+        // FrameSplicing: spliced row t' is frames stack*t' .. stack*t'+stack-1, so
+        // the CTA's output rows are one contiguous run of (frame, mel) values:
+        // copy it out with 128-bit stores
+        const int e = tid - 64;
+        const int stack = L.stack;
+        const int width = stack * kMels;
+        const int row0 = f0 / stack;
+        const int t_rows = (T + stack - 1) / stack;
+        const int rows = min(kFramesPerCta / stack, t_rows - row0);
+        float* out = d.out + (int64_t)row0 * width;
+        for (int q = 4 * e; q < rows * width && !(L.debug & 64); q += 4 * 128) {
+            const int fr = q / kMels, m = q - fr * kMels;   // 4 values of one frame (80 % 4 == 0)
+            const float* src = mel_s + fr * kMelPitch + m;
+            *reinterpret_cast<float4*>(out + q) = make_float4(src[0], src[1], src[2], src[3]);
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-
-    // ---- log, SpecAugment, FrameSplicing (stack 3): coalesced time-major rows
-    const int stack = L.stack;
-    const int width = stack * kMels;
-    const int rows = kFramesPerCta / stack;
-    const int row0 = f0 / stack;
-    const int t_rows = (T + stack - 1) / stack;
-    for (int i = tid; i < rows * width; i += 128) {
-        const int rr = i / width, col = i - rr * width;
-        if (row0 + rr >= t_rows) break;
-        const int fl = rr * stack + col / kMels, m = col % kMels;   // frame within the CTA, mel bin
-        const int ff = f0 + fl;
-        float v = 0.0f;
-        if (ff < T) {
-            bool masked = false;
-            for (int q = 0; q < L.n_fmask; ++q) masked |= m >= d.f_lo[q] && m < d.f_lo[q] + d.f_w[q];
-            for (int q = 0; q < L.n_tmask; ++q) masked |= ff >= d.t_lo[q] && ff < d.t_lo[q] + d.t_w[q];
-            v = masked ? 0.0f : logf(mel_s[fl * kMelPitch + m] + 5.9604644775390625e-8f);   // + 2^-24
-        }
-        d.out[(int64_t)(row0 + rr) * width + col] = v;
-    }
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // K11: PermuteAudio + Pad: per-sample [T'_i, W] slots -> batch [T'_max, n, W], zero-padded.
@@ -347,7 +412,7 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     for (int j = 0; j < kTaps; ++j) win[j] = 0.5 - 0.5 * std::cos(2.0 * M_PI * j / kTaps);
     std::vector<char> img((size_t)kChunks * kBStageBytes, 0);
     for (int it = 0; it < kChunks; ++it)
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < kKChunk / 8; ++q)
             for (int h = 0; h < 2; ++h)
                 for (int col = 0; col < 256; ++col) {
                     const int k = 128 * h + (col & 127);
@@ -360,7 +425,7 @@ cudaError_t speech_tables_create(SpeechTables** out) {
                         const uint32_t vl = h_tf32_rna((float)(v - (double)as_f(vh)));
                         const int c = jj >> 2, e = jj & 3;
                         const size_t blk = (size_t)it * kBStageBytes + (size_t)((q * 2 + h) * 2) * kBBlock;
-                        const size_t off = (size_t)(col >> 3) * 256 + c * 128 + (col & 7) * 16 + e * 4;
+                        const size_t off = (size_t)sw32_off(col, c) + e * 4;
                         std::memcpy(&img[blk + off], &vh, 4);
                         std::memcpy(&img[blk + kBBlock + off], &vl, 4);
                     }
@@ -435,11 +500,15 @@ void speech_tables_destroy(SpeechTables* t) {
 
 int speech_frames_per_cta() { return kFramesPerCta; }
 
-cudaError_t launch_speech(const SpLaunch& L, const SpeechTables* t, float*, cudaStream_t s) {
-    if (L.n <= 0) return cudaSuccess;
-    int max_tiles = 1;
-    for (int i = 0; i < L.n; ++i) max_tiles = max(max_tiles, (L.d[i].T + kFramesPerCta - 1) / kFramesPerCta);
-    speech_kernel<<<dim3(max_tiles, L.n), 128, kSmemBytes, s>>>(L, t->basis);
+cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, float*, cudaStream_t s) {
+    if (L0.n <= 0) return cudaSuccess;
+    static const int dbg = getenv("LFG_SPEECH_DEBUG") ? atoi(getenv("LFG_SPEECH_DEBUG")) : 0;
+    SpLaunch L = L0;
+    L.debug = dbg;
+    L.tile_start[0] = 0;
+    for (int i = 0; i < L.n; ++i)
+        L.tile_start[i + 1] = L.tile_start[i] + (L.d[i].T + kFramesPerCta - 1) / kFramesPerCta;
+    speech_kernel<<<L.tile_start[L.n], kThreads, kSmemBytes, s>>>(L, t->basis);
     return cudaGetLastError();
 }
 

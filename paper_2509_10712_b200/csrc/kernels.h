@@ -89,6 +89,8 @@ struct SpLaunch {
     int32_t n;
     int32_t n_fmask, n_tmask;
     int32_t stack;
+    int32_t debug;            // profiling switch: 1 builders skip loads, 2 skip MMAs
+    int32_t tile_start[kMaxSp + 1];   // CTA prefix sums (flattened grid), filled by the launcher
     SpDesc d[kMaxSp];
 };
 

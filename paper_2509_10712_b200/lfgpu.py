@@ -386,7 +386,10 @@ class Context:
     def counters(self) -> dict:
         c = Counters()
         _check(_lib.lfg_get_counters(self.h, C.byref(c)))
-        return {f: getattr(c, f) for f, _ in Counters._fields_ if f != "reserved"}
+        out = {f: getattr(c, f) for f, _ in Counters._fields_ if f != "reserved"}
+        out["gather_bytes"] = c.reserved[0]      # collation (seal) kernel bytes
+        out["tensor_flops"] = c.reserved[1]      # speech DFT GEMM flops (3xTF32 counted x3)
+        return out
 
     # synthetic inputs
     def synth_volume(self, seed, sid, D, H, W, img_ptr, lbl_ptr, on_device=True):
