@@ -45,8 +45,8 @@ sys.path.insert(0, ROOT)
 METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform HBM GB/s"
 
 # workload -> (batch size, samples per launch group, default timed steps)
-BATCH = {"rrc": (256, 64, 200), "img3d": (2, 1, 400), "img3d_heavy": (2, 1, 400),
-         "speech": (64, 64, 100)}
+BATCH = {"rrc": (256, 64, 1000), "img3d": (2, 2, 4000), "img3d_heavy": (2, 1, 400),
+         "speech": (64, 64, 500)}
 
 
 def peaks():
@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -327,29 +327,21 @@ def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
     every launch (the group's stage events); achieved = algorithmic bytes (or tensor
     FLOPs) / summed launch time."""
     chain = getattr(wl, "roof_chain", None) or wl.chain     # no synthetic spin stages
-    ctx.set_serial(True)
-    try:
-        rc = L.run_config(batch_size=wl.B, n_workers=64)
-        c0 = ctx.counters()
-        rep, _, _, _ = ctx.run_shard(chain, wl.descs(ids), rc, want_ids=False)
-        c1 = ctx.counters()
-    finally:
-        ctx.set_serial(False)
-    d = {k: c1[k] - c0[k] for k in c1}
-    launches = d["launches"] - d["gathered_batches"]
-    ms = rep.kernel_ms
+    t = ctx.time_kernels(chain, wl.descs(ids))              # launches back to back, CUDA events
+    launches = t["launches"]
+    ms = t["mean_ms"] * launches                            # total transform-kernel time
     kernel = {"rrc": "rrc2d_kernel", "img3d": "img3d_kernel", "speech": "speech_kernel"}[
         wl.name.split("_")[0]]
-    out = {"kernel": kernel, "launches": int(launches), "mean_launch_us": round(1e3 * ms / max(launches, 1), 2),
-           "traffic": None, "algo_bytes_per_launch": int(d["kernel_bytes"] / max(launches, 1))}
+    out = {"kernel": kernel, "launches": int(launches), "mean_launch_us": round(1e3 * t["mean_ms"], 2),
+           "traffic": None, "algo_bytes_per_launch": int(t["bytes"] / max(launches, 1))}
     if wl.name == "speech":
-        tf = d["tensor_flops"] / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        tf = t["flops"] / (ms / 1e3) / 1e12 if ms > 0 else 0.0
         out.update({"bound": "tensor", "achieved": round(tf, 1), "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": round(tf / tf32_peak, 4),
-                    "flops_per_launch": int(d["tensor_flops"] / max(launches, 1)),
-                    "hbm_gbs": round(d["kernel_bytes"] / (ms / 1e3) / 1e9, 1) if ms > 0 else 0.0})
+                    "flops_per_launch": int(t["flops"] / max(launches, 1)),
+                    "hbm_gbs": round(t["bytes"] / (ms / 1e3) / 1e9, 1) if ms > 0 else 0.0})
     else:
-        gbs = d["kernel_bytes"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        gbs = t["bytes"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0
         out.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(gbs / hbm_peak, 4)})
     return out

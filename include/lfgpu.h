@@ -218,6 +218,12 @@ int lfg_get_counters(lfg_ctx* ctx, lfg_counters* out);
  * events time each kernel in isolation (used for the roofline measurement). */
 int lfg_set_serial(lfg_ctx* ctx, int serial);
 
+/* Roofline timing: submits the samples with launches deferred, then issues all
+ * launch groups back to back on one stream; mean_ms = mean device time of one
+ * transform-stage launch (CUDA events), bytes / flops = algorithmic totals. */
+int lfg_time_kernels(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples, int n,
+                     double* mean_ms, int64_t* launches, int64_t* bytes, int64_t* flops);
+
 /* ---- event-driven shard runner: the whole Algorithm-1 loop for one GPU
  * (run_minato_pipeline, experiment.cpp:129-276, with workers -> streams,
  * resume -> completion events, batcher -> seal, consumer -> trainer stream). */

@@ -551,6 +551,16 @@ int lfg_get_counters(lfg_ctx* ctx, lfg_counters* out) {
     });
 }
 
+int lfg_time_kernels(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples, int n,
+                     double* mean_ms, int64_t* launches, int64_t* bytes, int64_t* flops) {
+    return guarded([&] {
+        Context& c = C(ctx);
+        if (!chain || !samples || !mean_ms || !launches || !bytes || !flops) fail(LFG_ERR_INVALID, "null argument");
+        std::lock_guard<std::mutex> g(c.mu);
+        c.time_kernels(chain->impl, samples, n, mean_ms, launches, bytes, flops);
+    });
+}
+
 int lfg_set_serial(lfg_ctx* ctx, int serial) {
     return guarded([&] {
         Context& c = C(ctx);

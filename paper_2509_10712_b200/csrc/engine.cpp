@@ -370,8 +370,8 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
         c->plane_bytes[0] = vox * 4;
         c->plane_bytes[1] = ((vox + 15) / 16) * 16;
     } else if (c->fam == FAM_RRC2D) {
-        if (c->oh < 1 || c->ow < 1 || c->ow > 256 || c->oh > 4096)
-            fail(LFG_ERR_UNSUPPORTED, "Resize output must be <= 256 wide");
+        if (c->oh < 1 || c->ow < 2 || c->ow > 256 || (c->ow & 1) || c->oh > 4096)
+            fail(LFG_ERR_UNSUPPORTED, "Resize output width must be even and <= 256");
         c->nplanes = 1;
         c->plane_bytes[0] = int64_t(3) * c->oh * c->ow * 4;
     } else {
@@ -658,7 +658,8 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
     const int cap = c->fam == FAM_IMG3D ? kMax3D : (c->fam == FAM_RRC2D ? kMax2D : kMaxSp);
     if (static_cast<int>(g.tickets.size()) >= std::min(cfg.max_group, cap)) {
         og.erase(c);
-        launch_group(g);
+        if (defer_launch) deferred_.push_back(gi);
+        else launch_group(g);
     }
     return ti;
 }
@@ -668,10 +669,62 @@ int64_t Context::open_group_count() const {
 }
 
 void Context::flush() {
+    for (int64_t gi : deferred_) launch_group(groups[gi]);
+    deferred_.clear();
     for (auto& og : open_group_) {
         for (auto& kv : og) launch_group(groups[kv.second]);
         og.clear();
     }
+}
+
+// Roofline timing of a chain's transform kernels: all samples are submitted
+// first (launches deferred), then every launch group is issued back to back on
+// one stream, so the per-stage CUDA events bracket kernel time only -- no host
+// submission gaps.  Returns the mean device time of one transform-stage launch.
+void Context::time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms,
+                           int64_t* launches, int64_t* bytes, int64_t* flops) {
+    if (n < 1) fail(LFG_ERR_INVALID, "no samples to time");
+    const int64_t fit = int64_t(cfg.max_slot_buffers - 1) * cfg.batch_size;
+    if (n > fit) n = static_cast<int>(fit);
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    const lfg_counters c0 = counters;
+    serial = true;
+    defer_launch = true;
+    std::vector<int64_t> ts;
+    try {
+        for (int i = 0; i < n; ++i) ts.push_back(submit(c, s[i]));
+        for (auto& og : open_group_) {
+            for (auto& kv : og)
+                if (groups[kv.second].chain == c) deferred_.push_back(kv.second);
+            og.erase(c);
+        }
+        defer_launch = false;
+        flush();
+    } catch (...) {
+        serial = defer_launch = false;
+        throw;
+    }
+    serial = false;
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    double ms = 0;
+    int64_t nl = 0;
+    std::vector<int64_t> seen;
+    for (int64_t t : ts) {
+        Group& g = groups[tickets[t].group];
+        if (std::find(seen.begin(), seen.end(), g.id) != seen.end()) continue;
+        seen.push_back(g.id);
+        poll_group(g);
+        for (size_t k = 0; k < c->stages.size(); ++k)
+            if (c->stages[k].kind != ST_SPIN) {
+                ms += g.stage_ms[k];
+                ++nl;
+            }
+    }
+    for (int64_t t : ts) ticket_release(t);
+    *mean_ms = nl ? ms / nl : 0.0;
+    *launches = nl;
+    *bytes = counters.kernel_bytes - c0.kernel_bytes;
+    *flops = counters.reserved[1] - c0.reserved[1];
 }
 
 void Context::launch_group(Group& g) {

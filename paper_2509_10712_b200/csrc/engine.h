@@ -191,6 +191,9 @@ public:
     int free_stream_count() const { return static_cast<int>(free_streams_.size()); }
     lfg_counters counters{};
     bool serial = false;
+    bool defer_launch = false;
+    void time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms, int64_t* launches,
+                      int64_t* bytes, int64_t* flops);
     std::mutex mu;   // one lock per context (C ABI calls serialise on it)
 
     cudaStream_t seal_stream = nullptr;
@@ -210,6 +213,7 @@ private:
     std::vector<RawBuf> raws_;
     std::vector<int64_t> free_raws_;
     std::unordered_map<const Chain*, int> open_buf_;     // chain -> open slot buffer
+    std::vector<int64_t> deferred_;                      // full groups awaiting launch (timing mode)
     std::unordered_map<const Chain*, int64_t> open_group_[2];  // [src_kind] chain -> group
 
     cudaEvent_t get_event();

@@ -10,15 +10,17 @@
 // tap indices always agree with the oracle and only the fp32 arithmetic
 // differs (~1e-7 relative).
 //
-// Mapping: grid (ceil(oh / kRows), n_samples), 256 threads.  A CTA owns kRows
+// Mapping: grid (ceil(oh / kRows), n_samples), 128 threads.  A CTA owns kRows
 // output rows of one sample:
 //   1. the source rows those outputs touch (<= (kRows-1)*h/oh + 3) are copied
-//      from HBM into shared memory with aligned 16-byte loads; row taps are
-//      computed once per CTA;
-//   2. one thread per output column reads its two horizontal taps (6 bytes
-//      per source row) with three 32-bit shared loads and two funnel shifts,
-//      converts bytes to floats with PRMT into the 2^23 mantissa (exact), and
-//      writes 3 coalesced f32 planes with streaming stores.
+//      from HBM into shared memory with aligned 16-byte loads (a warp per row);
+//      row taps are computed once per CTA and packed into one 16-B record;
+//   2. each thread owns TWO output columns (x and x + ow/2), so the per-row
+//      bookkeeping is shared by two pixels; it reads each horizontal tap pair
+//      (6 bytes per source row) with three 32-bit shared loads and two funnel
+//      shifts, converts bytes with PRMT into the 2^23 mantissa (exact), keeps
+//      the horizontally blended rows in a 2-entry cache (consecutive output rows
+//      share source rows), and writes 3 coalesced f32 planes with streaming stores.
 // The per-launch dynamic shared memory is the largest row window of the group
 // (computed on the host with the same formula); crops whose window exceeds the
 // budget (sources taller than ~2.6x oh) fall back to direct L2 byte loads.
@@ -30,7 +32,7 @@ namespace lfg {
 namespace {
 
 constexpr int kRows = 8;
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 constexpr int kMaxSmem = 64 * 1024;
 
 // PyTorch area_pixel_compute_source_index (align_corners=False, linear), fp64,
@@ -57,122 +59,146 @@ __device__ __forceinline__ float ubyte(uint32_t w, int k) {
     return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u | (uint32_t)k)) - 8388608.0f;
 }
 
+struct Col {                // one output column's horizontal taps
+    int off;                // byte offset of tap 0 within a source row (3 * x0)
+    bool edge;              // right border: tap 1 == tap 0
+    float w0, w1;
+    int x1;                 // (fallback path only)
+};
+
+__device__ __forceinline__ void blend_row(const uint8_t* smem, int row_off, const Col& c, float h[3]) {
+    const int off = row_off + c.off;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(smem + (off & ~3));
+    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+    const uint32_t sh = (off & 3) * 8;
+    const uint32_t lo = __funnelshift_r(w0, w1, sh);    // bytes 0..3: R0 G0 B0 R1
+    const uint32_t hi = __funnelshift_r(w1, w2, sh);    // bytes 4..7: G1 B1 . .
+    const float r0 = ubyte(lo, 0), g0 = ubyte(lo, 1), b0 = ubyte(lo, 2);
+    const float r1 = c.edge ? r0 : ubyte(lo, 3);
+    const float g1 = c.edge ? g0 : ubyte(hi, 0);
+    const float b1 = c.edge ? b0 : ubyte(hi, 1);
+    h[0] = fmaf(c.w0, r0, c.w1 * r1);
+    h[1] = fmaf(c.w0, g0, c.w1 * g1);
+    h[2] = fmaf(c.w0, b0, c.w1 * b1);
+}
+
+__device__ __forceinline__ void blend_row_l2(const RrcDesc& d, int y, int x0, const Col& c, float h[3]) {
+    const uint8_t* row = row_ptr(d, y);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float p0 = __ldg(row + 3 * x0 + k), p1 = __ldg(row + 3 * c.x1 + k);
+        h[k] = fmaf(c.w0, p0, c.w1 * p1);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads)
 rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ int row_off[64];           // byte offset of each staged row's first pixel
-    __shared__ int ty[kRows][2];
-    __shared__ float wy[kRows][2];
+    __shared__ int row_off[64];          // byte offset of each staged row's first pixel
+    __shared__ int4 taps[kRows];         // {y0, y1, ly0 bits, ly1 bits}
     const RrcDesc& d = L.d[blockIdx.y];
     const int oh = L.oh, ow = L.ow;
     const int y_begin = blockIdx.x * kRows;
-    const int y_end = min(y_begin + kRows, oh);
-    const double sy = __ddiv_rn((double)d.h, (double)oh);
-    if (threadIdx.x < y_end - y_begin) {
+    const int n_rows_out = min(kRows, oh - y_begin);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < n_rows_out) {
         int a, b;
         float l0, l1;
-        src_index(y_begin + threadIdx.x, d.h, sy, a, b, l0, l1);
-        ty[threadIdx.x][0] = a;
-        ty[threadIdx.x][1] = b;
-        wy[threadIdx.x][0] = l0;
-        wy[threadIdx.x][1] = l1;
+        src_index(y_begin + threadIdx.x, d.h, __ddiv_rn((double)d.h, (double)oh), a, b, l0, l1);
+        taps[threadIdx.x] = make_int4(a, b, __float_as_int(l0), __float_as_int(l1));
     }
     __syncthreads();
-    const int ylo = ty[0][0];
-    const int nrows = ty[y_end - y_begin - 1][1] - ylo + 1;
+    const int ylo = taps[0].x;
+    const int nrows = taps[n_rows_out - 1].y - ylo + 1;
     const int row_bytes = d.w * 3;
     const int spitch = ((row_bytes + 30) >> 4) << 4;        // 16-B chunks + alignment phase
     const bool staged = nrows <= 64 && nrows * spitch <= smem_bytes;
 
-    // 1. stage the touched source rows (aligned 16-byte superset of each row)
+    // 1. stage the touched source rows (aligned 16-byte superset of each row), a warp per row
     if (staged) {
-        const int chunks = spitch >> 4;
-        for (int i = threadIdx.x; i < nrows * chunks; i += kThreads) {
-            const int r = i / chunks, c = i - r * chunks;
+        for (int r = warp; r < nrows; r += kThreads / 32) {
             const uintptr_t s = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
-            const uintptr_t a = s & ~uintptr_t(15);
-            const uintptr_t e = (s + row_bytes + 15) & ~uintptr_t(15);
-            if (a + 16u * c < e) {
-                *reinterpret_cast<int4*>(smem + r * spitch + 16 * c) =
-                    __ldg(reinterpret_cast<const int4*>(a) + c);
-            }
-            if (c == 0) row_off[r] = r * spitch + (int)(s & 15);
+            const int4* a = reinterpret_cast<const int4*>(s & ~uintptr_t(15));
+            const int nch = (int)((((s + row_bytes + 15) & ~uintptr_t(15)) - (s & ~uintptr_t(15))) >> 4);
+            int4* dst = reinterpret_cast<int4*>(smem + r * spitch);
+            for (int c = lane; c < nch; c += 32) dst[c] = __ldg(a + c);
+            if (lane == 0) row_off[r] = r * spitch + (int)(s & 15);
         }
         __syncthreads();
     }
 
-    const int x = threadIdx.x;
-    if (x >= ow) return;
-    int x0, x1;
-    float lx0, lx1;
-    src_index(x, d.w, __ddiv_rn((double)d.w, (double)ow), x0, x1, lx0, lx1);
-    const bool edge = x1 == x0;                                     // right border: tap 1 = tap 0
-    const int xo = d.flip ? ow - 1 - x : x;                         // RandomHorizontalFlip
+    const int half = ow >> 1;                               // ow is even (checked on the host)
+    const int xa = threadIdx.x;
+    if (xa >= half) return;
+    const int xb = xa + half;
+    const double sx = __ddiv_rn((double)d.w, (double)ow);
+    Col ca, cb;
+    int xa0, xb0;
+    src_index(xa, d.w, sx, xa0, ca.x1, ca.w0, ca.w1);
+    src_index(xb, d.w, sx, xb0, cb.x1, cb.w0, cb.w1);
+    ca.off = 3 * xa0;
+    ca.edge = ca.x1 == xa0;
+    cb.off = 3 * xb0;
+    cb.edge = cb.x1 == xb0;
     const int64_t plane = (int64_t)oh * ow;
+    // RandomHorizontalFlip: output columns of this thread
+    float* oa = d.out + (int64_t)y_begin * ow + (d.flip ? ow - 1 - xa : xa);
+    float* ob = d.out + (int64_t)y_begin * ow + (d.flip ? ow - 1 - xb : xb);
     const float a0 = L.a[0], a1 = L.a[1], a2 = L.a[2];
     const float b0 = L.b[0], b1 = L.b[1], b2 = L.b[2];
 
-    // horizontal blend of one source row at this thread's column (3 channels)
-    auto hrow = [&](int y, float h[3]) {
-        float p[6];   // R0 G0 B0 R1 G1 B1
-        if (staged) {
-            const int off = row_off[y - ylo] + 3 * x0;
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(smem + (off & ~3));
-            const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
-            const uint32_t sh = (off & 3) * 8;
-            const uint32_t lo = __funnelshift_r(w0, w1, sh);        // bytes 0..3
-            const uint32_t hi = __funnelshift_r(w1, w2, sh);        // bytes 4..7
-            p[0] = ubyte(lo, 0);
-            p[1] = ubyte(lo, 1);
-            p[2] = ubyte(lo, 2);
-            p[3] = edge ? p[0] : ubyte(lo, 3);
-            p[4] = edge ? p[1] : ubyte(hi, 0);
-            p[5] = edge ? p[2] : ubyte(hi, 1);
-        } else {
-            const uint8_t* row = row_ptr(d, y);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                p[c] = __ldg(row + 3 * x0 + c);
-                p[3 + c] = __ldg(row + 3 * x1 + c);
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) h[c] = fmaf(lx0, p[c], lx1 * p[3 + c]);
-    };
-    // Two-entry cache of blended rows: consecutive output rows share source
-    // rows (y0(j) == y1(j-1) when downscaling < 2x, y0(j) == y0(j-1) when
-    // upscaling).  Row indices are CTA-uniform, so the branches do not diverge.
+    // Two-entry cache of blended rows (row indices are CTA-uniform: no divergence)
     int ra = -1, rb = -1;
-    float ha[3] = {0, 0, 0}, hb[3] = {0, 0, 0};
-    for (int j = 0; j < y_end - y_begin; ++j) {
-        const int y0 = ty[j][0], y1 = ty[j][1];
-        const float ly0 = wy[j][0], ly1 = wy[j][1];
-        float top[3], bot[3];
+    float ha[6] = {0, 0, 0, 0, 0, 0}, hb[6] = {0, 0, 0, 0, 0, 0};   // [col a rgb, col b rgb]
+    for (int j = 0; j < n_rows_out; ++j) {
+        const int4 t = taps[j];
+        const int y0 = t.x, y1 = t.y;
+        const float ly0 = __int_as_float(t.z), ly1 = __int_as_float(t.w);
+        float top[6], bot[6];
         if (y0 == rb) {
-            top[0] = hb[0]; top[1] = hb[1]; top[2] = hb[2];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) top[k] = hb[k];
         } else if (y0 == ra) {
-            top[0] = ha[0]; top[1] = ha[1]; top[2] = ha[2];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) top[k] = ha[k];
+        } else if (staged) {
+            const int ro = row_off[y0 - ylo];
+            blend_row(smem, ro, ca, top);
+            blend_row(smem, ro, cb, top + 3);
         } else {
-            hrow(y0, top);
+            blend_row_l2(d, y0, xa0, ca, top);
+            blend_row_l2(d, y0, xb0, cb, top + 3);
         }
         if (y1 == y0) {
-            bot[0] = top[0]; bot[1] = top[1]; bot[2] = top[2];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) bot[k] = top[k];
         } else if (y1 == rb) {
-            bot[0] = hb[0]; bot[1] = hb[1]; bot[2] = hb[2];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) bot[k] = hb[k];
+        } else if (staged) {
+            const int ro = row_off[y1 - ylo];
+            blend_row(smem, ro, ca, bot);
+            blend_row(smem, ro, cb, bot + 3);
         } else {
-            hrow(y1, bot);
+            blend_row_l2(d, y1, xa0, ca, bot);
+            blend_row_l2(d, y1, xb0, cb, bot + 3);
         }
         ra = y0;
-        ha[0] = top[0]; ha[1] = top[1]; ha[2] = top[2];
         rb = y1;
-        hb[0] = bot[0]; hb[1] = bot[1]; hb[2] = bot[2];
-        float out[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) out[c] = fmaf(ly0, top[c], ly1 * bot[c]);   // Resize (bilinear)
-        float* o = d.out + (int64_t)(y_begin + j) * ow + xo;
-        __stcs(o, fmaf(out[0], a0, b0));                           // ToTensor + Normalize
-        __stcs(o + plane, fmaf(out[1], a1, b1));
-        __stcs(o + 2 * plane, fmaf(out[2], a2, b2));
+        for (int k = 0; k < 6; ++k) {
+            ha[k] = top[k];
+            hb[k] = bot[k];
+        }
+        // Resize (vertical blend), then ToTensor + Normalize
+        __stcs(oa, fmaf(fmaf(ly0, top[0], ly1 * bot[0]), a0, b0));
+        __stcs(oa + plane, fmaf(fmaf(ly0, top[1], ly1 * bot[1]), a1, b1));
+        __stcs(oa + 2 * plane, fmaf(fmaf(ly0, top[2], ly1 * bot[2]), a2, b2));
+        __stcs(ob, fmaf(fmaf(ly0, top[3], ly1 * bot[3]), a0, b0));
+        __stcs(ob + plane, fmaf(fmaf(ly0, top[4], ly1 * bot[4]), a1, b1));
+        __stcs(ob + 2 * plane, fmaf(fmaf(ly0, top[5], ly1 * bot[5]), a2, b2));
+        oa += ow;
+        ob += ow;
     }
 }
 
@@ -193,7 +219,7 @@ int rrc2d_smem_bytes(const RrcLaunch& L) {
 
 cudaError_t launch_rrc2d(const RrcLaunch& L, cudaStream_t s) {
     if (L.n <= 0) return cudaSuccess;
-    if (L.ow > kThreads) return cudaErrorInvalidValue;
+    if (L.ow > 2 * kThreads || (L.ow & 1)) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(rrc2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

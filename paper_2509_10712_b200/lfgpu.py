@@ -133,6 +133,8 @@ _sig = {
     "lfg_synth_waveform": ([_vp, C.c_uint64, C.c_uint64, C.c_int64, _vp, C.c_int], C.c_int),
     "lfg_get_counters": ([_vp, _P(Counters)], C.c_int),
     "lfg_set_serial": ([_vp, C.c_int], C.c_int),
+    "lfg_time_kernels": ([_vp, _vp, _P(SampleDesc), C.c_int, _P(C.c_double), _P(C.c_int64),
+                          _P(C.c_int64), _P(C.c_int64)], C.c_int),
     "lfg_run_shard": ([_vp, _vp, _P(SampleDesc), C.c_int64, _P(RunConfig), _P(RunReport),
                        _P(C.c_uint64), _P(C.c_int32), _P(C.c_int32)], C.c_int),
 }
@@ -400,6 +402,13 @@ class Context:
 
     def synth_waveform(self, seed, sid, L, ptr, on_device=True):
         _check(_lib.lfg_synth_waveform(self.h, seed, sid, L, ptr, int(on_device)))
+
+    def time_kernels(self, ch: Chain, descs):
+        arr = (SampleDesc * len(descs))(*descs)
+        ms, nl, by, fl = C.c_double(), C.c_int64(), C.c_int64(), C.c_int64()
+        _check(_lib.lfg_time_kernels(self.h, ch.handle, arr, len(descs), C.byref(ms), C.byref(nl),
+                                     C.byref(by), C.byref(fl)))
+        return {"mean_ms": ms.value, "launches": nl.value, "bytes": by.value, "flops": fl.value}
 
     def set_serial(self, serial: bool):
         _check(_lib.lfg_set_serial(self.h, int(serial)))
