@@ -45,7 +45,7 @@ sys.path.insert(0, ROOT)
 METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform HBM GB/s"
 
 # workload -> (batch size, samples per launch group, default timed steps)
-BATCH = {"rrc": (256, 64, 1000), "img3d": (2, 2, 4000), "img3d_heavy": (2, 1, 400),
+BATCH = {"rrc": (256, 256, 1000), "img3d": (2, 8, 4000), "img3d_heavy": (2, 1, 400),
          "speech": (64, 64, 500)}
 
 
@@ -460,8 +460,10 @@ def main():
     hbm_peak, tf32_peak, peak_src = peaks()
     B = BATCH[args.workload][0]
     group = args.group or BATCH[args.workload][1]
+    # enough output slot buffers for every in-flight launch group (+ batches being consumed)
+    slots = max(8, -(-args.workers * group // B) + 4)
     ctx = L.Context(device=local, batch_size=B, n_workers=args.workers, max_group=group,
-                    max_slot_buffers=8, seed=args.seed)
+                    max_slot_buffers=slots, seed=args.seed)
     ids_all = shard_ids(args.warmup + args.steps, B, rank, world)
     ids_warm, ids_timed = ids_all[: args.warmup * B], ids_all[args.warmup * B:]
     heavy = args.workload == "img3d_heavy"

@@ -410,14 +410,14 @@ int lfg_batch_copy_to_host(lfg_ctx* ctx, lfg_batch b, void* host_dst, size_t byt
         if (ch.fam == FAM_SPEECH) {   // time-major [t_max, n, stack * 80]
             const int64_t need = int64_t(br.t_max) * br.n * ch.stack * ch.n_mels * 4;
             if (static_cast<int64_t>(bytes) < need) fail(LFG_ERR_INVALID, "host buffer too small");
-            cuda_check(cudaEventSynchronize(br.ready), "batch ready");
+            if (br.ready) cuda_check(cudaEventSynchronize(br.ready), "batch ready");
             cuda_check(cudaMemcpy(host_dst, p, need, cudaMemcpyDeviceToHost), "D2H batch");
             c.counters.d2h_bytes += need;
             return;
         }
         const int64_t need = static_cast<int64_t>(br.n) * ch.out_bytes;
         if (static_cast<int64_t>(bytes) < need) fail(LFG_ERR_INVALID, "host buffer too small");
-        cuda_check(cudaEventSynchronize(br.ready), "batch ready");
+        if (br.ready) cuda_check(cudaEventSynchronize(br.ready), "batch ready");
         char* d = static_cast<char*>(host_dst);
         const int64_t cap = c.cfg.batch_size;
         cuda_check(cudaMemcpy(d, p, br.n * ch.plane_bytes[0], cudaMemcpyDeviceToHost), "D2H batch");

@@ -194,6 +194,7 @@ Context::Context(const lfg_config& c) : cfg(c) {
     cuda_check(warm_rrc2d(), "load rrc2d kernel");
     cuda_check(warm_misc(), "load misc kernels");
     cuda_check(warm_speech(), "load speech kernels");
+    if (const char* e = std::getenv("LFG_IMG3D_TMA")) img3d_tma_ = std::atoi(e) != 0;
     for (int i = 0; i < 512; ++i) {
         cudaEvent_t e;
         cuda_check(cudaEventCreate(&e), "cudaEventCreate");
@@ -481,8 +482,14 @@ void Context::reserve_bufs(const Chain* c) {
     }
 }
 
+// Round-robin from the buffer after the last one handed out: the oldest
+// buffer is the likeliest to be free, so usually the first candidate is taken
+// after at most one event query (a full scan with queries costs microseconds).
 int Context::alloc_buf(const Chain* c, bool for_batch) {
-    for (size_t i = 0; i < bufs_.size(); ++i) {
+    const size_t nb = bufs_.size();
+    size_t& cur = alloc_cursor_[for_batch ? 1 : 0];
+    for (size_t k = 0; k < nb; ++k) {
+        const size_t i = (cur + 1 + k) % nb;
         SlotBuf& b = bufs_[i];
         if (b.gather_role != for_batch || b.chain != c) continue;
         if (buf_reusable(b)) {
@@ -490,6 +497,7 @@ int Context::alloc_buf(const Chain* c, bool for_batch) {
             b.live = 0;
             b.open = !for_batch;
             b.in_batch = for_batch;
+            cur = i;
             return static_cast<int>(i);
         }
     }
@@ -596,9 +604,6 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
     if (s.data == nullptr) fail(LFG_ERR_INVALID, "sample has no payload");
     if (s.src_kind != LFG_SRC_DEVICE && s.src_kind != LFG_SRC_HOST_PINNED)
         fail(LFG_ERR_INVALID, "bad src_kind");
-    Ticket t;
-    t.id = s.id;
-    t.desc = s;
     if (c->fam == FAM_IMG3D) {
         if (s.ndim != 3 || s.aux == nullptr) fail(LFG_ERR_INVALID, "img_seg sample needs a D,H,W volume and a label");
         for (int a = 0; a < 3; ++a)
@@ -622,35 +627,45 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
             }
         }
     }
+    for (int k = 0; k < c->n_spin; ++k)
+        if (s.spin_us[k] < 0) fail(LFG_ERR_STATE, "negative transform cost");  // balancer.cpp:16
     PreDraw local;
     if (pre == nullptr) {
         draw_params(*c, cfg.seed, s, local);
         pre = &local;
     }
-    t.p3 = pre->p3;
-    t.p2 = pre->p2;
-    t.ps = pre->ps;
-    for (int k = 0; k < c->n_spin; ++k)
-        if (s.spin_us[k] < 0) fail(LFG_ERR_STATE, "negative transform cost");  // balancer.cpp:16
-    assign_slot(t, c);
+    // the ticket is built in place (submit runs once per sample)
+    const int64_t ti = static_cast<int64_t>(tickets.size());
+    tickets.emplace_back();
+    Ticket& t = tickets.back();
+    t.id = s.id;
+    t.desc = s;
+    if (c->fam == FAM_IMG3D) t.p3 = pre->p3;
+    else if (c->fam == FAM_RRC2D) t.p2 = pre->p2;
+    else t.ps = pre->ps;
+    try {
+        assign_slot(t, c);
+    } catch (...) {
+        tickets.pop_back();
+        throw;
+    }
     auto& og = open_group_[s.src_kind == LFG_SRC_DEVICE ? 0 : 1];
     auto it = og.find(c);
     int64_t gi;
     if (it == og.end()) {
-        Group g;
-        g.id = static_cast<int64_t>(groups.size());
-        g.chain = c;
-        g.src_kind = s.src_kind;
-        groups.push_back(std::move(g));
-        gi = static_cast<int64_t>(groups.size()) - 1;
+        gi = static_cast<int64_t>(groups.size());
+        groups.emplace_back();
+        Group& ng = groups.back();
+        ng.id = gi;
+        ng.chain = c;
+        ng.src_kind = s.src_kind;
+        ng.tickets.reserve(static_cast<size_t>(std::max(1, cfg.max_group)));
         og[c] = gi;
     } else {
         gi = it->second;
     }
-    const int64_t ti = static_cast<int64_t>(tickets.size());
     t.group = gi;
     t.idx = static_cast<int>(groups[gi].tickets.size());
-    tickets.push_back(t);
     Group& g = groups[gi];
     g.tickets.push_back(ti);
     g.refs++;
@@ -728,6 +743,7 @@ void Context::time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* me
 }
 
 void Context::launch_group(Group& g) {
+    const auto t_enter = std::chrono::steady_clock::now();
     const Chain& c = *g.chain;
     g.stream_idx = get_stream();
     g.stream = streams_[g.stream_idx];
@@ -841,6 +857,15 @@ void Context::launch_group(Group& g) {
             Img3dLaunch L{};
             for (int a = 0; a < 3; ++a) L.crop[a] = c.crop[a];
             L.n = n;
+            // TMA tile path: HBM-resident volumes with 16-B aligned rows
+            bool tma = !staged && img3d_tma_;
+            for (int i = 0; i < n && tma; ++i) {
+                const lfg_sample_desc& sd = tickets[g.tickets[i]].desc;
+                tma = img3d_tma_ok(sd.data, sd.aux, sd.dims, c.crop) &&
+                      img3d_encode_maps(L, i, sd.data, sd.aux, sd.dims) == cudaSuccess;
+            }
+            L.tma = tma ? 1 : 0;
+            const auto t_l = std::chrono::steady_clock::now();
             for (int i = 0; i < n; ++i) {
                 Ticket& t = tickets[g.tickets[i]];
                 const View& v = views[i];
@@ -871,6 +896,7 @@ void Context::launch_group(Group& g) {
                 counters.kernel_bytes += c.algo_bytes_per_sample(t.desc);
             }
             cuda_check(launch_img3d(L, st), "img3d launch");
+            prof_launch_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_l).count();
             counters.launches++;
         } else if (S.kind == ST_RRC2D) {
             RrcLaunch L{};
@@ -896,7 +922,9 @@ void Context::launch_group(Group& g) {
                 d.flip = t.p2.flip;
                 counters.kernel_bytes += rrc_algo_bytes(c, t.p2);
             }
+            const auto t_l = std::chrono::steady_clock::now();
             cuda_check(launch_rrc2d(L, st), "rrc2d launch");
+            prof_launch_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_l).count();
             counters.launches++;
         } else {
             SpLaunch L{};
@@ -931,6 +959,7 @@ void Context::launch_group(Group& g) {
     }
     g.launched = true;
     g.t_launch_us = host_now_us();
+    prof_group_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_enter).count();
 }
 
 // ------------------------------------------------------------------ progress
@@ -1058,9 +1087,16 @@ int64_t Context::seal(const int64_t* ts, int n) {
         if (g.chain != c) fail(LFG_ERR_INVALID, "batch mixes chains");
         if (t.buf != tickets[ts[0]].buf) same_buf = false;
     }
-    for (int i = 0; i < n; ++i)
-        for (int j = i + 1; j < n; ++j)
-            if (ts[i] == ts[j]) fail(LFG_ERR_INVALID, "duplicate ticket in batch");
+    // duplicate check in O(n): mark, test, unmark
+    for (int i = 0; i < n; ++i) {
+        Ticket& t = tickets[ts[i]];
+        if (t.in_seal) {
+            for (int j = 0; j < i; ++j) tickets[ts[j]].in_seal = false;
+            fail(LFG_ERR_INVALID, "duplicate ticket in batch");
+        }
+        t.in_seal = true;
+    }
+    for (int i = 0; i < n; ++i) tickets[ts[i]].in_seal = false;
     const int b0 = tickets[ts[0]].buf;
     // speech batches are time-major (PermuteAudio), so they are always collated
     const bool in_place = c->fam != FAM_SPEECH && same_buf && bufs_[b0].assigned == n &&
@@ -1139,8 +1175,12 @@ int64_t Context::seal(const int64_t* ts, int n) {
         for (int i = 0; i < n; ++i) bufs_[tickets[ts[i]].buf].live--;
         counters.gathered_batches++;
     }
-    br.ready = get_event();
-    cuda_check(cudaEventRecord(br.ready, seal_stream), "record batch ready");
+    // An in-place batch is ready the moment it is sealed: every producing group
+    // was seen complete above, so there is nothing for a consumer stream to wait on.
+    if (!in_place) {
+        br.ready = get_event();
+        cuda_check(cudaEventRecord(br.ready, seal_stream), "record batch ready");
+    }
     for (int i = 0; i < n; ++i) {
         Ticket& t = tickets[ts[i]];
         t.consumed = true;
@@ -1158,19 +1198,25 @@ BatchRec& Context::batch(int64_t b) {
 }
 
 void Context::batch_wait_stream(int64_t b, cudaStream_t s) {
-    cuda_check(cudaStreamWaitEvent(s, batch(b).ready, 0), "batch wait");
+    BatchRec& br = batch(b);
+    if (br.ready) cuda_check(cudaStreamWaitEvent(s, br.ready, 0), "batch wait");
 }
 
-void Context::batch_release(int64_t b, cudaStream_t s) {
+// `readers`: work that reads the batch may still be queued on `s`, so the
+// buffer is reused only after an event recorded there; the shard runner
+// passes false when it enqueued nothing for the batch.
+void Context::batch_release(int64_t b, cudaStream_t s, bool readers) {
     BatchRec& br = batch(b);
     SlotBuf& buf = bufs_[br.buf];
-    cudaEvent_t e = get_event();
-    cuda_check(cudaEventRecord(e, s), "record batch release");
-    buf.pending.push_back(e);
+    if (readers) {
+        cudaEvent_t e = get_event();
+        cuda_check(cudaEventRecord(e, s), "record batch release");
+        buf.pending.push_back(e);
+    }
     buf.in_batch = false;
     if (br.in_place) buf.live -= br.n;
     br.released = true;
-    put_event(br.ready);
+    if (br.ready) put_event(br.ready);
     br.ready = nullptr;
 }
 

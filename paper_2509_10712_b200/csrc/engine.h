@@ -39,6 +39,36 @@ void cuda_check(cudaError_t e, const char* what);
 
 int64_t host_now_us();
 
+// Chain-keyed map for the submit path: a context holds a handful of chains,
+// so a linear scan of a small vector beats hashing (submit runs per sample).
+struct Chain;
+template <class V>
+struct SmallMap {
+    using Item = std::pair<const Chain*, V>;
+    std::vector<Item> v;
+    using iterator = typename std::vector<Item>::iterator;
+    iterator begin() { return v.begin(); }
+    iterator end() { return v.end(); }
+    iterator find(const Chain* k) {
+        for (auto it = v.begin(); it != v.end(); ++it)
+            if (it->first == k) return it;
+        return v.end();
+    }
+    V& operator[](const Chain* k) {
+        auto it = find(k);
+        if (it != v.end()) return it->second;
+        v.emplace_back(k, V{});
+        return v.back().second;
+    }
+    void erase(iterator it) { v.erase(it); }
+    void erase(const Chain* k) {
+        auto it = find(k);
+        if (it != v.end()) v.erase(it);
+    }
+    size_t size() const { return v.size(); }
+    void clear() { v.clear(); }
+};
+
 struct Stage {
     int kind;
     int first_op, last_op;   // ops [first, last) covered by this stage
@@ -132,6 +162,7 @@ struct Ticket {
     ParamsSp ps{};
     bool released = false;
     bool consumed = false;   // sealed into a batch
+    bool in_seal = false;    // scratch mark for seal's duplicate check
 };
 
 struct BatchRec {
@@ -169,7 +200,7 @@ public:
     int64_t seal(const int64_t* tickets, int n);
     BatchRec& batch(int64_t b);
     void batch_wait_stream(int64_t b, cudaStream_t s);
-    void batch_release(int64_t b, cudaStream_t s);
+    void batch_release(int64_t b, cudaStream_t s, bool readers = true);
     void trainer_step(int64_t b, cudaStream_t s, int64_t us);
     // samples assigned to slot buffer bi once it stopped accepting new ones; -1 otherwise
     int buf_closed_count(int bi) const {
@@ -190,6 +221,7 @@ public:
     static constexpr int kStreamPool = 28;
     int free_stream_count() const { return static_cast<int>(free_streams_.size()); }
     lfg_counters counters{};
+    double prof_group_ns = 0, prof_launch_ns = 0;   // host time in launch_group / kernel launch calls
     bool serial = false;
     bool defer_launch = false;
     void time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms, int64_t* launches,
@@ -206,15 +238,17 @@ public:
 private:
     std::vector<std::unique_ptr<Chain>> chains_;
     SpeechTables* speech_ = nullptr;   // DFT basis + mel tables, created with the first speech chain
+    bool img3d_tma_ = true;            // LFG_IMG3D_TMA=0 forces the row kernel (A/B checks)
     std::vector<cudaStream_t> streams_;
     std::vector<int> free_streams_;
     std::vector<cudaEvent_t> free_events_;
     std::vector<SlotBuf> bufs_;
+    size_t alloc_cursor_[2] = {0, 0};   // [for_batch] last buffer handed out
     std::vector<RawBuf> raws_;
     std::vector<int64_t> free_raws_;
-    std::unordered_map<const Chain*, int> open_buf_;     // chain -> open slot buffer
-    std::vector<int64_t> deferred_;                      // full groups awaiting launch (timing mode)
-    std::unordered_map<const Chain*, int64_t> open_group_[2];  // [src_kind] chain -> group
+    SmallMap<int> open_buf_;                 // chain -> open slot buffer
+    std::vector<int64_t> deferred_;          // full groups awaiting launch (timing mode)
+    SmallMap<int64_t> open_group_[2];        // [src_kind] chain -> group
 
     cudaEvent_t get_event();
     void put_event(cudaEvent_t e);

@@ -18,6 +18,12 @@
 // Image and label stores are 16-B / 4-B streaming stores.  GaussianNoise draws
 // one Philox4x32-10 block per 4 output voxels, so noise-on samples are
 // ALU-bound; noise-off samples are HBM-bound.
+//
+// HBM-resident volumes with 16-B aligned rows take the TMA tile path instead
+// (img3d_tma_kernel below); the row kernel serves K0-staged windows (skewed
+// rows) and unaligned geometries.
+#include <algorithm>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -121,10 +127,199 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
     }
 }
 
+// ------------------------------------------------------------------ TMA tile path
+// HBM-resident volumes whose rows are 16-B aligned (W % 16 == 0) take this
+// path.  A tile is kImg3dTileRows output rows of one z-slice of one sample; the
+// crop window's rows for it are one 3-D TMA box ((cw + 16) x 16 x 1) of the source
+// volume -- the copy engine handles the arbitrary crop offset and zero-fills
+// boxes hanging over the volume's edge (RandomCrop's padding), so the threads
+// issue no global loads and no address arithmetic.  Persistent CTAs: one
+// producer warp streams tiles into a kTmaStages-deep shared-memory ring;
+// 8 consumer warps read each row (flip = reversed row / quad order), apply
+// brightness + noise, and write the output with 16-B streaming stores.
+constexpr int kTR = kImg3dTileRows;
+constexpr int kTmaStages = 6;
+constexpr int kTmaWarps = 8;                       // consumer warps
+constexpr int kTmaThreads = 32 * (kTmaWarps + 1);  // + producer warp
+constexpr int kTmaHdr = 128;                       // barriers, then 128-B aligned tiles
+
+// The box starts at the crop column rounded down to 16 elements (a box whose
+// first byte is not 16-B aligned faults on sm_100a) and is cw + 16 wide; the
+// consumers realign by the warp-uniform remainder off[2] & 15.
+constexpr int kTmaPad = 16;
+__host__ __device__ inline int tma_smem_bytes(int cw) {
+    return kTmaHdr + kTmaStages * kTR * (cw + kTmaPad) * 5;
+}
+
+__device__ __forceinline__ void tile_of(int t, int cd, int nyb, int& i, int& z, int& y0) {
+    const int per = cd * nyb;
+    i = t / per;
+    const int r = t - i * per;
+    z = r / nyb;
+    y0 = (r - z * nyb) * kTR;
+}
+
+__global__ void __launch_bounds__(kTmaThreads)
+img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int cd = L.crop[0], ch = L.crop[1], cw = L.crop[2];
+    const int nyb = (ch + kTR - 1) / kTR;
+    const int total = L.n * cd * nyb;
+    const int bw = cw + kTmaPad;   // box / smem row width in elements
+    const uint32_t img_bytes = kTR * bw * 4, stage_bytes = kTR * bw * 5;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kTmaStages;
+    uint8_t* tiles = smem + kTmaHdr;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kTmaWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTmaWarps) {   // producer
+        if (lane == 0) {
+            int k = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++k) {
+                const int s = k % kTmaStages, use = k / kTmaStages;
+                if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
+                int i, z, y0;
+                tile_of(t, cd, nyb, i, z, y0);
+                const Img3dDesc& d = L.d[i];
+                const int fz = (d.flip & 1) ? cd - 1 - z : z;
+                const int fy0 = (d.flip & 2) ? ch - kTR - y0 : y0;   // may be < 0: zero rows, never stored
+                uint8_t* st = tiles + s * stage_bytes;
+                mbar_expect_tx(full + s, stage_bytes);
+                const int x0 = d.off[2] & ~(kTmaPad - 1);
+                tma_load_3d(st, &L.tm_img[i], x0, d.off[1] + fy0, d.off[0] + fz, full + s);
+                tma_load_3d(st + img_bytes, &L.tm_lbl[i], x0, d.off[1] + fy0, d.off[0] + fz, full + s);
+            }
+        }
+        return;
+    }
+
+    const int cw4 = cw >> 2;
+    int k = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++k) {
+        const int s = k % kTmaStages, use = k / kTmaStages;
+        int i, z, y0;
+        tile_of(t, cd, nyb, i, z, y0);
+        const Img3dDesc& d = L.d[i];
+        const bool flip_y = (d.flip & 2) != 0, flip_w = (d.flip & 4) != 0;
+        const bool noise = d.sigma != 0.0f;
+        mbar_wait(full + s, use & 1);
+        const float4* simg = reinterpret_cast<const float4*>(tiles + s * stage_bytes);
+        const uint32_t* slbl = reinterpret_cast<const uint32_t*>(tiles + s * stage_bytes + img_bytes);
+        const int e0 = d.off[2] & (kTmaPad - 1);   // crop column 0 inside the box row
+        const int m = e0 & 3, w0 = e0 >> 2;        // warp-uniform realignment
+        const int bw4 = bw >> 2;
+        for (int r = warp; r < kTR; r += kTmaWarps) {
+            const int y = y0 + r;
+            if (y >= ch) break;
+            const int sr = flip_y ? kTR - 1 - r : r;
+            for (int qx = lane; qx < cw4; qx += 32) {
+                const int qs = flip_w ? cw4 - 1 - qx : qx;
+                const int w = sr * bw4 + w0 + qs;
+                float4 x = simg[w];
+                uint32_t lb = slbl[w];
+                if (m != 0) {
+                    x = shift4(x, simg[w + 1], m);
+                    lb = __funnelshift_r(lb, slbl[w + 1], 8 * m);
+                }
+                if (flip_w) {
+                    x = make_float4(x.w, x.z, x.y, x.x);
+                    lb = __byte_perm(lb, 0, 0x0123);
+                }
+                const int64_t vox = ((int64_t)z * ch + y) * cw + 4 * qx;
+                float o[4] = {x.x * d.scale, x.y * d.scale, x.z * d.scale, x.w * d.scale};
+                if (noise) {
+                    const uint64_t g = (uint64_t)vox >> 2;
+                    const uint4 rnd = philox4x32_10(
+                        make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, 0u), d.key0, d.key1);
+                    const float2 z01 = box_muller(rnd.x, rnd.y);
+                    const float2 z23 = box_muller(rnd.z, rnd.w);
+                    o[0] = fmaf(d.sigma, z01.x, o[0]);
+                    o[1] = fmaf(d.sigma, z01.y, o[1]);
+                    o[2] = fmaf(d.sigma, z23.x, o[2]);
+                    o[3] = fmaf(d.sigma, z23.y, o[3]);
+                }
+                __stcs(reinterpret_cast<float4*>(d.out_img + vox), make_float4(o[0], o[1], o[2], o[3]));
+                __stcs(reinterpret_cast<unsigned int*>(d.out_lbl + vox), lb);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
 }  // namespace
+
+cudaError_t img3d_encode_maps(Img3dLaunch& L, int i, const void* img, const void* lbl, const int64_t dims[3]) {
+    EncodeTiledFn fn = encode_fn();
+    if (fn == nullptr) return cudaErrorNotSupported;
+    const cuuint64_t gdim[3] = {(cuuint64_t)dims[2], (cuuint64_t)dims[1], (cuuint64_t)dims[0]};
+    const cuuint32_t box[3] = {(cuuint32_t)(L.crop[2] + kTmaPad), (cuuint32_t)kTR, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint64_t si[2] = {(cuuint64_t)dims[2] * 4, (cuuint64_t)(dims[1] * dims[2]) * 4};
+    const cuuint64_t sl[2] = {(cuuint64_t)dims[2], (cuuint64_t)(dims[1] * dims[2])};
+    CUresult r = fn(&L.tm_img[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(img), gdim, si, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    r = fn(&L.tm_lbl[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(lbl), gdim, sl, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 
 cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s) {
     if (L.n <= 0) return cudaSuccess;
+    if (L.tma) {
+        const int cw = L.crop[2];
+        if (cw % 16 != 0 || cw > 240) return cudaErrorInvalidValue;
+        const int smem = tma_smem_bytes(cw);
+        static int occ[17] = {0};   // per cw / 16: resident CTAs per SM
+        int& o = occ[cw / 16];
+        if (o == 0) {
+            int v = 0;
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, img3d_tma_kernel, kTmaThreads, smem);
+            if (e != cudaSuccess) return e;
+            o = v > 0 ? v : 1;
+        }
+        const int64_t total = int64_t(L.n) * L.crop[0] * ((L.crop[1] + kTR - 1) / kTR);
+        const int grid = static_cast<int>(std::min<int64_t>(total, int64_t(sm_count()) * o));
+        img3d_tma_kernel<<<grid, kTmaThreads, smem, s>>>(L);
+        return cudaGetLastError();
+    }
     dim3 grid((L.crop[1] + kRowsPerCta - 1) / kRowsPerCta, L.crop[0], L.n);
     dim3 block(32, kRowsY);
     img3d_kernel<<<grid, block, 0, s>>>(L);
@@ -133,7 +328,13 @@ cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s) {
 
 cudaError_t warm_img3d() {
     cudaFuncAttributes a;
-    return cudaFuncGetAttributes(&a, img3d_kernel);
+    cudaError_t e = cudaFuncGetAttributes(&a, img3d_kernel);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(img3d_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem_bytes(240));
+    if (e != cudaSuccess) return e;
+    sm_count();
+    encode_fn();
+    return cudaFuncGetAttributes(&a, img3d_tma_kernel);
 }
 
 }  // namespace lfg

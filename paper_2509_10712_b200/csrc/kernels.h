@@ -5,12 +5,13 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace lfg {
 
 constexpr int kMax3D = 16;   // img_seg samples per launch group
-constexpr int kMax2D = 64;   // obj_det samples per launch group
+constexpr int kMax2D = 256;  // obj_det samples per launch group
 constexpr int kMaxSp = 64;   // speech utterances per launch group
 constexpr int kMaxSpin = 64;
 constexpr int kMaxGather = 256;
@@ -31,10 +32,12 @@ struct StageDesc {
     int32_t row_bytes, ny, nz;
     int32_t pad;
 };
+constexpr int kMaxStage = 256;   // boxes per K0 launch (>= kMax2D, 2 * kMax3D)
 struct StageLaunch {
     int32_t n;
-    StageDesc d[2 * 64];
+    StageDesc d[kMaxStage];
 };
+static_assert(kMaxStage >= 2 * 16 && kMaxStage >= 256, "K0 must hold a whole launch group");
 
 // ---- K1: RandomCrop + RandomFlip + RandomBrightness + GaussianNoise + Cast
 struct Img3dDesc {
@@ -56,8 +59,21 @@ struct Img3dDesc {
 struct Img3dLaunch {
     int32_t crop[3];
     int32_t n;
+    int32_t tma;             // 1: every sample has tm_img/tm_lbl (TMA tile path)
     Img3dDesc d[kMax3D];
+    // TMA path: 3-D tiled maps over the whole source volume (dims W, H, D),
+    // box (cw + 16, kImg3dTileRows, 1); out-of-bounds boxes fill zeros, which is
+    // exactly RandomCrop's zero padding.
+    CUtensorMap tm_img[kMax3D];
+    CUtensorMap tm_lbl[kMax3D];
 };
+constexpr int kImg3dTileRows = 16;
+// TMA path preconditions on the sample / crop geometry (else the row kernel runs)
+inline bool img3d_tma_ok(const void* img, const void* lbl, const int64_t dims[3], const int crop[3]) {
+    return (reinterpret_cast<uintptr_t>(img) & 15) == 0 && (reinterpret_cast<uintptr_t>(lbl) & 15) == 0 &&
+           dims[2] % 16 == 0 && crop[2] % 16 == 0 && crop[2] <= 240 && dims[0] < (int64_t(1) << 31) &&
+           dims[1] < (int64_t(1) << 31) && dims[2] < (int64_t(1) << 31);
+}
 
 // ---- K3: RandomResizedCrop (bilinear) + RandomHorizontalFlip + ToTensor + Normalize
 struct RrcDesc {
@@ -123,6 +139,9 @@ struct GatherLaunch {
 
 cudaError_t launch_stage(const StageLaunch& L, cudaStream_t s);
 cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s);
+// encodes L.tm_img[i] / L.tm_lbl[i] for a D,H,W f32 volume + u8 label (see img3d_tma_ok)
+cudaError_t img3d_encode_maps(Img3dLaunch& L, int i, const void* img, const void* lbl,
+                              const int64_t dims[3]);
 cudaError_t launch_rrc2d(const RrcLaunch& L, cudaStream_t s);
 cudaError_t launch_spin(const SpinLaunch& L, cudaStream_t s);
 cudaError_t launch_gather(const GatherLaunch& L, cudaStream_t s);

@@ -21,7 +21,10 @@
 //                  de-escalation on a full window below 0.15 (profiler.cpp:47-72)
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <deque>
 #include <thread>
@@ -61,6 +64,35 @@ struct Profile {
         size_t rank = static_cast<size_t>(std::ceil(pct / 100.0 * double(totals.size())));
         if (rank == 0) rank = 1;
         return totals[rank - 1];
+    }
+};
+
+// Host-loop phase clock (LFG_SHARD_PROF=1 prints the split to stderr): the
+// resident-input rate is bounded by this loop, so its cost is kept visible.
+struct Phases {
+    enum { POLL, PARKED, SUBMIT, FLUSH, SEAL, DELIVER, IDLE, DRAW, N };
+    bool on = std::getenv("LFG_SHARD_PROF") != nullptr;
+    double ns[N] = {};
+    std::chrono::steady_clock::time_point t;
+    void start() {
+        if (on) t = std::chrono::steady_clock::now();
+    }
+    void lap(int k) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        ns[k] += std::chrono::duration<double, std::nano>(now - t).count();
+        t = now;
+    }
+    void print(int64_t n, double group_ns, double launch_ns, int64_t groups) const {
+        if (!on || n <= 0) return;
+        static const char* names[N] = {"poll", "parked", "submit", "flush", "seal", "deliver", "idle",
+                                       "draw_wait"};
+        std::fprintf(stderr, "[lfg shard] ns/sample:");
+        for (int k = 0; k < N; ++k) std::fprintf(stderr, " %s=%.0f", names[k], ns[k] / double(n));
+        std::fprintf(stderr, " | per group (%lld): launch_group=%.0f kernel_launch=%.0f ns\n",
+                     static_cast<long long>(groups),
+                     group_ns / double(std::max<int64_t>(groups, 1)),
+                     launch_ns / double(std::max<int64_t>(groups, 1)));
     }
 };
 
@@ -109,8 +141,29 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     int64_t last_update = run_t0;
 
     const int64_t tbase = static_cast<int64_t>(ctx.tickets.size());
+    ctx.tickets.reserve(static_cast<size_t>(tbase + n));
+    ctx.groups.reserve(ctx.groups.size() + static_cast<size_t>(n));
     std::vector<int64_t> inflight, parked;
     std::deque<int64_t> fast, slow;
+    // Zero-copy bookkeeping: fast_cnt[buf] = tickets of slot buffer `buf` in
+    // `fast`; full_bufs = buffers whose every sample is in `fast` (candidates
+    // for an in-place seal).  Maintained incrementally so the batcher never
+    // rescans the fast list.
+    std::vector<int> fast_cnt;
+    std::deque<int> full_bufs;
+    auto fast_add = [&](int64_t t, bool front) {
+        const int b = ctx.tickets[t].buf;
+        if (b >= static_cast<int>(fast_cnt.size())) fast_cnt.resize(static_cast<size_t>(b) + 1, 0);
+        if (front) fast.push_front(t);
+        else fast.push_back(t);
+        if (++fast_cnt[b] == B && ctx.buf_closed_count(b) == B) full_bufs.push_back(b);
+    };
+    auto fast_take = [&]() {
+        const int64_t t = fast.front();
+        fast.pop_front();
+        --fast_cnt[ctx.tickets[t].buf];
+        return t;
+    };
     int64_t fed = 0, consumed = 0, nbatches = 0, timed_samples = 0;
     std::vector<uint64_t> all_ids;
     all_ids.reserve(static_cast<size_t>(n));
@@ -161,24 +214,42 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         }
     } joiner{drawers, stop_draw};
 
+    Phases ph;
+    const double g_ns0 = ctx.prof_group_ns, l_ns0 = ctx.prof_launch_ns;
+    const size_t groups0 = ctx.groups.size();
+    constexpr int64_t kScanUs = 10;
+    int64_t last_scan_us = 0;
+    ph.start();
     while (consumed < n) {
         bool progressed = false;
         const int64_t now = host_now_us();
 
-        // (1) in-flight groups: finished in budget -> fast; over budget -> slow (parked)
+        // (1) in-flight groups: finished in budget -> fast; over budget -> slow (parked).
+        // An event query costs ~0.5 us with 32 hardware queues, so the groups are
+        // queried in launch order up to the first unfinished one, and all of them
+        // only every kScanUs (out-of-order finishers are picked up within that);
+        // a group is always queried before it is parked for its timeout.
+        const bool full_scan = now - last_scan_us >= kScanUs;
+        if (full_scan) last_scan_us = now;
+        bool query = true;
         for (size_t k = 0; k < inflight.size();) {
             Group& g = ctx.groups[inflight[k]];
-            const bool done = ctx.poll_group(g);
+            const bool over = now - g.t_launch_us > t_out;
+            const bool done = (query || full_scan || over) && ctx.poll_group(g);
+            if (!done) query = false;
             bool remove = false;
             if (done) {
                 const int64_t dev_us = total_us(g);
                 const bool is_slow = dev_us > t_out;   // inclusive budget, balancer.cpp:17
                 classify(g, is_slow);
-                for (int64_t t : g.tickets) (is_slow ? slow : fast).push_back(t);
+                for (int64_t t : g.tickets) {
+                    if (is_slow) slow.push_back(t);
+                    else fast_add(t, false);
+                }
                 prof.record(dev_us, is_slow);
                 if (nbatches >= rc.warmup_batches) kernel_ms += dev_us / 1000.0;
                 remove = true;
-            } else if (now - g.t_launch_us > t_out) {
+            } else if (over) {
                 classify(g, true);
                 parked.push_back(inflight[k]);
                 remove = true;
@@ -190,8 +261,9 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 ++k;
             }
         }
+        ph.lap(Phases::POLL);
         // (2) parked (slow) groups finishing in the background -> slow list
-        for (size_t k = 0; k < parked.size();) {
+        for (size_t k = 0; k < parked.size() && full_scan;) {
             Group& g = ctx.groups[parked[k]];
             if (ctx.poll_group(g)) {
                 for (int64_t t : g.tickets) slow.push_back(t);
@@ -202,6 +274,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 ++k;
             }
         }
+        ph.lap(Phases::PARKED);
         // (3) feed new samples while a worker (stream) is free
         while (static_cast<int>(inflight.size()) < n_workers && fed < n &&
                (ctx.serial || ctx.free_stream_count() > 0)) {
@@ -211,15 +284,21 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             try {
                 for (; got < take; ++got) {
                     const int64_t i = fed + got;
-                    while (!ready[i / kChunk].load(std::memory_order_acquire)) std::this_thread::yield();
+                    if (!ready[i / kChunk].load(std::memory_order_acquire)) {
+                        ph.lap(Phases::SUBMIT);
+                        while (!ready[i / kChunk].load(std::memory_order_acquire)) std::this_thread::yield();
+                        ph.lap(Phases::DRAW);
+                    }
                     const int64_t t = ctx.submit(chain, samples[i], &pre[i]);
                     gid = ctx.tickets[t].group;
                 }
             } catch (const Error& e) {
                 if (e.code != LFG_ERR_AGAIN) throw;
             }
+            ph.lap(Phases::SUBMIT);
             if (got == 0) break;
             ctx.flush();
+            ph.lap(Phases::FLUSH);
             fed += got;
             inflight.push_back(gid);
             progressed = true;
@@ -236,16 +315,18 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             // in the fast list, seal exactly those (the buffer becomes the batch).
             // Eagerness is unchanged -- a batch is sealed whenever B samples are
             // ready -- only its membership is chosen to avoid the gather copy.
-            if (k == B && static_cast<int64_t>(fast.size()) >= B) {
-                std::unordered_map<int, int> per_buf;
-                for (int64_t t : fast) per_buf[ctx.tickets[t].buf]++;
-                int pick = -1;
-                for (auto& kv : per_buf)
-                    if (kv.second == B && ctx.buf_closed_count(kv.first) == B) {
-                        pick = kv.first;
-                        break;
-                    }
-                if (pick >= 0) {
+            while (!full_bufs.empty() && (fast_cnt[full_bufs.front()] != B ||
+                                          ctx.buf_closed_count(full_bufs.front()) != B))
+                full_bufs.pop_front();   // stale candidate
+            if (k == B && !full_bufs.empty()) {
+                const int pick = full_bufs.front();
+                full_bufs.pop_front();
+                bool at_front = true;   // common case: the buffer's samples lead the fast list
+                for (int64_t i = 0; i < B && at_front; ++i)
+                    at_front = ctx.tickets[fast[static_cast<size_t>(i)]].buf == pick;
+                if (at_front) {
+                    for (int64_t i = 0; i < B; ++i) ts.push_back(fast_take());
+                } else {
                     for (auto it = fast.begin(); it != fast.end();) {
                         if (ctx.tickets[*it].buf == pick) {
                             ts.push_back(*it);
@@ -254,12 +335,12 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                             ++it;
                         }
                     }
+                    fast_cnt[pick] = 0;
                 }
             }
             for (int64_t i = static_cast<int64_t>(ts.size()); i < k; ++i) {
                 if (!fast.empty()) {
-                    ts.push_back(fast.front());
-                    fast.pop_front();
+                    ts.push_back(fast_take());
                 } else {
                     ts.push_back(slow.front());
                     slow.pop_front();
@@ -268,11 +349,14 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             int64_t b;
             try {
                 b = ctx.seal(ts.data(), static_cast<int>(k));
+                ph.lap(Phases::SEAL);
             } catch (const Error& e) {
+                ph.lap(Phases::SEAL);
                 if (e.code != LFG_ERR_AGAIN) throw;
                 for (auto it = ts.rbegin(); it != ts.rend(); ++it) {
                     const int cls = sample_class ? sample_class[*it - tbase] : 1;
-                    (cls == 2 ? slow : fast).push_front(*it);
+                    if (cls == 2) slow.push_front(*it);
+                    else fast_add(*it, true);
                 }
                 break;
             }
@@ -285,7 +369,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 ctx.trainer_step(b, trainer, rc.trainer_us);
                 cuda_check(cudaEventRecord(s1, trainer), "record");
                 steps.emplace_back(s0, s1);
-            } else {
+            } else if (rc.trainer_us > 0 || probe) {
                 ctx.trainer_step(b, trainer, rc.trainer_us);
             }
             if (probe) {
@@ -304,7 +388,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             }
             if (batch_sizes) batch_sizes[nbatches] = br.n;
             if (timed) timed_samples += br.n;
-            ctx.batch_release(b, trainer);
+            ctx.batch_release(b, trainer, rc.trainer_us > 0 || probe != nullptr);
             for (int64_t t : ts) ctx.ticket_release(t);
             ++nbatches;
             if (nbatches == rc.warmup_batches) {
@@ -312,6 +396,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 cuda_check(cudaEventRecord(t_timed, trainer), "record");
             }
             progressed = true;
+            ph.lap(Phases::DELIVER);
         }
         // (5) profiler maintenance (profiler_loop, profiler.cpp:108-121)
         if (rc.policy == 1 && !prof.window.empty() && now - run_t0 >= rc.warmup_us &&
@@ -324,7 +409,10 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 fail(LFG_ERR_STATE, "shard stalled with samples unaccounted for");
             std::this_thread::yield();
         }
+        ph.lap(Phases::IDLE);
     }
+    ph.print(n, ctx.prof_group_ns - g_ns0, ctx.prof_launch_ns - l_ns0,
+             static_cast<int64_t>(ctx.groups.size() - groups0));
     cudaEvent_t t_end = mk();
     cuda_check(cudaEventRecord(t_end, trainer), "record");
     cuda_check(cudaEventSynchronize(t_end), "sync");

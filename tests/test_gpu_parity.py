@@ -55,6 +55,11 @@ CASES_3D = [
     ((12, 30, 20), (16, 16, 32), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),  # zero padding
     ((16, 16, 32), (16, 16, 32), dict(p_flip=1.0, p_bright=0.0, p_noise=1.0)),  # exact fit
     ((136, 140, 150), (128, 128, 128), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),
+    # W % 16 == 0: device-resident samples take the TMA tile path
+    ((20, 24, 48), (16, 16, 32), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),   # x offset
+    ((12, 30, 16), (16, 16, 32), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),   # zero padding (TMA OOB)
+    ((24, 26, 64), (10, 20, 48), dict(p_flip=1.0, p_bright=0.0, p_noise=0.0)),   # partial tile + flips
+    ((136, 140, 160), (128, 128, 128), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),
 ]
 
 
