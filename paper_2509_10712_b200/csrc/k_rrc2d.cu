@@ -12,15 +12,19 @@
 //
 // Mapping: grid (ceil(oh / kRows), n_samples), 128 threads.  A CTA owns kRows
 // output rows of one sample:
-//   1. the source rows those outputs touch (<= (kRows-1)*h/oh + 3) are copied
-//      from HBM into shared memory with aligned 16-byte loads (a warp per row);
-//      row taps are computed once per CTA and packed into one 16-B record;
-//   2. each thread owns TWO output columns (x and x + ow/2), so the per-row
-//      bookkeeping is shared by two pixels; it reads each horizontal tap pair
-//      (6 bytes per source row) with three 32-bit shared loads and two funnel
-//      shifts, converts bytes with PRMT into the 2^23 mantissa (exact), keeps
-//      the horizontally blended rows in a 2-entry cache (consecutive output rows
-//      share source rows), and writes 3 coalesced f32 planes with streaming stores.
+//   1. the source rows those outputs touch (<= (kRows-1)*h/oh + 4) land in
+//      shared memory by cp.async.bulk (one bulk copy per row, the 16-B aligned
+//      superset, all on one mbarrier) while the threads compute their taps; the
+//      row schedule (which source row to blend into which register, vertical
+//      weights with Normalize's scale folded in) is built once per CTA;
+//   2. each thread owns two ADJACENT output columns, carried as the two lanes of
+//      float2 values through Blackwell's paired FP32 instructions (FFMA2 / FMUL2
+//      / FADD2); it reads each horizontal tap pair (6 bytes) with three 32-bit
+//      shared loads and two funnel shifts, converts bytes with PRMT into the 2^23
+//      mantissa (exact), blends each source row once into the register of its
+//      parity (even / odd: the taps y0, y0 + 1 never collide, so no register
+//      moves), and writes 3 planes with 8-byte streaming stores (RandomHorizontal
+//      Flip swaps the lanes' roles, not the data).
 // The per-launch dynamic shared memory is the largest row window of the group
 // (computed on the host with the same formula); crops whose window exceeds the
 // budget (sources taller than ~2.6x oh) fall back to direct L2 byte loads.
@@ -31,7 +35,7 @@ namespace lfg {
 
 namespace {
 
-constexpr int kRows = 8;
+constexpr int kRows = 8;        // 16 measured slower (larger windows cut occupancy)
 constexpr int kThreads = 128;
 constexpr int kMaxSmem = 64 * 1024;
 
@@ -54,151 +58,198 @@ __device__ __forceinline__ const uint8_t* row_ptr(const RrcDesc& d, int y) {
     return d.src + (int64_t)y * d.pitch + ((d.sk0 + y * d.sky) & 15);
 }
 
+// byte offset of staged row y's first pixel: the row sits at (y - ylo) * spitch
+// with its 16-byte alignment phase preserved (only the low 4 address bits matter)
+__device__ __forceinline__ int staged_off(const RrcDesc& d, int y, int ylo, int spitch) {
+    const uint32_t lo = (uint32_t)reinterpret_cast<uintptr_t>(d.src) + (uint32_t)y * (uint32_t)d.pitch +
+                        (uint32_t)((d.sk0 + y * d.sky) & 15);
+    return (y - ylo) * spitch + (int)(lo & 15u);
+}
+
 // exact u8 -> f32: place byte k of w in the low mantissa of 2^23, subtract 2^23
 __device__ __forceinline__ float ubyte(uint32_t w, int k) {
     return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u | (uint32_t)k)) - 8388608.0f;
 }
 
-struct Col {                // one output column's horizontal taps
-    int off;                // byte offset of tap 0 within a source row (3 * x0)
-    bool edge;              // right border: tap 1 == tap 0
-    float w0, w1;
-    int x1;                 // (fallback path only)
+// The two output columns a thread owns (2t, 2t + 1) travel as the .x / .y
+// lanes of float2 values, so the blend runs on Blackwell's paired FP32 units
+// (FFMA2 / FMUL2 / FADD2: two IEEE fp32 results per instruction, each rounded
+// exactly like fmaf / fmul / fadd).
+struct ColPair {
+    int off_a, off_b;       // byte offset of tap 0 within a source row (3 * x0)
+    int x0_a, x0_b;         // (fallback path only)
+    float2 w0, w1;          // tap weights; at the right border tap 1 aliases tap 0,
+                            // folded as w0 = l0 + l1, w1 = 0
 };
 
-__device__ __forceinline__ void blend_row(const uint8_t* smem, int row_off, const Col& c, float h[3]) {
-    const int off = row_off + c.off;
+// bytes k of (wa, wb) -> exact (float, float)
+__device__ __forceinline__ float2 ubyte2(uint32_t wa, uint32_t wb, int k) {
+    const float2 m = make_float2(__uint_as_float(__byte_perm(wa, 0x4B000000u, 0x7650u | (uint32_t)k)),
+                                 __uint_as_float(__byte_perm(wb, 0x4B000000u, 0x7650u | (uint32_t)k)));
+    return __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f));
+}
+
+__device__ __forceinline__ void load6(const uint8_t* smem, int off, uint32_t& lo, uint32_t& hi) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(smem + (off & ~3));
     const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
     const uint32_t sh = (off & 3) * 8;
-    const uint32_t lo = __funnelshift_r(w0, w1, sh);    // bytes 0..3: R0 G0 B0 R1
-    const uint32_t hi = __funnelshift_r(w1, w2, sh);    // bytes 4..7: G1 B1 . .
-    const float r0 = ubyte(lo, 0), g0 = ubyte(lo, 1), b0 = ubyte(lo, 2);
-    const float r1 = c.edge ? r0 : ubyte(lo, 3);
-    const float g1 = c.edge ? g0 : ubyte(hi, 0);
-    const float b1 = c.edge ? b0 : ubyte(hi, 1);
-    h[0] = fmaf(c.w0, r0, c.w1 * r1);
-    h[1] = fmaf(c.w0, g0, c.w1 * g1);
-    h[2] = fmaf(c.w0, b0, c.w1 * b1);
+    lo = __funnelshift_r(w0, w1, sh);    // bytes 0..3: R0 G0 B0 R1
+    hi = __funnelshift_r(w1, w2, sh);    // bytes 4..7: G1 B1 . .
 }
 
-__device__ __forceinline__ void blend_row_l2(const RrcDesc& d, int y, int x0, const Col& c, float h[3]) {
+__device__ __forceinline__ void blend_row(const uint8_t* smem, int row_off, const ColPair& c, float2 h[3]) {
+    uint32_t la, ha, lb, hb;
+    load6(smem, row_off + c.off_a, la, ha);
+    load6(smem, row_off + c.off_b, lb, hb);
+    h[0] = __ffma2_rn(c.w0, ubyte2(la, lb, 0), __fmul2_rn(c.w1, ubyte2(la, lb, 3)));
+    h[1] = __ffma2_rn(c.w0, ubyte2(la, lb, 1), __fmul2_rn(c.w1, ubyte2(ha, hb, 0)));
+    h[2] = __ffma2_rn(c.w0, ubyte2(la, lb, 2), __fmul2_rn(c.w1, ubyte2(ha, hb, 1)));
+}
+
+__device__ __forceinline__ void blend_row_l2(const RrcDesc& d, int y, const ColPair& c, float2 h[3]) {
     const uint8_t* row = row_ptr(d, y);
+    const int x1a = min(c.x0_a + 1, d.w - 1), x1b = min(c.x0_b + 1, d.w - 1);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const float p0 = __ldg(row + 3 * x0 + k), p1 = __ldg(row + 3 * c.x1 + k);
-        h[k] = fmaf(c.w0, p0, c.w1 * p1);
+        const float2 p0 = make_float2(__ldg(row + 3 * c.x0_a + k), __ldg(row + 3 * c.x0_b + k));
+        const float2 p1 = make_float2(__ldg(row + 3 * x1a + k), __ldg(row + 3 * x1b + k));
+        h[k] = __ffma2_rn(c.w0, p0, __fmul2_rn(c.w1, p1));
     }
 }
 
 __global__ void __launch_bounds__(kThreads)
 rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ int row_off[64];          // byte offset of each staged row's first pixel
-    __shared__ int4 taps[kRows];         // {y0, y1, ly0 bits, ly1 bits}
+    __shared__ __align__(8) uint64_t stage_bar;   // staged rows landed
+    // Per output row j: which source rows to blend into the two row registers
+    // (row r always lives in register r & 1 -- the two taps y0, y0 + 1 of a
+    // row never collide) and the vertical weights with Normalize's scale folded
+    // in: out_c = wE_c * E_c + (wO_c * O_c + b_c).
+    __shared__ int2 sched_rows[kRows];            // {even row to load, odd row to load} (-1: kept)
+    __shared__ float sched_w[kRows][6];           // {wE * a_c (c = 0..2), wO * a_c}
+    __shared__ int yspan[2];                      // first / last source row of the CTA
     const RrcDesc& d = L.d[blockIdx.y];
     const int oh = L.oh, ow = L.ow;
     const int y_begin = blockIdx.x * kRows;
     const int n_rows_out = min(kRows, oh - y_begin);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 32) {
+        mbar_init(&stage_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (threadIdx.x < n_rows_out) {
-        int a, b;
-        float l0, l1;
-        src_index(y_begin + threadIdx.x, d.h, __ddiv_rn((double)d.h, (double)oh), a, b, l0, l1);
-        taps[threadIdx.x] = make_int4(a, b, __float_as_int(l0), __float_as_int(l1));
+        const int j = threadIdx.x;
+        const double sy = __ddiv_rn((double)d.h, (double)oh);
+        int y0, y1, p0 = -1, p1 = -1;
+        float l0, l1, q0, q1;
+        src_index(y_begin + j, d.h, sy, y0, y1, l0, l1);
+        if (j > 0) src_index(y_begin + j - 1, d.h, sy, p0, p1, q0, q1);
+        // a row is already in its register iff the previous output row used it
+        // (rows are non-decreasing and adjacent taps differ by at most one)
+        const bool new0 = y0 != p0 && y0 != p1;
+        const bool new1 = y1 != y0 && y1 != p0 && y1 != p1;
+        const bool odd0 = (y0 & 1) != 0;   // y1 (if distinct) has the other parity
+        const int ld_e = odd0 ? (new1 ? y1 : -1) : (new0 ? y0 : -1);
+        const int ld_o = odd0 ? (new0 ? y0 : -1) : (new1 ? y1 : -1);
+        float w_e, w_o;
+        if (y1 == y0) {
+            w_e = odd0 ? 0.f : l0 + l1;
+            w_o = odd0 ? l0 + l1 : 0.f;
+        } else {
+            w_e = odd0 ? l1 : l0;
+            w_o = odd0 ? l0 : l1;
+        }
+        sched_rows[j] = make_int2(ld_e, ld_o);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            sched_w[j][c] = w_e * L.a[c];
+            sched_w[j][3 + c] = w_o * L.a[c];
+        }
+        if (j == 0) yspan[0] = y0;
+        if (j == n_rows_out - 1) yspan[1] = y1;
     }
     __syncthreads();
-    const int ylo = taps[0].x;
-    const int nrows = taps[n_rows_out - 1].y - ylo + 1;
+    const int ylo = yspan[0];
+    const int nrows = yspan[1] - ylo + 1;
     const int row_bytes = d.w * 3;
     const int spitch = ((row_bytes + 30) >> 4) << 4;        // 16-B chunks + alignment phase
-    const bool staged = nrows <= 64 && nrows * spitch <= smem_bytes;
+    const bool staged = nrows * spitch <= smem_bytes;
 
-    // 1. stage the touched source rows (aligned 16-byte superset of each row), a warp per row
-    if (staged) {
-        for (int r = warp; r < nrows; r += kThreads / 32) {
+    // 1. stage the touched source rows (aligned 16-byte superset of each row) with
+    //    bulk async copies: warp 0 issues one cp.async.bulk per row (a lane per row),
+    //    all complete on one mbarrier; the threads meanwhile derive their column taps
+    if (staged && warp == 0) {
+        int bytes = 0;
+        for (int r = lane; r < nrows; r += 32) {
             const uintptr_t s = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
-            const int4* a = reinterpret_cast<const int4*>(s & ~uintptr_t(15));
-            const int nch = (int)((((s + row_bytes + 15) & ~uintptr_t(15)) - (s & ~uintptr_t(15))) >> 4);
-            int4* dst = reinterpret_cast<int4*>(smem + r * spitch);
-            for (int c = lane; c < nch; c += 32) dst[c] = __ldg(a + c);
-            if (lane == 0) row_off[r] = r * spitch + (int)(s & 15);
+            bytes += (int)(((s + row_bytes + 15) & ~uintptr_t(15)) - (s & ~uintptr_t(15)));
         }
-        __syncthreads();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        if (lane == 0) mbar_expect_tx(&stage_bar, (uint32_t)bytes);
+        __syncwarp();
+        for (int r = lane; r < nrows; r += 32) {
+            const uintptr_t s = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
+            const uintptr_t a = s & ~uintptr_t(15);
+            const uint32_t nb = (uint32_t)(((s + row_bytes + 15) & ~uintptr_t(15)) - a);
+            bulk_g2s(smem + r * spitch, reinterpret_cast<const void*>(a), nb, &stage_bar);
+        }
     }
 
-    const int half = ow >> 1;                               // ow is even (checked on the host)
-    const int xa = threadIdx.x;
-    if (xa >= half) return;
-    const int xb = xa + half;
-    const double sx = __ddiv_rn((double)d.w, (double)ow);
-    Col ca, cb;
-    int xa0, xb0;
-    src_index(xa, d.w, sx, xa0, ca.x1, ca.w0, ca.w1);
-    src_index(xb, d.w, sx, xb0, cb.x1, cb.w0, cb.w1);
-    ca.off = 3 * xa0;
-    ca.edge = ca.x1 == xa0;
-    cb.off = 3 * xb0;
-    cb.edge = cb.x1 == xb0;
+    const int xa = 2 * threadIdx.x;                         // columns xa, xa + 1 (ow is even)
+    if (xa >= ow) return;
+    ColPair cp;
+    {
+        const double sx = __ddiv_rn((double)d.w, (double)ow);
+        int x1a, x1b;
+        float l0a, l1a, l0b, l1b;
+        src_index(xa, d.w, sx, cp.x0_a, x1a, l0a, l1a);
+        src_index(xa + 1, d.w, sx, cp.x0_b, x1b, l0b, l1b);
+        cp.off_a = 3 * cp.x0_a;
+        cp.off_b = 3 * cp.x0_b;
+        // right border (tap 1 == tap 0): fold both weights onto tap 0
+        cp.w0 = make_float2(x1a == cp.x0_a ? l0a + l1a : l0a, x1b == cp.x0_b ? l0b + l1b : l0b);
+        cp.w1 = make_float2(x1a == cp.x0_a ? 0.0f : l1a, x1b == cp.x0_b ? 0.0f : l1b);
+        // RandomHorizontalFlip: the pair lands at (ow-2-xa, ow-1-xa), so the
+        // lanes swap roles (.x = column xa + 1) and every store stays a plain float2
+        if (d.flip) {
+            const int t0 = cp.off_a, t1 = cp.x0_a;
+            cp.off_a = cp.off_b, cp.x0_a = cp.x0_b;
+            cp.off_b = t0, cp.x0_b = t1;
+            cp.w0 = make_float2(cp.w0.y, cp.w0.x);
+            cp.w1 = make_float2(cp.w1.y, cp.w1.x);
+        }
+    }
     const int64_t plane = (int64_t)oh * ow;
-    // RandomHorizontalFlip: output columns of this thread
-    float* oa = d.out + (int64_t)y_begin * ow + (d.flip ? ow - 1 - xa : xa);
-    float* ob = d.out + (int64_t)y_begin * ow + (d.flip ? ow - 1 - xb : xb);
-    const float a0 = L.a[0], a1 = L.a[1], a2 = L.a[2];
-    const float b0 = L.b[0], b1 = L.b[1], b2 = L.b[2];
+    float2* o = reinterpret_cast<float2*>(d.out + (int64_t)y_begin * ow + (d.flip ? ow - 2 - xa : xa));
+    const int ow2 = ow >> 1;
+    const int64_t plane2 = plane >> 1;
+    const float2 nb[3] = {make_float2(L.b[0], L.b[0]), make_float2(L.b[1], L.b[1]), make_float2(L.b[2], L.b[2])};
 
-    // Two-entry cache of blended rows (row indices are CTA-uniform: no divergence)
-    int ra = -1, rb = -1;
-    float ha[6] = {0, 0, 0, 0, 0, 0}, hb[6] = {0, 0, 0, 0, 0, 0};   // [col a rgb, col b rgb]
+    // Horizontally blended source rows, even rows in E, odd rows in O (no
+    // register moves: each row is blended once, straight into its register).
+    float2 E[3], O[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) E[k] = O[k] = make_float2(0.f, 0.f);
+    if (staged) mbar_wait(&stage_bar, 0);
     for (int j = 0; j < n_rows_out; ++j) {
-        const int4 t = taps[j];
-        const int y0 = t.x, y1 = t.y;
-        const float ly0 = __int_as_float(t.z), ly1 = __int_as_float(t.w);
-        float top[6], bot[6];
-        if (y0 == rb) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) top[k] = hb[k];
-        } else if (y0 == ra) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) top[k] = ha[k];
-        } else if (staged) {
-            const int ro = row_off[y0 - ylo];
-            blend_row(smem, ro, ca, top);
-            blend_row(smem, ro, cb, top + 3);
-        } else {
-            blend_row_l2(d, y0, xa0, ca, top);
-            blend_row_l2(d, y0, xb0, cb, top + 3);
+        const int2 lr = sched_rows[j];   // CTA-uniform: no divergence
+        if (lr.x >= 0) {
+            if (staged) blend_row(smem, staged_off(d, lr.x, ylo, spitch), cp, E);
+            else blend_row_l2(d, lr.x, cp, E);
         }
-        if (y1 == y0) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) bot[k] = top[k];
-        } else if (y1 == rb) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) bot[k] = hb[k];
-        } else if (staged) {
-            const int ro = row_off[y1 - ylo];
-            blend_row(smem, ro, ca, bot);
-            blend_row(smem, ro, cb, bot + 3);
-        } else {
-            blend_row_l2(d, y1, xa0, ca, bot);
-            blend_row_l2(d, y1, xb0, cb, bot + 3);
+        if (lr.y >= 0) {
+            if (staged) blend_row(smem, staged_off(d, lr.y, ylo, spitch), cp, O);
+            else blend_row_l2(d, lr.y, cp, O);
         }
-        ra = y0;
-        rb = y1;
+        // Resize (vertical blend) + ToTensor + Normalize; 8-byte streaming stores
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            ha[k] = top[k];
-            hb[k] = bot[k];
+        for (int k = 0; k < 3; ++k) {
+            const float we = sched_w[j][k], wo = sched_w[j][3 + k];
+            __stcs(o + k * plane2,
+                   __ffma2_rn(make_float2(we, we), E[k], __ffma2_rn(make_float2(wo, wo), O[k], nb[k])));
         }
-        // Resize (vertical blend), then ToTensor + Normalize
-        __stcs(oa, fmaf(fmaf(ly0, top[0], ly1 * bot[0]), a0, b0));
-        __stcs(oa + plane, fmaf(fmaf(ly0, top[1], ly1 * bot[1]), a1, b1));
-        __stcs(oa + 2 * plane, fmaf(fmaf(ly0, top[2], ly1 * bot[2]), a2, b2));
-        __stcs(ob, fmaf(fmaf(ly0, top[3], ly1 * bot[3]), a0, b0));
-        __stcs(ob + plane, fmaf(fmaf(ly0, top[4], ly1 * bot[4]), a1, b1));
-        __stcs(ob + 2 * plane, fmaf(fmaf(ly0, top[5], ly1 * bot[5]), a2, b2));
-        oa += ow;
-        ob += ow;
+        o += ow2;
     }
 }
 
@@ -212,7 +263,7 @@ int rrc2d_smem_bytes(const RrcLaunch& L) {
         const RrcDesc& d = L.d[i];
         const int rows = (int)((double)(kRows - 1) * d.h / L.oh) + 4;
         const int spitch = ((d.w * 3 + 30) >> 4) << 4;
-        need = max(need, min(rows, 64) * spitch);
+        need = max(need, rows * spitch);
     }
     return min(need, kMaxSmem);
 }
