@@ -751,7 +751,17 @@ void Context::launch_group(Group& g) {
     g.ev.resize(nst + 1);
     for (auto& e : g.ev) e = get_event();
     cudaStream_t st = g.stream;
-    cuda_check(cudaEventRecord(g.ev[0], st), "record start");
+    // The start event goes in immediately before the group's first device
+    // operation, after the host has built that operation's parameters: stage
+    // times (timeout classification, the roofline) then measure device work,
+    // not host-side launch preparation (TMA map encoding, descriptor fills).
+    bool started = false;
+    auto start = [&] {
+        if (!started) {
+            cuda_check(cudaEventRecord(g.ev[0], st), "record start");
+            started = true;
+        }
+    };
     const int n = static_cast<int>(g.tickets.size());
     const bool staged = g.src_kind == LFG_SRC_HOST_PINNED;
 
@@ -776,6 +786,7 @@ void Context::launch_group(Group& g) {
             if (c.fam == FAM_SPEECH) {
                 // a waveform is one contiguous block: a single DMA copy is efficient
                 const int64_t bytes = t.desc.dims[0] * 4;
+                start();
                 cuda_check(cudaMemcpyAsync(dst, t.desc.data, bytes, cudaMemcpyHostToDevice, st),
                            "H2D waveform");
                 v.p[0] = dst;
@@ -814,6 +825,7 @@ void Context::launch_group(Group& g) {
             }
         }
         if (SL.n > 0) {
+            start();
             cuda_check(launch_stage(SL, st), "stage launch");
             counters.launches++;
         }
@@ -845,6 +857,7 @@ void Context::launch_group(Group& g) {
         SpinLaunch L{};
         L.n = n;
         for (int i = 0; i < n; ++i) L.ns[i] = tickets[g.tickets[i]].desc.spin_us[slot] * 1000;
+        start();
         cuda_check(launch_spin(L, st), "spin launch");
         counters.launches++;
     };
@@ -895,6 +908,7 @@ void Context::launch_group(Group& g) {
                 d.key1 = t.p3.key[1];
                 counters.kernel_bytes += c.algo_bytes_per_sample(t.desc);
             }
+            start();
             cuda_check(launch_img3d(L, st), "img3d launch");
             prof_launch_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_l).count();
             counters.launches++;
@@ -923,6 +937,7 @@ void Context::launch_group(Group& g) {
                 counters.kernel_bytes += rrc_algo_bytes(c, t.p2);
             }
             const auto t_l = std::chrono::steady_clock::now();
+            start();
             cuda_check(launch_rrc2d(L, st), "rrc2d launch");
             prof_launch_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_l).count();
             counters.launches++;
@@ -951,10 +966,12 @@ void Context::launch_group(Group& g) {
                                          4 * int64_t((t.ps.T + c.stack - 1) / c.stack) * c.stack * c.n_mels;
                 counters.reserved[1] += int64_t(t.ps.T) * 2 * kTapsDft * 512 * 3;   // tensor FLOPs
             }
+            start();
             cuda_check(launch_speech(L, speech_, nullptr, st), "speech launch");
             counters.launches++;
         }
         for (int slot : S.spin_ops) launch_spins(slot);
+        start();
         cuda_check(cudaEventRecord(g.ev[s + 1], st), "record stage end");
     }
     g.launched = true;

@@ -23,6 +23,7 @@
 // (img3d_tma_kernel below); the row kernel serves K0-staged windows (skewed
 // rows) and unaligned geometries.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -130,124 +131,170 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
 // ------------------------------------------------------------------ TMA tile path
 // HBM-resident volumes whose rows are 16-B aligned (W % 16 == 0) take this
 // path.  A tile is kImg3dTileRows output rows of one z-slice of one sample; the
-// crop window's rows for it are one 3-D TMA box ((cw + 16) x 16 x 1) of the source
-// volume -- the copy engine handles the arbitrary crop offset and zero-fills
-// boxes hanging over the volume's edge (RandomCrop's padding), so the threads
-// issue no global loads and no address arithmetic.  Persistent CTAs: one
-// producer warp streams tiles into a kTmaStages-deep shared-memory ring;
-// 8 consumer warps read each row (flip = reversed row / quad order), apply
-// brightness + noise, and write the output with 16-B streaming stores.
+// crop window's rows for it are two 3-D TMA boxes (image, label; kTR rows each) of the
+// source volume -- the copy engine handles the arbitrary crop offset and
+// zero-fills boxes hanging over the volume's edge (RandomCrop's padding), so
+// the threads issue no global loads and no address arithmetic.
+//
+// Persistent CTAs, one producer thread and 8 consumer warps.  The producer
+// streams tiles into a kTmaStages-deep shared-memory ring and publishes, next
+// to each tile, a 64-byte record with everything its consumer needs (output
+// addresses, brightness / noise parameters, flips, realignment), so consumers
+// never divide, never touch the parameter block and never wait on each other:
+// tile k of the CTA belongs to consumer warp k % 8 alone, which keeps 8 tiles
+// in flight per CTA (the per-tile latency chain -- barrier wait, record load,
+// shared loads, stores -- measured as the bottleneck when all 8 warps shared
+// every tile).  Flip = reversed row / quad order; 16-B streaming stores.
 constexpr int kTR = kImg3dTileRows;
-constexpr int kTmaStages = 6;
+constexpr int kTmaStages = 16;
 constexpr int kTmaWarps = 8;                       // consumer warps
 constexpr int kTmaThreads = 32 * (kTmaWarps + 1);  // + producer warp
-constexpr int kTmaHdr = 128;                       // barriers, then 128-B aligned tiles
+// header: full / empty barriers, tile records, the launch's sample descriptors
+constexpr int kTmaRecOff = 4 * kTmaStages * 8;
+constexpr int kTmaDescOff = kTmaRecOff + kTmaStages * 64;
+constexpr int kTmaHdr = (kTmaDescOff + kMax3D * (int)sizeof(Img3dDesc) + 127) / 128 * 128;
 
-// The box starts at the crop column rounded down to 16 elements (a box whose
-// first byte is not 16-B aligned faults on sm_100a) and is cw + 16 wide; the
-// consumers realign by the warp-uniform remainder off[2] & 15.
-constexpr int kTmaPad = 16;
-__host__ __device__ inline int tma_smem_bytes(int cw) {
-    return kTmaHdr + kTmaStages * kTR * (cw + kTmaPad) * 5;
-}
+// A box must start on a 16-B boundary (an unaligned first byte faults on
+// sm_100a), so the image box starts at the crop column rounded down to 4
+// elements and is cw + 4 wide, the label box at the column rounded down to 16
+// bytes and cw + 16 wide; the consumers realign both by the warp-uniform
+// element shift off[2] & 3.  The maps use no L2 sector promotion: 128-B
+// promotion fetched 1.4x the window's bytes (measured), 64-B DRAM atoms ~1.2x.
+constexpr int kPadImg = 4, kPadLbl = 16;
+__host__ __device__ inline int tma_stage_bytes(int cw) { return kTR * ((cw + kPadImg) * 4 + (cw + kPadLbl)); }
+__host__ __device__ inline int tma_smem_bytes(int cw) { return kTmaHdr + kTmaStages * tma_stage_bytes(cw); }
 
-__device__ __forceinline__ void tile_of(int t, int cd, int nyb, int& i, int& z, int& y0) {
-    const int per = cd * nyb;
-    i = t / per;
-    const int r = t - i * per;
-    z = r / nyb;
-    y0 = (r - z * nyb) * kTR;
-}
+struct __align__(16) TileRec {
+    float* out_img;          // output voxel (z, y0, 0) of this tile
+    uint8_t* out_lbl;
+    uint64_t q0;             // Philox group of the tile's first voxel
+    float scale, sigma;      // brightness multiplier, noise std (0 = none)
+    uint32_t key0, key1;
+    int32_t rows;            // valid output rows (y0 + r < ch)
+    int32_t flags;           // bit 0 flip_y, bit 1 flip_w
+    int32_t wl0, m;          // realignment: first label word inside the box row, element shift
+    int32_t pad[2];
+};
+static_assert(sizeof(TileRec) == 64, "tile record is one 64-B slot");
 
 __global__ void __launch_bounds__(kTmaThreads)
 img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int cd = L.crop[0], ch = L.crop[1], cw = L.crop[2];
     const int nyb = (ch + kTR - 1) / kTR;
-    const int total = L.n * cd * nyb;
-    const int bw = cw + kTmaPad;   // box / smem row width in elements
-    const uint32_t img_bytes = kTR * bw * 4, stage_bytes = kTR * bw * 5;
+    const int per = cd * nyb;
+    const int total = L.n * per;
+    const uint32_t img_bytes = kTR * (cw + kPadImg) * 4, stage_bytes = tma_stage_bytes(cw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kTmaStages;
+    TileRec* rec = reinterpret_cast<TileRec*>(smem + kTmaRecOff);
+    Img3dDesc* sdesc = reinterpret_cast<Img3dDesc*>(smem + kTmaDescOff);
     uint8_t* tiles = smem + kTmaHdr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTmaStages; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, kTmaWarps);
+            mbar_init(empty + s, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    {   // the descriptors the producer reads per tile, staged once (parameter-space
+        // loads with a dynamic index are slow and would sit on its critical path)
+        const int words = L.n * (int)sizeof(Img3dDesc) / 4;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(L.d);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(sdesc);
+        for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+    }
     __syncthreads();
 
-    if (warp == kTmaWarps) {   // producer
-        if (lane == 0) {
-            int k = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x, ++k) {
-                const int s = k % kTmaStages, use = k / kTmaStages;
+    if (warp == kTmaWarps) {
+        // producer: lane j < kTmaStages owns ring stage j and fills it with this
+        // CTA's tiles j, j + 16, ... (16 independent issue chains)
+        if (lane < kTmaStages) {
+            const int ntiles = (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+            const int s = lane;
+            for (int k = lane, use = 0; k < ntiles; k += kTmaStages, ++use) {
                 if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
-                int i, z, y0;
-                tile_of(t, cd, nyb, i, z, y0);
-                const Img3dDesc& d = L.d[i];
+                const int t = (int)blockIdx.x + k * (int)gridDim.x;
+                const int i = t / per, rr = t - i * per;
+                const int z = rr / nyb, y0 = (rr - z * nyb) * kTR;
+                const Img3dDesc& d = sdesc[i];
                 const int fz = (d.flip & 1) ? cd - 1 - z : z;
                 const int fy0 = (d.flip & 2) ? ch - kTR - y0 : y0;   // may be < 0: zero rows, never stored
-                uint8_t* st = tiles + s * stage_bytes;
-                mbar_expect_tx(full + s, stage_bytes);
-                const int x0 = d.off[2] & ~(kTmaPad - 1);
-                tma_load_3d(st, &L.tm_img[i], x0, d.off[1] + fy0, d.off[0] + fz, full + s);
-                tma_load_3d(st + img_bytes, &L.tm_lbl[i], x0, d.off[1] + fy0, d.off[0] + fz, full + s);
+                const int64_t v0 = ((int64_t)z * ch + y0) * cw;
+                TileRec tr;
+                tr.out_img = d.out_img + v0;
+                tr.out_lbl = d.out_lbl + v0;
+                tr.q0 = (uint64_t)v0 >> 2;
+                tr.scale = d.scale;
+                tr.sigma = d.sigma;
+                tr.key0 = d.key0;
+                tr.key1 = d.key1;
+                tr.rows = min(kTR, ch - y0);
+                tr.flags = ((d.flip >> 1) & 1) | (((d.flip >> 2) & 1) << 1);
+                tr.wl0 = (d.off[2] & (kPadLbl - 1)) >> 2;
+                tr.m = d.off[2] & 3;
+                tr.pad[0] = tr.pad[1] = 0;
+                rec[s] = tr;
+                if (L.debug & 2) {   // profiling switch: no loads
+                    mbar_arrive(full + s);
+                } else {
+                    uint8_t* st = tiles + s * stage_bytes;
+                    mbar_expect_tx(full + s, stage_bytes);
+                    tma_load_3d(st, &L.tm_img[i], d.off[2] & ~(kPadImg - 1), d.off[1] + fy0, d.off[0] + fz,
+                                full + s);
+                    tma_load_3d(st + img_bytes, &L.tm_lbl[i], d.off[2] & ~(kPadLbl - 1), d.off[1] + fy0,
+                                d.off[0] + fz, full + s);
+                }
             }
         }
         return;
     }
 
-    const int cw4 = cw >> 2;
-    int k = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++k) {
+    const int cw4 = cw >> 2, bi4 = (cw + kPadImg) >> 2, bl4 = (cw + kPadLbl) >> 2;
+    const int ntiles = (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    for (int k = warp; k < ntiles; k += kTmaWarps) {
         const int s = k % kTmaStages, use = k / kTmaStages;
-        int i, z, y0;
-        tile_of(t, cd, nyb, i, z, y0);
-        const Img3dDesc& d = L.d[i];
-        const bool flip_y = (d.flip & 2) != 0, flip_w = (d.flip & 4) != 0;
-        const bool noise = d.sigma != 0.0f;
         mbar_wait(full + s, use & 1);
+        const TileRec tr = rec[s];
+        const bool flip_y = (tr.flags & 1) != 0, flip_w = (tr.flags & 2) != 0;
         const float4* simg = reinterpret_cast<const float4*>(tiles + s * stage_bytes);
         const uint32_t* slbl = reinterpret_cast<const uint32_t*>(tiles + s * stage_bytes + img_bytes);
-        const int e0 = d.off[2] & (kTmaPad - 1);   // crop column 0 inside the box row
-        const int m = e0 & 3, w0 = e0 >> 2;        // warp-uniform realignment
-        const int bw4 = bw >> 2;
-        for (int r = warp; r < kTR; r += kTmaWarps) {
-            const int y = y0 + r;
-            if (y >= ch) break;
+#pragma unroll 2
+        for (int r = 0; r < tr.rows; ++r) {
             const int sr = flip_y ? kTR - 1 - r : r;
             for (int qx = lane; qx < cw4; qx += 32) {
                 const int qs = flip_w ? cw4 - 1 - qx : qx;
-                const int w = sr * bw4 + w0 + qs;
-                float4 x = simg[w];
-                uint32_t lb = slbl[w];
-                if (m != 0) {
-                    x = shift4(x, simg[w + 1], m);
-                    lb = __funnelshift_r(lb, slbl[w + 1], 8 * m);
+                const int wi = sr * bi4 + qs, wl = sr * bl4 + tr.wl0 + qs;
+                float4 x = simg[wi];
+                uint32_t lb = slbl[wl];
+                if (tr.m != 0) {
+                    x = shift4(x, simg[wi + 1], tr.m);
+                    lb = __funnelshift_r(lb, slbl[wl + 1], 8 * tr.m);
                 }
                 if (flip_w) {
                     x = make_float4(x.w, x.z, x.y, x.x);
                     lb = __byte_perm(lb, 0, 0x0123);
                 }
-                const int64_t vox = ((int64_t)z * ch + y) * cw + 4 * qx;
-                float o[4] = {x.x * d.scale, x.y * d.scale, x.z * d.scale, x.w * d.scale};
-                if (noise) {
-                    const uint64_t g = (uint64_t)vox >> 2;
+                const int vo = r * cw + 4 * qx;   // voxel offset inside the tile
+                float o[4] = {x.x * tr.scale, x.y * tr.scale, x.z * tr.scale, x.w * tr.scale};
+                if (tr.sigma != 0.0f) {
+                    const uint64_t g = tr.q0 + (uint64_t)(vo >> 2);
                     const uint4 rnd = philox4x32_10(
-                        make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, 0u), d.key0, d.key1);
+                        make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, 0u), tr.key0, tr.key1);
                     const float2 z01 = box_muller(rnd.x, rnd.y);
                     const float2 z23 = box_muller(rnd.z, rnd.w);
-                    o[0] = fmaf(d.sigma, z01.x, o[0]);
-                    o[1] = fmaf(d.sigma, z01.y, o[1]);
-                    o[2] = fmaf(d.sigma, z23.x, o[2]);
-                    o[3] = fmaf(d.sigma, z23.y, o[3]);
+                    o[0] = fmaf(tr.sigma, z01.x, o[0]);
+                    o[1] = fmaf(tr.sigma, z01.y, o[1]);
+                    o[2] = fmaf(tr.sigma, z23.x, o[2]);
+                    o[3] = fmaf(tr.sigma, z23.y, o[3]);
                 }
-                __stcs(reinterpret_cast<float4*>(d.out_img + vox), make_float4(o[0], o[1], o[2], o[3]));
-                __stcs(reinterpret_cast<unsigned int*>(d.out_lbl + vox), lb);
+                if (L.debug & 1) {   // profiling switch: no stores
+                    if (o[0] == 123.f && lb == 7u) tr.out_img[0] = o[1];
+                    continue;
+                }
+                __stcs(reinterpret_cast<float4*>(tr.out_img + vo), make_float4(o[0], o[1], o[2], o[3]));
+                __stcs(reinterpret_cast<unsigned int*>(tr.out_lbl + vo), lb);
             }
         }
         __syncwarp();
@@ -287,16 +334,17 @@ cudaError_t img3d_encode_maps(Img3dLaunch& L, int i, const void* img, const void
     EncodeTiledFn fn = encode_fn();
     if (fn == nullptr) return cudaErrorNotSupported;
     const cuuint64_t gdim[3] = {(cuuint64_t)dims[2], (cuuint64_t)dims[1], (cuuint64_t)dims[0]};
-    const cuuint32_t box[3] = {(cuuint32_t)(L.crop[2] + kTmaPad), (cuuint32_t)kTR, 1};
+    const cuuint32_t box_i[3] = {(cuuint32_t)(L.crop[2] + kPadImg), (cuuint32_t)kTR, 1};
+    const cuuint32_t box_l[3] = {(cuuint32_t)(L.crop[2] + kPadLbl), (cuuint32_t)kTR, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const cuuint64_t si[2] = {(cuuint64_t)dims[2] * 4, (cuuint64_t)(dims[1] * dims[2]) * 4};
     const cuuint64_t sl[2] = {(cuuint64_t)dims[2], (cuuint64_t)(dims[1] * dims[2])};
-    CUresult r = fn(&L.tm_img[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(img), gdim, si, box,
+    CUresult r = fn(&L.tm_img[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(img), gdim, si, box_i,
                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    r = fn(&L.tm_lbl[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(lbl), gdim, sl, box, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+    r = fn(&L.tm_lbl[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(lbl), gdim, sl, box_l, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -317,7 +365,16 @@ cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s) {
         }
         const int64_t total = int64_t(L.n) * L.crop[0] * ((L.crop[1] + kTR - 1) / kTR);
         const int grid = static_cast<int>(std::min<int64_t>(total, int64_t(sm_count()) * o));
-        img3d_tma_kernel<<<grid, kTmaThreads, smem, s>>>(L);
+        static const int dbg = getenv("LFG_IMG3D_DEBUG") ? atoi(getenv("LFG_IMG3D_DEBUG")) : 0;
+        static const int ctas = getenv("LFG_IMG3D_CTAS") ? atoi(getenv("LFG_IMG3D_CTAS")) : 0;
+        if (dbg == 0 && ctas == 0) {
+            img3d_tma_kernel<<<grid, kTmaThreads, smem, s>>>(L);
+        } else {
+            Img3dLaunch L2 = L;
+            L2.debug = dbg;
+            const int g2 = ctas ? static_cast<int>(std::min<int64_t>(total, int64_t(sm_count()) * ctas)) : grid;
+            img3d_tma_kernel<<<g2, kTmaThreads, smem, s>>>(L2);
+        }
         return cudaGetLastError();
     }
     dim3 grid((L.crop[1] + kRowsPerCta - 1) / kRowsPerCta, L.crop[0], L.n);

@@ -60,6 +60,7 @@ struct Img3dLaunch {
     int32_t crop[3];
     int32_t n;
     int32_t tma;             // 1: every sample has tm_img/tm_lbl (TMA tile path)
+    int32_t debug;           // profiling switch (LFG_IMG3D_DEBUG): 1 no stores, 2 no loads
     Img3dDesc d[kMax3D];
     // TMA path: 3-D tiled maps over the whole source volume (dims W, H, D),
     // box (cw + 16, kImg3dTileRows, 1); out-of-bounds boxes fill zeros, which is
@@ -67,7 +68,7 @@ struct Img3dLaunch {
     CUtensorMap tm_img[kMax3D];
     CUtensorMap tm_lbl[kMax3D];
 };
-constexpr int kImg3dTileRows = 16;
+constexpr int kImg3dTileRows = 8;
 // TMA path preconditions on the sample / crop geometry (else the row kernel runs)
 inline bool img3d_tma_ok(const void* img, const void* lbl, const int64_t dims[3], const int crop[3]) {
     return (reinterpret_cast<uintptr_t>(img) & 15) == 0 && (reinterpret_cast<uintptr_t>(lbl) & 15) == 0 &&
