@@ -125,7 +125,8 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     // (row r always lives in register r & 1 -- the two taps y0, y0 + 1 of a
     // row never collide) and the vertical weights with Normalize's scale folded
     // in: out_c = wE_c * E_c + (wO_c * O_c + b_c).
-    __shared__ int2 sched_rows[kRows];            // {even row to load, odd row to load} (-1: kept)
+    __shared__ int2 sched_rows[kRows];            // {even row, odd row} to blend (-1: kept) as a
+                                                  // staged byte offset (or a row index, unstaged)
     __shared__ float sched_w[kRows][6];           // {wE * a_c (c = 0..2), wO * a_c}
     __shared__ int yspan[2];                      // first / last source row of the CTA
     const RrcDesc& d = L.d[blockIdx.y];
@@ -133,6 +134,8 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     const int y_begin = blockIdx.x * kRows;
     const int n_rows_out = min(kRows, oh - y_begin);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row_bytes = d.w * 3;
+    const int spitch = ((row_bytes + 30) >> 4) << 4;        // 16-B chunks + alignment phase
     if (threadIdx.x == 32) {
         mbar_init(&stage_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -140,17 +143,24 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     if (threadIdx.x < n_rows_out) {
         const int j = threadIdx.x;
         const double sy = __ddiv_rn((double)d.h, (double)oh);
-        int y0, y1, p0 = -1, p1 = -1;
-        float l0, l1, q0, q1;
+        int y0, y1, p0 = -1, p1 = -1, ylo, yhi, t0, t1;
+        float l0, l1, q0, q1, u0, u1;
         src_index(y_begin + j, d.h, sy, y0, y1, l0, l1);
         if (j > 0) src_index(y_begin + j - 1, d.h, sy, p0, p1, q0, q1);
+        src_index(y_begin, d.h, sy, ylo, t0, u0, u1);                      // the CTA's row span
+        src_index(y_begin + n_rows_out - 1, d.h, sy, t1, yhi, u0, u1);
+        const bool staged = (yhi - ylo + 1) * spitch <= smem_bytes;
         // a row is already in its register iff the previous output row used it
         // (rows are non-decreasing and adjacent taps differ by at most one)
         const bool new0 = y0 != p0 && y0 != p1;
         const bool new1 = y1 != y0 && y1 != p0 && y1 != p1;
         const bool odd0 = (y0 & 1) != 0;   // y1 (if distinct) has the other parity
-        const int ld_e = odd0 ? (new1 ? y1 : -1) : (new0 ? y0 : -1);
-        const int ld_o = odd0 ? (new0 ? y0 : -1) : (new1 ? y1 : -1);
+        int ld_e = odd0 ? (new1 ? y1 : -1) : (new0 ? y0 : -1);
+        int ld_o = odd0 ? (new0 ? y0 : -1) : (new1 ? y1 : -1);
+        if (staged) {   // resolve rows to their byte offsets in the staged window once, here
+            if (ld_e >= 0) ld_e = staged_off(d, ld_e, ylo, spitch);
+            if (ld_o >= 0) ld_o = staged_off(d, ld_o, ylo, spitch);
+        }
         float w_e, w_o;
         if (y1 == y0) {
             w_e = odd0 ? 0.f : l0 + l1;
@@ -165,14 +175,14 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
             sched_w[j][c] = w_e * L.a[c];
             sched_w[j][3 + c] = w_o * L.a[c];
         }
-        if (j == 0) yspan[0] = y0;
-        if (j == n_rows_out - 1) yspan[1] = y1;
+        if (j == 0) {
+            yspan[0] = ylo;
+            yspan[1] = yhi;
+        }
     }
     __syncthreads();
     const int ylo = yspan[0];
     const int nrows = yspan[1] - ylo + 1;
-    const int row_bytes = d.w * 3;
-    const int spitch = ((row_bytes + 30) >> 4) << 4;        // 16-B chunks + alignment phase
     const bool staged = nrows * spitch <= smem_bytes;
 
     // 1. stage the touched source rows (aligned 16-byte superset of each row) with
@@ -235,11 +245,11 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     for (int j = 0; j < n_rows_out; ++j) {
         const int2 lr = sched_rows[j];   // CTA-uniform: no divergence
         if (lr.x >= 0) {
-            if (staged) blend_row(smem, staged_off(d, lr.x, ylo, spitch), cp, E);
+            if (staged) blend_row(smem, lr.x, cp, E);
             else blend_row_l2(d, lr.x, cp, E);
         }
         if (lr.y >= 0) {
-            if (staged) blend_row(smem, staged_off(d, lr.y, ylo, spitch), cp, O);
+            if (staged) blend_row(smem, lr.y, cp, O);
             else blend_row_l2(d, lr.y, cp, O);
         }
         // Resize (vertical blend) + ToTensor + Normalize; 8-byte streaming stores
