@@ -49,6 +49,11 @@ enum {
     LFG_OP_RANDOM_BRIGHTNESS = 3, /* param: p, lo, hi                       */
     LFG_OP_GAUSSIAN_NOISE = 4,    /* param: p, std_max                      */
     LFG_OP_CAST = 5,              /* no params: img f32, label u8           */
+    /* optional img_seg ops (north_star "trilinear resize", "brightness/contrast";
+     * not in the reference chain): chain order Crop, Zoom3D, Flip, Brightness,
+     * Contrast, Noise, Cast */
+    LFG_OP_RANDOM_ZOOM3D = 6,     /* param: p, lo, hi: window = round(crop*f), trilinear back to crop */
+    LFG_OP_RANDOM_CONTRAST = 7,   /* param: p, lo, hi: (v - mean) * f + mean over the crop */
     /* obj_det chain, proj/src/workloads.cpp:151-156 */
     LFG_OP_RESIZE = 10,           /* RandomResizedCrop; param: out_h, out_w, scale_lo, scale_hi, ratio_lo, ratio_hi */
     LFG_OP_RANDOM_HFLIP = 11,     /* param: p                               */

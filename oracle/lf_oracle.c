@@ -112,12 +112,10 @@ void lfo_normals4(uint64_t group, uint32_t k0, uint32_t k1, double z[4]) {
 
 /* ------------------------------------------------------------------ */
 /* img_seg chain: RandomCrop, RandomFlip, RandomBrightness, GaussianNoise, Cast
- * (proj/src/workloads.cpp:142-148).  Parameter draw order (fixed count of 11
- * draws per sample so the stream position never depends on outcomes):
- *   off_d, off_h, off_w   randint(0, max(dim-crop, 0))       RandomCrop
- *   flip_d, flip_h, flip_w  unif01 < p_flip                   RandomFlip
- *   b_apply, b_factor     unif01 < p_bright, uniform(lo, hi)  RandomBrightness
- *   n_apply, n_std, key   unif01 < p_noise, uniform(0, max), raw u64 -> Philox key
+ * (proj/src/workloads.cpp:142-148), plus the optional RandomZoom3D (trilinear
+ * resample of a zoomed window) and RandomContrast ops.  Parameter draws: see
+ * lfo_draw3d (11 draws for the reference chain; the stream position never
+ * depends on outcomes).
  * Output voxel v = (z*ch + y)*cw + x reads input
  *   (off_d + (flip_d ? cd-1-z : z), off_h + ..., off_w + ...), zero outside;
  *   img_out = img_in * scale + sigma * N_v, lbl_out = lbl_in,
@@ -131,20 +129,55 @@ void lfo_cfg3d_default(lfo_cfg3d* c) {
     c->bright_hi = 1.3;
     c->p_noise = 0.1;
     c->noise_std_max = 0.1;
+    c->has_zoom = 0;
+    c->p_zoom = 0.5;
+    c->zoom_lo = 0.8;
+    c->zoom_hi = 1.2;
+    c->has_contrast = 0;
+    c->p_contrast = 0.15;
+    c->contrast_lo = 0.75;
+    c->contrast_hi = 1.25;
 }
 
+/* Draw order, in chain order: RandomCrop u_off[3] (the offset uniforms; the
+ * offset is floor(u * (room + 1)) once the window edge is known, which equals
+ * randint(0, room) of the plain chain); [RandomZoom3D: apply, factor];
+ * RandomFlip x3; RandomBrightness apply, factor; [RandomContrast: apply,
+ * factor]; GaussianNoise apply, std; Philox key.  Bracketed draws happen only
+ * when the op is in the chain. */
 void lfo_draw3d(const lfo_cfg3d* c, uint64_t seed, uint64_t id, const int64_t dims[3],
                 lfo_params3d* p) {
     lfo_mt64 g;
     lfo_sample_rng(&g, seed, id);
+    double u_off[3];
+    for (int a = 0; a < 3; a++) u_off[a] = lfo_unif01(&g);
+    for (int a = 0; a < 3; a++) p->win[a] = c->crop[a];
+    if (c->has_zoom) {
+        int z_apply = lfo_unif01(&g) < c->p_zoom;
+        double zf = lfo_uniform(&g, c->zoom_lo, c->zoom_hi);
+        if (z_apply) {
+            for (int a = 0; a < 3; a++) {
+                int64_t w = (int64_t)floor((double)c->crop[a] * zf + 0.5);
+                p->win[a] = w < 1 ? 1 : w;
+            }
+        }
+    }
     for (int a = 0; a < 3; a++) {
-        int64_t room = dims[a] - c->crop[a];
-        p->off[a] = lfo_randint(&g, 0, room > 0 ? room : 0);
+        int64_t room = dims[a] - p->win[a];
+        int64_t span = (room > 0 ? room : 0) + 1;
+        int64_t k = (int64_t)floor(u_off[a] * (double)span);
+        p->off[a] = k >= span ? span - 1 : k;
     }
     for (int a = 0; a < 3; a++) p->flip[a] = lfo_unif01(&g) < c->p_flip;
     int b_apply = lfo_unif01(&g) < c->p_bright;
     double b_factor = lfo_uniform(&g, c->bright_lo, c->bright_hi);
     p->scale = b_apply ? b_factor : 1.0;
+    p->contrast = 1.0;
+    if (c->has_contrast) {
+        int c_apply = lfo_unif01(&g) < c->p_contrast;
+        double c_factor = lfo_uniform(&g, c->contrast_lo, c->contrast_hi);
+        if (c_apply) p->contrast = c_factor;
+    }
     int n_apply = lfo_unif01(&g) < c->p_noise;
     double n_std = lfo_uniform(&g, 0.0, c->noise_std_max);
     uint64_t key = lfo_mt64_next(&g);
@@ -153,34 +186,90 @@ void lfo_draw3d(const lfo_cfg3d* c, uint64_t seed, uint64_t id, const int64_t di
     p->key[1] = (uint32_t)(key >> 32);
 }
 
+/* PyTorch area_pixel_compute_source_index (align_corners=False, linear) on
+ * scale = in / out, then the upsample_linear tap pair and weights. */
+static void linear_taps(int64_t dst, int64_t in, int64_t out, int64_t* i0, int64_t* i1, double* l0,
+                        double* l1) {
+    double scale = (double)in / (double)out;
+    double src = scale * ((double)dst + 0.5) - 0.5;
+    if (src < 0.0) src = 0.0;
+    int64_t a = (int64_t)floor(src);
+    if (a > in - 1) a = in - 1;
+    *i0 = a;
+    *i1 = a < in - 1 ? a + 1 : a;
+    *l1 = src - (double)a;
+    *l0 = 1.0 - *l1;
+}
+
+static double vox_or_zero(const float* img, const int64_t dims[3], int64_t z, int64_t y, int64_t x) {
+    if (z >= dims[0] || y >= dims[1] || x >= dims[2]) return 0.0;
+    return (double)img[(z * dims[1] + y) * dims[2] + x];
+}
+
 void lfo_apply3d(const lfo_cfg3d* c, const lfo_params3d* p, const float* img,
                  const uint8_t* lbl, const int64_t dims[3], double* out_img,
                  uint8_t* out_lbl) {
     const int64_t cd = c->crop[0], ch = c->crop[1], cw = c->crop[2];
     const int64_t D = dims[0], H = dims[1], W = dims[2];
+    const int64_t* win = p->win;
+    const int64_t n = cd * ch * cw;
+    /* 1. RandomCrop [+ RandomZoom3D resample] + RandomFlip + RandomBrightness */
+    double sum = 0.0;
     for (int64_t z = 0; z < cd; z++) {
-        int64_t sz = p->off[0] + (p->flip[0] ? cd - 1 - z : z);
+        int64_t wz = p->flip[0] ? cd - 1 - z : z;   /* output position before the flip */
         for (int64_t y = 0; y < ch; y++) {
-            int64_t sy = p->off[1] + (p->flip[1] ? ch - 1 - y : y);
+            int64_t wy = p->flip[1] ? ch - 1 - y : y;
             for (int64_t x = 0; x < cw; x++) {
-                int64_t sx = p->off[2] + (p->flip[2] ? cw - 1 - x : x);
+                int64_t wx = p->flip[2] ? cw - 1 - x : x;
                 int64_t v = (z * ch + y) * cw + x;
                 double val = 0.0;
                 uint8_t l = 0;
-                if (sz < D && sy < H && sx < W) {
-                    int64_t si = (sz * H + sy) * W + sx;
-                    val = (double)img[si];
-                    l = lbl[si];
+                if (win[0] == cd && win[1] == ch && win[2] == cw) {
+                    int64_t sz = p->off[0] + wz, sy = p->off[1] + wy, sx = p->off[2] + wx;
+                    if (sz < D && sy < H && sx < W) {
+                        int64_t si = (sz * H + sy) * W + sx;
+                        val = (double)img[si];
+                        l = lbl[si];
+                    }
+                } else {
+                    int64_t z0, z1, y0, y1, x0, x1;
+                    double lz0, lz1, ly0, ly1, lx0, lx1;
+                    linear_taps(wz, win[0], cd, &z0, &z1, &lz0, &lz1);
+                    linear_taps(wy, win[1], ch, &y0, &y1, &ly0, &ly1);
+                    linear_taps(wx, win[2], cw, &x0, &x1, &lx0, &lx1);
+                    const int64_t oz = p->off[0], oy = p->off[1], ox = p->off[2];
+                    val = lz0 * (ly0 * (lx0 * vox_or_zero(img, dims, oz + z0, oy + y0, ox + x0) +
+                                        lx1 * vox_or_zero(img, dims, oz + z0, oy + y0, ox + x1)) +
+                                 ly1 * (lx0 * vox_or_zero(img, dims, oz + z0, oy + y1, ox + x0) +
+                                        lx1 * vox_or_zero(img, dims, oz + z0, oy + y1, ox + x1))) +
+                          lz1 * (ly0 * (lx0 * vox_or_zero(img, dims, oz + z1, oy + y0, ox + x0) +
+                                        lx1 * vox_or_zero(img, dims, oz + z1, oy + y0, ox + x1)) +
+                                 ly1 * (lx0 * vox_or_zero(img, dims, oz + z1, oy + y1, ox + x0) +
+                                        lx1 * vox_or_zero(img, dims, oz + z1, oy + y1, ox + x1)));
+                    int64_t nz = wz * win[0] / cd, ny = wy * win[1] / ch, nx = wx * win[2] / cw;
+                    if (nz > win[0] - 1) nz = win[0] - 1;
+                    if (ny > win[1] - 1) ny = win[1] - 1;
+                    if (nx > win[2] - 1) nx = win[2] - 1;
+                    int64_t sz = oz + nz, sy = oy + ny, sx = ox + nx;
+                    if (sz < D && sy < H && sx < W) l = lbl[(sz * H + sy) * W + sx];
                 }
-                val *= p->scale;                           /* RandomBrightness */
-                if (p->sigma != 0.0) {                     /* GaussianNoise */
-                    double zz[4];
-                    lfo_normals4((uint64_t)v >> 2, p->key[0], p->key[1], zz);
-                    val += p->sigma * zz[v & 3];
-                }
-                out_img[v] = val;                          /* Cast: f32 image */
-                out_lbl[v] = l;                            /*       u8 label  */
+                sum += val;
+                out_img[v] = val * p->scale;               /* RandomBrightness */
+                out_lbl[v] = l;                            /* Cast: u8 label */
             }
+        }
+    }
+    /* 2. RandomContrast: (v - m) * c + m, m = mean of the brightness-scaled crop */
+    if (p->contrast != 1.0) {
+        double m = sum / (double)n * p->scale;
+        for (int64_t v = 0; v < n; v++) out_img[v] = (out_img[v] - m) * p->contrast + m;
+    }
+    /* 3. GaussianNoise, Cast (f32 image) */
+    if (p->sigma != 0.0) {
+        for (int64_t v = 0; v < n; v++) {
+            double zz[4];
+            lfo_normals4((uint64_t)v >> 2, p->key[0], p->key[1], zz);
+            out_img[v] += p->sigma * zz[v & 3];
         }
     }
 }

@@ -75,20 +75,34 @@ typedef struct {
     double bright_lo, bright_hi; /* default 0.7, 1.3 */
     double p_noise;         /* default 0.1 (MLPerf GaussianNoise) */
     double noise_std_max;   /* default 0.1 */
+    /* optional ops (north_star "trilinear resize", "brightness/contrast"; not in
+     * the reference's img_seg chain, so off by default and their draws are
+     * skipped: the default chain's draw sequence is unchanged) */
+    int32_t has_zoom;       /* RandomZoom3D after RandomCrop */
+    double p_zoom;          /* default 0.5 */
+    double zoom_lo, zoom_hi;/* default 0.8, 1.2 (window edge = round(crop * f)) */
+    int32_t has_contrast;   /* RandomContrast after RandomBrightness */
+    double p_contrast;      /* default 0.15 (nnU-Net ContrastAugmentation) */
+    double contrast_lo, contrast_hi; /* default 0.75, 1.25 */
 } lfo_cfg3d;
 
 typedef struct {
-    int64_t off[3];         /* crop origin per axis (0 when dim < crop: zero pad) */
+    int64_t off[3];         /* window origin per axis (0 when dim < window: zero pad) */
     int32_t flip[3];        /* flip flags per axis */
     double scale;           /* brightness multiplier (1.0 when not applied) */
     double sigma;           /* noise std (0.0 when not applied) */
     uint32_t key[2];        /* Philox key */
+    int64_t win[3];         /* source window edge per axis (= crop unless zoomed) */
+    double contrast;        /* contrast factor (1.0 when not applied) */
 } lfo_params3d;
 
 void lfo_cfg3d_default(lfo_cfg3d* c);
 void lfo_draw3d(const lfo_cfg3d* c, uint64_t seed, uint64_t id, const int64_t dims[3],
                 lfo_params3d* p);
-/* img f32 [D,H,W], lbl u8 [D,H,W] -> out_img f64 [cd,ch,cw], out_lbl u8 */
+/* img f32 [D,H,W], lbl u8 [D,H,W] -> out_img f64 [cd,ch,cw], out_lbl u8.
+ * Zoomed windows (win != crop) are resampled to the crop: image trilinear
+ * (PyTorch upsample_trilinear3d, align_corners=False, source index in fp64),
+ * label nearest with the integer index min(dst * win / crop, win - 1). */
 void lfo_apply3d(const lfo_cfg3d* c, const lfo_params3d* p, const float* img,
                  const uint8_t* lbl, const int64_t dims[3], double* out_img,
                  uint8_t* out_lbl);

@@ -32,12 +32,16 @@ class MT64(C.Structure):
 class Cfg3D(C.Structure):
     _fields_ = [("crop", C.c_int64 * 3), ("p_flip", C.c_double), ("p_bright", C.c_double),
                 ("bright_lo", C.c_double), ("bright_hi", C.c_double),
-                ("p_noise", C.c_double), ("noise_std_max", C.c_double)]
+                ("p_noise", C.c_double), ("noise_std_max", C.c_double),
+                ("has_zoom", C.c_int32), ("p_zoom", C.c_double), ("zoom_lo", C.c_double),
+                ("zoom_hi", C.c_double), ("has_contrast", C.c_int32), ("p_contrast", C.c_double),
+                ("contrast_lo", C.c_double), ("contrast_hi", C.c_double)]
 
 
 class Params3D(C.Structure):
     _fields_ = [("off", C.c_int64 * 3), ("flip", C.c_int32 * 3), ("scale", C.c_double),
-                ("sigma", C.c_double), ("key", C.c_uint32 * 2)]
+                ("sigma", C.c_double), ("key", C.c_uint32 * 2), ("win", C.c_int64 * 3),
+                ("contrast", C.c_double)]
 
 
 class Cfg2D(C.Structure):

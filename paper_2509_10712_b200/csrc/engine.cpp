@@ -50,16 +50,38 @@ struct SampleRng {
 };
 }  // namespace
 
+// Draw order (chain order; oracle/lf_oracle.c lfo_draw3d): RandomCrop offset
+// uniforms, [RandomZoom3D apply + factor], flips, brightness, [RandomContrast
+// apply + factor], noise, Philox key.  The offset is floor(u * (room + 1)) once
+// the window edge is known -- randint(0, room) of the plain chain.
 void draw_3d(const Chain& c, uint64_t seed, uint64_t id, const int64_t dims[3], Params3D& p) {
     SampleRng r(seed, id);
+    double u_off[3];
+    for (int a = 0; a < 3; ++a) u_off[a] = r.unif01();
+    for (int a = 0; a < 3; ++a) p.win[a] = c.crop[a];
+    if (c.has_zoom) {
+        const bool z_apply = r.unif01() < c.p_zoom;
+        const double zf = r.uniform(c.z_lo, c.z_hi);
+        if (z_apply)
+            for (int a = 0; a < 3; ++a)
+                p.win[a] = std::max<int64_t>(1, static_cast<int64_t>(std::floor(c.crop[a] * zf + 0.5)));
+    }
     for (int a = 0; a < 3; ++a) {
-        const int64_t room = dims[a] - c.crop[a];
-        p.off[a] = r.randint(0, room > 0 ? room : 0);
+        const int64_t room = dims[a] - p.win[a];
+        const int64_t span = (room > 0 ? room : 0) + 1;
+        const int64_t k = static_cast<int64_t>(std::floor(u_off[a] * static_cast<double>(span)));
+        p.off[a] = k >= span ? span - 1 : k;
     }
     for (int a = 0; a < 3; ++a) p.flip[a] = r.unif01() < c.p_flip;
     const bool b_apply = r.unif01() < c.p_bright;
     const double b_factor = r.uniform(c.b_lo, c.b_hi);
     p.scale = b_apply ? b_factor : 1.0;
+    p.contrast = 1.0;
+    if (c.has_contrast) {
+        const bool c_apply = r.unif01() < c.p_contrast;
+        const double c_factor = r.uniform(c.c_lo, c.c_hi);
+        if (c_apply) p.contrast = c_factor;
+    }
     const bool n_apply = r.unif01() < c.p_noise;
     const double n_std = r.uniform(0.0, c.noise_max);
     const uint64_t key = r.g();
@@ -149,7 +171,7 @@ int64_t Chain::algo_bytes_per_sample(const lfg_sample_desc& s) const {
     switch (fam) {
         case FAM_IMG3D: {
             const int64_t vox = int64_t(crop[0]) * crop[1] * crop[2];
-            return vox * 10;  // read f32 + u8, write f32 + u8
+            return vox * 10;  // read f32 + u8, write f32 + u8 (zoomed windows: img3d_algo_bytes)
         }
         case FAM_RRC2D: {
             (void)s;
@@ -191,6 +213,8 @@ Context::Context(const lfg_config& c) : cfg(c) {
     }
     cuda_check(warm_stage(), "load stage kernel");
     cuda_check(warm_img3d(), "load img3d kernel");
+    cuda_check(warm_img3d_zoom(), "load img3d zoom kernels");
+    cuda_check(cudaMalloc(&csum_, kCsumSlots * sizeof(double)), "contrast sums");
     cuda_check(warm_rrc2d(), "load rrc2d kernel");
     cuda_check(warm_misc(), "load misc kernels");
     cuda_check(warm_speech(), "load speech kernels");
@@ -213,6 +237,7 @@ Context::~Context() {
         cudaFree(b.base);
     }
     for (auto& r : raws_) cudaFree(r.ptr);
+    if (csum_) cudaFree(csum_);
     for (auto s : streams_) cudaStreamDestroy(s);
     cudaStreamDestroy(seal_stream);
     cudaStreamDestroy(aux_stream);
@@ -250,10 +275,12 @@ namespace {
 int rank_of(int kind, Family& fam) {
     switch (kind) {
         case LFG_OP_RANDOM_CROP: fam = FAM_IMG3D; return 1;
-        case LFG_OP_RANDOM_FLIP: fam = FAM_IMG3D; return 2;
-        case LFG_OP_RANDOM_BRIGHTNESS: fam = FAM_IMG3D; return 3;
-        case LFG_OP_GAUSSIAN_NOISE: fam = FAM_IMG3D; return 4;
-        case LFG_OP_CAST: fam = FAM_IMG3D; return 5;
+        case LFG_OP_RANDOM_ZOOM3D: fam = FAM_IMG3D; return 2;
+        case LFG_OP_RANDOM_FLIP: fam = FAM_IMG3D; return 3;
+        case LFG_OP_RANDOM_BRIGHTNESS: fam = FAM_IMG3D; return 4;
+        case LFG_OP_RANDOM_CONTRAST: fam = FAM_IMG3D; return 5;
+        case LFG_OP_GAUSSIAN_NOISE: fam = FAM_IMG3D; return 6;
+        case LFG_OP_CAST: fam = FAM_IMG3D; return 7;
         case LFG_OP_RESIZE: fam = FAM_RRC2D; return 1;
         case LFG_OP_RANDOM_HFLIP: fam = FAM_RRC2D; return 2;
         case LFG_OP_TO_TENSOR: fam = FAM_RRC2D; return 3;
@@ -311,6 +338,20 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
             case LFG_OP_GAUSSIAN_NOISE:
                 c->p_noise = p[0];
                 c->noise_max = pdef(p[1], 0.1);
+                break;
+            case LFG_OP_RANDOM_ZOOM3D:
+                c->has_zoom = true;
+                c->p_zoom = p[0];
+                c->z_lo = pdef(p[1], 0.8);
+                c->z_hi = pdef(p[2], 1.2);
+                if (!(c->z_lo > 0 && c->z_hi >= c->z_lo && c->z_hi <= 2.0))
+                    fail(LFG_ERR_INVALID, "RandomZoom3D range must satisfy 0 < lo <= hi <= 2");
+                break;
+            case LFG_OP_RANDOM_CONTRAST:
+                c->has_contrast = true;
+                c->p_contrast = p[0];
+                c->c_lo = pdef(p[1], 0.75);
+                c->c_hi = pdef(p[2], 1.25);
                 break;
             case LFG_OP_CAST: break;
             case LFG_OP_RESIZE:
@@ -549,6 +590,17 @@ int64_t Context::get_raw(int64_t bytes) {
 
 static int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
+// Algorithmic bytes of K1 / K4 for one sample: the window voxels inside the
+// source, read once (f32 + u8), and the crop written (f32 + u8).  Without
+// RandomZoom3D the window is the crop: 128^3 * 10 B.
+int64_t img3d_algo_bytes(const Chain& c, const Ticket& t) {
+    if (!c.has_zoom) return c.algo_bytes_per_sample(t.desc);
+    int64_t in = 5;
+    for (int a = 0; a < 3; ++a)
+        in *= std::max<int64_t>(0, std::min<int64_t>(t.p3.win[a], t.desc.dims[a] - t.p3.off[a]));
+    return in + int64_t(c.crop[0]) * c.crop[1] * c.crop[2] * 5;
+}
+
 // Geometry of the bytes a sample's chain reads, as strided boxes (K0 copies
 // them from pinned host memory; see kernels.h for the row-skew convention).
 struct Box {
@@ -564,7 +616,7 @@ static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) 
     wd[0] = wd[1] = wd[2] = 0;
     if (c.fam == FAM_IMG3D) {
         const int64_t H = s.dims[1], W = s.dims[2];
-        for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(c.crop[a], s.dims[a] - t.p3.off[a]);
+        for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(t.p3.win[a], s.dims[a] - t.p3.off[a]);
         const int64_t first = (t.p3.off[0] * H + t.p3.off[1]) * W + t.p3.off[2];
         out[0] = Box{static_cast<const char*>(s.data) + first * 4, W * 4, H * W * 4,
                      static_cast<int32_t>(wd[2] * 4), static_cast<int32_t>(wd[1]),
@@ -871,7 +923,7 @@ void Context::launch_group(Group& g) {
             for (int a = 0; a < 3; ++a) L.crop[a] = c.crop[a];
             L.n = n;
             // TMA tile path: HBM-resident volumes with 16-B aligned rows
-            bool tma = !staged && img3d_tma_;
+            bool tma = !staged && img3d_tma_ && !c.has_zoom;
             for (int i = 0; i < n && tma; ++i) {
                 const lfg_sample_desc& sd = tickets[g.tickets[i]].desc;
                 tma = img3d_tma_ok(sd.data, sd.aux, sd.dims, c.crop) &&
@@ -906,10 +958,37 @@ void Context::launch_group(Group& g) {
                 d.sigma = static_cast<float>(t.p3.sigma);
                 d.key0 = t.p3.key[0];
                 d.key1 = t.p3.key[1];
-                counters.kernel_bytes += c.algo_bytes_per_sample(t.desc);
+                for (int a = 0; a < 3; ++a) d.win[a] = static_cast<int32_t>(t.p3.win[a]);
+                d.contrast = static_cast<float>(t.p3.contrast);
+                d.csum = nullptr;
+                counters.kernel_bytes += img3d_algo_bytes(c, t);
+            }
+            // RandomContrast: K5 sums each contrasted sample's crop first (same stream)
+            if (c.has_contrast) {
+                Img3dLaunch M{};
+                for (int a = 0; a < 3; ++a) M.crop[a] = c.crop[a];
+                for (int i = 0; i < n; ++i) {
+                    if (tickets[g.tickets[i]].p3.contrast == 1.0) continue;
+                    L.d[i].csum = csum_ + csum_next_;
+                    csum_next_ = (csum_next_ + 1) % kCsumSlots;
+                    M.d[M.n++] = L.d[i];
+                    const Img3dDesc& d = L.d[i];
+                    counters.kernel_bytes += int64_t(4) * std::min(d.win[0], d.sdim[0] - d.off[0]) *
+                                             std::min(d.win[1], d.sdim[1] - d.off[1]) *
+                                             std::min(d.win[2], d.sdim[2] - d.off[2]);
+                }
+                if (M.n > 0) {
+                    start();
+                    for (int i = 0; i < M.n; ++i)
+                        cuda_check(cudaMemsetAsync(const_cast<double*>(M.d[i].csum), 0, sizeof(double), st),
+                                   "csum reset");
+                    cuda_check(launch_img3d_mean(M, st), "img3d mean launch");
+                    counters.launches++;
+                }
             }
             start();
-            cuda_check(launch_img3d(L, st), "img3d launch");
+            if (c.has_zoom) cuda_check(launch_img3d_zoom(L, st), "img3d zoom launch");
+            else cuda_check(launch_img3d(L, st), "img3d launch");
             prof_launch_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_l).count();
             counters.launches++;
         } else if (S.kind == ST_RRC2D) {

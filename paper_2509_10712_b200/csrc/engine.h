@@ -83,6 +83,8 @@ struct Chain {
     // img3d
     int crop[3] = {128, 128, 128};
     double p_flip = 0, p_bright = 0, b_lo = 1, b_hi = 1, p_noise = 0, noise_max = 0;
+    bool has_zoom = false, has_contrast = false;     // optional RandomZoom3D / RandomContrast
+    double p_zoom = 0, z_lo = 1, z_hi = 1, p_contrast = 0, c_lo = 1, c_hi = 1;
     // rrc2d
     int oh = 224, ow = 224;
     double scale_lo = 0.08, scale_hi = 1.0, ratio_lo = 0.75, ratio_hi = 4.0 / 3.0, p_hflip = 0;
@@ -101,7 +103,14 @@ struct Chain {
 };
 
 // Per-sample drawn parameters (host, std::mt19937_64 keyed by sample id).
-struct Params3D { int64_t off[3]; int flip[3]; double scale, sigma; uint32_t key[2]; };
+struct Params3D {
+    int64_t off[3];
+    int flip[3];
+    double scale, sigma;
+    uint32_t key[2];
+    int64_t win[3];       // source window edge (RandomZoom3D; = crop otherwise)
+    double contrast;      // RandomContrast factor (1 = not applied)
+};
 struct Params2D { int64_t top, left, h, w; int flip; int64_t rows_touched; };
 struct ParamsSp { int T; int f_lo[2], f_w[2]; int t_lo[10], t_w[10]; };
 
@@ -239,6 +248,9 @@ private:
     std::vector<std::unique_ptr<Chain>> chains_;
     SpeechTables* speech_ = nullptr;   // DFT basis + mel tables, created with the first speech chain
     bool img3d_tma_ = true;            // LFG_IMG3D_TMA=0 forces the row kernel (A/B checks)
+    static constexpr int kCsumSlots = 4096;   // RandomContrast crop sums (a ring; stream-ordered)
+    double* csum_ = nullptr;
+    int csum_next_ = 0;
     std::vector<cudaStream_t> streams_;
     std::vector<int> free_streams_;
     std::vector<cudaEvent_t> free_events_;

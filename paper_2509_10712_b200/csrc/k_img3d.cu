@@ -58,6 +58,8 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
     const bool flip_w = (d.flip & 4) != 0;
     const int valid_w = d.sdim[2] - d.off[2];             // window columns inside the source
     const bool noise = d.sigma != 0.0f;
+    float A, B;                                           // brightness (+ contrast) affine
+    img3d_affine(d, (int64_t)cd * ch * cw, A, B);
 
     for (int qx = threadIdx.x; qx < cw4; qx += 32) {
         const int qs = flip_w ? cw4 - 1 - qx : qx;         // source quad (logical columns 4qs..4qs+3)
@@ -108,8 +110,8 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
             const int y = ys[r];
             if (y >= ch) continue;
             const int64_t vox = ((int64_t)z * ch + y) * cw + 4 * qx;   // output voxel index
-            float o[4] = {v[r].x * d.scale, v[r].y * d.scale, v[r].z * d.scale,
-                          v[r].w * d.scale};                          // RandomBrightness
+            float o[4] = {fmaf(v[r].x, A, B), fmaf(v[r].y, A, B), fmaf(v[r].z, A, B),
+                          fmaf(v[r].w, A, B)};                        // RandomBrightness / Contrast
             if (noise) {                                               // GaussianNoise
                 const uint64_t g = (uint64_t)vox >> 2;
                 const uint4 rnd = philox4x32_10(
@@ -168,12 +170,13 @@ struct __align__(16) TileRec {
     float* out_img;          // output voxel (z, y0, 0) of this tile
     uint8_t* out_lbl;
     uint64_t q0;             // Philox group of the tile's first voxel
-    float scale, sigma;      // brightness multiplier, noise std (0 = none)
+    float scale, sigma;      // affine A (brightness [x contrast]), noise std (0 = none)
     uint32_t key0, key1;
     int32_t rows;            // valid output rows (y0 + r < ch)
     int32_t flags;           // bit 0 flip_y, bit 1 flip_w
     int32_t wl0, m;          // realignment: first label word inside the box row, element shift
-    int32_t pad[2];
+    float bias;              // affine B (contrast; 0 otherwise)
+    int32_t pad;
 };
 static_assert(sizeof(TileRec) == 64, "tile record is one 64-B slot");
 
@@ -226,7 +229,7 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
                 tr.out_img = d.out_img + v0;
                 tr.out_lbl = d.out_lbl + v0;
                 tr.q0 = (uint64_t)v0 >> 2;
-                tr.scale = d.scale;
+                img3d_affine(d, (int64_t)cd * ch * cw, tr.scale, tr.bias);
                 tr.sigma = d.sigma;
                 tr.key0 = d.key0;
                 tr.key1 = d.key1;
@@ -234,7 +237,7 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
                 tr.flags = ((d.flip >> 1) & 1) | (((d.flip >> 2) & 1) << 1);
                 tr.wl0 = (d.off[2] & (kPadLbl - 1)) >> 2;
                 tr.m = d.off[2] & 3;
-                tr.pad[0] = tr.pad[1] = 0;
+                tr.pad = 0;
                 rec[s] = tr;
                 if (L.debug & 2) {   // profiling switch: no loads
                     mbar_arrive(full + s);
@@ -277,7 +280,8 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
                     lb = __byte_perm(lb, 0, 0x0123);
                 }
                 const int vo = r * cw + 4 * qx;   // voxel offset inside the tile
-                float o[4] = {x.x * tr.scale, x.y * tr.scale, x.z * tr.scale, x.w * tr.scale};
+                float o[4] = {fmaf(x.x, tr.scale, tr.bias), fmaf(x.y, tr.scale, tr.bias),
+                              fmaf(x.z, tr.scale, tr.bias), fmaf(x.w, tr.scale, tr.bias)};
                 if (tr.sigma != 0.0f) {
                     const uint64_t g = tr.q0 + (uint64_t)(vo >> 2);
                     const uint4 rnd = philox4x32_10(

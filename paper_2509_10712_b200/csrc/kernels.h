@@ -55,7 +55,22 @@ struct Img3dDesc {
     float scale;             // brightness multiplier
     float sigma;             // noise std (0 = no noise)
     uint32_t key0, key1;     // Philox key
+    int32_t win[3];          // source window edge (RandomZoom3D; = crop otherwise)
+    float contrast;          // RandomContrast factor (1 = not applied)
+    const double* csum;      // contrast: sum of the (resampled) crop, written by K5 (null: none)
 };
+// Contrast folded into one affine per sample: out = A * v + B (+ noise), with
+// A = scale * c and B = scale * (1 - c) * mean, mean = csum / crop voxels.
+__device__ __forceinline__ void img3d_affine(const Img3dDesc& d, int64_t crop_vox, float& A, float& B) {
+    if (d.csum == nullptr) {
+        A = d.scale;
+        B = 0.0f;
+        return;
+    }
+    const double mean = *d.csum / (double)crop_vox;
+    A = (float)((double)d.scale * (double)d.contrast);
+    B = (float)((double)d.scale * (1.0 - (double)d.contrast) * mean);
+}
 struct Img3dLaunch {
     int32_t crop[3];
     int32_t n;
@@ -140,6 +155,11 @@ struct GatherLaunch {
 
 cudaError_t launch_stage(const StageLaunch& L, cudaStream_t s);
 cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s);
+// K4: RandomZoom3D chains (trilinear image / nearest label resample of the window)
+cudaError_t launch_img3d_zoom(const Img3dLaunch& L, cudaStream_t s);
+// K5: per-sample sum of the (resampled) crop for RandomContrast; L.d[i].csum
+// must point at zeroed doubles
+cudaError_t launch_img3d_mean(const Img3dLaunch& L, cudaStream_t s);
 // encodes L.tm_img[i] / L.tm_lbl[i] for a D,H,W f32 volume + u8 label (see img3d_tma_ok)
 cudaError_t img3d_encode_maps(Img3dLaunch& L, int i, const void* img, const void* lbl,
                               const int64_t dims[3]);
@@ -153,6 +173,7 @@ int rrc2d_smem_bytes(const RrcLaunch& L);
 // of a kernel loads its module, which can stall the shard loop mid-run.
 cudaError_t warm_stage();
 cudaError_t warm_img3d();
+cudaError_t warm_img3d_zoom();
 cudaError_t warm_rrc2d();
 cudaError_t warm_misc();
 

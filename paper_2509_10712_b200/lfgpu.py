@@ -30,6 +30,7 @@ ERR_INVALID, ERR_STATE, ERR_CLOSED, ERR_AGAIN, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPOR
     -1, -2, -3, -4, -5, -6, -7)
 
 OP_RANDOM_CROP, OP_RANDOM_FLIP, OP_RANDOM_BRIGHTNESS, OP_GAUSSIAN_NOISE, OP_CAST = 1, 2, 3, 4, 5
+OP_RANDOM_ZOOM3D, OP_RANDOM_CONTRAST = 6, 7      # optional img_seg ops (not in the reference chain)
 OP_RESIZE, OP_RANDOM_HFLIP, OP_TO_TENSOR, OP_NORMALIZE = 10, 11, 12, 13
 OP_PAD, OP_SPEC_AUGMENT, OP_FILTER_BANK, OP_FRAME_SPLICING, OP_PERMUTE_AUDIO = 20, 21, 22, 23, 24
 OP_SPIN = 30
@@ -171,13 +172,25 @@ def op(kind: int, name: str, size_factor: float = 1.0, params: Sequence[float] =
 
 
 def img_seg_ops(crop=(128, 128, 128), p_flip=1 / 3, p_bright=0.1, bright=(0.7, 1.3),
-                p_noise=0.1, noise_std_max=0.1, spin_first: bool = False) -> list[Op]:
-    """img_seg chain, proj/src/workloads.cpp:142-148 (size factors included)."""
+                p_noise=0.1, noise_std_max=0.1, spin_first: bool = False,
+                zoom=None, contrast=None) -> list[Op]:
+    """img_seg chain, proj/src/workloads.cpp:142-148 (size factors included).
+
+    Optional ops (north_star "trilinear resize" / "brightness/contrast"; not in the
+    reference chain, so off by default): ``zoom=(p, lo, hi)`` adds RandomZoom3D after
+    RandomCrop (window edge round(crop * f), trilinear back to the crop; labels
+    nearest); ``contrast=(p, lo, hi)`` adds RandomContrast after RandomBrightness."""
     ops = [op(OP_SPIN, "SampleCost")] if spin_first else []
+    ops.append(op(OP_RANDOM_CROP, "RandomCrop", 0.0735, crop))
+    if zoom is not None:
+        ops.append(op(OP_RANDOM_ZOOM3D, "RandomZoom3D", 1.0, list(zoom)))
     ops += [
-        op(OP_RANDOM_CROP, "RandomCrop", 0.0735, crop),
         op(OP_RANDOM_FLIP, "RandomFlip", 1.0, [p_flip]),
         op(OP_RANDOM_BRIGHTNESS, "RandomBrightness", 1.0, [p_bright, bright[0], bright[1]]),
+    ]
+    if contrast is not None:
+        ops.append(op(OP_RANDOM_CONTRAST, "RandomContrast", 1.0, list(contrast)))
+    ops += [
         op(OP_GAUSSIAN_NOISE, "GaussianNoise", 1.0, [p_noise, noise_std_max]),
         op(OP_CAST, "Cast", 1.0),
     ]

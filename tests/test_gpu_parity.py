@@ -114,6 +114,70 @@ def test_img3d_matches_oracle(ctx, lfgpu, oracle, case, src_kind):
     ctx.destroy_chain(ch)
 
 
+# ------------------------------------------------------------------ optional img_seg ops (K4 / K5)
+CASES_ZC = [
+    # (dims, crop, zoom, contrast, probability overrides)
+    ((30, 34, 40), (16, 16, 32), (1.0, 0.7, 1.3), None, dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),
+    ((20, 24, 48), (16, 16, 32), None, (1.0, 0.75, 1.25), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),  # K1 TMA + K5
+    ((20, 24, 40), (16, 16, 32), None, (1.0, 0.75, 1.25), dict(p_flip=0.5, p_bright=1.0, p_noise=0.0)),  # K1 row + K5
+    ((30, 34, 40), (16, 16, 32), (1.0, 0.7, 1.3), (1.0, 0.5, 1.5), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),
+    ((12, 14, 20), (16, 16, 32), (1.0, 0.8, 1.2), (1.0, 0.75, 1.25), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),  # zero pad
+    ((140, 150, 160), (128, 128, 128), (0.5, 0.8, 1.2), (0.5, 0.75, 1.25), dict()),
+]
+
+
+@pytest.mark.parametrize("src_kind", [0, 1], ids=["device", "host_pinned"])
+@pytest.mark.parametrize("case", range(len(CASES_ZC)))
+def test_img3d_zoom_contrast_matches_oracle(ctx, lfgpu, oracle, case, src_kind):
+    """RandomZoom3D (K4: trilinear image, nearest label) and RandomContrast (K5 crop
+    sum + the affine in K1 / K4) against the oracle: labels bit-exact, window and
+    contrast draws exact, image within the 3D tolerance."""
+    dims, crop, zoom, contrast, probs = CASES_ZC[case]
+    kw = dict(p_flip=1 / 3, p_bright=0.1, p_noise=0.1)
+    kw.update(probs)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, zoom=zoom, contrast=contrast, **kw))
+    okw = dict(kw)
+    if zoom is not None:
+        okw.update(has_zoom=1, p_zoom=zoom[0], zoom_lo=zoom[1], zoom_hi=zoom[2])
+    if contrast is not None:
+        okw.update(has_contrast=1, p_contrast=contrast[0], contrast_lo=contrast[1],
+                   contrast_hi=contrast[2])
+    ocfg = oracle.cfg3d(crop=crop, **okw)
+    rng = np.random.default_rng(300 + case)
+    ids = [int(x) for x in rng.integers(0, 1 << 40, 4 if crop[0] == 128 else 10)]
+    vox = int(np.prod(crop))
+    bufs, tickets, expect = [], [], []
+    for sid in ids:
+        img = (rng.standard_normal(dims) + 0.5).astype(np.float32)
+        lbl = rng.integers(0, 3, dims, dtype=np.uint8)
+        if src_kind == 0:
+            pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+            bufs += [("d", pi), ("d", pl)]
+        else:
+            pi, pl = _pinned(ctx, img), _pinned(ctx, lbl)
+            bufs += [("h", pi), ("h", pl)]
+        desc = lfgpu.sample_desc(sid, dims, pi, pl, src_kind=src_kind)
+        p = ch.draw_params(SEED, desc)
+        op_ = oracle.draw3d(ocfg, SEED, sid, dims)
+        assert list(p[:3]) == list(op_.off) and list(p[3:6]) == list(op_.flip)
+        assert p[6] == op_.scale and p[7] == op_.sigma and list(p[8:10]) == list(op_.key)
+        assert list(p[10:13]) == list(op_.win) and p[13] == op_.contrast
+        tickets.append(ctx.submit(ch, desc))
+        expect.append(oracle.apply3d(ocfg, op_, img, lbl))
+    ctx.flush()
+    for t, (e_img, e_lbl) in zip(tickets, expect):
+        ctx.wait(t)
+        raw = ctx.ticket_output(t, vox * 4 + ((vox + 15) // 16) * 16)
+        g_img = raw[: vox * 4].view(np.float32).reshape(crop)
+        g_lbl = raw[vox * 4: vox * 5].reshape(crop)
+        assert np.array_equal(g_lbl, e_lbl), "label resample/crop/flip is not bit-exact"
+        _assert_close(g_img, e_img, atol=1e-6)
+        ctx.release(t)
+    for kind, p in bufs:
+        (ctx.device_free if kind == "d" else ctx.host_free)(p)
+    ctx.destroy_chain(ch)
+
+
 # ------------------------------------------------------------------ obj_det (K3)
 @pytest.mark.parametrize("src_kind", [0, 1], ids=["device", "host_pinned"])
 def test_rrc2d_matches_oracle(ctx, lfgpu, oracle, src_kind):

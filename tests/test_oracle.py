@@ -186,3 +186,74 @@ def test_specaugment_masks_in_range(oracle):
             assert 0 <= p.f_w[i] <= 27 and 0 <= p.f_lo[i] and p.f_lo[i] + p.f_w[i] <= 80
         for i in range(10):
             assert 0 <= p.t_w[i] <= int(0.05 * T) and p.t_lo[i] + p.t_w[i] <= T
+
+
+# ------------------------------------------------------------ optional ops (zoom, contrast)
+def test_zoom_trilinear_matches_torch_interpolate(oracle):
+    """RandomZoom3D: the zoomed window resampled to the crop equals torch's trilinear
+    F.interpolate(align_corners=False) of the zero-padded window (fp64, exact); labels
+    take the integer nearest index min(dst * win // crop, win - 1)."""
+    import torch
+    rng = np.random.default_rng(7)
+    dims = (30, 34, 40)
+    img = rng.standard_normal(dims).astype(np.float32)
+    lbl = rng.integers(0, 5, dims, dtype=np.uint8)
+    crop = (16, 16, 32)
+    cfg = oracle.cfg3d(crop=crop, has_zoom=1, p_zoom=1.0, zoom_lo=0.7, zoom_hi=1.3,
+                       p_flip=0.0, p_bright=0.0, p_noise=0.0)
+    zoomed = 0
+    for sid in range(12):
+        (o_img, o_lbl), p = oracle.chain3d(cfg, SEED, sid, img, lbl)
+        w, o = list(p.win), list(p.off)
+        zoomed += w != list(crop)
+        win = np.zeros(w)
+        wl = np.zeros(w, np.uint8)
+        src = img[o[0]:o[0] + w[0], o[1]:o[1] + w[1], o[2]:o[2] + w[2]]
+        win[:src.shape[0], :src.shape[1], :src.shape[2]] = src
+        wl[:src.shape[0], :src.shape[1], :src.shape[2]] = lbl[o[0]:o[0] + w[0], o[1]:o[1] + w[1],
+                                                              o[2]:o[2] + w[2]]
+        t = torch.nn.functional.interpolate(torch.from_numpy(win)[None, None], size=crop,
+                                            mode="trilinear", align_corners=False)[0, 0].numpy()
+        assert np.abs(t - o_img).max() < 1e-12
+        idx = [np.minimum(np.arange(crop[a]) * w[a] // crop[a], w[a] - 1) for a in range(3)]
+        assert np.array_equal(o_lbl, wl[np.ix_(*idx)])
+    assert zoomed >= 8
+
+
+def test_zoom_window_equal_to_crop_is_a_plain_crop(oracle):
+    cfg = oracle.cfg3d(crop=(8, 8, 16), has_zoom=1, p_zoom=1.0, zoom_lo=1.0, zoom_hi=1.0,
+                       p_flip=0.5, p_bright=0.0, p_noise=0.0)
+    dims = (10, 12, 20)
+    img = np.arange(int(np.prod(dims)), dtype=np.float32).reshape(dims)
+    lbl = (img.astype(np.int64) % 251).astype(np.uint8)
+    for sid in range(20):
+        (o_img, o_lbl), p = oracle.chain3d(cfg, SEED, sid, img, lbl)
+        assert list(p.win) == [8, 8, 16]
+        want = img[tuple(slice(p.off[a], p.off[a] + (8, 8, 16)[a]) for a in range(3))]
+        for a in range(3):
+            if p.flip[a]:
+                want = np.flip(want, axis=a)
+        assert np.array_equal(o_img, want.astype(np.float64))
+
+
+def test_contrast_scales_deviation_about_the_crop_mean(oracle):
+    """RandomContrast: (v - m) * c + m with m the crop mean (after brightness)."""
+    rng = np.random.default_rng(9)
+    dims = (12, 20, 24)
+    img = (rng.standard_normal(dims) + 0.3).astype(np.float32)
+    lbl = np.zeros(dims, np.uint8)
+    base = oracle.cfg3d(crop=(8, 8, 16), p_flip=0.0, p_bright=1.0, p_noise=0.0)
+    cfg = oracle.cfg3d(crop=(8, 8, 16), p_flip=0.0, p_bright=1.0, p_noise=0.0,
+                       has_contrast=1, p_contrast=1.0)
+    for sid in range(10):
+        p = oracle.draw3d(cfg, SEED, sid, dims)
+        assert 0.75 <= p.contrast <= 1.25
+        out, _ = oracle.apply3d(cfg, p, img, lbl)
+        q = oracle.draw3d(base, SEED, sid, dims)   # same crop, no contrast
+        for a in range(3):
+            q.off[a] = p.off[a]
+        q.scale = p.scale
+        plain, _ = oracle.apply3d(base, q, img, lbl)
+        m = plain.mean()
+        assert abs(out.mean() - m) < 1e-12
+        assert np.abs((out - m) - p.contrast * (plain - m)).max() < 1e-12
