@@ -958,7 +958,10 @@ void Context::launch_group(Group& g) {
                 d.sigma = static_cast<float>(t.p3.sigma);
                 d.key0 = t.p3.key[0];
                 d.key1 = t.p3.key[1];
-                for (int a = 0; a < 3; ++a) d.win[a] = static_cast<int32_t>(t.p3.win[a]);
+                for (int a = 0; a < 3; ++a) {
+                    d.win[a] = static_cast<int32_t>(t.p3.win[a]);
+                    d.zscale[a] = static_cast<double>(t.p3.win[a]) / static_cast<double>(c.crop[a]);
+                }
                 d.contrast = static_cast<float>(t.p3.contrast);
                 d.csum = nullptr;
                 counters.kernel_bytes += img3d_algo_bytes(c, t);

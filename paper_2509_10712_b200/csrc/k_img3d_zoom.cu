@@ -8,8 +8,9 @@
 // transforms, added as optional ops.  Semantics: oracle/lf_oracle.c
 // lfo_draw3d / lfo_apply3d.
 //
-// K4 mapping: grid (ceil(ch / 8), cd, n), block (32, 8): a warp per output
-// row, a lane per 4 consecutive output voxels (one Philox block, as K1).  The
+// K4 mapping: grid (ceil(ch / 8), ceil(cd / 8), n), block (32, 8): a warp per
+// output row (for 8 consecutive output planes), a lane per 4 consecutive output
+// voxels (one Philox block, as K1).  The
 // CTA's per-column taps (source columns, fp32 weights, nearest label column)
 // are computed once into shared memory in fp64 with the oracle's exact
 // (non-contracted) operations, so tap indices always agree with the oracle;
@@ -34,13 +35,14 @@ namespace lfg {
 namespace {
 
 constexpr int kZRows = 8;          // output rows per CTA (threadIdx.y)
+constexpr int kZPlanes = 8;        // output planes per CTA
 constexpr int kMaxCrop = 1024;
 
 // PyTorch area_pixel_compute_source_index (align_corners=False) + linear taps,
 // fp64 with _rn intrinsics (no FMA contraction): identical to linear_taps() of
 // the oracle.
-__device__ __forceinline__ void taps(int dst, int in, int out, int& i0, int& i1, double& l0, double& l1) {
-    const double scale = __ddiv_rn((double)in, (double)out);
+// `scale` is (double)in / (double)out, divided once on the host (IEEE, as the oracle).
+__device__ __forceinline__ void taps(int dst, int in, double scale, int& i0, int& i1, double& l0, double& l1) {
     double src = __dadd_rn(__dmul_rn(scale, __dadd_rn((double)dst, 0.5)), -0.5);
     if (src < 0.0) src = 0.0;
     int a = (int)floor(src);
@@ -77,20 +79,13 @@ __global__ void __launch_bounds__(32 * kZRows) img3d_zoom_kernel(const __grid_co
         const int wx = flip_w ? cw - 1 - x : x;
         int i0, i1;
         double l0, l1;
-        taps(wx, d.win[2], cw, i0, i1, l0, l1);
+        taps(wx, d.win[2], d.zscale[2], i0, i1, l0, l1);
         // taps past the source edge read zero: fold that into the weights
         sx_tap[x] = make_int2(i0 < valid_w ? i0 : 0, i1 < valid_w ? i1 : 0);
         sx_w[x] = make_float2(i0 < valid_w ? (float)l0 : 0.f, i1 < valid_w ? (float)l1 : 0.f);
-        const int nx = min((int)(((int64_t)wx * d.win[2]) / cw), d.win[2] - 1);
+        const int nx = min(wx * d.win[2] / cw, d.win[2] - 1);
         sx_near[x] = nx < valid_w ? nx : -1;
     }
-    const int z = blockIdx.y;
-    const int wz = (d.flip & 1) ? cd - 1 - z : z;
-    int z0, z1;
-    double lz0d, lz1d;
-    taps(wz, d.win[0], cd, z0, z1, lz0d, lz1d);
-    const float lz0 = (float)lz0d, lz1 = (float)lz1d;
-    const int nz = min((int)(((int64_t)wz * d.win[0]) / cd), d.win[0] - 1);
     float A, B;
     img3d_affine(d, (int64_t)cd * ch * cw, A, B);
     const bool noise = d.sigma != 0.0f;
@@ -101,52 +96,63 @@ __global__ void __launch_bounds__(32 * kZRows) img3d_zoom_kernel(const __grid_co
     const int wy = (d.flip & 2) ? ch - 1 - y : y;
     int y0, y1;
     double ly0d, ly1d;
-    taps(wy, d.win[1], ch, y0, y1, ly0d, ly1d);
+    taps(wy, d.win[1], d.zscale[1], y0, y1, ly0d, ly1d);
     const float ly0 = (float)ly0d, ly1 = (float)ly1d;
-    const int ny = min((int)(((int64_t)wy * d.win[1]) / ch), d.win[1] - 1);
-    const float* r00 = img_row(d, z0, y0);
-    const float* r01 = img_row(d, z0, y1);
-    const float* r10 = img_row(d, z1, y0);
-    const float* r11 = img_row(d, z1, y1);
-    const uint8_t* rl = lbl_row(d, nz, ny);
-    auto tap_row = [&](const float* r, int2 t, float2 w) -> float {
-        if (r == nullptr) return 0.0f;
-        return fmaf(w.x, __ldg(r + t.x), w.y * __ldg(r + t.y));
-    };
+    const int ny = min(wy * d.win[1] / ch, d.win[1] - 1);
     const int cw4 = cw >> 2;
-    for (int q = threadIdx.x; q < cw4; q += 32) {
-        float o[4];
-        uint32_t lb = 0;
+    // the CTA's rows, for kZPlanes consecutive output planes (amortises the column table)
+    const int z_end = min(cd, (int)(blockIdx.y + 1) * kZPlanes);
+    for (int z = blockIdx.y * kZPlanes; z < z_end; ++z) {
+        const int wz = (d.flip & 1) ? cd - 1 - z : z;
+        int z0, z1;
+        double lz0d, lz1d;
+        taps(wz, d.win[0], d.zscale[0], z0, z1, lz0d, lz1d);
+        const float lz0 = (float)lz0d, lz1 = (float)lz1d;
+        const int nz = min(wz * d.win[0] / cd, d.win[0] - 1);
+        const float* r00 = img_row(d, z0, y0);
+        const float* r01 = img_row(d, z0, y1);
+        const float* r10 = img_row(d, z1, y0);
+        const float* r11 = img_row(d, z1, y1);
+        const uint8_t* rl = lbl_row(d, nz, ny);
+        auto tap_row = [&](const float* r, int2 t, float2 w) -> float {
+            if (r == nullptr) return 0.0f;
+            return fmaf(w.x, __ldg(r + t.x), w.y * __ldg(r + t.y));
+        };
+        for (int q = threadIdx.x; q < cw4; q += 32) {
+            float o[4];
+            uint32_t lb = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int x = 4 * q + k;
-            const int2 t = sx_tap[x];
-            const float2 w = sx_w[x];
-            const float a = fmaf(ly0, tap_row(r00, t, w), ly1 * tap_row(r01, t, w));
-            const float b = fmaf(ly0, tap_row(r10, t, w), ly1 * tap_row(r11, t, w));
-            o[k] = fmaf(A, fmaf(lz0, a, lz1 * b), B);
-            const int nx = sx_near[x];
-            if (rl != nullptr && nx >= 0) lb |= (uint32_t)__ldg(rl + nx) << (8 * k);
+            for (int k = 0; k < 4; ++k) {
+                const int x = 4 * q + k;
+                const int2 t = sx_tap[x];
+                const float2 w = sx_w[x];
+                const float a = fmaf(ly0, tap_row(r00, t, w), ly1 * tap_row(r01, t, w));
+                const float b = fmaf(ly0, tap_row(r10, t, w), ly1 * tap_row(r11, t, w));
+                o[k] = fmaf(A, fmaf(lz0, a, lz1 * b), B);
+                const int nx = sx_near[x];
+                if (rl != nullptr && nx >= 0) lb |= (uint32_t)__ldg(rl + nx) << (8 * k);
+            }
+            const int64_t vox = ((int64_t)z * ch + y) * cw + 4 * q;
+            if (noise) {
+                const uint64_t g = (uint64_t)vox >> 2;
+                const uint4 rnd =
+                    philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, 0u), d.key0, d.key1);
+                const float2 z01 = box_muller(rnd.x, rnd.y);
+                const float2 z23 = box_muller(rnd.z, rnd.w);
+                o[0] = fmaf(d.sigma, z01.x, o[0]);
+                o[1] = fmaf(d.sigma, z01.y, o[1]);
+                o[2] = fmaf(d.sigma, z23.x, o[2]);
+                o[3] = fmaf(d.sigma, z23.y, o[3]);
+            }
+            __stcs(reinterpret_cast<float4*>(d.out_img + vox), make_float4(o[0], o[1], o[2], o[3]));
+            __stcs(reinterpret_cast<unsigned int*>(d.out_lbl + vox), lb);
         }
-        const int64_t vox = ((int64_t)z * ch + y) * cw + 4 * q;
-        if (noise) {
-            const uint64_t g = (uint64_t)vox >> 2;
-            const uint4 rnd = philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, 0u), d.key0, d.key1);
-            const float2 z01 = box_muller(rnd.x, rnd.y);
-            const float2 z23 = box_muller(rnd.z, rnd.w);
-            o[0] = fmaf(d.sigma, z01.x, o[0]);
-            o[1] = fmaf(d.sigma, z01.y, o[1]);
-            o[2] = fmaf(d.sigma, z23.x, o[2]);
-            o[3] = fmaf(d.sigma, z23.y, o[3]);
-        }
-        __stcs(reinterpret_cast<float4*>(d.out_img + vox), make_float4(o[0], o[1], o[2], o[3]));
-        __stcs(reinterpret_cast<unsigned int*>(d.out_lbl + vox), lb);
     }
 }
 
 // c_a[i]: total linear weight source index i receives over all output positions
 // (deterministic: thread i walks the output positions that can tap it)
-__device__ __forceinline__ float axis_weight(int i, int win, int crop) {
+__device__ __forceinline__ float axis_weight(int i, int win, int crop, double scale) {
     if (win == crop) return 1.0f;
     const double inv = (double)crop / (double)win;
     int lo = (int)floor(((double)i - 0.5) * inv - 0.5) - 1;
@@ -157,7 +163,7 @@ __device__ __forceinline__ float axis_weight(int i, int win, int crop) {
     for (int dst = lo; dst <= hi; ++dst) {
         int i0, i1;
         double l0, l1;
-        taps(dst, win, crop, i0, i1, l0, l1);
+        taps(dst, win, scale, i0, i1, l0, l1);
         if (i0 == i) c += l0;
         if (i1 == i) c += l1;
     }
@@ -176,8 +182,8 @@ __global__ void __launch_bounds__(kMeanThreads) img3d_mean_kernel(const __grid_c
     const int ww = min(d.win[2], d.sdim[2] - d.off[2]);   // window extent inside the source
     const int wh = min(d.win[1], d.sdim[1] - d.off[1]);
     if (d.off[0] + z >= d.sdim[0] || ww <= 0 || wh <= 0) return;
-    for (int i = threadIdx.x; i < ww; i += kMeanThreads) cx[i] = axis_weight(i, d.win[2], L.crop[2]);
-    for (int i = threadIdx.x; i < wh; i += kMeanThreads) cy[i] = axis_weight(i, d.win[1], L.crop[1]);
+    for (int i = threadIdx.x; i < ww; i += kMeanThreads) cx[i] = axis_weight(i, d.win[2], L.crop[2], d.zscale[2]);
+    for (int i = threadIdx.x; i < wh; i += kMeanThreads) cy[i] = axis_weight(i, d.win[1], L.crop[1], d.zscale[1]);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double acc = 0.0;
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(kMeanThreads) img3d_mean_kernel(const __grid_c
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < kMeanThreads / 32; ++w) t += red[w];
-        atomicAdd(const_cast<double*>(d.csum), t * (double)axis_weight(z, d.win[0], L.crop[0]));
+        atomicAdd(const_cast<double*>(d.csum), t * (double)axis_weight(z, d.win[0], L.crop[0], d.zscale[0]));
     }
 }
 
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kMeanThreads) img3d_mean_kernel(const __grid_c
 cudaError_t launch_img3d_zoom(const Img3dLaunch& L, cudaStream_t s) {
     if (L.n <= 0) return cudaSuccess;
     if (L.crop[2] > kMaxCrop || (L.crop[2] & 3)) return cudaErrorInvalidValue;
-    dim3 grid((L.crop[1] + kZRows - 1) / kZRows, L.crop[0], L.n);
+    dim3 grid((L.crop[1] + kZRows - 1) / kZRows, (L.crop[0] + kZPlanes - 1) / kZPlanes, L.n);
     img3d_zoom_kernel<<<grid, dim3(32, kZRows), 0, s>>>(L);
     return cudaGetLastError();
 }

@@ -58,6 +58,7 @@ struct Img3dDesc {
     int32_t win[3];          // source window edge (RandomZoom3D; = crop otherwise)
     float contrast;          // RandomContrast factor (1 = not applied)
     const double* csum;      // contrast: sum of the (resampled) crop, written by K5 (null: none)
+    double zscale[3];        // RandomZoom3D source-index scale win / crop (IEEE division, host)
 };
 // Contrast folded into one affine per sample: out = A * v + B (+ noise), with
 // A = scale * c and B = scale * (1 - c) * mean, mean = csum / crop voxels.
