@@ -234,7 +234,8 @@ int lfg_time_kernels(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samp
  * resume -> completion events, batcher -> seal, consumer -> trainer stream). */
 typedef struct {
     int32_t batch_size;
-    int32_t policy;             /* 0 fixed t_out, 1 profiler (p75 -> p90 escalation) */
+    int32_t policy;             /* 0 fixed t_out, 1 profiler (p75 -> p90 escalation),
+                                   2 profiler at a fixed percentile (see `percentile`) */
     int64_t t_out_us;           /* fixed budget (policy 0) or initial budget (policy 1); <=0 = none */
     int64_t warmup_us;          /* profiler warm-up before the first percentile (profiler.hpp:41) */
     int64_t update_interval_us; /* profiler refresh period */
@@ -246,6 +247,8 @@ typedef struct {
     int32_t record_trace;       /* keep per-sample / per-batch records */
     int32_t d2h_probe;          /* read 16 bytes of every delivered batch back to the host
                                    on the trainer stream (end-to-end result check) */
+    int32_t percentile;         /* policy 2: nearest-rank percentile of the window (1..100);
+                                   the C5 timeout sweep (p50 / p75 / p90) */
 } lfg_run_config;
 
 typedef struct {

@@ -20,6 +20,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <memory>
 #include <random>
 #include <string>
@@ -224,12 +226,32 @@ int main(int argc, char** argv) {
     const int warmup = arg_int(argc, argv, "--warmup", 2);
     const int cores = arg_int(argc, argv, "--workers", (int)std::max(1u, std::thread::hardware_concurrency()));
     const int max_s = arg_int(argc, argv, "--max-seconds", 150);
+    // C5 sweep knobs: a heavy-tailed fraction of samples gets an
+    // extra synthetic cost (a leading "SampleCost" transform that sleeps), the
+    // consumer computes for trainer_ms per batch (trainer.hpp:15), and the
+    // timeout is the Profiler's p75/p90 policy (pct = -1, default) or a fixed
+    // nearest-rank percentile of the window (pct > 0) or none (pct = 0).
+    const double heavy_frac = std::atof(arg_str(argc, argv, "--heavy-frac", "0").c_str());
+    const int heavy_ms = arg_int(argc, argv, "--heavy-ms", 470);   // img_seg median cost, workloads.cpp:84-95
+    const int trainer_ms = arg_int(argc, argv, "--trainer-ms", 0);
+    const int pct = arg_int(argc, argv, "--pct", -1);
+    const int prof_warmup_ms = arg_int(argc, argv, "--profiler-warmup-ms", 2000);
     lfo_cfg2d_default(&g_c2);
     lfo_cfg3d_default(&g_c3);
     const bool rrc = wl == "rrc";
     const int B = rrc ? 256 : 2;
     const int64_t n = (int64_t)(steps + warmup) * B;
 
+    std::vector<Transform> heavy_ops;
+    if (heavy_frac > 0) {
+        heavy_ops.push_back(real("SampleCost", 1.0, [heavy_frac, heavy_ms](Payload p) {
+            // heavy iff a per-id uniform < heavy_frac (the id rides in the payload header)
+            std::mt19937_64 g(0x5eedULL ^ (0x9e3779b97f4a7c15ULL * ((uint64_t)p[0] + 1)));
+            if ((double)(g() >> 11) * 0x1.0p-53 < heavy_frac)
+                std::this_thread::sleep_for(std::chrono::milliseconds(heavy_ms));
+            return p;
+        }));
+    }
     TransformChain chain(rrc ? std::vector<Transform>{real("Resize", 1.2, resize_step),
                                                       real("RandomHorizontalFlip", 1.0, hflip_step),
                                                       real("ToTensor", 8.0, to_tensor_step),
@@ -239,10 +261,15 @@ int main(int argc, char** argv) {
                                                       real("RandomBrightness", 1.0, brightness_step),
                                                       real("GaussianNoise", 1.0, noise_step),
                                                       real("Cast", 1.0, cast_step)});
+    if (!heavy_ops.empty()) {
+        std::vector<Transform> ts = heavy_ops;
+        for (const auto& t : chain.transforms()) ts.push_back(t);
+        chain = TransformChain(std::move(ts));
+    }
     if (rrc) {
         // Resize needs the original (H, W) again at RandomHorizontalFlip to
         // re-derive the per-sample stream: carry it at the payload's tail
-        chain.transforms()[0].apply = [](Payload p) {
+        chain.transforms()[heavy_ops.size()].apply = [](Payload p) {
             const double H = p[1], W = p[2];
             Payload out = resize_step(std::move(p));
             out.push_back(W);
@@ -295,11 +322,21 @@ int main(int argc, char** argv) {
     BatchQueue batch_q(*rt, cap, QueueRole::batch);
     TimeoutPolicy policy;
     ProfilerConfig pc;
-    pc.warmup = 2000;   // ms; shortened from the 10 s default so the bounded run reaches p75
+    pc.warmup = prof_warmup_ms;   // ms; shortened from the 10 s default so the bounded run reaches p75
     Profiler prof(*rt, pc);
     std::vector<Rng> rngs;
     for (int i = 0; i < cores; ++i) rngs.emplace_back(kSeed ^ (0x9e3779b97f4a7c15ULL * (i + 1)));
     std::atomic<int64_t> n_slow{0};
+    // per-sample totals for the fixed-percentile policy (--pct > 0)
+    std::mutex win_mu;
+    std::deque<DurationMs> win;
+    auto record_total = [&](const std::vector<DurationMs>& c) {
+        DurationMs t = 0;
+        for (auto x : c) t += x;
+        std::lock_guard<std::mutex> lk(win_mu);
+        win.push_back(t);
+        if (win.size() > pc.window) win.pop_front();
+    };
     std::atomic<bool> give_up{false};
     const auto wall0 = std::chrono::steady_clock::now();
 
@@ -310,10 +347,12 @@ int main(int argc, char** argv) {
             const double sz = s.bytes_in;
             RouteResult r = process_sample(std::move(s), policy.timeout(), *fast[slot], *temp[slot],
                                            *rt, rngs[slot]);
-            if (r.route == Route::fast)
+            if (r.route == Route::fast) {
+                record_total(r.exec_costs);
                 prof.record(SampleStats::from_costs(id, sz, std::move(r.exec_costs), false));
-            else
+            } else {
                 n_slow++;
+            }
         },
         [&](int slot) {
             fast[slot]->close();
@@ -324,6 +363,7 @@ int main(int argc, char** argv) {
             Rng r(kSeed ^ (0xc2b2ae3d27d4eb4fULL * (i + 1)));
             resume_slow(*temp[i], *slow[i], *rt, r,
                         [&](const Sample& s, const std::vector<DurationMs>& c, DurationMs) {
+                            record_total(c);
                             prof.record(SampleStats::from_costs(s.id, s.bytes_in, c, true));
                         });
             slow[i]->close();
@@ -370,10 +410,25 @@ int main(int argc, char** argv) {
     ConsumerStats cs;
     rt->spawn("consumer", [&] {
         ConsumerConfig cc;
-        cc.compute_per_batch = 0;   // drain as fast as batches arrive: loader throughput
+        cc.compute_per_batch = trainer_ms;   // 0: drain as fast as batches arrive (loader throughput)
         cs = run_consumer(cc, batch_q, *rt);
     });
-    rt->spawn("profiler", [&] { profiler_loop(prof, policy, *rt, [&] { return pool_w.stopped(); }); });
+    if (pct < 0) {
+        rt->spawn("profiler", [&] { profiler_loop(prof, policy, *rt, [&] { return pool_w.stopped(); }); });
+    } else if (pct > 0) {   // fixed percentile: the reference's percentile() over the window
+        rt->spawn("profiler", [&] {
+            rt->sleep(pc.warmup);
+            while (!pool_w.stopped()) {
+                std::vector<DurationMs> v;
+                {
+                    std::lock_guard<std::mutex> lk(win_mu);
+                    v.assign(win.begin(), win.end());
+                }
+                if (!v.empty()) policy.set(percentile(std::move(v), pct), TimeoutPolicy::Source::configured);
+                rt->sleep(pc.update_interval);
+            }
+        });
+    }
     pool_w.start();
     rt->run();
 
@@ -387,10 +442,12 @@ int main(int argc, char** argv) {
         value = span_ms > 0 ? timed / (span_ms / 1000.0) : 0;
     }
     std::printf("{\"value\": %.3f, \"unit\": \"samples/s\", \"cores\": %d, \"kind\": \"reference\", "
+                "\"idle_frac\": %.4f, \"final_t_out_ms\": %lld, "
                 "\"samples\": %.0f, \"span_ms\": %.0f, \"slow\": %lld, \"truncated\": %s, "
                 "\"sample\": \"reference libloadflow (proj/src, realtime Minato wiring) with oracle "
                 "transforms over fp64 Payload: %s, %lld samples fed, batch %d, %d workers\"}\n",
-                value, cores, timed, span_ms, (long long)n_slow.load(), give_up ? "true" : "false",
+                value, cores, cs.idle_fraction(), (long long)policy.timeout(), timed, span_ms,
+                (long long)n_slow.load(), give_up ? "true" : "false",
                 rrc ? "RRC224+flip+ToTensor+Normalize on u8 3x(256..512)^2"
                     : "crop128^3+flip+brightness+noise+cast on 128x384x384",
                 (long long)cs.samples, B, cores);

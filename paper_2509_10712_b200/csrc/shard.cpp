@@ -43,6 +43,7 @@ struct Profile {
     std::deque<std::pair<int64_t, bool>> window;
     size_t cap = 1024;
     int pct = 75;
+    bool adaptive = true;   // false: a fixed percentile (policy 2, the C5 sweep)
     double escalate = 0.35, deescalate = 0.15;
 
     void record(int64_t total_us, bool slow) {
@@ -58,8 +59,8 @@ struct Profile {
             slow += w.second;
         }
         const double rate = double(slow) / double(window.size());
-        if (pct == 75 && rate > escalate) pct = 90;
-        else if (pct == 90 && window.size() == cap && rate < deescalate) pct = 75;
+        if (adaptive && pct == 75 && rate > escalate) pct = 90;
+        else if (adaptive && pct == 90 && window.size() == cap && rate < deescalate) pct = 75;
         std::sort(totals.begin(), totals.end());
         size_t rank = static_cast<size_t>(std::ceil(pct / 100.0 * double(totals.size())));
         if (rank == 0) rank = 1;
@@ -136,6 +137,11 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
 
     Profile prof;
     prof.cap = rc.window > 0 ? static_cast<size_t>(rc.window) : 1024;
+    if (rc.policy == 2) {
+        if (rc.percentile < 1 || rc.percentile > 100) fail(LFG_ERR_INVALID, "percentile must be in 1..100");
+        prof.pct = rc.percentile;
+        prof.adaptive = false;
+    }
     int64_t t_out = rc.t_out_us > 0 ? rc.t_out_us : kNoTimeoutUs;
     const int64_t run_t0 = host_now_us();
     int64_t last_update = run_t0;
@@ -399,7 +405,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             ph.lap(Phases::DELIVER);
         }
         // (5) profiler maintenance (profiler_loop, profiler.cpp:108-121)
-        if (rc.policy == 1 && !prof.window.empty() && now - run_t0 >= rc.warmup_us &&
+        if ((rc.policy == 1 || rc.policy == 2) && !prof.window.empty() && now - run_t0 >= rc.warmup_us &&
             now - last_update >= std::max<int64_t>(1, rc.update_interval_us)) {
             t_out = prof.update();
             last_update = now;

@@ -74,7 +74,7 @@ class RunConfig(C.Structure):
                 ("warmup_us", C.c_int64), ("update_interval_us", C.c_int64),
                 ("window", C.c_int32), ("n_workers", C.c_int32), ("trainer_us", C.c_int64),
                 ("trainer_priority", C.c_int32), ("warmup_batches", C.c_int32),
-                ("record_trace", C.c_int32), ("d2h_probe", C.c_int32)]
+                ("record_trace", C.c_int32), ("d2h_probe", C.c_int32), ("percentile", C.c_int32)]
 
 
 class RunReport(C.Structure):
@@ -445,7 +445,7 @@ class Context:
 def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: int = 0,
                warmup_batches: int = 0, n_workers: int = 0, warmup_us: int = 0,
                update_interval_us: int = 1000, window: int = 1024,
-               trainer_priority: int = 1, d2h_probe: int = 0) -> RunConfig:
+               trainer_priority: int = 1, d2h_probe: int = 0, percentile: int = 75) -> RunConfig:
     rc = RunConfig()
     rc.batch_size = batch_size
     rc.policy = policy
@@ -458,4 +458,5 @@ def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: 
     rc.trainer_priority = trainer_priority
     rc.warmup_batches = warmup_batches
     rc.d2h_probe = d2h_probe
+    rc.percentile = percentile
     return rc
