@@ -249,6 +249,11 @@ typedef struct {
                                    on the trainer stream (end-to-end result check) */
     int32_t percentile;         /* policy 2: nearest-rank percentile of the window (1..100);
                                    the C5 timeout sweep (p50 / p75 / p90) */
+    int32_t scheduler;          /* 1: adaptive in-flight group count (MinatoLoader Eq. 1-2,
+                                   scheduler.cpp:16-58 via loadflow/sched_rule.h): n_workers is
+                                   the initial count, grown / shrunk every sched_tick_us */
+    int32_t max_workers;        /* scheduler upper bound (0 = 2 x n_workers, <= 28 streams) */
+    int64_t sched_tick_us;      /* scheduler period (0 = 500 us) */
 } lfg_run_config;
 
 typedef struct {
@@ -264,6 +269,9 @@ typedef struct {
     double kernel_ms;           /* summed device time of transform stages in the timed window */
     int64_t h2d_bytes, d2h_bytes;
     int64_t launches;
+    int32_t final_workers;      /* in-flight group limit at the end (scheduler) */
+    int32_t sched_ticks;        /* scheduler decisions taken */
+    double mean_workers;        /* time-average of the in-flight group limit */
 } lfg_run_report;
 
 /* samples[i] are fed in order (the feeder, experiment.cpp:221-228).

@@ -28,6 +28,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -407,6 +408,43 @@ private:
     bool input_done_ = false;
     bool started_ = false;
 };
+
+// ---------------------------------------------------------------- adaptive scheduler (scheduler.hpp:13-52)
+// SURVEY 8(f) row 1.  Host pool: the reference's control loop over WorkerPool.
+// GPU shard: the same rule (sched_rule.h) resizes the number of in-flight
+// launch groups (lfg_run_config.scheduler), with c_usage = the stream pool's
+// busy fraction from CUDA events and q = delivered batches the trainer has not
+// consumed yet.
+struct SchedulerConfig {
+    double alpha = 2.0;   // queue-sensitivity scale
+    double beta = 2.0;    // CPU-sensitivity scale
+    double theta_c = 0.7; // utilization threshold
+    double q_max = 100;   // batch queue capacity
+    int delta_clip = 2;
+    int initial_workers = 12;
+    int max_workers = static_cast<int>(std::thread::hardware_concurrency());
+    DurationMs tick = 500;
+    double ema_alpha = 0.3; // smoothing for the queue-size moving average
+};
+
+struct SchedulerObservation {
+    double q_size_avg = 0; // moving average of batch-queue length, in [0, q_max]
+    double c_usage = 0;    // worker-pool busy fraction, in [0, 1]
+};
+
+struct SchedulerTraceRow {
+    TimeMs t = 0;
+    int workers = 0;
+    double q_avg = 0;
+    double c_usage = 0;
+    int delta = 0;
+};
+
+int compute_delta(const SchedulerObservation& obs, const SchedulerConfig& cfg);
+int update_workers(int current, int delta, const SchedulerConfig& cfg);
+void scheduler_loop(WorkerPool& pool, std::span<BatchQueue* const> batch_queues,
+                    const SchedulerConfig& cfg, Runtime& rt,
+                    std::vector<SchedulerTraceRow>* trace = nullptr);
 
 // ---------------------------------------------------------------- profiler (profiler.hpp:17-85)
 class InsufficientProfileData : public std::runtime_error {

@@ -28,6 +28,8 @@
 #include <memory>
 #include <deque>
 #include <thread>
+
+#include "loadflow/sched_rule.h"
 #include <unordered_map>
 
 #include "engine.h"
@@ -105,7 +107,18 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     if (n < 0 || (n > 0 && samples == nullptr)) fail(LFG_ERR_INVALID, "bad sample list");
     const int B = rc.batch_size > 0 ? rc.batch_size : ctx.cfg.batch_size;
     if (B > ctx.cfg.batch_size) fail(LFG_ERR_INVALID, "run batch_size exceeds context batch_size");
-    const int n_workers = rc.n_workers > 0 ? rc.n_workers : ctx.cfg.n_workers;
+    int n_workers = rc.n_workers > 0 ? rc.n_workers : ctx.cfg.n_workers;
+    // adaptive scheduler (scheduler.cpp:26-58 on the GPU): workers = in-flight groups,
+    // q = delivered batches the trainer has not finished, c = busy fraction of the
+    // in-flight slots over the tick (time-integral of inflight / limit)
+    const int max_workers = std::max(1, std::min(rc.max_workers > 0 ? rc.max_workers : 2 * n_workers,
+                                                 Context::kStreamPool));
+    if (rc.scheduler) n_workers = std::min(n_workers, max_workers);
+    const int64_t sched_tick = rc.sched_tick_us > 0 ? rc.sched_tick_us : 500;
+    const double q_max = std::max(1, ctx.cfg.max_slot_buffers);
+    double sched_ema = 0.0, busy_integral = 0.0, workers_integral = 0.0;
+    int64_t sched_last = 0, sched_prev_t = 0, sched_t0 = 0, sched_ticks = 0;
+    std::deque<cudaEvent_t> consume_q;   // one event per delivered batch, recorded after its trainer step
     const int cap = chain->fam == FAM_IMG3D ? kMax3D : (chain->fam == FAM_RRC2D ? kMax2D : kMaxSp);
     const int group = std::max(1, std::min(ctx.cfg.max_group, cap));
 
@@ -394,6 +407,11 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             }
             if (batch_sizes) batch_sizes[nbatches] = br.n;
             if (timed) timed_samples += br.n;
+            if (rc.scheduler) {
+                cudaEvent_t ce = mk();
+                cuda_check(cudaEventRecord(ce, trainer), "record consume");
+                consume_q.push_back(ce);
+            }
             ctx.batch_release(b, trainer, rc.trainer_us > 0 || probe != nullptr);
             for (int64_t t : ts) ctx.ticket_release(t);
             ++nbatches;
@@ -403,6 +421,28 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             }
             progressed = true;
             ph.lap(Phases::DELIVER);
+        }
+        // (5a) adaptive scheduler tick
+        if (rc.scheduler) {
+            const int64_t t = host_now_us();
+            if (sched_prev_t == 0) sched_prev_t = sched_last = sched_t0 = t;
+            const double dt = static_cast<double>(t - sched_prev_t);
+            busy_integral += dt * static_cast<double>(inflight.size());
+            workers_integral += dt * static_cast<double>(n_workers);
+            sched_prev_t = t;
+            if (t - sched_last >= sched_tick) {
+                while (!consume_q.empty() && cudaEventQuery(consume_q.front()) == cudaSuccess)
+                    consume_q.pop_front();
+                sched_ema = 0.3 * static_cast<double>(consume_q.size()) + 0.7 * sched_ema;
+                const double span = static_cast<double>(t - sched_last) * std::max(1, n_workers);
+                const double c_usage = std::clamp(busy_integral / span, 0.0, 1.0);
+                const int delta = lf_sched_delta(std::clamp(sched_ema, 0.0, q_max), c_usage, 2.0, 2.0, 0.7,
+                                                 q_max, 2);
+                n_workers = lf_sched_update(n_workers, delta, max_workers);
+                busy_integral = 0.0;
+                sched_last = t;
+                ++sched_ticks;
+            }
         }
         // (5) profiler maintenance (profiler_loop, profiler.cpp:108-121)
         if ((rc.policy == 1 || rc.policy == 2) && !prof.window.empty() && now - run_t0 >= rc.warmup_us &&
@@ -463,6 +503,11 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     rep.h2d_bytes = ctx.counters.h2d_bytes - c0.h2d_bytes;
     rep.d2h_bytes = ctx.counters.d2h_bytes - c0.d2h_bytes + probe_bytes;
     rep.launches = ctx.counters.launches - c0.launches;
+    rep.final_workers = n_workers;
+    rep.sched_ticks = static_cast<int32_t>(sched_ticks);
+    rep.mean_workers = workers_integral > 0 && sched_prev_t > sched_t0
+                           ? workers_integral / static_cast<double>(sched_prev_t - sched_t0)
+                           : static_cast<double>(n_workers);
     return LFG_OK;
 }
 

@@ -74,7 +74,8 @@ class RunConfig(C.Structure):
                 ("warmup_us", C.c_int64), ("update_interval_us", C.c_int64),
                 ("window", C.c_int32), ("n_workers", C.c_int32), ("trainer_us", C.c_int64),
                 ("trainer_priority", C.c_int32), ("warmup_batches", C.c_int32),
-                ("record_trace", C.c_int32), ("d2h_probe", C.c_int32), ("percentile", C.c_int32)]
+                ("record_trace", C.c_int32), ("d2h_probe", C.c_int32), ("percentile", C.c_int32),
+                ("scheduler", C.c_int32), ("max_workers", C.c_int32), ("sched_tick_us", C.c_int64)]
 
 
 class RunReport(C.Structure):
@@ -85,7 +86,8 @@ class RunReport(C.Structure):
                 ("consumer_span_ms", C.c_double), ("consumer_idle_frac", C.c_double),
                 ("final_t_out_us", C.c_double), ("final_percentile", C.c_int32),
                 ("exactly_once", C.c_int32), ("duplicates", C.c_int64), ("kernel_ms", C.c_double),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("launches", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("launches", C.c_int64),
+                ("final_workers", C.c_int32), ("sched_ticks", C.c_int32), ("mean_workers", C.c_double)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -445,7 +447,8 @@ class Context:
 def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: int = 0,
                warmup_batches: int = 0, n_workers: int = 0, warmup_us: int = 0,
                update_interval_us: int = 1000, window: int = 1024,
-               trainer_priority: int = 1, d2h_probe: int = 0, percentile: int = 75) -> RunConfig:
+               trainer_priority: int = 1, d2h_probe: int = 0, percentile: int = 75,
+               scheduler: int = 0, max_workers: int = 0, sched_tick_us: int = 0) -> RunConfig:
     rc = RunConfig()
     rc.batch_size = batch_size
     rc.policy = policy
@@ -459,4 +462,7 @@ def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: 
     rc.warmup_batches = warmup_batches
     rc.d2h_probe = d2h_probe
     rc.percentile = percentile
+    rc.scheduler = scheduler
+    rc.max_workers = max_workers
+    rc.sched_tick_us = sched_tick_us
     return rc

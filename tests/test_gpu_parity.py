@@ -289,6 +289,37 @@ def test_progress_reports_stage_boundaries(ctx, lfgpu):
 
 
 # ------------------------------------------------------------------ shard loop
+def test_shard_scheduler_adapts_in_flight_groups(lfgpu):
+    """SURVEY 8(f) row 1 on the device: the reference's Eq. 1-2 rule resizes the number
+    of in-flight launch groups.  Loader-bound (no trainer, every sample a 300 us cost,
+    empty consumer queue, saturated slots): the count grows to its bound.  Trainer-bound
+    (a 3 ms trainer step per batch: delivered batches pile up): it shrinks.  Exactly-once
+    delivery holds throughout."""
+    ctx = lfgpu.Context(batch_size=4, n_workers=4, max_group=1, max_slot_buffers=12, seed=SEED)
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, spin_first=True))
+    dims = (10, 10, 20)
+    rng = np.random.default_rng(12)
+    pi = _upload(ctx, rng.standard_normal(dims).astype(np.float32))
+    pl = _upload(ctx, rng.integers(0, 3, dims, dtype=np.uint8))
+    n = 600
+    descs = [lfgpu.sample_desc(i, dims, pi, pl, spin_us=[300]) for i in range(n)]
+    grow = lfgpu.run_config(batch_size=4, n_workers=4, scheduler=1, max_workers=12, sched_tick_us=500)
+    rep, ids, _, _ = ctx.run_shard(ch, descs, grow)
+    assert rep.exactly_once == 1 and sorted(ids.tolist()) == list(range(n))
+    assert rep.sched_ticks > 5 and rep.final_workers == 12 and rep.mean_workers > 4
+    shrink = lfgpu.run_config(batch_size=4, n_workers=8, trainer_us=3000, scheduler=1, max_workers=12,
+                              sched_tick_us=500)
+    descs = [lfgpu.sample_desc(n + i, dims, pi, pl, spin_us=[50]) for i in range(200)]
+    rep, ids, _, _ = ctx.run_shard(ch, descs, shrink)
+    assert rep.exactly_once == 1 and sorted(ids.tolist()) == list(range(n, n + 200))
+    assert rep.sched_ticks > 5 and rep.final_workers < 8 and rep.mean_workers < 8
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
 def test_shard_exactly_once_fast_first(lfgpu):
     """Algorithm 1 on the device: samples whose synthetic cost exceeds t_out are
     classified slow, finish in the background and are batched after the fast
