@@ -235,7 +235,10 @@ int lfg_time_kernels(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samp
 typedef struct {
     int32_t batch_size;
     int32_t policy;             /* 0 fixed t_out, 1 profiler (p75 -> p90 escalation),
-                                   2 profiler at a fixed percentile (see `percentile`) */
+                                   2 profiler at a fixed percentile (see `percentile`),
+                                   3 synchronous baseline (start_sync_loader, baselines.cpp:12-151):
+                                     batch k = the k-th B samples, sealed when all are done,
+                                     in order -- head-of-line blocking, no timeouts */
     int64_t t_out_us;           /* fixed budget (policy 0) or initial budget (policy 1); <=0 = none */
     int64_t warmup_us;          /* profiler warm-up before the first percentile (profiler.hpp:41) */
     int64_t update_interval_us; /* profiler refresh period */

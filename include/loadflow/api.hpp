@@ -446,6 +446,26 @@ void scheduler_loop(WorkerPool& pool, std::span<BatchQueue* const> batch_queues,
                     const SchedulerConfig& cfg, Runtime& rt,
                     std::vector<SchedulerTraceRow>* trace = nullptr);
 
+// ---------------------------------------------------------------- baselines (baselines.hpp:12-47)
+// the synchronous (PyTorch-DataLoader-like) loader with
+// head-of-line blocking, Pecan AutoOrder and the size heuristic.
+struct SyncLoaderConfig {
+    std::size_t batch_size = 1;
+    int n_workers = 1;
+    int prefetch_factor = 2; // batches loaded in advance per worker
+};
+
+struct SyncBatchRecord {
+    std::size_t batch_index = 0;
+    TimeMs published_at = 0;          // seal time
+    TimeMs max_member_completion = 0; // completion time of the slowest member
+};
+
+void start_sync_loader(Runtime& rt, std::vector<Sample> samples, const SyncLoaderConfig& cfg,
+                       BatchQueue& batch_q, std::vector<SyncBatchRecord>* records = nullptr);
+TransformChain autoorder(const TransformChain& chain);
+SampleClass size_heuristic_classify(const Sample& sample, double size_cutoff_bytes);
+
 // ---------------------------------------------------------------- profiler (profiler.hpp:17-85)
 class InsufficientProfileData : public std::runtime_error {
 public:

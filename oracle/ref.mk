@@ -1,12 +1,12 @@
 # Builds the reference CPU loader from its own sources where they lie
 # (/root/reference/proj/src), outputs only into oracle/_ref/ (git-ignored,
 # travels to the GPU box).  Plain g++ on the hot-path translation units; the
-# reporting/CLI units (metrics, config, experiment, baselines) are
+# reporting/CLI units (metrics, config, experiment) are
 # not needed and not built.  -include cstdint works around config.hpp:25.
 CXX ?= g++
 REF ?= /root/reference/proj
 OUT := _ref
-SRCS := runtime_realtime runtime_virtual sample balancer batcher trainer worker_pool profiler workloads scheduler
+SRCS := runtime_realtime runtime_virtual sample balancer batcher trainer worker_pool profiler workloads scheduler baselines
 OBJS := $(patsubst %,$(OUT)/obj/%.o,$(SRCS))
 CXXFLAGS := -O2 -std=c++20 -fPIC -include cstdint -I$(REF)/include -w
 

@@ -30,6 +30,7 @@
 
 #include "lf_oracle.h"
 #include "loadflow/balancer.hpp"
+#include "loadflow/baselines.hpp"
 #include "loadflow/batcher.hpp"
 #include "loadflow/profiler.hpp"
 #include "loadflow/runtime.hpp"
@@ -236,6 +237,9 @@ int main(int argc, char** argv) {
     const int trainer_ms = arg_int(argc, argv, "--trainer-ms", 0);
     const int pct = arg_int(argc, argv, "--pct", -1);
     const int prof_warmup_ms = arg_int(argc, argv, "--profiler-warmup-ms", 2000);
+    // --loader sync: the reference's synchronous PyTorch-DataLoader-like loader
+    // (start_sync_loader, baselines.cpp:12-151) instead of the Minato pipeline
+    const bool sync = arg_str(argc, argv, "--loader", "minato") == "sync";
     lfo_cfg2d_default(&g_c2);
     lfo_cfg3d_default(&g_c3);
     const bool rrc = wl == "rrc";
@@ -358,6 +362,35 @@ int main(int argc, char** argv) {
             fast[slot]->close();
             temp[slot]->close();
         });
+    // a sample with its fp64 payload [id, dims..., data...] (one of the pool's inputs)
+    auto make_payload_sample = [&](int64_t i) {
+        Sample s;
+        s.id = (uint64_t)i;
+        s.chain = &chain;
+        if (rrc) {
+            const auto& im = images[i % pool];
+            const auto [h, w] = hw[i % pool];
+            s.payload.resize(kHdr2d + im.size());
+            s.payload[0] = (double)i;
+            s.payload[1] = h;
+            s.payload[2] = w;
+            for (size_t k = 0; k < im.size(); ++k) s.payload[kHdr2d + k] = im[k];
+        } else {
+            const auto& v = vols[i % pool];
+            const auto& l = lbls[i % pool];
+            s.payload.resize(kHdr3d + 2 * v.size());
+            s.payload[0] = (double)i;
+            s.payload[1] = D;
+            s.payload[2] = H3;
+            s.payload[3] = W3;
+            for (size_t k = 0; k < v.size(); ++k) s.payload[kHdr3d + k] = v[k];
+            for (size_t k = 0; k < l.size(); ++k) s.payload[kHdr3d + v.size() + k] = l[k];
+        }
+        s.bytes_in = s.size_bytes = (double)s.payload.size() * 8;
+        s.t_enqueue = rt->now();
+        return s;
+    };
+    if (!sync) {
     for (int i = 0; i < cores; ++i) {
         rt->spawn("resume." + std::to_string(i), [&, i] {
             Rng r(kSeed ^ (0xc2b2ae3d27d4eb4fULL * (i + 1)));
@@ -376,44 +409,29 @@ int main(int argc, char** argv) {
                 give_up = true;
                 break;
             }
-            Sample s;
-            s.id = (uint64_t)i;
-            s.chain = &chain;
-            if (rrc) {
-                const auto& im = images[i % pool];
-                const auto [h, w] = hw[i % pool];
-                s.payload.resize(kHdr2d + im.size());
-                s.payload[0] = (double)i;
-                s.payload[1] = h;
-                s.payload[2] = w;
-                for (size_t k = 0; k < im.size(); ++k) s.payload[kHdr2d + k] = im[k];
-            } else {
-                const auto& v = vols[i % pool];
-                const auto& l = lbls[i % pool];
-                s.payload.resize(kHdr3d + 2 * v.size());
-                s.payload[0] = (double)i;
-                s.payload[1] = D;
-                s.payload[2] = H3;
-                s.payload[3] = W3;
-                for (size_t k = 0; k < v.size(); ++k) s.payload[kHdr3d + k] = v[k];
-                for (size_t k = 0; k < l.size(); ++k) s.payload[kHdr3d + v.size() + k] = l[k];
-            }
-            s.bytes_in = s.size_bytes = (double)s.payload.size() * 8;
-            s.t_enqueue = rt->now();
-            input.put(std::move(s));
+            input.put(make_payload_sample(i));
         }
         input.close();
     });
-    rt->spawn("batcher", [&] {
-        build_batches(fast_p, slow_p, batch_q, BatcherConfig{(size_t)B, 10}, *rt);
-    });
+    }
+    if (sync) {
+        // all samples up front (start_sync_loader takes the stream by value)
+        std::vector<Sample> all;
+        for (int64_t i = 0; i < n; ++i) all.push_back(make_payload_sample(i));
+        start_sync_loader(*rt, std::move(all), SyncLoaderConfig{(size_t)B, cores, 2}, batch_q);
+    } else {
+        rt->spawn("batcher", [&] {
+            build_batches(fast_p, slow_p, batch_q, BatcherConfig{(size_t)B, 10}, *rt);
+        });
+    }
     ConsumerStats cs;
     rt->spawn("consumer", [&] {
         ConsumerConfig cc;
         cc.compute_per_batch = trainer_ms;   // 0: drain as fast as batches arrive (loader throughput)
         cs = run_consumer(cc, batch_q, *rt);
     });
-    if (pct < 0) {
+    if (sync) {
+    } else if (pct < 0) {
         rt->spawn("profiler", [&] { profiler_loop(prof, policy, *rt, [&] { return pool_w.stopped(); }); });
     } else if (pct > 0) {   // fixed percentile: the reference's percentile() over the window
         rt->spawn("profiler", [&] {
@@ -429,7 +447,7 @@ int main(int argc, char** argv) {
             }
         });
     }
-    pool_w.start();
+    if (!sync) pool_w.start();
     rt->run();
 
     // timed window: batches after the warm-up ones (compute_end in ms)

@@ -155,7 +155,13 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         prof.pct = rc.percentile;
         prof.adaptive = false;
     }
-    int64_t t_out = rc.t_out_us > 0 ? rc.t_out_us : kNoTimeoutUs;
+    // policy 3: the synchronous (PyTorch-DataLoader-like) baseline, baselines.cpp:12-151 --
+    // batch k = the k-th B samples fed, sealed only when all of them are done, in
+    // batch order (head-of-line blocking); no timeouts.
+    const bool sync = rc.policy == 3;
+    int64_t t_out = (rc.t_out_us > 0 && !sync) ? rc.t_out_us : kNoTimeoutUs;
+    std::vector<char> ready_pos(sync ? static_cast<size_t>(n) : 0, 0);
+    int64_t sync_next = 0;   // first position of the next batch to seal
     const int64_t run_t0 = host_now_us();
     int64_t last_update = run_t0;
 
@@ -262,7 +268,8 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 const bool is_slow = dev_us > t_out;   // inclusive budget, balancer.cpp:17
                 classify(g, is_slow);
                 for (int64_t t : g.tickets) {
-                    if (is_slow) slow.push_back(t);
+                    if (sync) ready_pos[static_cast<size_t>(t - tbase)] = 1;
+                    else if (is_slow) slow.push_back(t);
                     else fast_add(t, false);
                 }
                 prof.record(dev_us, is_slow);
@@ -325,11 +332,23 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         }
         // (4) batcher: seal eagerly, fast first
         const bool tail = fed == n && inflight.empty() && parked.empty();
-        while (static_cast<int64_t>(fast.size() + slow.size()) >= B ||
-               (tail && !fast.empty()) || (tail && !slow.empty())) {
-            const int64_t k = std::min<int64_t>(B, static_cast<int64_t>(fast.size() + slow.size()));
+        auto sync_ready = [&]() {
+            if (sync_next >= n) return false;
+            const int64_t k = std::min<int64_t>(B, n - sync_next);
+            if (sync_next + k > fed) return false;
+            for (int64_t i = sync_next; i < sync_next + k; ++i)
+                if (!ready_pos[static_cast<size_t>(i)]) return false;
+            return true;
+        };
+        while (sync ? sync_ready()
+                    : (static_cast<int64_t>(fast.size() + slow.size()) >= B || (tail && !fast.empty()) ||
+                       (tail && !slow.empty()))) {
+            const int64_t k = sync ? std::min<int64_t>(B, n - sync_next)
+                                   : std::min<int64_t>(B, static_cast<int64_t>(fast.size() + slow.size()));
             std::vector<int64_t> ts;
             ts.reserve(static_cast<size_t>(k));
+            if (sync)
+                for (int64_t i = 0; i < k; ++i) ts.push_back(tbase + sync_next + i);
             // Zero-copy preference: if every sample of some closed slot buffer is
             // in the fast list, seal exactly those (the buffer becomes the batch).
             // Eagerness is unchanged -- a batch is sealed whenever B samples are
@@ -337,7 +356,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             while (!full_bufs.empty() && (fast_cnt[full_bufs.front()] != B ||
                                           ctx.buf_closed_count(full_bufs.front()) != B))
                 full_bufs.pop_front();   // stale candidate
-            if (k == B && !full_bufs.empty()) {
+            if (!sync && k == B && !full_bufs.empty()) {
                 const int pick = full_bufs.front();
                 full_bufs.pop_front();
                 bool at_front = true;   // common case: the buffer's samples lead the fast list
@@ -372,6 +391,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             } catch (const Error& e) {
                 ph.lap(Phases::SEAL);
                 if (e.code != LFG_ERR_AGAIN) throw;
+                if (sync) break;   // the batch stays ready; retried next pass
                 for (auto it = ts.rbegin(); it != ts.rend(); ++it) {
                     const int cls = sample_class ? sample_class[*it - tbase] : 1;
                     if (cls == 2) slow.push_front(*it);
@@ -380,6 +400,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 break;
             }
             BatchRec& br = ctx.batch(b);
+            if (sync) sync_next += k;
             const bool timed = nbatches >= rc.warmup_batches;
             if (timed && rc.trainer_us > 0) {
                 cudaEvent_t s0 = mk(), s1 = mk();
@@ -451,7 +472,8 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             last_update = now;
         }
         if (!progressed) {
-            if (inflight.empty() && parked.empty() && fed == n && fast.empty() && slow.empty())
+            if (inflight.empty() && parked.empty() && fed == n && fast.empty() && slow.empty() &&
+                !(sync && sync_next < n))
                 fail(LFG_ERR_STATE, "shard stalled with samples unaccounted for");
             std::this_thread::yield();
         }

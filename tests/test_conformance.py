@@ -18,8 +18,8 @@ REF_TESTS = "/root/reference/proj/tests"
 PKG = os.path.join(ROOT, "paper_2509_10712_b200")
 BUILD = os.path.join(ROOT, "tests", "conformance", "build")
 
-# hot-path suites + the adaptive scheduler; baselines are a "next" row
-SUITES = ["core", "queue", "runtime", "balancer", "batcher", "trainer", "profiler", "workloads", "scheduler"]
+# hot-path suites + the adaptive scheduler and baselines
+SUITES = ["core", "queue", "runtime", "balancer", "batcher", "trainer", "profiler", "workloads", "scheduler", "baselines"]
 
 pytestmark = pytest.mark.skipif(not os.path.isdir(REF_TESTS),
                                 reason="reference test sources not present")

@@ -320,6 +320,36 @@ def test_shard_scheduler_adapts_in_flight_groups(lfgpu):
     ctx.close()
 
 
+def test_shard_sync_baseline_is_head_of_line(lfgpu):
+    """SURVEY 8(f) row 3 on the device: policy 3 is the reference's synchronous loader
+    (baselines.cpp:12-151) -- batch k holds exactly ids [kB, (k+1)B), in order, so one
+    slow sample holds back its batch; the Minato policy on the same stream seals fast
+    samples around it, and the synthetic trainer idles less."""
+    ctx = lfgpu.Context(batch_size=4, n_workers=8, max_group=1, max_slot_buffers=24, seed=SEED)
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, spin_first=True))
+    dims = (10, 10, 20)
+    rng = np.random.default_rng(13)
+    pi = _upload(ctx, rng.standard_normal(dims).astype(np.float32))
+    pl = _upload(ctx, rng.integers(0, 3, dims, dtype=np.uint8))
+    n = 160
+    heavy = set(range(2, n, 9))
+    descs = [lfgpu.sample_desc(i, dims, pi, pl, spin_us=[6_000 if i in heavy else 300]) for i in range(n)]
+    rep_s, ids_s, bsz_s, _ = ctx.run_shard(ch, descs, lfgpu.run_config(batch_size=4, policy=3, trainer_us=400))
+    assert rep_s.exactly_once == 1 and rep_s.slow == 0
+    assert ids_s.tolist() == list(range(n))                 # FIFO batches of consecutive ids
+    assert (bsz_s == 4).all()
+    rep_m, ids_m, _, _ = ctx.run_shard(ch, descs, lfgpu.run_config(batch_size=4, policy=0, t_out_us=2_000,
+                                                                     trainer_us=400))
+    assert rep_m.exactly_once == 1 and rep_m.slow == len(heavy)
+    assert ids_m.tolist() != list(range(n))                 # eager: fast samples overtake
+    assert rep_m.consumer_idle_frac < rep_s.consumer_idle_frac
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
 def test_shard_exactly_once_fast_first(lfgpu):
     """Algorithm 1 on the device: samples whose synthetic cost exceeds t_out are
     classified slow, finish in the background and are batched after the fast

@@ -34,7 +34,9 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 FRACS = (0.1, 0.2, 0.3)
-POLICIES = (("p50", 50), ("p75", 75), ("p90", 90), ("none", 0))
+# (name, percentile): 0 = no timeout; -1 = the synchronous head-of-line baseline
+# (start_sync_loader, baselines.cpp:12-151; GPU: lfg_run_config.policy 3)
+POLICIES = (("p50", 50), ("p75", 75), ("p90", 90), ("none", 0), ("sync", -1))
 
 
 class _Args:
@@ -51,7 +53,8 @@ def gpu_point(L, wl, frac, pct, steps, warmup, rank, world, dist, local):
     a = _Args()
     ids = bench.shard_ids(warmup + steps, B, rank, world)
     warm, timed = ids[: warmup * B], ids[warmup * B:]
-    rc = L.run_config(batch_size=B, policy=2 if pct else 0, percentile=pct or 75, t_out_us=0,
+    rc = L.run_config(batch_size=B, policy=3 if pct < 0 else (2 if pct else 0), percentile=pct if pct > 0 else 75,
+                      t_out_us=0,
                       trainer_us=2000, n_workers=a.workers, warmup_us=20000, update_interval_us=1000)
     ctx.run_shard(wl.chain, wl.descs(warm), rc, want_ids=False)
     ctx.synchronize()
@@ -65,7 +68,7 @@ def gpu_point(L, wl, frac, pct, steps, warmup, rank, world, dist, local):
     return {"samples_per_s": round(tot[0] / (el / 1e3), 1),
             "idle_pct": round(100 * (1 - tot[3] / tot[4]), 2) if tot[4] > 0 else None,
             "slow_frac": round(tot[1] / max(1, tot[2]), 3),
-            "final_t_out_us": round(rep.final_t_out_us, 1) if pct else None}
+            "final_t_out_us": round(rep.final_t_out_us, 1) if pct > 0 else None}
 
 
 def cpu_point(frac, pct, steps):
@@ -73,15 +76,16 @@ def cpu_point(frac, pct, steps):
     if h is None:
         return None
     cores = os.cpu_count() or 1
-    out = subprocess.run([h, "--workload", "img3d", "--steps", str(steps), "--warmup", "2",
-                          "--workers", str(cores), "--heavy-frac", str(frac), "--heavy-ms", "470",
-                          "--trainer-ms", "200", "--pct", str(pct), "--profiler-warmup-ms", "1500",
-                          "--max-seconds", "40"],
+    extra = ["--loader", "sync", "--pct", "0"] if pct < 0 else ["--pct", str(pct)]
+    out = subprocess.run([h, "--workload", "img3d", "--steps", str(steps if pct >= 0 else min(steps, 6)),
+                          "--warmup", "2", "--workers", str(cores), "--heavy-frac", str(frac),
+                          "--heavy-ms", "470", "--trainer-ms", "200", "--profiler-warmup-ms", "1500",
+                          "--max-seconds", "40"] + extra,
                          capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
     b = json.loads(out)
     return {"samples_per_s": b["value"], "idle_pct": round(100 * b["idle_frac"], 2),
             "slow_frac": round(b["slow"] / max(1.0, b["samples"] + 4), 3),
-            "final_t_out_ms": b["final_t_out_ms"] if pct else None, "cores": b["cores"]}
+            "final_t_out_ms": b["final_t_out_ms"] if pct > 0 else None, "cores": b["cores"]}
 
 
 def main():
@@ -115,7 +119,9 @@ def main():
              "step per batch of 2). CPU: reference libloadflow Minato pipeline + oracle transforms, "
              "heavy samples sleep 470 ms, 200 ms trainer step per batch of 2.",
              "t_out = fixed nearest-rank percentile of the per-sample totals window after warm-up "
-             "(none = kNoTimeout).",
+             "(none = kNoTimeout); sync = the synchronous head-of-line loader (batch k = ids "
+             "[kB, (k+1)B), sealed when complete, in order: start_sync_loader on the CPU, "
+             "lfg_run_config.policy 3 on the GPU).",
              "",
              "| slow frac | t_out | GPU samples/s | GPU idle % | GPU slow | GPU t_out (us) | "
              "CPU samples/s | CPU idle % | CPU slow | CPU t_out (ms) |",
