@@ -128,7 +128,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     __shared__ int2 sched_rows[kRows];            // {even row, odd row} to blend (-1: kept) as a
                                                   // staged byte offset (or a row index, unstaged)
     __shared__ float sched_w[kRows][6];           // {wE * a_c (c = 0..2), wO * a_c}
-    __shared__ int yspan[2];                      // first / last source row of the CTA
+    __shared__ int yspan[2];                      // [0]: the block's rows are staged
     const RrcDesc& d = L.d[blockIdx.y];
     const int oh = L.oh, ow = L.ow;
     const int y_begin = blockIdx.x * kRows;
@@ -136,80 +136,82 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row_bytes = d.w * 3;
     const int spitch = ((row_bytes + 30) >> 4) << 4;        // 16-B chunks + alignment phase
-    if (threadIdx.x == 32) {
-        mbar_init(&stage_bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (threadIdx.x < n_rows_out) {
-        const int j = threadIdx.x;
+    // Warp 0, lane j < n_rows_out: output row j's vertical taps.  The block's source
+    // row span (first tap of row 0 .. last tap of the last row) is known after one
+    // shuffle, so the bulk copies go out before the rest of the schedule is built;
+    // the other warps derive their column taps meanwhile.
+    bool staged = false;
+    int ylo = 0;
+    if (warp == 0) {
+        const int j = lane;
         const double sy = __ddiv_rn((double)d.h, (double)oh);
-        int y0, y1, p0 = -1, p1 = -1, ylo, yhi, t0, t1;
-        float l0, l1, q0, q1, u0, u1;
-        src_index(y_begin + j, d.h, sy, y0, y1, l0, l1);
-        if (j > 0) src_index(y_begin + j - 1, d.h, sy, p0, p1, q0, q1);
-        src_index(y_begin, d.h, sy, ylo, t0, u0, u1);                      // the CTA's row span
-        src_index(y_begin + n_rows_out - 1, d.h, sy, t1, yhi, u0, u1);
-        const bool staged = (yhi - ylo + 1) * spitch <= smem_bytes;
-        // a row is already in its register iff the previous output row used it
-        // (rows are non-decreasing and adjacent taps differ by at most one)
-        const bool new0 = y0 != p0 && y0 != p1;
-        const bool new1 = y1 != y0 && y1 != p0 && y1 != p1;
-        const bool odd0 = (y0 & 1) != 0;   // y1 (if distinct) has the other parity
-        int ld_e = odd0 ? (new1 ? y1 : -1) : (new0 ? y0 : -1);
-        int ld_o = odd0 ? (new0 ? y0 : -1) : (new1 ? y1 : -1);
-        if (staged) {   // resolve rows to their byte offsets in the staged window once, here
-            if (ld_e >= 0) ld_e = staged_off(d, ld_e, ylo, spitch);
-            if (ld_o >= 0) ld_o = staged_off(d, ld_o, ylo, spitch);
-        }
-        float w_e, w_o;
-        if (y1 == y0) {
-            w_e = odd0 ? 0.f : l0 + l1;
-            w_o = odd0 ? l0 + l1 : 0.f;
-        } else {
-            w_e = odd0 ? l1 : l0;
-            w_o = odd0 ? l0 : l1;
-        }
-        sched_rows[j] = make_int2(ld_e, ld_o);
+        int y0 = 0, y1 = 0;
+        float l0 = 0.f, l1 = 0.f;
+        if (j < n_rows_out) src_index(y_begin + j, d.h, sy, y0, y1, l0, l1);
+        ylo = __shfl_sync(0xffffffffu, y0, 0);
+        const int yhi = __shfl_sync(0xffffffffu, y1, n_rows_out - 1);
+        const int nrows = yhi - ylo + 1;
+        staged = nrows * spitch <= smem_bytes;
+        if (staged) {
+            if (lane == 0) {
+                mbar_init(&stage_bar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            __syncwarp();
+            // stage the touched source rows (aligned 16-byte superset of each row) with
+            // bulk async copies, one per row (a lane per row), all on one mbarrier
+            int bytes = 0;
+            for (int r = lane; r < nrows; r += 32) {
+                const uintptr_t sa = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
+                bytes += (int)(((sa + row_bytes + 15) & ~uintptr_t(15)) - (sa & ~uintptr_t(15)));
+            }
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            sched_w[j][c] = w_e * L.a[c];
-            sched_w[j][3 + c] = w_o * L.a[c];
+            for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+            if (lane == 0) mbar_expect_tx(&stage_bar, (uint32_t)bytes);
+            __syncwarp();
+            for (int r = lane; r < nrows; r += 32) {
+                const uintptr_t sa = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
+                const uintptr_t al = sa & ~uintptr_t(15);
+                const uint32_t nb = (uint32_t)(((sa + row_bytes + 15) & ~uintptr_t(15)) - al);
+                bulk_g2s(smem + r * spitch, reinterpret_cast<const void*>(al), nb, &stage_bar);
+            }
         }
-        if (j == 0) {
-            yspan[0] = ylo;
-            yspan[1] = yhi;
-        }
-    }
-    __syncthreads();
-    const int ylo = yspan[0];
-    const int nrows = yspan[1] - ylo + 1;
-    const bool staged = nrows * spitch <= smem_bytes;
-
-    // 1. stage the touched source rows (aligned 16-byte superset of each row) with
-    //    bulk async copies: warp 0 issues one cp.async.bulk per row (a lane per row),
-    //    all complete on one mbarrier; the threads meanwhile derive their column taps
-    if (staged && warp == 0) {
-        int bytes = 0;
-        for (int r = lane; r < nrows; r += 32) {
-            const uintptr_t s = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
-            bytes += (int)(((s + row_bytes + 15) & ~uintptr_t(15)) - (s & ~uintptr_t(15)));
-        }
+        // the previous output row's taps (row j - 1 is lane j - 1)
+        int p0 = __shfl_up_sync(0xffffffffu, y0, 1), p1 = __shfl_up_sync(0xffffffffu, y1, 1);
+        if (j == 0) p0 = p1 = -1;
+        if (j < n_rows_out) {
+            // a row is already in its register iff the previous output row used it
+            // (rows are non-decreasing and adjacent taps differ by at most one)
+            const bool new0 = y0 != p0 && y0 != p1;
+            const bool new1 = y1 != y0 && y1 != p0 && y1 != p1;
+            const bool odd0 = (y0 & 1) != 0;   // y1 (if distinct) has the other parity
+            int ld_e = odd0 ? (new1 ? y1 : -1) : (new0 ? y0 : -1);
+            int ld_o = odd0 ? (new0 ? y0 : -1) : (new1 ? y1 : -1);
+            if (staged) {   // resolve rows to their byte offsets in the staged window once, here
+                if (ld_e >= 0) ld_e = staged_off(d, ld_e, ylo, spitch);
+                if (ld_o >= 0) ld_o = staged_off(d, ld_o, ylo, spitch);
+            }
+            float w_e, w_o;
+            if (y1 == y0) {
+                w_e = odd0 ? 0.f : l0 + l1;
+                w_o = odd0 ? l0 + l1 : 0.f;
+            } else {
+                w_e = odd0 ? l1 : l0;
+                w_o = odd0 ? l0 : l1;
+            }
+            sched_rows[j] = make_int2(ld_e, ld_o);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-        if (lane == 0) mbar_expect_tx(&stage_bar, (uint32_t)bytes);
-        __syncwarp();
-        for (int r = lane; r < nrows; r += 32) {
-            const uintptr_t s = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
-            const uintptr_t a = s & ~uintptr_t(15);
-            const uint32_t nb = (uint32_t)(((s + row_bytes + 15) & ~uintptr_t(15)) - a);
-            bulk_g2s(smem + r * spitch, reinterpret_cast<const void*>(a), nb, &stage_bar);
+            for (int c = 0; c < 3; ++c) {
+                sched_w[j][c] = w_e * L.a[c];
+                sched_w[j][3 + c] = w_o * L.a[c];
+            }
         }
+        if (lane == 0) yspan[0] = staged ? 1 : 0;
     }
 
     const int xa = 2 * threadIdx.x;                         // columns xa, xa + 1 (ow is even)
-    if (xa >= ow) return;
     ColPair cp;
-    {
+    if (xa < ow) {
         const double sx = __ddiv_rn((double)d.w, (double)ow);
         int x1a, x1b;
         float l0a, l1a, l0b, l1b;
@@ -230,6 +232,9 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
             cp.w1 = make_float2(cp.w1.y, cp.w1.x);
         }
     }
+    __syncthreads();   // schedule visible; the mbarrier was initialised before the copies
+    staged = yspan[0] != 0;
+    if (xa >= ow) return;
     const int64_t plane = (int64_t)oh * ow;
     float2* o = reinterpret_cast<float2*>(d.out + (int64_t)y_begin * ow + (d.flip ? ow - 2 - xa : xa));
     const int ow2 = ow >> 1;
