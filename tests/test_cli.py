@@ -1,0 +1,54 @@
+"""`loadflow_b200 run | compare` -- the reference CLI's experiment commands
+(proj/tools/loadflow_main.cpp:34-134) for the GPU loaders."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_2509_10712_b200", "loadflow_b200")
+
+
+@pytest.fixture(scope="module")
+def cli():
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "paper_2509_10712_b200", "csrc")])
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "paper_2509_10712_b200", "host")])
+    return CLI
+
+
+def test_cli_usage_and_config_errors(cli, tmp_path):
+    r = subprocess.run([cli], capture_output=True, text=True)
+    assert r.returncode == 1 and "usage" in r.stderr
+    bad = tmp_path / "bad.ini"
+    bad.write_text("[workload]\nname img_seg\n")
+    r = subprocess.run([cli, "run", str(bad)], capture_output=True, text=True)
+    assert r.returncode == 2 and "expected key = value" in r.stderr
+    cfg = tmp_path / "c.ini"
+    cfg.write_text("[pipeline]\nloader = pytorch\n")
+    r = subprocess.run([cli, "run", str(cfg)], capture_output=True, text=True)
+    assert r.returncode == 2 and "minato-gpu or sync-gpu" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_run_and_compare_on_gpu(cli, tmp_path):
+    """The reference img_seg stream (generate(spec): same ids and costs) through the GPU
+    loaders: Minato exactly-once with slow samples classified, sync without; the Minato
+    run completes no later and idles the trainer less; compare prints both."""
+    cfg = os.path.join(ROOT, "configs", "img_seg_gpu.ini")
+    reps = {}
+    for loader in ("sync-gpu", "minato-gpu"):
+        out = tmp_path / loader
+        r = subprocess.run([cli, "run", cfg, "--loader", loader, "--out", str(out)],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        assert "exactly_once=yes" in r.stdout
+        reps[loader] = json.loads((out / "report.json").read_text())
+        assert reps[loader]["samples"] == 400
+    assert reps["sync-gpu"]["slow_rate"] == 0.0
+    assert reps["minato-gpu"]["slow_rate"] > 0.0
+    assert reps["minato-gpu"]["completion_ms"] <= reps["sync-gpu"]["completion_ms"] * 1.02
+    r = subprocess.run([cli, "compare", str(tmp_path / "sync-gpu" / "report.json"),
+                        str(tmp_path / "minato-gpu" / "report.json"), "--csv", str(tmp_path / "cmp.csv")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0 and "minato-gpu" in r.stdout and (tmp_path / "cmp.csv").exists()
