@@ -192,6 +192,8 @@ def test_rrc2d_matches_oracle(ctx, lfgpu, oracle, src_kind):
             H, W = 40, 500     # extreme aspect -> centre-crop fallback
         if k == 1:
             H, W = 100, 100    # upsampling
+        if k == 2:
+            H, W = 1400, 1200  # tall crop boxes: the row window exceeds shared memory -> L2 taps
         img = rng.integers(0, 256, (H, W, 3), dtype=np.uint8)
         p = _upload(ctx, img) if src_kind == 0 else _pinned(ctx, img)
         bufs.append(p)
@@ -414,6 +416,39 @@ def _splice(logmel, stack=3):
         ok = idx < T
         out[ok, s * m:(s + 1) * m] = logmel[:, idx[ok]].T
     return out
+
+
+def test_speech_pinned_host_source_matches_device(lfgpu, oracle):
+    """Speech from pinned host memory (the e2e path: one batched DMA call per launch
+    group, cudaMemcpyBatchAsync) produces bit-identical outputs to HBM-resident input."""
+    ctx = lfgpu.Context(batch_size=8, n_workers=4, max_group=8, max_slot_buffers=8, seed=SEED)
+    ch = ctx.chain(lfgpu.speech_ops(max_len=40000))
+    rng = np.random.default_rng(22)
+    lens = [4000, 4321, 20000, 39999, 257, 300, 16000, 12345]
+    dev, host, keep = [], [], []
+    for k, L in enumerate(lens):
+        wav = (0.3 * rng.standard_normal(L)).astype(np.float32)
+        pd = _upload(ctx, wav)
+        ph = _pinned(ctx, wav)
+        keep += [("d", pd), ("h", ph)]
+        dev.append(ctx.submit(ch, lfgpu.sample_desc(500 + k, (L,), pd)))
+        host.append(ctx.submit(ch, lfgpu.sample_desc(500 + k, (L,), ph, src_kind=lfgpu.SRC_HOST_PINNED)))
+    ctx.flush()
+    _, out_bytes, _ = ch.info()
+    for L, td, th in zip(lens, dev, host):
+        ctx.wait(td)
+        ctx.wait(th)
+        rows = -(-(1 + L // 160) // 3)                   # spliced rows the kernel writes
+        a = ctx.ticket_output(td, out_bytes).view(np.float32)[: rows * 240]
+        b = ctx.ticket_output(th, out_bytes).view(np.float32)[: rows * 240]
+        bad = np.flatnonzero(a != b)
+        assert bad.size == 0, (f"{bad.size} of {a.size} differ; first {bad[:5]}, "
+                               f"dev {a[bad[:5]]}, host {b[bad[:5]]}")
+        ctx.release(td)
+        ctx.release(th)
+    for kind, p in keep:
+        (ctx.device_free if kind == "d" else ctx.host_free)(p)
+    ctx.close()
 
 
 def test_speech_matches_oracle(lfgpu, oracle):
