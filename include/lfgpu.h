@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define LFG_ABI_VERSION 1
+#define LFG_ABI_VERSION 2   /* 2: run config percentile / scheduler fields, report scheduler fields, lfg_run_shard_source */
 
 #define LFG_OK 0
 #define LFG_ERR_INVALID -1
@@ -285,6 +285,23 @@ typedef struct {
 int lfg_run_shard(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples, int64_t n,
                   const lfg_run_config* cfg, lfg_run_report* report, uint64_t* consumed_ids,
                   int32_t* batch_sizes, int32_t* sample_class);
+
+/* ---- streaming input (raw reads from storage, the feeder of
+ * experiment.cpp:221-228): the shard pulls samples in order from `next` as it has
+ * free workers, and hands each sample back through `release` once the device no
+ * longer reads its payload (its launch group completed), so a bounded pool of
+ * pinned buffers can be refilled by reader threads while earlier samples run. */
+typedef struct {
+    void* user;
+    /* fill *out with the next sample: returns 1 (a sample), 2 (not ready yet: the
+     * shard keeps polling and sealing, and asks again), 0 (end) or < 0 (error) */
+    int (*next)(void* user, lfg_sample_desc* out);
+    void (*release)(void* user, uint64_t id);   /* may be NULL */
+} lfg_source;
+
+int lfg_run_shard_source(lfg_ctx* ctx, lfg_chain* chain, const lfg_source* src, int64_t n,
+                         const lfg_run_config* cfg, lfg_run_report* report, uint64_t* consumed_ids,
+                         int32_t* batch_sizes, int32_t* sample_class);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@
 namespace lfg {
 int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_t n,
               const lfg_run_config& rc, lfg_run_report& rep, uint64_t* consumed_ids,
-              int32_t* batch_sizes, int32_t* sample_class);
+              int32_t* batch_sizes, int32_t* sample_class, const lfg_source* src = nullptr);
 }
 
 using namespace lfg;
@@ -578,6 +578,17 @@ int lfg_run_shard(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples
         std::lock_guard<std::mutex> g(c.mu);
         run_shard(c, chain->impl, samples, n, *cfg, *report, consumed_ids, batch_sizes,
                   sample_class);
+    });
+}
+
+int lfg_run_shard_source(lfg_ctx* ctx, lfg_chain* chain, const lfg_source* src, int64_t n,
+                         const lfg_run_config* cfg, lfg_run_report* report, uint64_t* consumed_ids,
+                         int32_t* batch_sizes, int32_t* sample_class) {
+    return guarded([&] {
+        Context& c = C(ctx);
+        if (!chain || !cfg || !report || !src) fail(LFG_ERR_INVALID, "null argument");
+        std::lock_guard<std::mutex> g(c.mu);
+        run_shard(c, chain->impl, nullptr, n, *cfg, *report, consumed_ids, batch_sizes, sample_class, src);
     });
 }
 

@@ -103,7 +103,19 @@ struct Phases {
 
 int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_t n,
               const lfg_run_config& rc, lfg_run_report& rep, uint64_t* consumed_ids,
-              int32_t* batch_sizes, int32_t* sample_class) {
+              int32_t* batch_sizes, int32_t* sample_class, const lfg_source* src) {
+    if (src != nullptr && src->next == nullptr) fail(LFG_ERR_INVALID, "source without next()");
+    // streaming input: descriptors arrive through src->next, in feed order
+    std::vector<lfg_sample_desc> src_descs;
+    if (src != nullptr) {
+        src_descs.resize(static_cast<size_t>(std::max<int64_t>(n, 0)));
+        samples = src_descs.data();
+    }
+    int64_t fetched = 0;
+    auto release_group = [&](const Group& g) {
+        if (src != nullptr && src->release != nullptr)
+            for (int64_t t : g.tickets) src->release(src->user, ctx.tickets[t].id);
+    };
     if (n < 0 || (n > 0 && samples == nullptr)) fail(LFG_ERR_INVALID, "bad sample list");
     const int B = rc.batch_size > 0 ? rc.batch_size : ctx.cfg.batch_size;
     if (B > ctx.cfg.batch_size) fail(LFG_ERR_INVALID, "run batch_size exceeds context batch_size");
@@ -216,7 +228,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     for (int64_t i = 0; i < n_chunks; ++i) ready[i].store(0, std::memory_order_relaxed);
     std::atomic<int64_t> next_chunk{0};
     std::atomic<bool> stop_draw{false};
-    const int n_threads = static_cast<int>(std::max<int64_t>(
+    const int n_threads = src != nullptr ? 0 : static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>({8, std::max(1u, std::thread::hardware_concurrency()) / 2, n_chunks})));
     std::vector<std::thread> drawers;
     for (int t = 0; t < n_threads; ++t) {
@@ -274,6 +286,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 }
                 prof.record(dev_us, is_slow);
                 if (nbatches >= rc.warmup_batches) kernel_ms += dev_us / 1000.0;
+                release_group(g);
                 remove = true;
             } else if (over) {
                 classify(g, true);
@@ -292,8 +305,12 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         for (size_t k = 0; k < parked.size() && full_scan;) {
             Group& g = ctx.groups[parked[k]];
             if (ctx.poll_group(g)) {
-                for (int64_t t : g.tickets) slow.push_back(t);
+                for (int64_t t : g.tickets) {
+                    if (sync) ready_pos[static_cast<size_t>(t - tbase)] = 1;
+                    else slow.push_back(t);
+                }
                 prof.record(total_us(g), true);
+                release_group(g);
                 parked.erase(parked.begin() + static_cast<long>(k));
                 progressed = true;
             } else {
@@ -310,7 +327,16 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             try {
                 for (; got < take; ++got) {
                     const int64_t i = fed + got;
-                    if (!ready[i / kChunk].load(std::memory_order_acquire)) {
+                    if (src != nullptr) {   // streaming input: fetch and draw in feed order
+                        if (i >= fetched) {
+                            const int r = src->next(src->user, &src_descs[static_cast<size_t>(i)]);
+                            if (r == 2) break;
+                            if (r == 0) fail(LFG_ERR_STATE, "source ended before n samples");
+                            if (r != 1) fail(LFG_ERR_INVALID, "source next() failed");
+                            draw_params(*chain, ctx.cfg.seed, src_descs[static_cast<size_t>(i)], pre[i]);
+                            fetched = i + 1;
+                        }
+                    } else if (!ready[i / kChunk].load(std::memory_order_acquire)) {
                         ph.lap(Phases::SUBMIT);
                         while (!ready[i / kChunk].load(std::memory_order_acquire)) std::this_thread::yield();
                         ph.lap(Phases::DRAW);

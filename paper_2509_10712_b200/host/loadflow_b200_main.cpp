@@ -11,8 +11,11 @@
 // initial_workers / max_workers / tick_ms, profiler.window / warmup_ms /
 // update_interval_ms / initial_timeout_ms, run.out_dir; plus gpu.* extensions:
 // gpu.device, gpu.time_scale_us_per_ms (reference milliseconds -> device
-// microseconds, default 10), gpu.pool (distinct synthetic payloads), gpu.src
-// (device | pinned).  The sample stream is the reference workload generator's
+// microseconds, default 10), gpu.pool (distinct synthetic payloads), gpu.group
+// (samples per launch group, default 1), gpu.src
+// (device | pinned | file: payloads written once as sample files under gpu.data_dir and
+// read back by gpu.readers threads into gpu.slots pinned buffers, lfgpu_files.h).  The
+// sample stream is the reference workload generator's
 // (generate(spec): same ids, costs and sizes); every sample runs the workload's
 // real transform chain on the GPU plus a synthetic device cost of its reference
 // cost x time_scale, and a synthetic trainer step of consumer.compute_ms x
@@ -33,6 +36,7 @@
 #include <vector>
 
 #include "lfgpu.h"
+#include "lfgpu_files.h"
 #include "loadflow/api.hpp"
 
 namespace {
@@ -146,7 +150,11 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
     const int B = static_cast<int>(getd(kv, "pipeline.batch_size", 24));
     const double scale = getd(kv, "gpu.time_scale_us_per_ms", 10.0);
     const int pool = static_cast<int>(getd(kv, "gpu.pool", 16));
-    const bool pinned = get(kv, "gpu.src", "device") == "pinned";
+    const std::string src_kind = get(kv, "gpu.src", "device");   // device | pinned | file
+    if (src_kind != "device" && src_kind != "pinned" && src_kind != "file")
+        throw std::invalid_argument("gpu.src must be device, pinned or file");
+    const bool from_file = src_kind == "file";
+    const bool pinned = src_kind == "pinned" || from_file;   // file payloads are synthesised in pinned memory
     if (static_cast<int>(getd(kv, "pipeline.n_consumers", 1)) != 1)
         throw std::invalid_argument("one consumer per process: run one process per GPU for more");
 
@@ -159,7 +167,9 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
     cfg.batch_size = B;
     const int workers = static_cast<int>(getd(kv, "scheduler.initial_workers", 12));
     cfg.n_workers = workers;
-    cfg.max_group = 1;   // per-sample classification, as the reference's per-sample timeouts
+    // samples per launch group: 1 = per-sample classification, as the reference's
+    // per-sample timeouts (default); larger groups for loader-throughput runs
+    cfg.max_group = static_cast<int>(getd(kv, "gpu.group", 1));
     cfg.max_slot_buffers = std::max(8, 2 * workers / std::max(1, B) + 8);
     cfg.seed = seed;
     lfg_ctx* ctx = nullptr;
@@ -238,7 +248,62 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
     lfg_run_report rep{};
     std::vector<uint64_t> ids(static_cast<size_t>(n));
     std::vector<int32_t> bsz(static_cast<size_t>(n)), cls(static_cast<size_t>(n));
-    check(lfg_run_shard(ctx, chain, descs.data(), n, &rc, &rep, ids.data(), bsz.data(), cls.data()), "run");
+    int64_t file_bytes = 0;
+    double file_seconds = 0;
+    if (from_file) {
+        // raw reads from storage: the pool's payloads become sample
+        // files once; reader threads pread them into recycled pinned slots ahead of the shard
+        const std::string dir = get(kv, "gpu.data_dir", "/tmp/lfg_data_" + std::string(loadflow::workload_name(kind)));
+        mkdir(dir.c_str(), 0755);
+        std::vector<std::string> files;
+        const int fkind = kind == loadflow::WorkloadKind::img_seg
+                              ? LFG_FILE_VOLUME
+                              : (kind == loadflow::WorkloadKind::obj_det ? LFG_FILE_IMAGE : LFG_FILE_WAVEFORM);
+        for (size_t i = 0; i < pay.size(); ++i) {
+            files.push_back(dir + "/sample_" + std::to_string(i) + ".lfgs");
+            check(lfg_write_sample_file(files.back().c_str(), fkind, pay[i].ndim, pay[i].dims, pay[i].data, pay[i].aux),
+                  "write sample file");
+        }
+        std::vector<const char*> paths(static_cast<size_t>(n));
+        std::vector<uint64_t> fids(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            paths[static_cast<size_t>(i)] = files[static_cast<size_t>(i) % files.size()].c_str();
+            fids[static_cast<size_t>(i)] = descs[static_cast<size_t>(i)].id;
+        }
+        lfg_file_source* fs = nullptr;
+        if (lfg_file_source_open(ctx, paths.data(), fids.data(), n, static_cast<int>(getd(kv, "gpu.readers", 8)),
+                                 static_cast<int>(getd(kv, "gpu.slots", 64)), &fs) != LFG_OK)
+            throw std::runtime_error(std::string("file source: ") + lfg_files_last_error());
+        // the per-sample synthetic costs ride on the descriptors the source cannot know:
+        // wrap its next() to copy them in
+        struct Wrap {
+            lfg_source inner;
+            const std::vector<lfg_sample_desc>* descs;
+            int64_t i = 0;
+        } w{};
+        check(lfg_file_source_get(fs, &w.inner), "file source");
+        w.descs = &descs;
+        lfg_source wrapped{&w,
+                           [](void* u, lfg_sample_desc* d) {
+                               auto* ww = static_cast<Wrap*>(u);
+                               const int r = ww->inner.next(ww->inner.user, d);
+                               if (r == 1) {
+                                   for (int k = 0; k < 4; ++k) d->spin_us[k] = (*ww->descs)[static_cast<size_t>(ww->i)].spin_us[k];
+                                   ++ww->i;
+                               }
+                               return r;
+                           },
+                           [](void* u, uint64_t id) {
+                               auto* ww = static_cast<Wrap*>(u);
+                               ww->inner.release(ww->inner.user, id);
+                           }};
+        const int rc_run = lfg_run_shard_source(ctx, chain, &wrapped, n, &rc, &rep, ids.data(), bsz.data(), cls.data());
+        lfg_file_source_stats(fs, &file_bytes, &file_seconds);
+        lfg_file_source_close(fs);
+        check(rc_run, "run");
+    } else {
+        check(lfg_run_shard(ctx, chain, descs.data(), n, &rc, &rep, ids.data(), bsz.data(), cls.data()), "run");
+    }
 
     const double completion_ms = rep.elapsed_ms;
     const double slow_rate = rep.samples ? static_cast<double>(rep.slow) / static_cast<double>(rep.samples) : 0;
@@ -247,7 +312,7 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
     js << "{\n  \"workload\": \"" << loadflow::workload_name(kind) << "\",\n  \"loader\": \"" << loader
        << "\",\n  \"mode\": \"gpu\",\n  \"n_samples\": " << n << ",\n  \"batch_size\": " << B
        << ",\n  \"completion_ms\": " << completion_ms << ",\n  \"completion_ref_ms\": "
-       << completion_ms * 1000.0 / scale << ",\n  \"samples\": " << rep.samples << ",\n  \"batches\": "
+       << (scale > 0 ? std::to_string(completion_ms * 1000.0 / scale) : std::string("null")) << ",\n  \"samples\": " << rep.samples << ",\n  \"batches\": "
        << rep.batches << ",\n  \"short_batches\": " << rep.short_batches << ",\n  \"slow_rate\": " << slow_rate
        << ",\n  \"avg_throughput_mbps\": " << (completion_ms > 0 ? bytes_out / 1e6 / (completion_ms / 1e3) : 0)
        << ",\n  \"exactly_once\": " << (rep.exactly_once ? "true" : "false") << ",\n  \"duplicates\": "
@@ -259,7 +324,8 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
        << ", \"h2d_bytes\": " << rep.h2d_bytes << ", \"launches\": " << rep.launches
        << ", \"final_t_out_us\": " << rep.final_t_out_us << ", \"final_percentile\": " << rep.final_percentile
        << ", \"final_workers\": " << rep.final_workers << ", \"mean_workers\": " << rep.mean_workers
-       << "}\n}\n";
+       << ", \"src\": \"" << src_kind << "\", \"file_bytes_read\": " << file_bytes
+       << ", \"file_read_seconds\": " << file_seconds << "}\n}\n";
     std::cout << "workload=" << loadflow::workload_name(kind) << " loader=" << loader
               << " completion_ms=" << completion_ms << " throughput_mbps="
               << (completion_ms > 0 ? bytes_out / 1e6 / (completion_ms / 1e3) : 0) << " slow_rate=" << slow_rate

@@ -140,6 +140,8 @@ _sig = {
                           _P(C.c_int64), _P(C.c_int64)], C.c_int),
     "lfg_run_shard": ([_vp, _vp, _P(SampleDesc), C.c_int64, _P(RunConfig), _P(RunReport),
                        _P(C.c_uint64), _P(C.c_int32), _P(C.c_int32)], C.c_int),
+    "lfg_run_shard_source": ([_vp, _vp, _vp, C.c_int64, _P(RunConfig), _P(RunReport),
+                              _P(C.c_uint64), _P(C.c_int32), _P(C.c_int32)], C.c_int),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
@@ -442,6 +444,80 @@ class Context:
                                   cls if want_ids else None))
         nb = rep.batches
         return rep, np.array(ids[:n], dtype=np.uint64), np.array(bs[:nb]), np.array(cls[:n])
+
+    def run_shard_source(self, ch: Chain, src: "FileSource", rc: RunConfig):
+        """lfg_run_shard_source: the shard pulls samples from a streaming source."""
+        n = src.n
+        rep = RunReport()
+        ids = (C.c_uint64 * n)()
+        bs = (C.c_int32 * n)()
+        cls = (C.c_int32 * n)()
+        _check(_lib.lfg_run_shard_source(self.h, ch.handle, C.addressof(src.src), n, C.byref(rc), C.byref(rep),
+                                         ids, bs, cls))
+        return rep, np.array(ids[:n], dtype=np.uint64), np.array(bs[:rep.batches]), np.array(cls[:n])
+
+
+# ---- raw sample files + reader-thread source (include/lfgpu_files.h, host library) ----
+FILE_VOLUME, FILE_IMAGE, FILE_WAVEFORM = 1, 2, 3
+HOST_LIB_PATH = os.path.join(_PKG, "libloadflow_b200.so")
+_host = None
+
+
+def _hostlib():
+    global _host
+    if _host is None:
+        if not os.path.exists(HOST_LIB_PATH):
+            raise ImportError(f"{HOST_LIB_PATH} is missing: build it with __graft_entry__.build()")
+        h = C.CDLL(HOST_LIB_PATH)
+        h.lfg_write_sample_file.argtypes = [C.c_char_p, C.c_int, C.c_int, _P(C.c_int64), _vp, _vp]
+        h.lfg_file_source_open.argtypes = [_vp, _P(C.c_char_p), _P(C.c_uint64), C.c_int64, C.c_int, C.c_int,
+                                           _P(_vp)]
+        h.lfg_file_source_get.argtypes = [_vp, _vp]
+        h.lfg_file_source_stats.argtypes = [_vp, _P(C.c_int64), _P(C.c_double)]
+        h.lfg_file_source_close.argtypes = [_vp]
+        h.lfg_files_last_error.restype = C.c_char_p
+        _host = h
+    return _host
+
+
+def _hcheck(rc: int):
+    if rc != LFG_OK:
+        raise LfgError(rc, _hostlib().lfg_files_last_error().decode(errors="replace"))
+
+
+def write_sample_file(path: str, kind: int, dims, data: np.ndarray, aux: np.ndarray | None = None):
+    d = (C.c_int64 * 4)(*(list(dims) + [0] * (4 - len(dims))))
+    data = np.ascontiguousarray(data)
+    a = np.ascontiguousarray(aux) if aux is not None else None
+    _hcheck(_hostlib().lfg_write_sample_file(path.encode(), kind, len(dims), d, data.ctypes.data,
+                                             a.ctypes.data if a is not None else None))
+
+
+class FileSource:
+    """Reads sample files with `readers` threads into `slots` pinned buffers, in order,
+    ahead of the shard (lfg_run_shard_source); buffers are refilled on release."""
+
+    def __init__(self, ctx: "Context", paths: Sequence[str], ids: Sequence[int], readers: int = 4,
+                 slots: int = 16):
+        n = len(paths)
+        self._paths = (C.c_char_p * n)(*[p.encode() for p in paths])
+        self._ids = (C.c_uint64 * n)(*ids)
+        self.h = _vp()
+        self.n = n
+        _hcheck(_hostlib().lfg_file_source_open(ctx.h, self._paths, self._ids, n, readers, slots,
+                                                C.byref(self.h)))
+        self.src = (C.c_byte * 32)()   # lfg_source {void*, fn*, fn*}
+        _hcheck(_hostlib().lfg_file_source_get(self.h, self.src))
+
+    def stats(self):
+        b, t = C.c_int64(), C.c_double()
+        _hcheck(_hostlib().lfg_file_source_stats(self.h, C.byref(b), C.byref(t)))
+        return b.value, t.value
+
+    def close(self):
+        if self.h:
+            _hostlib().lfg_file_source_close(self.h)
+            self.h = _vp()
 
 
 def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: int = 0,
