@@ -1031,6 +1031,8 @@ void Context::launch_group(Group& g) {
                 d.h = static_cast<int32_t>(t.p2.h);
                 d.w = static_cast<int32_t>(t.p2.w);
                 d.flip = t.p2.flip;
+                d.sy = static_cast<double>(d.h) / static_cast<double>(c.oh);
+                d.sx = static_cast<double>(d.w) / static_cast<double>(c.ow);
                 counters.kernel_bytes += rrc_algo_bytes(c, t.p2);
             }
             const auto t_l = std::chrono::steady_clock::now();

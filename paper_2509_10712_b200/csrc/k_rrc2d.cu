@@ -144,7 +144,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     int ylo = 0;
     if (warp == 0) {
         const int j = lane;
-        const double sy = __ddiv_rn((double)d.h, (double)oh);
+        const double sy = d.sy;
         int y0 = 0, y1 = 0;
         float l0 = 0.f, l1 = 0.f;
         if (j < n_rows_out) src_index(y_begin + j, d.h, sy, y0, y1, l0, l1);
@@ -212,7 +212,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     const int xa = 2 * threadIdx.x;                         // columns xa, xa + 1 (ow is even)
     ColPair cp;
     if (xa < ow) {
-        const double sx = __ddiv_rn((double)d.w, (double)ow);
+        const double sx = d.sx;
         int x1a, x1b;
         float l0a, l1a, l0b, l1b;
         src_index(xa, d.w, sx, cp.x0_a, x1a, l0a, l1a);

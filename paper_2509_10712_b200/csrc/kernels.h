@@ -101,6 +101,7 @@ struct RrcDesc {
     int32_t h, w;            // crop box size
     int32_t flip;
     int32_t pad;
+    double sy, sx;           // h / oh, w / ow: source-index scales (IEEE division on the host)
 };
 struct RrcLaunch {
     int32_t oh, ow;
