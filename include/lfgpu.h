@@ -44,7 +44,8 @@ extern "C" {
 /* ---- transform op kinds: 1:1 with the reference Transform::name values ---- */
 enum {
     /* img_seg chain, proj/src/workloads.cpp:142-148 */
-    LFG_OP_RANDOM_CROP = 1,       /* param: crop_d, crop_h, crop_w          */
+    LFG_OP_RANDOM_CROP = 1,       /* param: crop_d, crop_h, crop_w, p_fg (foreground oversampling,
+                                     MLPerf RandBalancedCrop; 0 = plain random crop) */
     LFG_OP_RANDOM_FLIP = 2,       /* param: p_flip                          */
     LFG_OP_RANDOM_BRIGHTNESS = 3, /* param: p, lo, hi                       */
     LFG_OP_GAUSSIAN_NOISE = 4,    /* param: p, std_max                      */

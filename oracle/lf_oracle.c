@@ -8,6 +8,7 @@
 #include "lf_oracle.h"
 
 #include <math.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -137,6 +138,8 @@ void lfo_cfg3d_default(lfo_cfg3d* c) {
     c->p_contrast = 0.15;
     c->contrast_lo = 0.75;
     c->contrast_hi = 1.25;
+    c->has_fg = 0;
+    c->p_fg = 0.4;
 }
 
 /* Draw order, in chain order: RandomCrop u_off[3] (the offset uniforms; the
@@ -151,6 +154,14 @@ void lfo_draw3d(const lfo_cfg3d* c, uint64_t seed, uint64_t id, const int64_t di
     lfo_sample_rng(&g, seed, id);
     double u_off[3];
     for (int a = 0; a < 3; a++) u_off[a] = lfo_unif01(&g);
+    p->fg = 0;
+    p->u_cls = 0.0;
+    p->u_adj[0] = p->u_adj[1] = p->u_adj[2] = 0.0;
+    if (c->has_fg) {   /* RandomCrop's foreground draws */
+        p->fg = lfo_unif01(&g) < c->p_fg;
+        p->u_cls = lfo_unif01(&g);
+        for (int a = 0; a < 3; a++) p->u_adj[a] = lfo_unif01(&g);
+    }
     for (int a = 0; a < 3; a++) p->win[a] = c->crop[a];
     if (c->has_zoom) {
         int z_apply = lfo_unif01(&g) < c->p_zoom;
@@ -206,9 +217,62 @@ static double vox_or_zero(const float* img, const int64_t dims[3], int64_t z, in
     return (double)img[(z * dims[1] + y) * dims[2] + x];
 }
 
-void lfo_apply3d(const lfo_cfg3d* c, const lfo_params3d* p, const float* img,
+int lfo_fg_offsets(const lfo_params3d* p, const uint8_t* lbl, const int64_t dims[3], int64_t off[3]) {
+    if (!p->fg) return -1;
+    int64_t lo[8][3], hi[8][3];
+    int present[8] = {0};
+    for (int k = 0; k < 8; k++)
+        for (int a = 0; a < 3; a++) {
+            lo[k][a] = INT64_MAX;
+            hi[k][a] = -1;
+        }
+    for (int64_t z = 0; z < dims[0]; z++)
+        for (int64_t y = 0; y < dims[1]; y++)
+            for (int64_t x = 0; x < dims[2]; x++) {
+                const int v = lbl[(z * dims[1] + y) * dims[2] + x];
+                if (v < 1 || v > 7) continue;
+                const int64_t q[3] = {z, y, x};
+                present[v] = 1;
+                for (int a = 0; a < 3; a++) {
+                    if (q[a] < lo[v][a]) lo[v][a] = q[a];
+                    if (q[a] > hi[v][a]) hi[v][a] = q[a];
+                }
+            }
+    int cls[7], n = 0;
+    for (int v = 1; v <= 7; v++)
+        if (present[v]) cls[n++] = v;
+    if (n == 0) return -1;
+    int64_t k = (int64_t)floor(p->u_cls * (double)n);
+    if (k >= n) k = n - 1;
+    const int cl = cls[k];
+    for (int a = 0; a < 3; a++) {
+        const int64_t patch = p->win[a], l = lo[cl][a], h = hi[cl][a] + 1;
+        int64_t diff = patch - (h - l);
+        const int64_t sign = diff < 0 ? -1 : 1;
+        if (diff < 0) diff = -diff;
+        int64_t ladj = diff > 0 ? (int64_t)floor(p->u_adj[a] * (double)diff) : 0;
+        if (ladj >= diff && diff > 0) ladj = diff - 1;
+        const int64_t hadj = diff - ladj;
+        int64_t low = l - sign * ladj, high = h + sign * hadj;
+        if (low < 0) low = 0;
+        if (high > dims[a]) high = dims[a];
+        const int64_t d2 = patch - (high - low);
+        if (d2 > 0) {
+            if (low == 0) high += d2;
+            else low -= d2;
+        }
+        const int64_t room = dims[a] - patch > 0 ? dims[a] - patch : 0;
+        off[a] = low < 0 ? 0 : (low > room ? room : low);
+    }
+    return 0;
+}
+
+void lfo_apply3d(const lfo_cfg3d* c, const lfo_params3d* p0, const float* img,
                  const uint8_t* lbl, const int64_t dims[3], double* out_img,
                  uint8_t* out_lbl) {
+    lfo_params3d fgp = *p0;   /* foreground-biased crops move the window */
+    const lfo_params3d* p = p0;
+    if (c->has_fg && lfo_fg_offsets(p0, lbl, dims, fgp.off) == 0) p = &fgp;
     const int64_t cd = c->crop[0], ch = c->crop[1], cw = c->crop[2];
     const int64_t D = dims[0], H = dims[1], W = dims[2];
     const int64_t* win = p->win;

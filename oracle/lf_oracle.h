@@ -84,6 +84,11 @@ typedef struct {
     int32_t has_contrast;   /* RandomContrast after RandomBrightness */
     double p_contrast;      /* default 0.15 (nnU-Net ContrastAugmentation) */
     double contrast_lo, contrast_hi; /* default 0.75, 1.25 */
+    /* RandomCrop's foreground oversampling (MLPerf 3D-UNet RandBalancedCrop): with
+     * probability p_fg the window is placed around a random foreground class
+     * (labels 1..7) -- see lfo_fg_offsets */
+    int32_t has_fg;
+    double p_fg;            /* default 0.4 (MLPerf oversampling) */
 } lfo_cfg3d;
 
 typedef struct {
@@ -94,6 +99,8 @@ typedef struct {
     uint32_t key[2];        /* Philox key */
     int64_t win[3];         /* source window edge per axis (= crop unless zoomed) */
     double contrast;        /* contrast factor (1.0 when not applied) */
+    int32_t fg;             /* foreground-biased crop drawn for this sample */
+    double u_cls, u_adj[3]; /* its uniforms: class choice, per-axis placement */
 } lfo_params3d;
 
 void lfo_cfg3d_default(lfo_cfg3d* c);
@@ -106,6 +113,17 @@ void lfo_draw3d(const lfo_cfg3d* c, uint64_t seed, uint64_t id, const int64_t di
 void lfo_apply3d(const lfo_cfg3d* c, const lfo_params3d* p, const float* img,
                  const uint8_t* lbl, const int64_t dims[3], double* out_img,
                  uint8_t* out_lbl);
+/* Window origin of a foreground-biased crop (MLPerf RandBalancedCrop, with the
+ * bounding box of ALL voxels of the chosen class instead of its two largest
+ * connected components): classes present = labels 1..7 found in the volume,
+ * ascending; cl = present[floor(u_cls * n)]; per axis with the class box [lo, hi):
+ *   diff = win - (hi - lo), sign = diff < 0 ? -1 : 1, diff = |diff|,
+ *   ladj = floor(u_adj * diff), hadj = diff - ladj,
+ *   low = max(0, lo - sign*ladj), high = min(dim, hi + sign*hadj),
+ *   d2 = win - (high - low); if d2 > 0: (low == 0 ? high += d2 : low -= d2),
+ *   off = clamp(low, 0, max(dim - win, 0)).
+ * Returns 0 (off[] written) or -1 (not drawn / no foreground: the random offsets hold). */
+int lfo_fg_offsets(const lfo_params3d* p, const uint8_t* lbl, const int64_t dims[3], int64_t off[3]);
 
 /* ---------------- obj_det / ImageNet (2D) chain ---------------- */
 

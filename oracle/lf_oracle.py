@@ -35,13 +35,15 @@ class Cfg3D(C.Structure):
                 ("p_noise", C.c_double), ("noise_std_max", C.c_double),
                 ("has_zoom", C.c_int32), ("p_zoom", C.c_double), ("zoom_lo", C.c_double),
                 ("zoom_hi", C.c_double), ("has_contrast", C.c_int32), ("p_contrast", C.c_double),
-                ("contrast_lo", C.c_double), ("contrast_hi", C.c_double)]
+                ("contrast_lo", C.c_double), ("contrast_hi", C.c_double), ("has_fg", C.c_int32),
+                ("p_fg", C.c_double)]
 
 
 class Params3D(C.Structure):
     _fields_ = [("off", C.c_int64 * 3), ("flip", C.c_int32 * 3), ("scale", C.c_double),
                 ("sigma", C.c_double), ("key", C.c_uint32 * 2), ("win", C.c_int64 * 3),
-                ("contrast", C.c_double)]
+                ("contrast", C.c_double), ("fg", C.c_int32), ("u_cls", C.c_double),
+                ("u_adj", C.c_double * 3)]
 
 
 class Cfg2D(C.Structure):
@@ -79,6 +81,7 @@ _lib.lfo_cfg3d_default.argtypes = [_P(Cfg3D)]
 _lib.lfo_draw3d.argtypes = [_P(Cfg3D), C.c_uint64, C.c_uint64, _P(C.c_int64), _P(Params3D)]
 _lib.lfo_apply3d.argtypes = [_P(Cfg3D), _P(Params3D), C.c_void_p, C.c_void_p, _P(C.c_int64),
                              C.c_void_p, C.c_void_p]
+_lib.lfo_fg_offsets.argtypes = [_P(Params3D), C.c_void_p, _P(C.c_int64), _P(C.c_int64)]
 _lib.lfo_cfg2d_default.argtypes = [_P(Cfg2D)]
 _lib.lfo_draw2d.argtypes = [_P(Cfg2D), C.c_uint64, C.c_uint64, C.c_int64, C.c_int64,
                             _P(Params2D)]
@@ -149,6 +152,15 @@ def apply3d(cfg: Cfg3D, p: Params3D, img: np.ndarray, lbl: np.ndarray):
     _lib.lfo_apply3d(C.byref(cfg), C.byref(p), _ptr(img), _ptr(lbl), dims, _ptr(out_img),
                      _ptr(out_lbl))
     return out_img, out_lbl
+
+
+def fg_offsets(p: Params3D, lbl: np.ndarray):
+    """Final window origin of a foreground-biased crop, or None (random offsets hold)."""
+    lbl = np.ascontiguousarray(lbl, dtype=np.uint8)
+    dims = (C.c_int64 * 3)(*lbl.shape)
+    off = (C.c_int64 * 3)()
+    r = _lib.lfo_fg_offsets(C.byref(p), _ptr(lbl), dims, off)
+    return None if r != 0 else list(off)
 
 
 def chain3d(cfg: Cfg3D, seed: int, sid: int, img: np.ndarray, lbl: np.ndarray):

@@ -251,7 +251,8 @@ int lfg_draw_params(lfg_chain* chain, uint64_t seed, const lfg_sample_desc* s, d
             draw_3d(c, seed, s->id, s->dims, p);
             v = {double(p.off[0]), double(p.off[1]), double(p.off[2]), double(p.flip[0]),
                  double(p.flip[1]), double(p.flip[2]), p.scale, p.sigma, double(p.key[0]),
-                 double(p.key[1]), double(p.win[0]), double(p.win[1]), double(p.win[2]), p.contrast};
+                 double(p.key[1]), double(p.win[0]), double(p.win[1]), double(p.win[2]), p.contrast,
+                 double(p.fg), p.u_cls, p.u_adj[0], p.u_adj[1], p.u_adj[2]};
         } else if (c.fam == FAM_RRC2D) {
             Params2D p;
             draw_2d(c, seed, s->id, s->dims[0], s->dims[1], p);

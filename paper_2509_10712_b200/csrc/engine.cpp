@@ -51,13 +51,22 @@ struct SampleRng {
 }  // namespace
 
 // Draw order (chain order; oracle/lf_oracle.c lfo_draw3d): RandomCrop offset
-// uniforms, [RandomZoom3D apply + factor], flips, brightness, [RandomContrast
+// uniforms, [its foreground draws: apply, class, 3 placements], [RandomZoom3D
+// apply + factor], flips, brightness, [RandomContrast
 // apply + factor], noise, Philox key.  The offset is floor(u * (room + 1)) once
 // the window edge is known -- randint(0, room) of the plain chain.
 void draw_3d(const Chain& c, uint64_t seed, uint64_t id, const int64_t dims[3], Params3D& p) {
     SampleRng r(seed, id);
     double u_off[3];
     for (int a = 0; a < 3; ++a) u_off[a] = r.unif01();
+    p.fg = 0;
+    p.u_cls = 0.0;
+    p.u_adj[0] = p.u_adj[1] = p.u_adj[2] = 0.0;
+    if (c.has_fg) {   // RandomCrop's foreground draws
+        p.fg = r.unif01() < c.p_fg;
+        p.u_cls = r.unif01();
+        for (int a = 0; a < 3; ++a) p.u_adj[a] = r.unif01();
+    }
     for (int a = 0; a < 3; ++a) p.win[a] = c.crop[a];
     if (c.has_zoom) {
         const bool z_apply = r.unif01() < c.p_zoom;
@@ -215,6 +224,8 @@ Context::Context(const lfg_config& c) : cfg(c) {
     cuda_check(warm_img3d(), "load img3d kernel");
     cuda_check(warm_img3d_zoom(), "load img3d zoom kernels");
     cuda_check(cudaMalloc(&csum_, kCsumSlots * sizeof(double)), "contrast sums");
+    cuda_check(cudaMalloc(&fg_box_, size_t(kFgSlots) * kMax3D * 48 * sizeof(int32_t)), "fg boxes");
+    cuda_check(cudaMalloc(&fg_offs_, size_t(kFgSlots) * kMax3D * sizeof(int4)), "fg offsets");
     cuda_check(warm_rrc2d(), "load rrc2d kernel");
     cuda_check(warm_misc(), "load misc kernels");
     cuda_check(warm_speech(), "load speech kernels");
@@ -238,6 +249,8 @@ Context::~Context() {
     }
     for (auto& r : raws_) cudaFree(r.ptr);
     if (csum_) cudaFree(csum_);
+    if (fg_box_) cudaFree(fg_box_);
+    if (fg_offs_) cudaFree(fg_offs_);
     for (auto s : streams_) cudaStreamDestroy(s);
     cudaStreamDestroy(seal_stream);
     cudaStreamDestroy(aux_stream);
@@ -327,6 +340,9 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
         switch (o.kind) {
             case LFG_OP_RANDOM_CROP:
                 for (int a = 0; a < 3; ++a) c->crop[a] = p[a] > 0 ? static_cast<int>(p[a]) : 128;
+                if (p[3] < 0 || p[3] > 1) fail(LFG_ERR_INVALID, "RandomCrop foreground probability must be in [0, 1]");
+                c->has_fg = p[3] > 0;
+                c->p_fg = p[3];
                 has_anchor = true;
                 break;
             case LFG_OP_RANDOM_FLIP: c->p_flip = p[0]; break;
@@ -668,6 +684,9 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
         if (s.ndim != 1 || s.dims[0] < c->n_fft / 2 + 1 || s.dims[0] > c->max_L)
             fail(LFG_ERR_INVALID, "speech sample needs a waveform of length in [n_fft/2 + 1, max_L]");
     }
+    if (s.src_kind == LFG_SRC_HOST_PINNED && c->fam == FAM_IMG3D && c->has_fg)
+        fail(LFG_ERR_UNSUPPORTED,
+             "foreground-biased RandomCrop needs HBM-resident volumes (the window depends on the label scan)");
     if (s.src_kind == LFG_SRC_HOST_PINNED) {
         // K0 reads the payload over PCIe through its UVA mapping: it must be pinned
         for (const void* p : {s.data, s.aux}) {
@@ -981,26 +1000,58 @@ void Context::launch_group(Group& g) {
                 d.csum = nullptr;
                 counters.kernel_bytes += img3d_algo_bytes(c, t);
             }
-            // RandomContrast: K5 sums each contrasted sample's crop first (same stream)
+            // RandomCrop foreground oversampling: K2 scans the label volumes of the
+            // samples that drew it, then resolves every window origin (same stream)
+            if (c.has_fg) {
+                FgLaunch F{};
+                int n_fg = 0;
+                for (int i = 0; i < n; ++i) {
+                    const Params3D& p3 = tickets[g.tickets[i]].p3;
+                    F.d[i].fg = p3.fg;
+                    F.d[i].u_cls = p3.u_cls;
+                    for (int a = 0; a < 3; ++a) F.d[i].u_adj[a] = p3.u_adj[a];
+                    if (p3.fg) {
+                        ++n_fg;
+                        counters.kernel_bytes += L.d[i].lbl_pz * L.d[i].sdim[0];   // the label volume, once
+                    }
+                }
+                if (n_fg > 0) {
+                    const int slot = fg_next_;
+                    fg_next_ = (fg_next_ + 1) % kFgSlots;
+                    int32_t* box = fg_box_ + size_t(slot) * kMax3D * 48;
+                    int4* offs = fg_offs_ + size_t(slot) * kMax3D;
+                    start();
+                    for (int i = 0; i < n; ++i) {   // mins preset large, maxs to -1
+                        cuda_check(cudaMemsetAsync(box + i * 48, 0x7f, 24 * sizeof(int32_t), st), "fg box reset");
+                        cuda_check(cudaMemsetAsync(box + i * 48 + 24, 0xff, 24 * sizeof(int32_t), st), "fg box reset");
+                    }
+                    cuda_check(launch_fg_scan(L, F, box, st), "fg scan launch");
+                    cuda_check(launch_fg_offsets(L, F, box, offs, st), "fg offsets launch");
+                    counters.launches += 2;
+                    L.offs = offs;
+                }
+            }
+            // RandomContrast: K5 sums each contrasted sample's crop first (same stream);
+            // it runs over the whole group and skips the samples without contrast
             if (c.has_contrast) {
-                Img3dLaunch M{};
-                for (int a = 0; a < 3; ++a) M.crop[a] = c.crop[a];
+                int n_c = 0;
                 for (int i = 0; i < n; ++i) {
                     if (tickets[g.tickets[i]].p3.contrast == 1.0) continue;
                     L.d[i].csum = csum_ + csum_next_;
                     csum_next_ = (csum_next_ + 1) % kCsumSlots;
-                    M.d[M.n++] = L.d[i];
+                    ++n_c;
                     const Img3dDesc& d = L.d[i];
                     counters.kernel_bytes += int64_t(4) * std::min(d.win[0], d.sdim[0] - d.off[0]) *
                                              std::min(d.win[1], d.sdim[1] - d.off[1]) *
                                              std::min(d.win[2], d.sdim[2] - d.off[2]);
                 }
-                if (M.n > 0) {
+                if (n_c > 0) {
                     start();
-                    for (int i = 0; i < M.n; ++i)
-                        cuda_check(cudaMemsetAsync(const_cast<double*>(M.d[i].csum), 0, sizeof(double), st),
-                                   "csum reset");
-                    cuda_check(launch_img3d_mean(M, st), "img3d mean launch");
+                    for (int i = 0; i < n; ++i)
+                        if (L.d[i].csum != nullptr)
+                            cuda_check(cudaMemsetAsync(const_cast<double*>(L.d[i].csum), 0, sizeof(double), st),
+                                       "csum reset");
+                    cuda_check(launch_img3d_mean(L, st), "img3d mean launch");
                     counters.launches++;
                 }
             }

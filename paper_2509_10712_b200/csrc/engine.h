@@ -84,6 +84,8 @@ struct Chain {
     int crop[3] = {128, 128, 128};
     double p_flip = 0, p_bright = 0, b_lo = 1, b_hi = 1, p_noise = 0, noise_max = 0;
     bool has_zoom = false, has_contrast = false;     // optional RandomZoom3D / RandomContrast
+    bool has_fg = false;                              // RandomCrop foreground oversampling (K2)
+    double p_fg = 0;
     double p_zoom = 0, z_lo = 1, z_hi = 1, p_contrast = 0, c_lo = 1, c_hi = 1;
     // rrc2d
     int oh = 224, ow = 224;
@@ -110,6 +112,8 @@ struct Params3D {
     uint32_t key[2];
     int64_t win[3];       // source window edge (RandomZoom3D; = crop otherwise)
     double contrast;      // RandomContrast factor (1 = not applied)
+    int fg;               // foreground-biased crop drawn: the window origin comes from K2
+    double u_cls, u_adj[3];
 };
 struct Params2D { int64_t top, left, h, w; int flip; int64_t rows_touched; };
 struct ParamsSp { int T; int f_lo[2], f_w[2]; int t_lo[10], t_w[10]; };
@@ -256,6 +260,10 @@ private:
     static constexpr int kCsumSlots = 4096;   // RandomContrast crop sums (a ring; stream-ordered)
     double* csum_ = nullptr;
     int csum_next_ = 0;
+    static constexpr int kFgSlots = 256;   // K2 scratch rings (launch groups; stream-ordered)
+    int32_t* fg_box_ = nullptr;            // [kFgSlots][kMax3D][8 classes][6]
+    int4* fg_offs_ = nullptr;              // [kFgSlots][kMax3D]
+    int fg_next_ = 0;
     std::vector<cudaStream_t> streams_;
     std::vector<int> free_streams_;
     std::vector<cudaEvent_t> free_events_;

@@ -1,0 +1,182 @@
+// k_fgcrop.cu -- K2: RandomCrop's foreground oversampling (MLPerf 3D-UNet
+// RandBalancedCrop; RandomCrop carries the img_seg chain's 68% cost share,
+// proj/src/workloads.cpp:149).  Semantics: oracle/lf_oracle.c lfo_fg_offsets.
+//
+// fg_scan_kernel: one CTA per (label plane, scanned sample); warps walk rows,
+// lanes 16-byte chunks (all-background chunks cost one compare), and keep the
+// per-class (labels 1..7) x / y extents in registers; warp min/max reductions
+// (redux.sync), shared-memory atomics per CTA, then one global atomicMin /
+// atomicMax per class and bound.  HBM-bound: the whole label volume is read
+// once (D*H*W bytes) -- the genuinely heavy step that makes foreground-biased
+// samples the slow tail.
+//
+// fg_offsets_kernel: one thread per sample of the launch group turns the class
+// boxes and the sample's host-drawn uniforms into the window origin, exactly as
+// the oracle (fp64 floor of u * span), or marks it "random offsets hold".
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace lfg {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kClasses = 8;   // index = label value; 1..7 are foreground classes
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void note(int v, uint32_t x, uint32_t xmin[kClasses], uint32_t xmax[kClasses],
+                                     uint32_t& seen) {
+#pragma unroll
+    for (int c = 1; c < kClasses; ++c) {
+        if (v == c) {
+            xmin[c] = min(xmin[c], x);
+            xmax[c] = (xmax[c] == kNone) ? x : max(xmax[c], x);
+            seen |= 1u << c;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_constant__ Img3dLaunch L,
+                                                               const __grid_constant__ FgLaunch F,
+                                                               int32_t* __restrict__ box) {
+    const int i = blockIdx.y;
+    if (!F.d[i].fg) return;
+    const Img3dDesc& d = L.d[i];
+    const int z = blockIdx.x;
+    if (z >= d.sdim[0]) return;
+    __shared__ uint32_t s_min[kClasses][3], s_max[kClasses][3];
+    __shared__ uint32_t s_seen;
+    if (threadIdx.x < kClasses * 3) {
+        (&s_min[0][0])[threadIdx.x] = kNone;
+        (&s_max[0][0])[threadIdx.x] = 0;
+    }
+    if (threadIdx.x == 0) s_seen = 0;
+    __syncthreads();
+    const int H = d.sdim[1], W = d.sdim[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t xmin[kClasses], xmax[kClasses], ymin[kClasses], ymax[kClasses];
+#pragma unroll
+    for (int c = 0; c < kClasses; ++c) xmin[c] = ymin[c] = kNone, xmax[c] = ymax[c] = kNone;
+    uint32_t seen_all = 0;
+    for (int y = warp; y < H; y += kScanThreads / 32) {
+        const uint8_t* row = d.lbl + (int64_t)z * d.lbl_pz + (int64_t)y * d.lbl_py;
+        uint32_t seen = 0;
+        if ((reinterpret_cast<uintptr_t>(row) & 15) == 0 && (W & 15) == 0) {
+            const uint4* r4 = reinterpret_cast<const uint4*>(row);
+            for (int q = lane; q < (W >> 4); q += 32) {
+                const uint4 v = __ldcs(r4 + q);   // streamed: read once
+                if ((v.x | v.y | v.z | v.w) == 0u) continue;   // background chunk
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int b = (int)((w[k >> 2] >> (8 * (k & 3))) & 0xFFu);
+                    if (b != 0) note(b, (uint32_t)(16 * q + k), xmin, xmax, seen);
+                }
+            }
+        } else {
+            for (int x = lane; x < W; x += 32) {
+                const int b = row[x];
+                if (b != 0) note(b, (uint32_t)x, xmin, xmax, seen);
+            }
+        }
+#pragma unroll
+        for (int c = 1; c < kClasses; ++c)
+            if (seen & (1u << c)) {
+                ymin[c] = min(ymin[c], (uint32_t)y);
+                ymax[c] = (ymax[c] == kNone) ? (uint32_t)y : max(ymax[c], (uint32_t)y);
+            }
+        seen_all |= seen;
+    }
+    // warp reductions (kNone = absent: min ignores it; max treats it as absent via 0-shift)
+    seen_all = __reduce_or_sync(0xFFFFFFFFu, seen_all);
+#pragma unroll
+    for (int c = 1; c < kClasses; ++c) {
+        if (!(seen_all & (1u << c))) continue;   // warp-uniform
+        const uint32_t a = __reduce_min_sync(0xFFFFFFFFu, xmin[c]);
+        const uint32_t b = __reduce_max_sync(0xFFFFFFFFu, xmax[c] == kNone ? 0u : xmax[c] + 1u);
+        const uint32_t e = __reduce_min_sync(0xFFFFFFFFu, ymin[c]);
+        const uint32_t f = __reduce_max_sync(0xFFFFFFFFu, ymax[c] == kNone ? 0u : ymax[c] + 1u);
+        if (lane == 0) {
+            atomicMin(&s_min[c][2], a);
+            atomicMax(&s_max[c][2], b);
+            atomicMin(&s_min[c][1], e);
+            atomicMax(&s_max[c][1], f);
+            atomicOr(&s_seen, 1u << c);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < kClasses && (s_seen & (1u << threadIdx.x))) {
+        const int c = threadIdx.x;
+        int32_t* mins = box + (int64_t)i * kClasses * 6;
+        int32_t* maxs = mins + kClasses * 3;
+        atomicMin(&mins[c * 3 + 0], z);
+        atomicMax(&maxs[c * 3 + 0], z);
+        atomicMin(&mins[c * 3 + 1], (int32_t)s_min[c][1]);
+        atomicMax(&maxs[c * 3 + 1], (int32_t)s_max[c][1] - 1);
+        atomicMin(&mins[c * 3 + 2], (int32_t)s_min[c][2]);
+        atomicMax(&maxs[c * 3 + 2], (int32_t)s_max[c][2] - 1);
+    }
+}
+
+__global__ void fg_offsets_kernel(const __grid_constant__ Img3dLaunch L, const __grid_constant__ FgLaunch F,
+                                  const int32_t* __restrict__ box, int4* __restrict__ offs) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L.n) return;
+    const Img3dDesc& d = L.d[i];
+    const FgDraw& g = F.d[i];
+    int4 o = make_int4(d.off[0], d.off[1], d.off[2], 0);
+    if (g.fg) {
+        const int32_t* mins = box + (int64_t)i * kClasses * 6;
+        const int32_t* maxs = mins + kClasses * 3;
+        int cls[7], n = 0;
+        for (int c = 1; c < kClasses; ++c)
+            if (maxs[c * 3] >= 0) cls[n++] = c;
+        if (n > 0) {
+            int k = (int)floor(g.u_cls * (double)n);
+            if (k >= n) k = n - 1;
+            const int cl = cls[k];
+            int off[3];
+            for (int a = 0; a < 3; ++a) {
+                const int64_t patch = d.win[a], lo = mins[cl * 3 + a], hi = (int64_t)maxs[cl * 3 + a] + 1;
+                const int64_t dim = d.sdim[a];
+                int64_t diff = patch - (hi - lo);
+                const int64_t sign = diff < 0 ? -1 : 1;
+                if (diff < 0) diff = -diff;
+                int64_t ladj = diff > 0 ? (int64_t)floor(g.u_adj[a] * (double)diff) : 0;
+                if (ladj >= diff && diff > 0) ladj = diff - 1;
+                const int64_t hadj = diff - ladj;
+                int64_t low = lo - sign * ladj, high = hi + sign * hadj;
+                if (low < 0) low = 0;
+                if (high > dim) high = dim;
+                const int64_t d2 = patch - (high - low);
+                if (d2 > 0) {
+                    if (low == 0) high += d2;
+                    else low -= d2;
+                }
+                const int64_t room = dim - patch > 0 ? dim - patch : 0;
+                off[a] = (int)(low < 0 ? 0 : (low > room ? room : low));
+            }
+            o = make_int4(off[0], off[1], off[2], 1);
+        }
+    }
+    offs[i] = o;
+}
+
+}  // namespace
+
+cudaError_t launch_fg_scan(const Img3dLaunch& L, const FgLaunch& F, int32_t* box, cudaStream_t s) {
+    if (L.n <= 0) return cudaSuccess;
+    int planes = 1;
+    for (int i = 0; i < L.n; ++i) planes = planes > L.d[i].sdim[0] ? planes : L.d[i].sdim[0];
+    fg_scan_kernel<<<dim3(planes, L.n), kScanThreads, 0, s>>>(L, F, box);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fg_offsets(const Img3dLaunch& L, const FgLaunch& F, const int32_t* box, int4* offs,
+                              cudaStream_t s) {
+    if (L.n <= 0) return cudaSuccess;
+    fg_offsets_kernel<<<1, 32, 0, s>>>(L, F, box, offs);
+    return cudaGetLastError();
+}
+
+}  // namespace lfg

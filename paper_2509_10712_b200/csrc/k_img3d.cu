@@ -49,14 +49,16 @@ __device__ __forceinline__ float4 shift4(float4 a, float4 b, int m) {
 __global__ void __launch_bounds__(32 * kRowsY)
 img3d_kernel(const __grid_constant__ Img3dLaunch L) {
     const Img3dDesc& d = L.d[blockIdx.z];
+    int off[3];
+    img3d_offsets(L, blockIdx.z, off);
     const int cd = L.crop[0], ch = L.crop[1], cw = L.crop[2];
     const int cw4 = cw >> 2;
     const int z = blockIdx.y;
     const int fz = (d.flip & 1) ? cd - 1 - z : z;
-    const int sz = d.off[0] + fz;
+    const int sz = off[0] + fz;
     const bool z_ok = sz < d.sdim[0];
     const bool flip_w = (d.flip & 4) != 0;
-    const int valid_w = d.sdim[2] - d.off[2];             // window columns inside the source
+    const int valid_w = d.sdim[2] - off[2];             // window columns inside the source
     const bool noise = d.sigma != 0.0f;
     float A, B;                                           // brightness (+ contrast) affine
     img3d_affine(d, (int64_t)cd * ch * cw, A, B);
@@ -71,15 +73,15 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
             const int y = blockIdx.x * kRowsPerCta + threadIdx.y + r * kRowsY;
             ys[r] = y;
             const int fy = (d.flip & 2) ? ch - 1 - y : y;
-            const int sy = d.off[1] + fy;
+            const int sy = off[1] + fy;
             v[r] = make_float4(0.f, 0.f, 0.f, 0.f);
             l[r] = 0u;
             if (!(z_ok && y < ch && sy < d.sdim[1]) || 4 * qs >= valid_w) continue;
             // logical column 0 of this window row (row start + skew + crop offset)
             const float* irow = d.img + sz * d.img_pz + sy * d.img_py +
-                                ((d.img_sk0 + sz * d.img_skz + sy * d.img_sky) & 3) + d.off[2];
+                                ((d.img_sk0 + sz * d.img_skz + sy * d.img_sky) & 3) + off[2];
             const uint8_t* lrow = d.lbl + sz * d.lbl_pz + sy * d.lbl_py +
-                                  ((d.lbl_sk0 + sz * d.lbl_skz + sy * d.lbl_sky) & 15) + d.off[2];
+                                  ((d.lbl_sk0 + sz * d.lbl_skz + sy * d.lbl_sky) & 15) + off[2];
             const int mi = (int)((reinterpret_cast<uintptr_t>(irow) >> 2) & 3);   // warp-uniform
             const int mb = (int)(reinterpret_cast<uintptr_t>(lrow) & 3);
             const float4* ia = reinterpret_cast<const float4*>(irow - mi) + qs;
@@ -207,6 +209,14 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(L.d);
         uint32_t* dst = reinterpret_cast<uint32_t*>(sdesc);
         for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+    }
+    if (L.offs != nullptr) {   // foreground-biased crops: window origins resolved by K2
+        __syncthreads();
+        if ((int)threadIdx.x < L.n) {
+            int off[3];
+            img3d_offsets(L, threadIdx.x, off);
+            for (int a = 0; a < 3; ++a) sdesc[threadIdx.x].off[a] = off[a];
+        }
     }
     __syncthreads();
 

@@ -55,15 +55,15 @@ __device__ __forceinline__ void taps(int dst, int in, double scale, int& i0, int
 
 // start of source row (z, y) of the window (window coordinates), or null if the
 // row lies outside the source's valid extent (zero padding)
-__device__ __forceinline__ const float* img_row(const Img3dDesc& d, int z, int y) {
-    const int sz = d.off[0] + z, sy = d.off[1] + y;
+__device__ __forceinline__ const float* img_row(const Img3dDesc& d, const int off[3], int z, int y) {
+    const int sz = off[0] + z, sy = off[1] + y;
     if (sz >= d.sdim[0] || sy >= d.sdim[1]) return nullptr;
-    return d.img + sz * d.img_pz + sy * d.img_py + ((d.img_sk0 + sz * d.img_skz + sy * d.img_sky) & 3) + d.off[2];
+    return d.img + sz * d.img_pz + sy * d.img_py + ((d.img_sk0 + sz * d.img_skz + sy * d.img_sky) & 3) + off[2];
 }
-__device__ __forceinline__ const uint8_t* lbl_row(const Img3dDesc& d, int z, int y) {
-    const int sz = d.off[0] + z, sy = d.off[1] + y;
+__device__ __forceinline__ const uint8_t* lbl_row(const Img3dDesc& d, const int off[3], int z, int y) {
+    const int sz = off[0] + z, sy = off[1] + y;
     if (sz >= d.sdim[0] || sy >= d.sdim[1]) return nullptr;
-    return d.lbl + sz * d.lbl_pz + sy * d.lbl_py + ((d.lbl_sk0 + sz * d.lbl_skz + sy * d.lbl_sky) & 15) + d.off[2];
+    return d.lbl + sz * d.lbl_pz + sy * d.lbl_py + ((d.lbl_sk0 + sz * d.lbl_skz + sy * d.lbl_sky) & 15) + off[2];
 }
 
 __global__ void __launch_bounds__(32 * kZRows) img3d_zoom_kernel(const __grid_constant__ Img3dLaunch L) {
@@ -71,10 +71,12 @@ __global__ void __launch_bounds__(32 * kZRows) img3d_zoom_kernel(const __grid_co
     __shared__ float2 sx_w[kMaxCrop];     // weights l0, l1
     __shared__ int sx_near[kMaxCrop];     // nearest label column
     const Img3dDesc& d = L.d[blockIdx.z];
+    int off[3];
+    img3d_offsets(L, blockIdx.z, off);
     const int cd = L.crop[0], ch = L.crop[1], cw = L.crop[2];
     const int tid = threadIdx.y * 32 + threadIdx.x;
     const bool flip_w = (d.flip & 4) != 0;
-    const int valid_w = d.sdim[2] - d.off[2];      // window columns inside the source
+    const int valid_w = d.sdim[2] - off[2];      // window columns inside the source
     for (int x = tid; x < cw; x += 32 * kZRows) {
         const int wx = flip_w ? cw - 1 - x : x;
         int i0, i1;
@@ -109,11 +111,11 @@ __global__ void __launch_bounds__(32 * kZRows) img3d_zoom_kernel(const __grid_co
         taps(wz, d.win[0], d.zscale[0], z0, z1, lz0d, lz1d);
         const float lz0 = (float)lz0d, lz1 = (float)lz1d;
         const int nz = min(wz * d.win[0] / cd, d.win[0] - 1);
-        const float* r00 = img_row(d, z0, y0);
-        const float* r01 = img_row(d, z0, y1);
-        const float* r10 = img_row(d, z1, y0);
-        const float* r11 = img_row(d, z1, y1);
-        const uint8_t* rl = lbl_row(d, nz, ny);
+        const float* r00 = img_row(d, off, z0, y0);
+        const float* r01 = img_row(d, off, z0, y1);
+        const float* r10 = img_row(d, off, z1, y0);
+        const float* r11 = img_row(d, off, z1, y1);
+        const uint8_t* rl = lbl_row(d, off, nz, ny);
         auto tap_row = [&](const float* r, int2 t, float2 w) -> float {
             if (r == nullptr) return 0.0f;
             return fmaf(w.x, __ldg(r + t.x), w.y * __ldg(r + t.y));
@@ -177,18 +179,21 @@ __global__ void __launch_bounds__(kMeanThreads) img3d_mean_kernel(const __grid_c
     __shared__ float cy[kMaxCrop * 2];
     __shared__ double red[kMeanThreads / 32];
     const Img3dDesc& d = L.d[blockIdx.y];
+    if (d.csum == nullptr) return;                 // not a contrasted sample
+    int off[3];
+    img3d_offsets(L, blockIdx.y, off);
     const int z = blockIdx.x;                      // window plane
     if (z >= d.win[0]) return;
-    const int ww = min(d.win[2], d.sdim[2] - d.off[2]);   // window extent inside the source
-    const int wh = min(d.win[1], d.sdim[1] - d.off[1]);
-    if (d.off[0] + z >= d.sdim[0] || ww <= 0 || wh <= 0) return;
+    const int ww = min(d.win[2], d.sdim[2] - off[2]);   // window extent inside the source
+    const int wh = min(d.win[1], d.sdim[1] - off[1]);
+    if (off[0] + z >= d.sdim[0] || ww <= 0 || wh <= 0) return;
     for (int i = threadIdx.x; i < ww; i += kMeanThreads) cx[i] = axis_weight(i, d.win[2], L.crop[2], d.zscale[2]);
     for (int i = threadIdx.x; i < wh; i += kMeanThreads) cy[i] = axis_weight(i, d.win[1], L.crop[1], d.zscale[1]);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double acc = 0.0;
     for (int y = warp; y < wh; y += kMeanThreads / 32) {
-        const float* r = img_row(d, z, y);
+        const float* r = img_row(d, off, z, y);
         float s = 0.0f;
         for (int x = lane; x < ww; x += 32) s = fmaf(cx[x], __ldg(r + x), s);
         acc += (double)cy[y] * (double)s;

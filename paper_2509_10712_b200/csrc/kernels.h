@@ -75,6 +75,9 @@ __device__ __forceinline__ void img3d_affine(const Img3dDesc& d, int64_t crop_vo
 struct Img3dLaunch {
     int32_t crop[3];
     int32_t n;
+    // RandomCrop foreground oversampling: window origins resolved on the device by K2
+    // (offs[i].w = 1: use offs[i].xyz = (d, h, w) instead of d[i].off); null: none
+    const int4* offs;
     int32_t tma;             // 1: every sample has tm_img/tm_lbl (TMA tile path)
     int32_t debug;           // profiling switch (LFG_IMG3D_DEBUG): 1 no stores, 2 no loads
     Img3dDesc d[kMax3D];
@@ -84,6 +87,20 @@ struct Img3dLaunch {
     CUtensorMap tm_img[kMax3D];
     CUtensorMap tm_lbl[kMax3D];
 };
+__device__ __forceinline__ void img3d_offsets(const Img3dLaunch& L, int i, int off[3]) {
+    const Img3dDesc& d = L.d[i];
+    off[0] = d.off[0];
+    off[1] = d.off[1];
+    off[2] = d.off[2];
+    if (L.offs != nullptr) {
+        const int4 o = L.offs[i];
+        if (o.w) {
+            off[0] = o.x;
+            off[1] = o.y;
+            off[2] = o.z;
+        }
+    }
+}
 constexpr int kImg3dTileRows = 8;
 // TMA path preconditions on the sample / crop geometry (else the row kernel runs)
 inline bool img3d_tma_ok(const void* img, const void* lbl, const int64_t dims[3], const int crop[3]) {
@@ -162,6 +179,21 @@ cudaError_t launch_img3d_zoom(const Img3dLaunch& L, cudaStream_t s);
 // K5: per-sample sum of the (resampled) crop for RandomContrast; L.d[i].csum
 // must point at zeroed doubles
 cudaError_t launch_img3d_mean(const Img3dLaunch& L, cudaStream_t s);
+// K2: RandomCrop foreground oversampling.  fg_scan: per-class (labels 1..7)
+// bounding boxes of the samples with scan[i] = 1 into box[i] (mins then maxs, 8
+// classes x 3 axes each; mins preset to 0x7f7f7f7f, maxs to -1); fg_offsets: the
+// window origins of every sample into offs (w = 0 where the random offsets hold).
+struct FgDraw {
+    int32_t fg;              // foreground crop drawn (its label volume is scanned)
+    int32_t pad;
+    double u_cls, u_adj[3];
+};
+struct FgLaunch {
+    FgDraw d[kMax3D];        // per sample of the Img3dLaunch
+};
+cudaError_t launch_fg_scan(const Img3dLaunch& L, const FgLaunch& F, int32_t* box, cudaStream_t s);
+cudaError_t launch_fg_offsets(const Img3dLaunch& L, const FgLaunch& F, const int32_t* box, int4* offs,
+                              cudaStream_t s);
 // encodes L.tm_img[i] / L.tm_lbl[i] for a D,H,W f32 volume + u8 label (see img3d_tma_ok)
 cudaError_t img3d_encode_maps(Img3dLaunch& L, int i, const void* img, const void* lbl,
                               const int64_t dims[3]);

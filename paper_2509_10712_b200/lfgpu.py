@@ -177,15 +177,17 @@ def op(kind: int, name: str, size_factor: float = 1.0, params: Sequence[float] =
 
 def img_seg_ops(crop=(128, 128, 128), p_flip=1 / 3, p_bright=0.1, bright=(0.7, 1.3),
                 p_noise=0.1, noise_std_max=0.1, spin_first: bool = False,
-                zoom=None, contrast=None) -> list[Op]:
+                zoom=None, contrast=None, p_fg: float = 0.0) -> list[Op]:
     """img_seg chain, proj/src/workloads.cpp:142-148 (size factors included).
 
     Optional ops (north_star "trilinear resize" / "brightness/contrast"; not in the
-    reference chain, so off by default): ``zoom=(p, lo, hi)`` adds RandomZoom3D after
+    reference chain, so off by default): ``p_fg`` > 0 makes RandomCrop oversample the
+    foreground with that probability (MLPerf RandBalancedCrop, kernel K2; HBM-resident
+    volumes only); ``zoom=(p, lo, hi)`` adds RandomZoom3D after
     RandomCrop (window edge round(crop * f), trilinear back to the crop; labels
     nearest); ``contrast=(p, lo, hi)`` adds RandomContrast after RandomBrightness."""
     ops = [op(OP_SPIN, "SampleCost")] if spin_first else []
-    ops.append(op(OP_RANDOM_CROP, "RandomCrop", 0.0735, crop))
+    ops.append(op(OP_RANDOM_CROP, "RandomCrop", 0.0735, list(crop) + [p_fg]))
     if zoom is not None:
         ops.append(op(OP_RANDOM_ZOOM3D, "RandomZoom3D", 1.0, list(zoom)))
     ops += [

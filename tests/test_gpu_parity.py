@@ -178,6 +178,67 @@ def test_img3d_zoom_contrast_matches_oracle(ctx, lfgpu, oracle, case, src_kind):
     ctx.destroy_chain(ch)
 
 
+# ------------------------------------------------------------------ foreground crop (K2)
+@pytest.mark.parametrize("case", range(4))
+def test_img3d_foreground_crop_matches_oracle(ctx, lfgpu, oracle, case):
+    """RandomCrop with foreground oversampling (K2 label scan + window resolution on
+    the device, then K1 TMA / row path, K4 with zoom, K5 with contrast): labels
+    bit-exact and images within tolerance of the oracle, whose window origin is pinned
+    to a numpy restatement in test_oracle."""
+    dims, crop, extra = [
+        ((40, 48, 64), (16, 16, 32), {}),                                   # TMA path
+        ((40, 48, 60), (16, 16, 32), {}),                                   # row path (W % 16 != 0)
+        ((40, 48, 64), (16, 16, 32), dict(zoom=(1.0, 0.8, 1.2))),            # K4
+        ((40, 48, 64), (16, 16, 32), dict(contrast=(1.0, 0.75, 1.25))),      # K5 + K1
+    ][case]
+    kw = dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, p_fg=0.6, **kw, **extra))
+    okw = dict(kw, has_fg=1, p_fg=0.6)
+    if "zoom" in extra:
+        okw.update(has_zoom=1, p_zoom=1.0, zoom_lo=0.8, zoom_hi=1.2)
+    if "contrast" in extra:
+        okw.update(has_contrast=1, p_contrast=1.0, contrast_lo=0.75, contrast_hi=1.25)
+    ocfg = oracle.cfg3d(crop=crop, **okw)
+    rng = np.random.default_rng(400 + case)
+    z, y, x = np.meshgrid(*[np.arange(d) for d in dims], indexing="ij")
+    vox = int(np.prod(crop))
+    bufs, tickets, expect, n_fg = [], [], [], 0
+    for k in range(12):
+        sid = int(rng.integers(0, 1 << 40))
+        img = rng.standard_normal(dims).astype(np.float32)
+        lbl = np.zeros(dims, np.uint8)
+        c0 = rng.integers(8, np.array(dims) - 8)
+        lbl[((z - c0[0]) / 5) ** 2 + ((y - c0[1]) / 6) ** 2 + ((x - c0[2]) / 7) ** 2 <= 1] = 1 + k % 3
+        if k % 4 == 0:
+            lbl[:] = 0                                           # no foreground: random offsets
+        pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+        bufs += [pi, pl]
+        desc = lfgpu.sample_desc(sid, dims, pi, pl)
+        p = ch.draw_params(SEED, desc)
+        op_ = oracle.draw3d(ocfg, SEED, sid, dims)
+        assert p[14] == op_.fg and p[15] == op_.u_cls and list(p[16:19]) == list(op_.u_adj)
+        n_fg += oracle.fg_offsets(op_, lbl) is not None
+        tickets.append(ctx.submit(ch, desc))
+        expect.append(oracle.apply3d(ocfg, op_, img, lbl))
+    ctx.flush()
+    for t, (e_img, e_lbl) in zip(tickets, expect):
+        ctx.wait(t)
+        raw = ctx.ticket_output(t, vox * 4 + ((vox + 15) // 16) * 16)
+        assert np.array_equal(raw[vox * 4: vox * 5].reshape(crop), e_lbl), "label window differs"
+        _assert_close(raw[: vox * 4].view(np.float32).reshape(crop), e_img, atol=1e-6)
+        ctx.release(t)
+    assert n_fg >= 2
+    with pytest.raises(lfgpu.LfgError):                     # the window needs the scan: HBM only
+        hp = _pinned(ctx, np.zeros(dims, np.float32))
+        try:
+            ctx.submit(ch, lfgpu.sample_desc(1, dims, hp, hp, src_kind=1))
+        finally:
+            ctx.host_free(hp)
+    for p in bufs:
+        ctx.device_free(p)
+    ctx.destroy_chain(ch)
+
+
 # ------------------------------------------------------------------ obj_det (K3)
 @pytest.mark.parametrize("src_kind", [0, 1], ids=["device", "host_pinned"])
 def test_rrc2d_matches_oracle(ctx, lfgpu, oracle, src_kind):

@@ -257,3 +257,63 @@ def test_contrast_scales_deviation_about_the_crop_mean(oracle):
         m = plain.mean()
         assert abs(out.mean() - m) < 1e-12
         assert np.abs((out - m) - p.contrast * (plain - m)).max() < 1e-12
+
+
+def _fg_offsets_numpy(p, lbl):
+    """Independent restatement of RandBalancedCrop's window placement (MLPerf adjust()
+    on the bounding box of every voxel of the chosen class)."""
+    if not p.fg:
+        return None
+    present = [v for v in range(1, 8) if (lbl == v).any()]
+    if not present:
+        return None
+    cl = present[min(int(np.floor(p.u_cls * len(present))), len(present) - 1)]
+    idx = np.nonzero(lbl == cl)
+    off = []
+    for a in range(3):
+        lo, hi = int(idx[a].min()), int(idx[a].max()) + 1
+        patch, dim = int(p.win[a]), lbl.shape[a]
+        diff = patch - (hi - lo)
+        sign = -1 if diff < 0 else 1
+        diff = abs(diff)
+        ladj = min(int(np.floor(p.u_adj[a] * diff)), diff - 1) if diff > 0 else 0
+        hadj = diff - ladj
+        low, high = max(0, lo - sign * ladj), min(dim, hi + sign * hadj)
+        d2 = patch - (high - low)
+        if d2 > 0:
+            if low == 0:
+                high += d2
+            else:
+                low -= d2
+        off.append(int(np.clip(low, 0, max(dim - patch, 0))))
+    return off
+
+
+def test_foreground_crop_matches_numpy_restatement(oracle):
+    """RandomCrop with foreground oversampling: the oracle's window origin equals an
+    independent numpy restatement, the window holds foreground of the chosen class
+    when it fits, and non-oversampled draws keep the random offsets."""
+    rng = np.random.default_rng(3)
+    dims = (40, 48, 56)
+    z, y, x = np.meshgrid(*[np.arange(d) for d in dims], indexing="ij")
+    lbl = np.zeros(dims, np.uint8)
+    lbl[((z - 25) / 6) ** 2 + ((y - 30) / 8) ** 2 + ((x - 15) / 9) ** 2 <= 1] = 1
+    lbl[((z - 12) / 4) ** 2 + ((y - 10) / 5) ** 2 + ((x - 40) / 6) ** 2 <= 1] = 2
+    img = rng.standard_normal(dims).astype(np.float32)
+    cfg = oracle.cfg3d(crop=(16, 16, 32), has_fg=1, p_fg=0.5, p_flip=0.0, p_bright=0.0, p_noise=0.0)
+    n_fg = 0
+    for sid in range(60):
+        p = oracle.draw3d(cfg, 1, sid, dims)
+        got = oracle.fg_offsets(p, lbl)
+        assert got == _fg_offsets_numpy(p, lbl)
+        (out_img, out_lbl), _ = oracle.chain3d(cfg, 1, sid, img, lbl)
+        off = got if got is not None else list(p.off)
+        want = img[off[0]:off[0] + 16, off[1]:off[1] + 16, off[2]:off[2] + 32]
+        assert np.array_equal(out_img, want.astype(np.float64))
+        if got is not None:
+            n_fg += 1
+            assert (out_lbl > 0).any()
+    assert 15 <= n_fg <= 45
+    # no foreground at all: the random offsets hold
+    p = oracle.draw3d(cfg, 1, 0, dims)
+    assert oracle.fg_offsets(p, np.zeros(dims, np.uint8)) is None
