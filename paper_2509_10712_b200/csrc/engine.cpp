@@ -632,8 +632,11 @@ static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) 
     wd[0] = wd[1] = wd[2] = 0;
     if (c.fam == FAM_IMG3D) {
         const int64_t H = s.dims[1], W = s.dims[2];
-        for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(t.p3.win[a], s.dims[a] - t.p3.off[a]);
-        const int64_t first = (t.p3.off[0] * H + t.p3.off[1]) * W + t.p3.off[2];
+        // a foreground-biased crop's window depends on the label scan: stage the whole volume
+        const bool whole = c.has_fg && t.p3.fg;
+        for (int a = 0; a < 3; ++a)
+            wd[a] = whole ? s.dims[a] : std::min<int64_t>(t.p3.win[a], s.dims[a] - t.p3.off[a]);
+        const int64_t first = whole ? 0 : (t.p3.off[0] * H + t.p3.off[1]) * W + t.p3.off[2];
         out[0] = Box{static_cast<const char*>(s.data) + first * 4, W * 4, H * W * 4,
                      static_cast<int32_t>(wd[2] * 4), static_cast<int32_t>(wd[1]),
                      static_cast<int32_t>(wd[0])};
@@ -684,9 +687,6 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
         if (s.ndim != 1 || s.dims[0] < c->n_fft / 2 + 1 || s.dims[0] > c->max_L)
             fail(LFG_ERR_INVALID, "speech sample needs a waveform of length in [n_fft/2 + 1, max_L]");
     }
-    if (s.src_kind == LFG_SRC_HOST_PINNED && c->fam == FAM_IMG3D && c->has_fg)
-        fail(LFG_ERR_UNSUPPORTED,
-             "foreground-biased RandomCrop needs HBM-resident volumes (the window depends on the label scan)");
     if (s.src_kind == LFG_SRC_HOST_PINNED) {
         // K0 reads the payload over PCIe through its UVA mapping: it must be pinned
         for (const void* p : {s.data, s.aux}) {
@@ -893,9 +893,10 @@ void Context::launch_group(Group& g) {
                 counters.h2d_bytes += static_cast<int64_t>(b[k].row_bytes) * b[k].ny * b[k].nz;
                 dst += align256(b[k].bytes());
             }
+            const bool whole = c.fam == FAM_IMG3D && c.has_fg && t.p3.fg;   // see boxes_of
             for (int a = 0; a < 3; ++a) {
                 v.sdim[a] = wd[a];
-                v.off[a] = 0;
+                v.off[a] = whole ? t.p3.off[a] : 0;
             }
         }
         if (!wav_dst.empty()) {

@@ -59,7 +59,9 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
     for (int c = 0; c < kClasses; ++c) xmin[c] = ymin[c] = kNone, xmax[c] = ymax[c] = kNone;
     uint32_t seen_all = 0;
     for (int y = warp; y < H; y += kScanThreads / 32) {
-        const uint8_t* row = d.lbl + (int64_t)z * d.lbl_pz + (int64_t)y * d.lbl_py;
+        // row start (K0-staged volumes keep the source's 16-B alignment phase: skews)
+        const uint8_t* row = d.lbl + (int64_t)z * d.lbl_pz + (int64_t)y * d.lbl_py +
+                             ((d.lbl_sk0 + z * d.lbl_skz + y * d.lbl_sky) & 15);
         uint32_t seen = 0;
         if ((reinterpret_cast<uintptr_t>(row) & 15) == 0 && (W & 15) == 0) {
             const uint4* r4 = reinterpret_cast<const uint4*>(row);

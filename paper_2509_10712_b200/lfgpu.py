@@ -182,8 +182,8 @@ def img_seg_ops(crop=(128, 128, 128), p_flip=1 / 3, p_bright=0.1, bright=(0.7, 1
 
     Optional ops (north_star "trilinear resize" / "brightness/contrast"; not in the
     reference chain, so off by default): ``p_fg`` > 0 makes RandomCrop oversample the
-    foreground with that probability (MLPerf RandBalancedCrop, kernel K2; HBM-resident
-    volumes only); ``zoom=(p, lo, hi)`` adds RandomZoom3D after
+    foreground with that probability (MLPerf RandBalancedCrop, kernel K2; from pinned
+    host memory such samples stage their whole volume); ``zoom=(p, lo, hi)`` adds RandomZoom3D after
     RandomCrop (window edge round(crop * f), trilinear back to the crop; labels
     nearest); ``contrast=(p, lo, hi)`` adds RandomContrast after RandomBrightness."""
     ops = [op(OP_SPIN, "SampleCost")] if spin_first else []

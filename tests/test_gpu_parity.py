@@ -179,8 +179,9 @@ def test_img3d_zoom_contrast_matches_oracle(ctx, lfgpu, oracle, case, src_kind):
 
 
 # ------------------------------------------------------------------ foreground crop (K2)
+@pytest.mark.parametrize("src_kind", [0, 1], ids=["device", "host_pinned"])
 @pytest.mark.parametrize("case", range(4))
-def test_img3d_foreground_crop_matches_oracle(ctx, lfgpu, oracle, case):
+def test_img3d_foreground_crop_matches_oracle(ctx, lfgpu, oracle, case, src_kind):
     """RandomCrop with foreground oversampling (K2 label scan + window resolution on
     the device, then K1 TMA / row path, K4 with zoom, K5 with contrast): labels
     bit-exact and images within tolerance of the oracle, whose window origin is pinned
@@ -211,9 +212,13 @@ def test_img3d_foreground_crop_matches_oracle(ctx, lfgpu, oracle, case):
         lbl[((z - c0[0]) / 5) ** 2 + ((y - c0[1]) / 6) ** 2 + ((x - c0[2]) / 7) ** 2 <= 1] = 1 + k % 3
         if k % 4 == 0:
             lbl[:] = 0                                           # no foreground: random offsets
-        pi, pl = _upload(ctx, img), _upload(ctx, lbl)
-        bufs += [pi, pl]
-        desc = lfgpu.sample_desc(sid, dims, pi, pl)
+        if src_kind == 0:
+            pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+            bufs += [("d", pi), ("d", pl)]
+        else:   # pinned: foreground samples stage the whole volume (the window needs the scan)
+            pi, pl = _pinned(ctx, img), _pinned(ctx, lbl)
+            bufs += [("h", pi), ("h", pl)]
+        desc = lfgpu.sample_desc(sid, dims, pi, pl, src_kind=src_kind)
         p = ch.draw_params(SEED, desc)
         op_ = oracle.draw3d(ocfg, SEED, sid, dims)
         assert p[14] == op_.fg and p[15] == op_.u_cls and list(p[16:19]) == list(op_.u_adj)
@@ -228,14 +233,8 @@ def test_img3d_foreground_crop_matches_oracle(ctx, lfgpu, oracle, case):
         _assert_close(raw[: vox * 4].view(np.float32).reshape(crop), e_img, atol=1e-6)
         ctx.release(t)
     assert n_fg >= 2
-    with pytest.raises(lfgpu.LfgError):                     # the window needs the scan: HBM only
-        hp = _pinned(ctx, np.zeros(dims, np.float32))
-        try:
-            ctx.submit(ch, lfgpu.sample_desc(1, dims, hp, hp, src_kind=1))
-        finally:
-            ctx.host_free(hp)
-    for p in bufs:
-        ctx.device_free(p)
+    for kind, p in bufs:
+        (ctx.device_free if kind == "d" else ctx.host_free)(p)
     ctx.destroy_chain(ch)
 
 
