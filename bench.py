@@ -14,6 +14,8 @@ Workloads:
                normalize, batch 256 (BASELINE configs[1], the N=1 headline)
   img3d        C1/C3 shapes: KiTS19-shaped volumes (H=W=384, D from gen_empirical
                img_seg sizes) -> crop 128^3 + flip + brightness + noise, batch 2
+  img3d_fg     C1 shapes with RandomCrop's MLPerf foreground oversampling (p 0.4): those
+               samples scan their whole label volume (K2) -- a real heavy tail
   img3d_heavy  C3: as img3d with a heavy-tailed per-sample cost (spin) on a fraction
                of samples and a synthetic trainer: reports consumer idle %
 
@@ -45,7 +47,8 @@ sys.path.insert(0, ROOT)
 METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform HBM GB/s"
 
 # workload -> (batch size, samples per launch group, default timed steps)
-BATCH = {"rrc": (256, 256, 1000), "img3d": (2, 16, 4000), "img3d_heavy": (2, 1, 400),
+BATCH = {"rrc": (256, 256, 1000), "img3d": (2, 16, 4000), "img3d_fg": (2, 16, 2000),
+         "img3d_heavy": (2, 1, 400),
          "speech": (64, 64, 500)}
 
 
@@ -219,7 +222,7 @@ class Img3dWorkload:
     B = 2
 
     def __init__(self, L, ctx, pool: int, host: bool, seed: int, heavy_frac: float = 0.0,
-                 time_scale_us_per_ms: float = 0.0):
+                 time_scale_us_per_ms: float = 0.0, p_fg: float = 0.0):
         self.L, self.ctx, self.seed, self.host = L, ctx, seed, host
         self.D, self.cost_ms = img_seg_dims(pool, seed)
         self.pool = pool
@@ -234,7 +237,8 @@ class Img3dWorkload:
         self.pool_bytes = int(sum(int(d) * 384 * 384 * 5 for d in self.D))
         self.heavy_frac = heavy_frac
         self.scale = time_scale_us_per_ms
-        self.chain = ctx.chain(L.img_seg_ops(spin_first=heavy_frac > 0))
+        self.p_fg = p_fg
+        self.chain = ctx.chain(L.img_seg_ops(spin_first=heavy_frac > 0, p_fg=p_fg))
         self.roof_chain = ctx.chain(L.img_seg_ops()) if heavy_frac > 0 else self.chain
 
     def descs(self, ids):
@@ -297,6 +301,8 @@ def make_workload(name, L, ctx, host, seed, args):
     vols = args.pool or (12 if host else 48)
     if name == "img3d":
         return Img3dWorkload(L, ctx, pool=vols, host=host, seed=seed)
+    if name == "img3d_fg":   # MLPerf RandBalancedCrop: 40% of crops scan the label volume (K2)
+        return Img3dWorkload(L, ctx, pool=vols, host=host, seed=seed, p_fg=0.4)
     if name == "img3d_heavy":
         return Img3dWorkload(L, ctx, pool=vols, host=host, seed=seed,
                              heavy_frac=args.heavy_frac, time_scale_us_per_ms=args.time_scale)
@@ -335,6 +341,8 @@ def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
     ms = t["mean_ms"] * launches                            # total transform-kernel time
     kernel = {"rrc": "rrc2d_kernel", "img3d": "img3d_tma_kernel", "speech": "speech_kernel"}[
         wl.name.split("_")[0]]
+    if getattr(wl, "p_fg", 0) > 0:
+        kernel = "fg_scan_kernel + img3d_tma_kernel (one stage)"
     out = {"kernel": kernel, "launches": int(launches), "mean_launch_us": round(1e3 * t["mean_ms"], 2),
            "traffic": None, "algo_bytes_per_launch": int(t["bytes"] / max(launches, 1))}
     if wl.name == "speech":
@@ -364,8 +372,9 @@ def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: i
     wl = {"rrc": "rrc", "speech": "speech"}.get(workload, "img3d")
     if h and wl != "speech":
         k = steps or (8 if wl == "rrc" else 10)
+        fg = ["--fg", "0.4"] if workload == "img3d_fg" else []
         out = subprocess.run([h, "--workload", wl, "--steps", str(k), "--warmup", str(warmup),
-                              "--workers", str(cores), "--max-seconds", "150"],
+                              "--workers", str(cores), "--max-seconds", "150"] + fg,
                              capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
         b = json.loads(out)
         return {"value": b["value"], "unit": "samples/s", "cores": b["cores"], "kind": "reference",
@@ -511,6 +520,7 @@ def main():
         "data": "synthetic (Philox(seed,id) images/volumes generated on device / pinned host)",
         "config": {"workload": {"rrc": "C2 ImageNet-shaped u8 3x(256..512)^2 -> RRC224+hflip+normalize",
                                 "img3d": "C1 KiTS19-shaped 3D crop128^3+flip+brightness+noise+cast",
+                                "img3d_fg": "C1 shapes, RandomCrop with MLPerf foreground oversampling 0.4 (K2 label scan + K1)",
                                 "img3d_heavy": "C3 heavy-tailed 3D + synthetic trainer",
                                 "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT + log-mel (tcgen05 3xTF32) + SpecAugment + splice, batch 64"}[args.workload],
                    "batch": B, "launch_group": group, "workers": args.workers,

@@ -133,7 +133,15 @@ lfo_params3d params3d(const Payload& p, const int64_t dims[3]) {
 // Payload after RandomCrop: [id, cd, ch, cw, D, H, W (original dims), img..., lbl...]
 Payload crop_step(Payload p) {
     const int64_t dims[3] = {(int64_t)p[1], (int64_t)p[2], (int64_t)p[3]};
-    const lfo_params3d pr = params3d(p, dims);
+    lfo_params3d pr = params3d(p, dims);
+    if (g_c3.has_fg && pr.fg) {   // foreground oversampling: scan the label volume
+        const int64_t nv = dims[0] * dims[1] * dims[2];
+        std::vector<uint8_t> lab((size_t)nv);
+        for (int64_t i = 0; i < nv; ++i) lab[(size_t)i] = (uint8_t)p[kHdr3d + nv + i];
+        int64_t off[3];
+        if (lfo_fg_offsets(&pr, lab.data(), dims, off) == 0)
+            for (int a = 0; a < 3; ++a) pr.off[a] = off[a];
+    }
     const int64_t cd = g_c3.crop[0], ch = g_c3.crop[1], cw = g_c3.crop[2];
     const int64_t vox = cd * ch * cw, n = dims[0] * dims[1] * dims[2];
     Payload out(7 + 2 * vox, 0.0);
@@ -240,8 +248,11 @@ int main(int argc, char** argv) {
     // --loader sync: the reference's synchronous PyTorch-DataLoader-like loader
     // (start_sync_loader, baselines.cpp:12-151) instead of the Minato pipeline
     const bool sync = arg_str(argc, argv, "--loader", "minato") == "sync";
+    const double p_fg = std::atof(arg_str(argc, argv, "--fg", "0").c_str());   // RandomCrop oversampling
     lfo_cfg2d_default(&g_c2);
     lfo_cfg3d_default(&g_c3);
+    g_c3.has_fg = p_fg > 0;
+    g_c3.p_fg = p_fg;
     const bool rrc = wl == "rrc";
     const int B = rrc ? 256 : 2;
     const int64_t n = (int64_t)(steps + warmup) * B;

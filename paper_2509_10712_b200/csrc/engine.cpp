@@ -1022,10 +1022,10 @@ void Context::launch_group(Group& g) {
                     int32_t* box = fg_box_ + size_t(slot) * kMax3D * 48;
                     int4* offs = fg_offs_ + size_t(slot) * kMax3D;
                     start();
-                    for (int i = 0; i < n; ++i) {   // mins preset large, maxs to -1
-                        cuda_check(cudaMemsetAsync(box + i * 48, 0x7f, 24 * sizeof(int32_t), st), "fg box reset");
-                        cuda_check(cudaMemsetAsync(box + i * 48 + 24, 0xff, 24 * sizeof(int32_t), st), "fg box reset");
-                    }
+                    // mins ([kMax3D][8][3]) preset large, maxs (the next block) to -1
+                    cuda_check(cudaMemsetAsync(box, 0x7f, kMax3D * 24 * sizeof(int32_t), st), "fg box reset");
+                    cuda_check(cudaMemsetAsync(box + kMax3D * 24, 0xff, kMax3D * 24 * sizeof(int32_t), st),
+                               "fg box reset");
                     cuda_check(launch_fg_scan(L, F, box, st), "fg scan launch");
                     cuda_check(launch_fg_offsets(L, F, box, offs, st), "fg offsets launch");
                     counters.launches += 2;

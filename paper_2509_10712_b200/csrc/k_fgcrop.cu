@@ -58,29 +58,48 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
 #pragma unroll
     for (int c = 0; c < kClasses; ++c) xmin[c] = ymin[c] = kNone, xmax[c] = ymax[c] = kNone;
     uint32_t seen_all = 0;
-    for (int y = warp; y < H; y += kScanThreads / 32) {
-        // row start (K0-staged volumes keep the source's 16-B alignment phase: skews)
-        const uint8_t* row = d.lbl + (int64_t)z * d.lbl_pz + (int64_t)y * d.lbl_py +
-                             ((d.lbl_sk0 + z * d.lbl_skz + y * d.lbl_sky) & 15);
-        uint32_t seen = 0;
-        if ((reinterpret_cast<uintptr_t>(row) & 15) == 0 && (W & 15) == 0) {
-            const uint4* r4 = reinterpret_cast<const uint4*>(row);
-            for (int q = lane; q < (W >> 4); q += 32) {
-                const uint4 v = __ldcs(r4 + q);   // streamed: read once
-                if ((v.x | v.y | v.z | v.w) == 0u) continue;   // background chunk
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    // one 16-B chunk of a label row against the per-class extents
+    auto chunk = [&](const uint4 v, int q, uint32_t& seen) {
+        if ((v.x | v.y | v.z | v.w) == 0u) return;   // background chunk
+        const uint32_t b0 = v.x & 0xFFu;
+        if (v.x == v.y && v.y == v.z && v.z == v.w && v.x == 0x01010101u * b0) {
+            // uniform chunk (inside a region): one class spans all 16 bytes
+            if (b0 >= 1 && b0 < (uint32_t)kClasses) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int b = (int)((w[k >> 2] >> (8 * (k & 3))) & 0xFFu);
-                    if (b != 0) note(b, (uint32_t)(16 * q + k), xmin, xmax, seen);
-                }
+                for (int c = 1; c < kClasses; ++c)
+                    if (b0 == (uint32_t)c) {
+                        xmin[c] = min(xmin[c], (uint32_t)(16 * q));
+                        xmax[c] = (xmax[c] == kNone) ? (uint32_t)(16 * q + 15) : max(xmax[c], (uint32_t)(16 * q + 15));
+                    }
+                seen |= 1u << b0;
             }
-        } else {
-            for (int x = lane; x < W; x += 32) {
-                const int b = row[x];
-                if (b != 0) note(b, (uint32_t)x, xmin, xmax, seen);
-            }
+            return;
         }
+        // per class: SIMD byte compares give the chunk's match mask (one bit per
+        // byte), whose lowest / highest set bits are the class's x extent in the chunk
+#pragma unroll
+        for (int c = 1; c < kClasses; ++c) {
+            const uint32_t rep = 0x01010101u * (uint32_t)c;
+            const uint32_t m[4] = {__vcmpeq4(v.x, rep), __vcmpeq4(v.y, rep), __vcmpeq4(v.z, rep),
+                                   __vcmpeq4(v.w, rep)};
+            if ((m[0] | m[1] | m[2] | m[3]) == 0u) continue;
+            uint32_t bm = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                bm |= ((m[k] & 0x01u) | ((m[k] >> 7) & 0x02u) | ((m[k] >> 14) & 0x04u) | ((m[k] >> 21) & 0x08u))
+                      << (4 * k);
+            const uint32_t lo = (uint32_t)(16 * q) + (uint32_t)(__ffs(bm) - 1);
+            const uint32_t hi = (uint32_t)(16 * q) + (uint32_t)(31 - __clz(bm));
+            xmin[c] = min(xmin[c], lo);
+            xmax[c] = (xmax[c] == kNone) ? hi : max(xmax[c], hi);
+            seen |= 1u << c;
+        }
+    };
+    auto row_ptr = [&](int y) {
+        // row start (K0-staged volumes keep the source's 16-B alignment phase: skews)
+        return d.lbl + (int64_t)z * d.lbl_pz + (int64_t)y * d.lbl_py + ((d.lbl_sk0 + z * d.lbl_skz + y * d.lbl_sky) & 15);
+    };
+    auto close_row = [&](int y, uint32_t seen) {
 #pragma unroll
         for (int c = 1; c < kClasses; ++c)
             if (seen & (1u << c)) {
@@ -88,6 +107,45 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
                 ymax[c] = (ymax[c] == kNone) ? (uint32_t)y : max(ymax[c], (uint32_t)y);
             }
         seen_all |= seen;
+    };
+    constexpr int kRowsInFlight = 4;    // rows per warp with their loads issued together
+    constexpr int kWarps = kScanThreads / 32;
+    const bool vec = (reinterpret_cast<uintptr_t>(row_ptr(0)) & 15) == 0 && (d.lbl_py & 15) == 0 &&
+                     (d.lbl_pz & 15) == 0 && (W & 15) == 0;
+    if (vec && (W >> 4) <= 32) {
+        // rows of <= 512 B: a lane per 16-B chunk, kRowsInFlight rows per warp at once
+        const bool lane_live = lane < (W >> 4);
+        for (int y0 = warp; y0 < H; y0 += kWarps * kRowsInFlight) {
+            uint4 v[kRowsInFlight];
+#pragma unroll
+            for (int r = 0; r < kRowsInFlight; ++r) {
+                const int y = y0 + r * kWarps;
+                v[r] = (lane_live && y < H) ? __ldcs(reinterpret_cast<const uint4*>(row_ptr(y)) + lane)
+                                            : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int r = 0; r < kRowsInFlight; ++r) {
+                const int y = y0 + r * kWarps;
+                if (y >= H) break;
+                uint32_t seen = 0;
+                chunk(v[r], lane, seen);
+                close_row(y, seen);
+            }
+        }
+    } else {
+        for (int y = warp; y < H; y += kWarps) {
+            const uint8_t* row = row_ptr(y);
+            uint32_t seen = 0;
+            if (vec) {
+                for (int q = lane; q < (W >> 4); q += 32) chunk(__ldcs(reinterpret_cast<const uint4*>(row) + q), q, seen);
+            } else {
+                for (int x = lane; x < W; x += 32) {
+                    const int b = row[x];
+                    if (b != 0) note(b, (uint32_t)x, xmin, xmax, seen);
+                }
+            }
+            close_row(y, seen);
+        }
     }
     // warp reductions (kNone = absent: min ignores it; max treats it as absent via 0-shift)
     seen_all = __reduce_or_sync(0xFFFFFFFFu, seen_all);
@@ -109,8 +167,8 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
     __syncthreads();
     if (threadIdx.x < kClasses && (s_seen & (1u << threadIdx.x))) {
         const int c = threadIdx.x;
-        int32_t* mins = box + (int64_t)i * kClasses * 6;
-        int32_t* maxs = mins + kClasses * 3;
+        int32_t* mins = box + (int64_t)i * kClasses * 3;                  // [kMax3D][8][3] mins,
+        int32_t* maxs = box + (int64_t)(kMax3D + i) * kClasses * 3;       // then [kMax3D][8][3] maxs
         atomicMin(&mins[c * 3 + 0], z);
         atomicMax(&maxs[c * 3 + 0], z);
         atomicMin(&mins[c * 3 + 1], (int32_t)s_min[c][1]);
@@ -128,8 +186,8 @@ __global__ void fg_offsets_kernel(const __grid_constant__ Img3dLaunch L, const _
     const FgDraw& g = F.d[i];
     int4 o = make_int4(d.off[0], d.off[1], d.off[2], 0);
     if (g.fg) {
-        const int32_t* mins = box + (int64_t)i * kClasses * 6;
-        const int32_t* maxs = mins + kClasses * 3;
+        const int32_t* mins = box + (int64_t)i * kClasses * 3;
+        const int32_t* maxs = box + (int64_t)(kMax3D + i) * kClasses * 3;
         int cls[7], n = 0;
         for (int c = 1; c < kClasses; ++c)
             if (maxs[c * 3] >= 0) cls[n++] = c;

@@ -180,8 +180,8 @@ cudaError_t launch_img3d_zoom(const Img3dLaunch& L, cudaStream_t s);
 // must point at zeroed doubles
 cudaError_t launch_img3d_mean(const Img3dLaunch& L, cudaStream_t s);
 // K2: RandomCrop foreground oversampling.  fg_scan: per-class (labels 1..7)
-// bounding boxes of the samples with scan[i] = 1 into box[i] (mins then maxs, 8
-// classes x 3 axes each; mins preset to 0x7f7f7f7f, maxs to -1); fg_offsets: the
+// bounding boxes of the samples that drew it into box: mins [kMax3D][8][3] then
+// maxs [kMax3D][8][3] (mins preset to 0x7f7f7f7f, maxs to -1); fg_offsets: the
 // window origins of every sample into offs (w = 0 where the random offsets hold).
 struct FgDraw {
     int32_t fg;              // foreground crop drawn (its label volume is scanned)
