@@ -35,6 +35,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "device_common.cuh"
@@ -63,7 +64,8 @@ constexpr int kBStageBytes = (kKChunk / 8) * 2 * 2 * kBBlock;   // 32 KB
 constexpr int kStageBytes = 2 * kAPartBytes + kBStageBytes;     // 40 KB
 constexpr int kSmemBytes = kStages * kStageBytes + 1024;        // + barriers
 constexpr int kMelPitch = kMels + 1;
-constexpr int kThreads = 192;         // warp 0 producer, warp 1 MMA, warps 2-5 A builders / epilogue
+constexpr int kThreads = 320;         // warp 0 producer, warp 1 MMA, warps 2-5 A builders + epilogue
+                                      // (bins 128..255), warps 6-9 epilogue (bins 0..127)
 
 // instruction descriptor: D f32, A/B tf32, K-major both, N = 256, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
@@ -113,8 +115,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void epilogue_sync() {   // the 4 builder / epilogue warps only
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void epilogue_sync() {   // the 8 epilogue warps (2..9) only
+    asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -202,7 +204,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
         }
         __syncwarp();
     } else {
-        // ---------------- A builders (then the epilogue): one frame per thread,
+        // ---------------- A builders (warps 2-5, then the epilogue with warps 6-9): one frame per thread,
         // thread row = TMEM lane (warp w may only read lanes 32*(w%4) .. +31)
         const int r = 32 * (warp & 3) + lane;
         const int f = f0 + r;
@@ -231,64 +233,72 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
                 }
             }
         };
-        float x[kKChunk];
-        const bool skip_loads = (L.debug & 1) != 0;
-        if (skip_loads) {
-#pragma unroll
-            for (int j = 0; j < kKChunk; ++j) x[j] = 0.001f * j;
-        } else {
-            load(0, x);
-        }
-        for (int it = 0; it < kChunks; ++it) {
-            const int s = it % kStages, use = it / kStages;
-            float xn[kKChunk];
+        if (warp < 6) {   // warps 6-9 have no A rows to build
+            float x[kKChunk];
+            const bool skip_loads = (L.debug & 1) != 0;
             if (skip_loads) {
 #pragma unroll
-                for (int j = 0; j < kKChunk; ++j) xn[j] = x[j];
-            } else if (it + 1 < kChunks) {
-                load(it + 1, xn);                            // prefetch the next chunk's taps
+                for (int j = 0; j < kKChunk; ++j) x[j] = 0.001f * j;
+            } else {
+                load(0, x);
             }
-            uint32_t hi[kKChunk], lo[kKChunk];
+            for (int it = 0; it < kChunks; ++it) {
+                const int s = it % kStages, use = it / kStages;
+                float xn[kKChunk];
+                if (skip_loads) {
 #pragma unroll
-            for (int j = 0; j < kKChunk; ++j) {
-                nyq = fmaf(x[j], c_win_nyq[it * kKChunk + j], nyq);
-                hi[j] = tf32_rna(x[j]);
-                lo[j] = tf32_rna(x[j] - __uint_as_float(hi[j]));
-            }
-            if (use > 0) {                                   // one poller per warp
-                if (lane == 0) mbar_wait(empty + s, (use - 1) & 1);
+                    for (int j = 0; j < kKChunk; ++j) xn[j] = x[j];
+                } else if (it + 1 < kChunks) {
+                    load(it + 1, xn);                            // prefetch the next chunk's taps
+                }
+                uint32_t hi[kKChunk], lo[kKChunk];
+#pragma unroll
+                for (int j = 0; j < kKChunk; ++j) {
+                    nyq = fmaf(x[j], c_win_nyq[it * kKChunk + j], nyq);
+                    hi[j] = tf32_rna(x[j]);
+                    lo[j] = tf32_rna(x[j] - __uint_as_float(hi[j]));
+                }
+                if (use > 0) {                                   // one poller per warp
+                    if (lane == 0) mbar_wait(empty + s, (use - 1) & 1);
+                    __syncwarp();
+                }
+                uint8_t* sa = smem + s * kStageBytes;
+                // canonical K-major, 32-byte swizzle (see smem_desc)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int off = sw32_off(r, c);
+                    *reinterpret_cast<uint4*>(sa + off) =
+                        make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+                    *reinterpret_cast<uint4*>(sa + kAPartBytes + off) =
+                        make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
                 __syncwarp();
-            }
-            uint8_t* sa = smem + s * kStageBytes;
-            // canonical K-major, 32-byte swizzle (see smem_desc)
+                if (lane == 0) mbar_arrive(full_a + s);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int off = sw32_off(r, c);
-                *reinterpret_cast<uint4*>(sa + off) =
-                    make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
-                *reinterpret_cast<uint4*>(sa + kAPartBytes + off) =
-                    make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+                for (int j = 0; j < kKChunk; ++j) x[j] = xn[j];
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full_a + s);
-#pragma unroll
-            for (int j = 0; j < kKChunk; ++j) x[j] = xn[j];
         }
 
-        // ---------------- epilogue: power -> mel, all 80 filters in registers.
-        // The bank is a compile-time table (mel_table.h): with the bin loops fully
-        // unrolled every filter index is a constant, so this is 2 FMAs per bin with
-        // immediate weights -- no table loads, no branches.
+        // ---------------- epilogue: power -> mel with the filter bank as compile-time
+        // constants (mel_table.h: with the bin loops unrolled every filter index is a
+        // constant -- 2 FMAs per bin with immediate weights, no loads, no branches).
+        // Two warps per TMEM lane quarter split the bins: warps 6-9 bins 0..127
+        // (filters 0..62), warps 2-5 bins 128..255 (filters 61..79); the filters
+        // both halves feed are summed through shared memory, then both halves of a
+        // row take 40 filters each for log + SpecAugment.
         mbar_wait(done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
         float* mel_s = reinterpret_cast<float*>(smem);    // the operand ring is free now
+        // filters fed by both bin halves: [kHiMin, kLoMax] (bins 127 / 128 straddle them)
+        constexpr int kLoMax = kMelM[127] + 1, kHiMin = kMelM[128], kOvl = kLoMax - kHiMin + 1;
+        static_assert(kOvl >= 1 && kOvl <= 4, "shared filters between the bin halves");
+        float* ovl_s = mel_s + kRowsM * kMelPitch;        // [row][kOvl]: the upper half's share
         const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-        float mel[kMels];
-#pragma unroll
-        for (int m = 0; m < kMels; ++m) mel[m] = 0.0f;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        const bool low_bins = warp >= 6;
+        float* row = mel_s + r * kMelPitch;
+        auto half_bins = [&](auto H, float mel[kMels]) {
+            constexpr int h = decltype(H)::value;
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
                 float re[16], im[16];
@@ -303,30 +313,48 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
                         mel[kMelM[kk] + 1] = fmaf(kMelWb[kk], p, mel[kMelM[kk] + 1]);
                 }
             }
+        };
+        {
+            float mel[kMels];
+#pragma unroll
+            for (int m = 0; m < kMels; ++m) mel[m] = 0.0f;
+            if (low_bins) {
+                half_bins(std::integral_constant<int, 0>{}, mel);
+#pragma unroll
+                for (int m = 0; m <= kLoMax; ++m) row[m] = mel[m];
+            } else {
+                half_bins(std::integral_constant<int, 1>{}, mel);
+                if (kMelM[kBins] >= 0) {                       // Nyquist bin (CUDA cores)
+                    const float p = nyq * nyq;
+                    mel[kMelM[kBins]] = fmaf(kMelWa[kBins], p, mel[kMelM[kBins]]);
+                }
+#pragma unroll
+                for (int m = kHiMin; m <= kLoMax; ++m) ovl_s[r * kOvl + (m - kHiMin)] = mel[m];
+#pragma unroll
+                for (int m = kLoMax + 1; m < kMels; ++m) row[m] = mel[m];
+            }
         }
-        if (kMelM[kBins] >= 0) {                           // Nyquist bin (CUDA cores)
-            const float p = nyq * nyq;
-            mel[kMelM[kBins]] = fmaf(kMelWa[kBins], p, mel[kMelM[kBins]]);
-        }
-        // log + SpecAugment on this thread's own frame (one time-mask test per
-        // frame; the freq-mask tests are CTA-uniform); padding frames are zero
+        epilogue_sync();
+        // log + SpecAugment on this row's 40 filters; padding frames are zero
         {
             bool tmask = f >= T || r >= kFramesPerCta;
             for (int q = 0; q < L.n_tmask; ++q) tmask |= f >= d.t_lo[q] && f < d.t_lo[q] + d.t_w[q];
             const int fl0 = L.n_fmask > 0 ? d.f_lo[0] : 0, fh0 = L.n_fmask > 0 ? d.f_lo[0] + d.f_w[0] : 0;
             const int fl1 = L.n_fmask > 1 ? d.f_lo[1] : 0, fh1 = L.n_fmask > 1 ? d.f_lo[1] + d.f_w[1] : 0;
-            float* row = mel_s + r * kMelPitch;
+            const int m0 = low_bins ? 0 : kMels / 2;
 #pragma unroll
-            for (int m = 0; m < kMels; ++m) {
+            for (int mm = 0; mm < kMels / 2; ++mm) {
+                const int m = m0 + mm;
+                const float v = row[m] + ((m >= kHiMin && m <= kLoMax) ? ovl_s[r * kOvl + (m - kHiMin)] : 0.0f);
                 const bool masked = tmask || (m >= fl0 && m < fh0) || (m >= fl1 && m < fh1);
-                row[m] = masked ? 0.0f : logf(mel[m] + 5.9604644775390625e-8f);   // + 2^-24
+                row[m] = masked ? 0.0f : logf(v + 5.9604644775390625e-8f);   // + 2^-24
             }
         }
         epilogue_sync();
 
         // FrameSplicing: spliced row t' is frames stack*t' .. stack*t'+stack-1, so
         // the CTA's output rows are one contiguous run of (frame, mel) values:
-        // copy it out with 128-bit stores
+        // copy it out with 128-bit stores (256 epilogue threads)
         const int e = tid - 64;
         const int stack = L.stack;
         const int width = stack * kMels;
@@ -334,7 +362,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
         const int t_rows = (T + stack - 1) / stack;
         const int rows = min(kFramesPerCta / stack, t_rows - row0);
         float* out = d.out + (int64_t)row0 * width;
-        for (int q = 4 * e; q < rows * width && !(L.debug & 64); q += 4 * 128) {
+        for (int q = 4 * e; q < rows * width && !(L.debug & 64); q += 4 * 256) {
             const int fr = q / kMels, m = q - fr * kMels;   // 4 values of one frame (80 % 4 == 0)
             const float* src = mel_s + fr * kMelPitch + m;
             *reinterpret_cast<float4*>(out + q) = make_float4(src[0], src[1], src[2], src[3]);
