@@ -331,6 +331,17 @@ def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, 
     return rep, ids, wall, {k: c1[k] - c0[k] for k in c1}
 
 
+def traffic_of(workload: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/r1_traffic.json), or None when there is no capture for this workload."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            t = json.load(f).get(workload)
+        return int(t["dram_read"] + t["dram_write"]) if t else None
+    except Exception:
+        return None
+
+
 def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
     """Dominant kernel alone: serial stream, device-resident inputs, CUDA events around
     every launch (the group's stage events); achieved = algorithmic bytes (or tensor
@@ -344,7 +355,7 @@ def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
     if getattr(wl, "p_fg", 0) > 0:
         kernel = "fg_scan_kernel + img3d_tma_kernel (one stage)"
     out = {"kernel": kernel, "launches": int(launches), "mean_launch_us": round(1e3 * t["mean_ms"], 2),
-           "traffic": None, "algo_bytes_per_launch": int(t["bytes"] / max(launches, 1))}
+           "traffic": traffic_of(wl.name), "algo_bytes_per_launch": int(t["bytes"] / max(launches, 1))}
     if wl.name == "speech":
         tf = t["flops"] / (ms / 1e3) / 1e12 if ms > 0 else 0.0
         out.update({"bound": "tensor", "achieved": round(tf, 1), "peak": tf32_peak, "unit": "TFLOP/s",
