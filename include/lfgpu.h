@@ -30,7 +30,8 @@
 extern "C" {
 #endif
 
-#define LFG_ABI_VERSION 2   /* 2: run config percentile / scheduler fields, report scheduler fields, lfg_run_shard_source */
+#define LFG_ABI_VERSION 3   /* 2: run config percentile / scheduler fields, report scheduler fields, lfg_run_shard_source;
+                               3: run config prefetch_factor */
 
 #define LFG_OK 0
 #define LFG_ERR_INVALID -1
@@ -258,6 +259,9 @@ typedef struct {
                                    the initial count, grown / shrunk every sched_tick_us */
     int32_t max_workers;        /* scheduler upper bound (0 = 2 x n_workers, <= 28 streams) */
     int64_t sched_tick_us;      /* scheduler period (0 = 500 us) */
+    int32_t prefetch_factor;    /* policy 3: at most prefetch_factor x n_workers batches fed ahead of
+                                   the oldest unsealed batch (SyncLoaderConfig::prefetch_factor,
+                                   baselines.cpp:115-151, pipeline.prefetch_factor); 0 = unbounded */
 } lfg_run_config;
 
 typedef struct {

@@ -319,9 +319,14 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         }
         ph.lap(Phases::PARKED);
         // (3) feed new samples while a worker (stream) is free
-        while (static_cast<int>(inflight.size()) < n_workers && fed < n &&
+        // policy 3 feeds at most prefetch_factor x workers batches ahead of the oldest
+        // unsealed one (the sync loader's claim window, baselines.cpp:115-151)
+        const int64_t sync_window = sync && rc.prefetch_factor > 0
+                                        ? (sync_next / B + int64_t(rc.prefetch_factor) * n_workers) * B
+                                        : n;
+        while (static_cast<int>(inflight.size()) < n_workers && fed < std::min(n, sync_window) &&
                (ctx.serial || ctx.free_stream_count() > 0)) {
-            const int64_t take = std::min<int64_t>(group, n - fed);
+            const int64_t take = std::min<int64_t>(group, std::min(n, sync_window) - fed);
             int64_t got = 0;
             int64_t gid = -1;
             try {

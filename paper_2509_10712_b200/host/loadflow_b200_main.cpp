@@ -245,6 +245,7 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
     rc.scheduler = (loader == "minato-gpu" && getb(kv, "scheduler.enabled", true)) ? 1 : 0;
     rc.max_workers = static_cast<int32_t>(getd(kv, "scheduler.max_workers", 2 * workers));
     rc.sched_tick_us = static_cast<int64_t>(getd(kv, "scheduler.tick_ms", 500) * scale);
+    rc.prefetch_factor = static_cast<int32_t>(getd(kv, "pipeline.prefetch_factor", 2));   // experiment.cpp:83
     lfg_run_report rep{};
     std::vector<uint64_t> ids(static_cast<size_t>(n));
     std::vector<int32_t> bsz(static_cast<size_t>(n)), cls(static_cast<size_t>(n));

@@ -75,7 +75,8 @@ class RunConfig(C.Structure):
                 ("window", C.c_int32), ("n_workers", C.c_int32), ("trainer_us", C.c_int64),
                 ("trainer_priority", C.c_int32), ("warmup_batches", C.c_int32),
                 ("record_trace", C.c_int32), ("d2h_probe", C.c_int32), ("percentile", C.c_int32),
-                ("scheduler", C.c_int32), ("max_workers", C.c_int32), ("sched_tick_us", C.c_int64)]
+                ("scheduler", C.c_int32), ("max_workers", C.c_int32), ("sched_tick_us", C.c_int64),
+                ("prefetch_factor", C.c_int32)]
 
 
 class RunReport(C.Structure):
@@ -526,7 +527,8 @@ def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: 
                warmup_batches: int = 0, n_workers: int = 0, warmup_us: int = 0,
                update_interval_us: int = 1000, window: int = 1024,
                trainer_priority: int = 1, d2h_probe: int = 0, percentile: int = 75,
-               scheduler: int = 0, max_workers: int = 0, sched_tick_us: int = 0) -> RunConfig:
+               scheduler: int = 0, max_workers: int = 0, sched_tick_us: int = 0,
+               prefetch_factor: int = 0) -> RunConfig:
     rc = RunConfig()
     rc.batch_size = batch_size
     rc.policy = policy
@@ -543,4 +545,5 @@ def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: 
     rc.scheduler = scheduler
     rc.max_workers = max_workers
     rc.sched_tick_us = sched_tick_us
+    rc.prefetch_factor = prefetch_factor
     return rc

@@ -412,6 +412,68 @@ def test_shard_sync_baseline_is_head_of_line(lfgpu):
     ctx.close()
 
 
+def test_shard_sync_prefetch_sweep(lfgpu):
+    """test_baselines.cpp:182-209 on the device: the synchronous loader (policy 3) with
+    a claim window of prefetch_factor x workers batches; preprocessing-bound (batch 24 >=
+    12 workers, lognormal costs), so the window size changes the completion time by
+    little -- the reference bounds it at 5% on its virtual clock, the device run at 10%
+    (real streams) -- and every prefetch factor delivers FIFO batches exactly once."""
+    ctx = lfgpu.Context(batch_size=24, n_workers=12, max_group=1, max_slot_buffers=48, seed=SEED)
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, spin_first=True))
+    dims = (10, 10, 20)
+    rng = np.random.default_rng(23)
+    pi = _upload(ctx, rng.standard_normal(dims).astype(np.float32))
+    pl = _upload(ctx, rng.integers(0, 3, dims, dtype=np.uint8))
+    n = 480
+    cost_us = np.minimum(1500.0, rng.lognormal(np.log(100.0), 0.5, n)) * 4 + 4
+    descs = [lfgpu.sample_desc(i, dims, pi, pl, spin_us=[int(cost_us[i])]) for i in range(n)]
+    elapsed = {}
+    for k in (1, 2, 4, 8):
+        best = None
+        for _ in range(2):
+            rep, ids, bsz, _ = ctx.run_shard(ch, descs, lfgpu.run_config(batch_size=24, policy=3, n_workers=12,
+                                                                         prefetch_factor=k))
+            assert rep.exactly_once == 1 and ids.tolist() == list(range(n)) and (bsz == 24).all()
+            best = rep.elapsed_ms if best is None else min(best, rep.elapsed_ms)
+        elapsed[k] = best
+    for k in (2, 4, 8):
+        assert abs(elapsed[k] - elapsed[1]) / elapsed[1] < 0.10, elapsed
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
+def test_shard_sync_prefetch_window_bounds_feed(lfgpu):
+    """The claim window binds: with one worker-batch of prefetch and a head-of-line
+    sample costing 30 ms, at most prefetch_factor x workers batches of the cheap samples
+    behind it are fed, so the run takes about the slow sample plus the rest run after it
+    (not overlapped with it); unbounded (0) overlaps them."""
+    ctx = lfgpu.Context(batch_size=4, n_workers=2, max_group=1, max_slot_buffers=24, seed=SEED)
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, spin_first=True))
+    dims = (10, 10, 20)
+    rng = np.random.default_rng(29)
+    pi = _upload(ctx, rng.standard_normal(dims).astype(np.float32))
+    pl = _upload(ctx, rng.integers(0, 3, dims, dtype=np.uint8))
+    n = 64
+    descs = [lfgpu.sample_desc(i, dims, pi, pl, spin_us=[30_000 if i == 0 else 1_000]) for i in range(n)]
+    t = {}
+    for k in (1, 0):
+        rep, ids, _, _ = ctx.run_shard(ch, descs, lfgpu.run_config(batch_size=4, policy=3, n_workers=2,
+                                                                   prefetch_factor=k))
+        assert rep.exactly_once == 1 and ids.tolist() == list(range(n))
+        t[k] = rep.elapsed_ms
+    # window 1 x 2 workers = 8 samples: ~7 cheap samples overlap the slow one, the other
+    # 56 run after it on 2 streams (~28 ms); unbounded, ~30 of them overlap it
+    assert t[1] > t[0] + 8.0, t
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
 def test_shard_exactly_once_fast_first(lfgpu):
     """Algorithm 1 on the device: samples whose synthetic cost exceeds t_out are
     classified slow, finish in the background and are batched after the fast
