@@ -64,8 +64,8 @@ constexpr int kBStageBytes = (kKChunk / 8) * 2 * 2 * kBBlock;   // 32 KB
 constexpr int kStageBytes = 2 * kAPartBytes + kBStageBytes;     // 40 KB
 constexpr int kSmemBytes = kStages * kStageBytes + 1024;        // + barriers
 constexpr int kMelPitch = kMels + 1;
-constexpr int kThreads = 320;         // warp 0 producer, warp 1 MMA, warps 2-5 A builders + epilogue
-                                      // (bins 128..255), warps 6-9 epilogue (bins 0..127)
+constexpr int kThreads = 320;         // warp 0 producer, warp 1 MMA, warps 2-9 A builders (taps 0-3 /
+                                      // 4-7 of each K step) + epilogue (bins 128..255 / 0..127)
 
 // instruction descriptor: D f32, A/B tf32, K-major both, N = 256, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
@@ -121,12 +121,14 @@ __device__ __forceinline__ void epilogue_sync() {   // the 8 epilogue warps (2..
 
 // ------------------------------------------------------------------ the kernel
 // Warp-specialised: warp 0 streams the constant B chunks (cp.async.bulk) into a
-// 5-deep ring, warp 1 issues the MMAs (one elected thread), warps 2-5 build the
-// A chunks from the waveform and then run the epilogue.  Per stage: full_a (128
-// builder arrivals), full_b (bulk-copy bytes), empty (tcgen05.commit).
+// 5-deep ring, warp 1 issues the MMAs (one elected thread), warps 2-9 build the
+// A chunks from the waveform (two warps per row quarter, one 16-B half of each
+// row's K step each) and then run the epilogue.  Per stage: full_a (8 builder-warp
+// arrivals), full_b (bulk-copy bytes), empty (tcgen05.commit).
 __global__ void __launch_bounds__(kThreads, 1)
 speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis) {
     extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ float nyq_s[kRowsM];                       // warps 6-9's half of the Nyquist sums
     // flattened grid: CTA -> (utterance, tile) through the tile prefix sums
     int u = 0;
     while (u + 1 < L.n && L.tile_start[u + 1] <= (int)blockIdx.x) ++u;
@@ -145,7 +147,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(full_a + s, 4);          // one arrival per builder warp
+            mbar_init(full_a + s, 8);          // one arrival per builder warp
             mbar_init(full_b + s, 1);
             mbar_init(empty + s, 1);
         }
@@ -204,7 +206,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
         }
         __syncwarp();
     } else {
-        // ---------------- A builders (warps 2-5, then the epilogue with warps 6-9): one frame per thread,
+        // ---------------- A builders (warps 2-9), then the epilogue: one frame per thread,
         // thread row = TMEM lane (warp w may only read lanes 32*(w%4) .. +31)
         const int r = 32 * (warp & 3) + lane;
         const int f = f0 + r;
@@ -213,18 +215,20 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
         const bool interior = row_live && n0 >= 0 && n0 + kTaps <= d.L &&
                               ((reinterpret_cast<uintptr_t>(d.wav + n0) & 15) == 0);
         float nyq = 0.0f;
-        auto load = [&](int it, float x[kKChunk]) {
+        // All 8 warps build A: warps 2-5 taps 0-3 of every K step (16-B chunk 0 of
+        // the row), warps 6-9 taps 4-7 (chunk 1), each into its own half of the
+        // Nyquist bin's sum (combined in the epilogue).
+        const int half = warp >= 6 ? 1 : 0;
+        auto load = [&](int it, float x[4]) {
             if (interior) {
-                const float4* p = reinterpret_cast<const float4*>(d.wav + n0 + it * kKChunk);
-                const float4 a = __ldg(p), b = __ldg(p + 1);
+                const float4 a = __ldg(reinterpret_cast<const float4*>(d.wav + n0 + it * kKChunk + 4 * half));
                 x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-                x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
             } else {
 #pragma unroll
-                for (int j = 0; j < kKChunk; ++j) {
+                for (int j = 0; j < 4; ++j) {
                     float v = 0.0f;
                     if (row_live) {
-                        int64_t n = n0 + it * kKChunk + j;     // reflect padding
+                        int64_t n = n0 + it * kKChunk + 4 * half + j;     // reflect padding
                         if (n < 0) n = -n;
                         if (n >= d.L) n = 2 * ((int64_t)d.L - 1) - n;
                         v = __ldg(d.wav + n);
@@ -233,28 +237,28 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
                 }
             }
         };
-        if (warp < 6) {   // warps 6-9 have no A rows to build
-            float x[kKChunk];
+        {
+            float x[4];
             const bool skip_loads = (L.debug & 1) != 0;
             if (skip_loads) {
 #pragma unroll
-                for (int j = 0; j < kKChunk; ++j) x[j] = 0.001f * j;
+                for (int j = 0; j < 4; ++j) x[j] = 0.001f * j;
             } else {
                 load(0, x);
             }
             for (int it = 0; it < kChunks; ++it) {
                 const int s = it % kStages, use = it / kStages;
-                float xn[kKChunk];
+                float xn[4];
                 if (skip_loads) {
 #pragma unroll
-                    for (int j = 0; j < kKChunk; ++j) xn[j] = x[j];
+                    for (int j = 0; j < 4; ++j) xn[j] = x[j];
                 } else if (it + 1 < kChunks) {
                     load(it + 1, xn);                            // prefetch the next chunk's taps
                 }
-                uint32_t hi[kKChunk], lo[kKChunk];
+                uint32_t hi[4], lo[4];
 #pragma unroll
-                for (int j = 0; j < kKChunk; ++j) {
-                    nyq = fmaf(x[j], c_win_nyq[it * kKChunk + j], nyq);
+                for (int j = 0; j < 4; ++j) {
+                    nyq = fmaf(x[j], c_win_nyq[it * kKChunk + 4 * half + j], nyq);
                     hi[j] = tf32_rna(x[j]);
                     lo[j] = tf32_rna(x[j] - __uint_as_float(hi[j]));
                 }
@@ -264,21 +268,17 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
                 }
                 uint8_t* sa = smem + s * kStageBytes;
                 // canonical K-major, 32-byte swizzle (see smem_desc)
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int off = sw32_off(r, c);
-                    *reinterpret_cast<uint4*>(sa + off) =
-                        make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
-                    *reinterpret_cast<uint4*>(sa + kAPartBytes + off) =
-                        make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
-                }
+                const int off = sw32_off(r, half);
+                *reinterpret_cast<uint4*>(sa + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(sa + kAPartBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to the tensor core
                 __syncwarp();
                 if (lane == 0) mbar_arrive(full_a + s);
 #pragma unroll
-                for (int j = 0; j < kKChunk; ++j) x[j] = xn[j];
+                for (int j = 0; j < 4; ++j) x[j] = xn[j];
             }
         }
+        if (half == 1) nyq_s[r] = nyq;   // read after the first epilogue barrier
 
         // ---------------- epilogue: power -> mel with the filter bank as compile-time
         // constants (mel_table.h: with the bin loops unrolled every filter index is a
@@ -324,10 +324,6 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
                 for (int m = 0; m <= kLoMax; ++m) row[m] = mel[m];
             } else {
                 half_bins(std::integral_constant<int, 1>{}, mel);
-                if (kMelM[kBins] >= 0) {                       // Nyquist bin (CUDA cores)
-                    const float p = nyq * nyq;
-                    mel[kMelM[kBins]] = fmaf(kMelWa[kBins], p, mel[kMelM[kBins]]);
-                }
 #pragma unroll
                 for (int m = kHiMin; m <= kLoMax; ++m) ovl_s[r * kOvl + (m - kHiMin)] = mel[m];
 #pragma unroll
@@ -335,6 +331,12 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
             }
         }
         epilogue_sync();
+        // Nyquist bin (CUDA cores): its filter is the upper half's own (row[m], m > kLoMax)
+        static_assert(kMelM[kBins] < 0 || kMelM[kBins] > kLoMax, "Nyquist filter owned by warps 2-5");
+        if (kMelM[kBins] >= 0 && !low_bins) {
+            const float x = nyq + nyq_s[r];
+            row[kMelM[kBins]] = fmaf(kMelWa[kBins], x * x, row[kMelM[kBins]]);
+        }
         // log + SpecAugment on this row's 40 filters; padding frames are zero
         {
             bool tmask = f >= T || r >= kFramesPerCta;
