@@ -498,6 +498,10 @@ def main():
         rep, ids, wall, dc = run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local,
                                        trainer_us=trainer_us, policy=1 if heavy else 0)
     clocks = clk.summary()
+    if os.environ.get("LFG_BENCH_DIAG"):
+        print(json.dumps({"diag": {"elapsed_ms": rep.elapsed_ms, "wall_s": wall, "kernel_ms": rep.kernel_ms,
+                                   "launches": rep.launches, "batches": rep.batches,
+                                   "inplace": rep.inplace_batches}}), file=sys.stderr, flush=True)
     el_max = allreduce_max(dist, rep.elapsed_ms, local)
     samples_total = allreduce_sum(dist, [rep.timed_samples], local)[0]
     value = samples_total / (el_max / 1e3)
