@@ -665,9 +665,16 @@ int64_t Context::stage_raw_bytes(const Chain& c, const Ticket& t) const {
 
 // ------------------------------------------------------------------ submit
 void draw_params(const Chain& c, uint64_t seed, const lfg_sample_desc& s, PreDraw& out) {
-    if (c.fam == FAM_IMG3D) draw_3d(c, seed, s.id, s.dims, out.p3);
-    else if (c.fam == FAM_RRC2D) draw_2d(c, seed, s.id, s.dims[0], s.dims[1], out.p2);
-    else draw_sp(c, seed, s.id, s.dims[0], out.ps);
+    if (c.fam == FAM_IMG3D) {
+        out.p3 = Params3D{};
+        draw_3d(c, seed, s.id, s.dims, out.p3);
+    } else if (c.fam == FAM_RRC2D) {
+        out.p2 = Params2D{};
+        draw_2d(c, seed, s.id, s.dims[0], s.dims[1], out.p2);
+    } else {
+        out.ps = ParamsSp{};
+        draw_sp(c, seed, s.id, s.dims[0], out.ps);
+    }
 }
 
 int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) {

@@ -125,7 +125,18 @@ void draw_sp(const Chain& c, uint64_t seed, uint64_t id, int64_t L, ParamsSp& p)
 // One sample's drawn parameters (whichever family applies); pure function of
 // (chain, seed, sample id, dims), so the shard runner draws them ahead of time
 // on a host thread pool.
-struct PreDraw { Params3D p3{}; Params2D p2{}; ParamsSp ps{}; };
+// One sample's drawn parameters (the chain's family only).  Deliberately not
+// zero-initialised: a run allocates n of these up front and the draw threads
+// write (and first-touch) each one, so the submitting thread never pays for
+// clearing or faulting in the table.
+struct PreDraw {
+    union {
+        Params3D p3;
+        Params2D p2;
+        ParamsSp ps;
+    };
+    PreDraw() {}
+};
 void draw_params(const Chain& c, uint64_t seed, const lfg_sample_desc& s, PreDraw& out);
 int64_t rrc_algo_bytes(const Chain& c, const Params2D& p);
 
@@ -180,7 +191,7 @@ struct Ticket {
         Params2D p2;
         ParamsSp ps;
     };
-    Ticket() : desc{}, p3{} {}
+    Ticket() {}   // submit assigns desc and the chain's params member (no clearing per sample)
 };
 
 struct BatchRec {
