@@ -29,6 +29,8 @@
 #include <deque>
 #include <thread>
 
+#include <sys/mman.h>
+
 #include "loadflow/sched_rule.h"
 #include <unordered_map>
 
@@ -72,6 +74,12 @@ struct Profile {
 
 // Host-loop phase clock (LFG_SHARD_PROF=1 prints the split to stderr): the
 // resident-input rate is bounded by this loop, so its cost is kept visible.
+#ifdef MADV_POPULATE_WRITE
+constexpr int kMadvPopulateWrite = MADV_POPULATE_WRITE;
+#else
+constexpr int kMadvPopulateWrite = 23;   // Linux >= 5.14; older kernels reject it (harmless)
+#endif
+
 struct Phases {
     enum { POLL, PARKED, SUBMIT, FLUSH, SEAL, DELIVER, IDLE, DRAW, N };
     bool on = std::getenv("LFG_SHARD_PROF") != nullptr;
@@ -180,6 +188,27 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     const int64_t tbase = static_cast<int64_t>(ctx.tickets.size());
     ctx.tickets.reserve(static_cast<size_t>(tbase + n));
     ctx.groups.reserve(ctx.groups.size() + static_cast<size_t>(n));
+    // The run's ticket storage is fresh memory: a helper thread has the kernel
+    // populate its pages (MADV_POPULATE_WRITE leaves contents untouched, so it may
+    // run while submit constructs tickets), instead of the submitting thread taking
+    // one page fault per ~15 tickets.
+    std::thread populate;
+    {
+        const uintptr_t pg = 4096;
+        const uintptr_t lo = (reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase) + pg - 1) & ~(pg - 1);
+        const uintptr_t hi = reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase + n) & ~(pg - 1);
+        if (hi > lo + (1u << 20))
+            populate = std::thread([lo, hi] {
+                for (uintptr_t p = lo; p < hi; p += (1u << 20))   // in 1 MB steps, front first
+                    madvise(reinterpret_cast<void*>(p), std::min<uintptr_t>(1u << 20, hi - p), kMadvPopulateWrite);
+            });
+    }
+    struct PopulateJoin {
+        std::thread& t;
+        ~PopulateJoin() {
+            if (t.joinable()) t.join();
+        }
+    } populate_join{populate};
     std::vector<int64_t> inflight, parked;
     std::deque<int64_t> fast, slow;
     // Zero-copy bookkeeping: fast_cnt[buf] = tickets of slot buffer `buf` in
