@@ -761,6 +761,17 @@ int64_t Context::open_group_count() const {
     return static_cast<int64_t>(open_group_[0].size() + open_group_[1].size());
 }
 
+bool Context::recycle_tables() {
+    if (!deferred_.empty() || open_group_count() != 0) return false;
+    for (const Group& g : groups)
+        if (!g.complete || g.refs != 0) return false;
+    for (const Ticket& t : tickets)
+        if (!t.released) return false;
+    tickets.clear();
+    groups.clear();
+    return true;
+}
+
 void Context::flush() {
     for (int64_t gi : deferred_) launch_group(groups[gi]);
     deferred_.clear();

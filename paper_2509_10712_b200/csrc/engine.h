@@ -246,6 +246,10 @@ public:
     bool poll_group(Group& g);          // updates stages_done/complete; true if complete
     void finalize_group_timing(Group& g);
     int64_t open_group_count() const;
+    // Drop every ticket and group if none is still referenced (all tickets released,
+    // all groups complete, nothing open or deferred), keeping the tables' storage:
+    // the next run reuses memory that is already faulted in.  Returns whether it did.
+    bool recycle_tables();
 
     static constexpr int kStreamPool = 28;
     int free_stream_count() const { return static_cast<int>(free_streams_.size()); }

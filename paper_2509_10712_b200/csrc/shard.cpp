@@ -84,6 +84,7 @@ struct Phases {
     enum { POLL, PARKED, SUBMIT, FLUSH, SEAL, DELIVER, IDLE, DRAW, N };
     bool on = std::getenv("LFG_SHARD_PROF") != nullptr;
     double ns[N] = {};
+    double setup_ns = 0;
     std::chrono::steady_clock::time_point t;
     void start() {
         if (on) t = std::chrono::steady_clock::now();
@@ -98,7 +99,7 @@ struct Phases {
         if (!on || n <= 0) return;
         static const char* names[N] = {"poll", "parked", "submit", "flush", "seal", "deliver", "idle",
                                        "draw_wait"};
-        std::fprintf(stderr, "[lfg shard] ns/sample:");
+        std::fprintf(stderr, "[lfg shard] setup=%.2f ms; ns/sample:", setup_ns / 1e6);
         for (int k = 0; k < N; ++k) std::fprintf(stderr, " %s=%.0f", names[k], ns[k] / double(n));
         std::fprintf(stderr, " | per group (%lld): launch_group=%.0f kernel_launch=%.0f ns\n",
                      static_cast<long long>(groups),
@@ -160,6 +161,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     };
     cudaEvent_t t_start = mk();
     cuda_check(cudaEventRecord(t_start, trainer), "record");
+    const auto setup_t0 = std::chrono::steady_clock::now();
     cudaEvent_t t_timed = t_start;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> steps;   // timed-window trainer steps
 
@@ -185,6 +187,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     const int64_t run_t0 = host_now_us();
     int64_t last_update = run_t0;
 
+    ctx.recycle_tables();   // a previous run's finished tickets: reuse their storage
     const int64_t tbase = static_cast<int64_t>(ctx.tickets.size());
     ctx.tickets.reserve(static_cast<size_t>(tbase + n));
     ctx.groups.reserve(ctx.groups.size() + static_cast<size_t>(n));
@@ -192,23 +195,6 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     // populate its pages (MADV_POPULATE_WRITE leaves contents untouched, so it may
     // run while submit constructs tickets), instead of the submitting thread taking
     // one page fault per ~15 tickets.
-    std::thread populate;
-    {
-        const uintptr_t pg = 4096;
-        const uintptr_t lo = (reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase) + pg - 1) & ~(pg - 1);
-        const uintptr_t hi = reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase + n) & ~(pg - 1);
-        if (hi > lo + (1u << 20))
-            populate = std::thread([lo, hi] {
-                for (uintptr_t p = lo; p < hi; p += (1u << 20))   // in 1 MB steps, front first
-                    madvise(reinterpret_cast<void*>(p), std::min<uintptr_t>(1u << 20, hi - p), kMadvPopulateWrite);
-            });
-    }
-    struct PopulateJoin {
-        std::thread& t;
-        ~PopulateJoin() {
-            if (t.joinable()) t.join();
-        }
-    } populate_join{populate};
     std::vector<int64_t> inflight, parked;
     std::deque<int64_t> fast, slow;
     // Zero-copy bookkeeping: fast_cnt[buf] = tickets of slot buffer `buf` in
@@ -279,6 +265,25 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             for (auto& t : th) t.join();
         }
     } joiner{drawers, stop_draw};
+    // (spawned after the draw threads: its page-table work holds the mm lock that
+    // thread creation needs)
+    std::thread populate;
+    if (!std::getenv("LFG_NO_POPULATE")) {   // (A/B switch)
+        const uintptr_t pg = 4096;
+        const uintptr_t lo = (reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase) + pg - 1) & ~(pg - 1);
+        const uintptr_t hi = reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase + n) & ~(pg - 1);
+        if (hi > lo + (1u << 20))
+            populate = std::thread([lo, hi] {
+                for (uintptr_t p = lo; p < hi; p += (1u << 20))   // in 1 MB steps, front first
+                    madvise(reinterpret_cast<void*>(p), std::min<uintptr_t>(1u << 20, hi - p), kMadvPopulateWrite);
+            });
+    }
+    struct PopulateJoin {
+        std::thread& t;
+        ~PopulateJoin() {
+            if (t.joinable()) t.join();
+        }
+    } populate_join{populate};
 
     Phases ph;
     const double g_ns0 = ctx.prof_group_ns, l_ns0 = ctx.prof_launch_ns;
@@ -286,6 +291,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     constexpr int64_t kScanUs = 10;
     int64_t last_scan_us = 0;
     ph.start();
+    ph.setup_ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - setup_t0).count();
     while (consumed < n) {
         bool progressed = false;
         const int64_t now = host_now_us();
