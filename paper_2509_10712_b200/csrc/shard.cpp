@@ -159,16 +159,17 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         evs.push_back(e);
         return e;
     };
+    // end-to-end probe: 16 bytes of every delivered batch are read back on the trainer
+    // stream (pinned before the run's clock starts: cudaMallocHost can take milliseconds)
+    char* probe = nullptr;
+    if (rc.d2h_probe) cuda_check(cudaMallocHost(&probe, 16 * 1024), "probe buffer");
+    int64_t probe_bytes = 0;
     cudaEvent_t t_start = mk();
     cuda_check(cudaEventRecord(t_start, trainer), "record");
     const auto setup_t0 = std::chrono::steady_clock::now();
     cudaEvent_t t_timed = t_start;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> steps;   // timed-window trainer steps
 
-    // end-to-end probe: 16 bytes of every delivered batch are read back on the trainer stream
-    char* probe = nullptr;
-    if (rc.d2h_probe) cuda_check(cudaMallocHost(&probe, 16 * 1024), "probe buffer");
-    int64_t probe_bytes = 0;
 
     Profile prof;
     prof.cap = rc.window > 0 ? static_cast<size_t>(rc.window) : 1024;
