@@ -176,6 +176,8 @@ int lfg_wait(lfg_ctx* ctx, lfg_ticket t);
 int lfg_exec_costs(lfg_ctx* ctx, lfg_ticket t, double* costs_us, int cap, int* n_out);
 /* Copy a completed sample's output slot to host memory (tests). */
 int lfg_ticket_output(lfg_ctx* ctx, lfg_ticket t, void* host_dst, size_t bytes);
+/* Ends the caller's use of t.  A released handle is dead: once every ticket of the
+ * context is released, the next lfg_run_shard reuses the ticket numbers. */
 int lfg_ticket_release(lfg_ctx* ctx, lfg_ticket t);
 
 /* ---- batches: build_batches seal (batcher.cpp:50-58) ----

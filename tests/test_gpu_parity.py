@@ -474,6 +474,47 @@ def test_shard_sync_prefetch_window_bounds_feed(lfgpu):
     ctx.close()
 
 
+def test_shard_recycles_finished_tables(lfgpu):
+    """A run reuses the ticket / group storage of earlier runs once nothing references
+    it (Context::recycle_tables): repeated runs stay exactly-once with identical
+    outputs order-independently, the ticket numbering restarts, and a ticket the user
+    still holds blocks the recycling (its handle stays valid)."""
+    ctx = lfgpu.Context(batch_size=4, n_workers=4, max_group=2, max_slot_buffers=16, seed=SEED)
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop))
+    dims = (10, 10, 20)
+    rng = np.random.default_rng(31)
+    pi = _upload(ctx, rng.standard_normal(dims).astype(np.float32))
+    pl = _upload(ctx, rng.integers(0, 3, dims, dtype=np.uint8))
+    n = 40
+    descs = [lfgpu.sample_desc(i, dims, pi, pl) for i in range(n)]
+    rc = lfgpu.run_config(batch_size=4, n_workers=4)
+    for _ in range(3):
+        rep, ids, _, _ = ctx.run_shard(ch, descs, rc)
+        assert rep.exactly_once == 1 and sorted(ids.tolist()) == list(range(n))
+    # three runs of n: the third started from an empty table, so the next ticket is n
+    t = ctx.submit(ch, descs[0])
+    assert t == n
+    ctx.flush()
+    ctx.wait(t)
+    vox = crop[0] * crop[1] * crop[2]
+    nbytes = vox * 4 + ((vox + 15) // 16) * 16
+    held = ctx.ticket_output(t, nbytes)       # the held ticket is readable ...
+    rep, ids, _, _ = ctx.run_shard(ch, descs, rc)
+    assert rep.exactly_once == 1
+    assert (ctx.ticket_output(t, nbytes) == held).all()   # ... and not recycled under the user
+    t2 = ctx.submit(ch, descs[1])
+    assert t2 == 2 * n + 1                     # tables kept: n (run 3) + 1 (held) + n (run 4)
+    ctx.flush()
+    ctx.wait(t2)
+    ctx.release(t)
+    ctx.release(t2)
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
 def test_shard_exactly_once_fast_first(lfgpu):
     """Algorithm 1 on the device: samples whose synthetic cost exceeds t_out are
     classified slow, finish in the background and are batched after the fast
