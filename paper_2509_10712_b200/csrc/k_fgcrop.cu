@@ -95,11 +95,14 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
             seen |= 1u << c;
         }
     };
+    const uint8_t* plane = d.lbl + (int64_t)z * d.lbl_pz;
+    const int zsk = d.lbl_sk0 + z * d.lbl_skz;
     auto row_ptr = [&](int y) {
         // row start (K0-staged volumes keep the source's 16-B alignment phase: skews)
-        return d.lbl + (int64_t)z * d.lbl_pz + (int64_t)y * d.lbl_py + ((d.lbl_sk0 + z * d.lbl_skz + y * d.lbl_sky) & 15);
+        return plane + (int64_t)y * d.lbl_py + ((zsk + y * d.lbl_sky) & 15);
     };
     auto close_row = [&](int y, uint32_t seen) {
+        if (seen == 0u) return;   // all-background row segment (most of a volume)
 #pragma unroll
         for (int c = 1; c < kClasses; ++c)
             if (seen & (1u << c)) {
