@@ -76,9 +76,14 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
             return;
         }
         // per class: SIMD byte compares give the chunk's match mask (one bit per
-        // byte), whose lowest / highest set bits are the class's x extent in the chunk
+        // byte), whose lowest / highest set bits are the class's x extent in the chunk;
+        // classes above the chunk's largest label are skipped
+        uint32_t mx = __vmaxu4(__vmaxu4(v.x, v.y), __vmaxu4(v.z, v.w));
+        mx = __vmaxu4(mx, mx >> 16);
+        mx = max(mx & 0xFFu, (mx >> 8) & 0xFFu);
 #pragma unroll
         for (int c = 1; c < kClasses; ++c) {
+            if ((uint32_t)c > mx) break;
             const uint32_t rep = 0x01010101u * (uint32_t)c;
             const uint32_t m[4] = {__vcmpeq4(v.x, rep), __vcmpeq4(v.y, rep), __vcmpeq4(v.z, rep),
                                    __vcmpeq4(v.w, rep)};
