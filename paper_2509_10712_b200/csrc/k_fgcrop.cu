@@ -66,11 +66,13 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
             // uniform chunk (inside a region): one class spans all 16 bytes
             if (b0 >= 1 && b0 < (uint32_t)kClasses) {
 #pragma unroll
-                for (int c = 1; c < kClasses; ++c)
+                for (int c = 1; c < kClasses; ++c) {
+                    if ((uint32_t)c > b0) break;
                     if (b0 == (uint32_t)c) {
                         xmin[c] = min(xmin[c], (uint32_t)(16 * q));
                         xmax[c] = (xmax[c] == kNone) ? (uint32_t)(16 * q + 15) : max(xmax[c], (uint32_t)(16 * q + 15));
                     }
+                }
                 seen |= 1u << b0;
             }
             return;
@@ -108,12 +110,15 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
     };
     auto close_row = [&](int y, uint32_t seen) {
         if (seen == 0u) return;   // all-background row segment (most of a volume)
+        const int top = 31 - __clz(seen);
 #pragma unroll
-        for (int c = 1; c < kClasses; ++c)
+        for (int c = 1; c < kClasses; ++c) {
+            if (c > top) break;
             if (seen & (1u << c)) {
                 ymin[c] = min(ymin[c], (uint32_t)y);
                 ymax[c] = (ymax[c] == kNone) ? (uint32_t)y : max(ymax[c], (uint32_t)y);
             }
+        }
         seen_all |= seen;
     };
     constexpr int kRowsInFlight = 4;    // rows per warp with their loads issued together
