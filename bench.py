@@ -125,7 +125,10 @@ def dist_setup(n_gpus: int):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        try:   # bind the process group to this rank's GPU up front (eager NCCL init)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        except TypeError:
+            dist.init_process_group("nccl")
         return rank, local, world, dist
     return 0, 0, 1, None
 
@@ -154,7 +157,12 @@ def allreduce_sum(dist, xs, local: int):
 
 
 def barrier(dist):
-    if dist is not None:
+    if dist is None:
+        return
+    if dist.get_backend() == "nccl":
+        import torch
+        dist.barrier(device_ids=[torch.cuda.current_device()])
+    else:
         dist.barrier()
 
 
