@@ -1136,7 +1136,7 @@ void Context::launch_group(Group& g) {
                 counters.reserved[1] += int64_t(t.ps.T) * 2 * kTapsDft * 512 * 3;   // tensor FLOPs
             }
             start();
-            cuda_check(launch_speech(L, speech_, nullptr, st), "speech launch");
+            cuda_check(launch_speech(L, speech_, st), "speech launch");
             counters.launches++;
         }
         for (int slot : S.spin_ops) launch_spins(slot);

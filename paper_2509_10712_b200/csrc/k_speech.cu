@@ -518,7 +518,7 @@ void speech_tables_destroy(SpeechTables* t) {
 
 int speech_frames_per_cta() { return kFramesPerCta; }
 
-cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, float*, cudaStream_t s) {
+cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, cudaStream_t s) {
     if (L0.n <= 0) return cudaSuccess;
     static const int dbg = getenv("LFG_SPEECH_DEBUG") ? atoi(getenv("LFG_SPEECH_DEBUG")) : 0;
     SpLaunch L = L0;
@@ -535,8 +535,6 @@ cudaError_t launch_speech_collate(const SpCollate& C, cudaStream_t s) {
     speech_collate_kernel<<<dim3(C.t_max, (C.n + 3) / 4), 256, 0, s>>>(C);
     return cudaGetLastError();
 }
-
-int64_t speech_scratch_bytes(int, int) { return 0; }
 
 cudaError_t warm_speech() {
     cudaFuncAttributes a;

@@ -215,10 +215,8 @@ cudaError_t warm_misc();
 struct SpeechTables;
 cudaError_t speech_tables_create(SpeechTables** out);
 void speech_tables_destroy(SpeechTables* t);
-cudaError_t launch_speech(const SpLaunch& L, const SpeechTables* t, float* scratch,
-                          cudaStream_t s);
+cudaError_t launch_speech(const SpLaunch& L, const SpeechTables* t, cudaStream_t s);
 cudaError_t launch_speech_collate(const SpCollate& C, cudaStream_t s);
-int64_t speech_scratch_bytes(int n, int max_T);
 int speech_frames_per_cta();
 cudaError_t warm_speech();
 
