@@ -687,8 +687,9 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
         for (int a = 0; a < 3; ++a)
             if (s.dims[a] < 1 || s.dims[a] > (1 << 20)) fail(LFG_ERR_INVALID, "volume dims out of range");
     } else if (c->fam == FAM_RRC2D) {
-        if (s.ndim != 3 || s.dims[2] != 3 || s.dims[0] < 1 || s.dims[1] < 1)
-            fail(LFG_ERR_INVALID, "obj_det sample needs an H,W,3 image");
+        if (s.ndim != 3 || s.dims[2] != 3 || s.dims[0] < 1 || s.dims[1] < 1 || s.dims[0] > 65535 ||
+            s.dims[1] > 65535)
+            fail(LFG_ERR_INVALID, "obj_det sample needs an H,W,3 image (H, W <= 65535)");
     } else {
         // reflect padding by n_fft/2 needs L > n_fft/2 (torch.stft center=True has the same rule)
         if (s.ndim != 1 || s.dims[0] < c->n_fft / 2 + 1 || s.dims[0] > c->max_L)
@@ -1095,14 +1096,13 @@ void Context::launch_group(Group& g) {
                 RrcDesc& d = L.d[i];
                 d.src = reinterpret_cast<const uint8_t*>(v.p[0]);
                 d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
-                d.pitch = v.py[0];
-                d.sk0 = v.sk0[0];
-                d.sky = v.sky[0];
-                d.h = static_cast<int32_t>(t.p2.h);
-                d.w = static_cast<int32_t>(t.p2.w);
-                d.flip = t.p2.flip;
-                d.sy = static_cast<double>(d.h) / static_cast<double>(c.oh);
-                d.sx = static_cast<double>(d.w) / static_cast<double>(c.ow);
+                d.pitch = static_cast<int32_t>(v.py[0]);   // < 2^31: image width <= 65535
+                d.sk0 = static_cast<uint8_t>(v.sk0[0] & 15);
+                d.sky = static_cast<uint8_t>(v.sky[0] & 15);
+                d.h = static_cast<uint16_t>(t.p2.h);
+                d.w = static_cast<uint16_t>(t.p2.w);
+                d.flip = static_cast<uint8_t>(t.p2.flip);
+                d.sx = static_cast<double>(t.p2.w) / static_cast<double>(c.ow);
                 counters.kernel_bytes += rrc_algo_bytes(c, t.p2);
             }
             const auto t_l = std::chrono::steady_clock::now();

@@ -144,7 +144,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     int ylo = 0;
     if (warp == 0) {
         const int j = lane;
-        const double sy = d.sy;
+        const double sy = __ddiv_rn((double)d.h, (double)oh);   // IEEE: as the oracle / host
         int y0 = 0, y1 = 0;
         float l0 = 0.f, l1 = 0.f;
         if (j < n_rows_out) src_index(y_begin + j, d.h, sy, y0, y1, l0, l1);
