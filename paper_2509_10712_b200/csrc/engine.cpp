@@ -1102,7 +1102,6 @@ void Context::launch_group(Group& g) {
                 d.h = static_cast<uint16_t>(t.p2.h);
                 d.w = static_cast<uint16_t>(t.p2.w);
                 d.flip = static_cast<uint8_t>(t.p2.flip);
-                d.sx = static_cast<double>(t.p2.w) / static_cast<double>(c.ow);
                 counters.kernel_bytes += rrc_algo_bytes(c, t.p2);
             }
             const auto t_l = std::chrono::steady_clock::now();

@@ -212,7 +212,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     const int xa = 2 * threadIdx.x;                         // columns xa, xa + 1 (ow is even)
     ColPair cp;
     if (xa < ow) {
-        const double sx = d.sx;
+        const double sx = __ddiv_rn((double)d.w, (double)ow);
         int x1a, x1b;
         float l0a, l1a, l0b, l1b;
         src_index(xa, d.w, sx, cp.x0_a, x1a, l0a, l1a);

@@ -110,19 +110,19 @@ inline bool img3d_tma_ok(const void* img, const void* lbl, const int64_t dims[3]
 }
 
 // ---- K3: RandomResizedCrop (bilinear) + RandomHorizontalFlip + ToTensor + Normalize
-// 40 B per image: the launch passes 256 of these as kernel parameters, and the
-// launch call's cost grows with the parameter block (h / oh is divided on the device)
+// 32 B per image: the launch passes 256 of these as kernel parameters, and the
+// launch call's cost grows with the parameter block (h / oh and w / ow are divided
+// on the device, IEEE-rounded like the host / oracle)
 struct RrcDesc {
     const uint8_t* src;      // crop-box origin (row 0, column 0) of an HWC u8 image
     float* out;              // [3, oh, ow] f32
-    double sx;               // w / ow: column source-index scale (IEEE division on the host)
     int32_t pitch;           // bytes per source row
     uint16_t h, w;           // crop box size
     uint8_t sk0, sky;        // row skew (only the low 4 bits matter), see above
     uint8_t flip;
     uint8_t pad[5];
 };
-static_assert(sizeof(RrcDesc) == 40, "RrcDesc layout");
+static_assert(sizeof(RrcDesc) == 32, "RrcDesc layout");
 struct RrcLaunch {
     int32_t oh, ow;
     float a[3], b[3];        // out = v * a_c + b_c  (= (v/255 - mean_c) / std_c)
