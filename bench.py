@@ -42,6 +42,9 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# one hardware queue per launch-group stream (CUDA reads it at context creation;
+# the library never sets it: engine.cpp Context())
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform HBM GB/s"
@@ -117,18 +120,42 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed
+def launch_ranks(args) -> int | None:
+    """`--gpus N` (N > 1) without a launcher: re-run this very command under
+    torch.distributed.run, one process per GPU (the driver's own launch line).
+    Returns the launcher's exit code, or None when already inside a launcher."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_setup(n_gpus: int):
+    """One process per GPU: RANK / LOCAL_RANK / WORLD_SIZE from the launcher; the
+    world must be exactly --gpus.  NCCL (gloo with LFG_BENCH_BACKEND=gloo: the CPU
+    test of this plumbing)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but WORLD_SIZE={world} (one rank per GPU)")
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        try:   # bind the process group to this rank's GPU up front (eager NCCL init)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        except TypeError:
-            dist.init_process_group("nccl")
+        backend = os.environ.get("LFG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            try:   # bind the process group to this rank's GPU up front (eager NCCL init)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            except TypeError:
+                dist.init_process_group("nccl")
+        else:
+            dist.init_process_group(backend)
         return rank, local, world, dist
     return 0, 0, 1, None
 
@@ -156,6 +183,15 @@ def allreduce_sum(dist, xs, local: int):
     return t.tolist()
 
 
+def allreduce_sum_i64(dist, xs, local: int):
+    if dist is None:
+        return [int(x) for x in xs]
+    import torch
+    t = torch.tensor([int(x) for x in xs], dtype=torch.int64, device=_coll_device(dist, local))
+    dist.all_reduce(t)
+    return [int(v) for v in t.tolist()]
+
+
 def barrier(dist):
     if dist is None:
         return
@@ -164,6 +200,22 @@ def barrier(dist):
         dist.barrier(device_ids=[torch.cuda.current_device()])
     else:
         dist.barrier()
+
+
+def id_digest(ids) -> list[int]:
+    """Order-independent digest of a set of sample ids, summable across ranks without
+    overflow (<= 2^23 ids): [count, sum id, sum h1, sum h2] with h1 / h2 the low 40
+    bits of two splitmix64 hashes.  The union of the shards is exactly-once iff the
+    summed digest equals the digest of the expected ids (and no shard saw a duplicate)."""
+    a = np.asarray(ids, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = a + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    m = np.uint64((1 << 40) - 1)
+    return [int(a.size), int(a.sum(dtype=np.uint64)), int((z & m).sum(dtype=np.uint64)),
+            int(((z >> np.uint64(24)) & m).sum(dtype=np.uint64))]
 
 
 # ------------------------------------------------------------------ workloads
@@ -206,8 +258,30 @@ class RrcWorkload:
                                      src_kind=L.SRC_HOST_PINNED if self.host else L.SRC_DEVICE))
         return out
 
+    def source(self, i):
+        """HWC u8 source image of sample id i (for the oracle check)."""
+        k = i % self.pool
+        h, w = (int(x) for x in self.hw[k])
+        return (_read(self.ctx, self.base + int(self.offs[k]), h * w * 3, np.uint8, self.host).reshape(h, w, 3),)
+
+    @staticmethod
+    def pool_bytes_of(pool: int, seed: int) -> int:
+        hw = np.random.default_rng(seed).integers(256, 513, size=(pool, 2))
+        return int(sum((int(h * w * 3) + 255) // 256 * 256 for h, w in hw))
+
     def close(self):
         (self.ctx.host_free if self.host else self.ctx.device_free)(self.base)
+
+
+def _read(ctx, ptr: int, n: int, dtype, host: bool) -> np.ndarray:
+    """n elements at ptr (pinned host: a copy of the view; device: D2H)."""
+    nb = n * np.dtype(dtype).itemsize
+    if host:
+        import ctypes
+        return np.frombuffer((ctypes.c_uint8 * nb).from_address(ptr), dtype=np.uint8).view(dtype).copy()
+    out = np.empty(nb, dtype=np.uint8)
+    ctx.d2h(out, ptr)
+    return out.view(dtype)
 
 
 def img_seg_dims(n: int, seed: int):
@@ -230,9 +304,11 @@ class Img3dWorkload:
     B = 2
 
     def __init__(self, L, ctx, pool: int, host: bool, seed: int, heavy_frac: float = 0.0,
-                 time_scale_us_per_ms: float = 0.0, p_fg: float = 0.0):
+                 time_scale_us_per_ms: float = 0.0, p_fg: float = 0.0, depths=None):
         self.L, self.ctx, self.seed, self.host = L, ctx, seed, host
         self.D, self.cost_ms = img_seg_dims(pool, seed)
+        if depths is not None:                    # explicit volume depths (parity tests)
+            self.D = np.asarray(depths, dtype=int)[:pool]
         self.pool = pool
         self.bufs = []
         for i in range(pool):
@@ -263,6 +339,19 @@ class Img3dWorkload:
                                      spin_us=spin))
         return out
 
+    def source(self, i):
+        """(f32 image, u8 label) volumes of sample id i (for the oracle check)."""
+        k = i % self.pool
+        dims = (int(self.D[k]), 384, 384)
+        vox = int(np.prod(dims))
+        pi, pl = self.bufs[k]
+        return (_read(self.ctx, pi, vox, np.float32, self.host).reshape(dims),
+                _read(self.ctx, pl, vox, np.uint8, self.host).reshape(dims))
+
+    @staticmethod
+    def pool_bytes_of(pool: int, seed: int) -> int:
+        return int(sum(int(d) * 384 * 384 * 5 for d in img_seg_dims(pool, seed)[0]))
+
     def close(self):
         f = self.ctx.host_free if self.host else self.ctx.device_free
         for pi, pl in self.bufs:
@@ -276,10 +365,12 @@ class SpeechWorkload:
     name = "speech"
     B = 64
 
-    def __init__(self, L, ctx, pool: int, host: bool, seed: int):
+    def __init__(self, L, ctx, pool: int, host: bool, seed: int, lens=None):
         self.L, self.ctx, self.host = L, ctx, host
         rng = np.random.default_rng(seed)
         self.lens = rng.integers(30000, 170001, size=pool)
+        if lens is not None:                      # explicit lengths (parity tests)
+            self.lens = np.asarray(lens, dtype=int)[:pool]
         offs = np.concatenate([[0], np.cumsum([(int(n) * 4 + 255) // 256 * 256 for n in self.lens])])
         self.offs = offs
         total = int(offs[-1])
@@ -295,31 +386,86 @@ class SpeechWorkload:
         return [L.sample_desc(i, (int(self.lens[i % self.pool]),), self.base + int(self.offs[i % self.pool]),
                               src_kind=L.SRC_HOST_PINNED if self.host else L.SRC_DEVICE) for i in ids]
 
+    def source(self, i):
+        """f32 waveform of sample id i (for the oracle check)."""
+        k = i % self.pool
+        return (_read(self.ctx, self.base + int(self.offs[k]), int(self.lens[k]), np.float32, self.host),)
+
+    @staticmethod
+    def pool_bytes_of(pool: int, seed: int) -> int:
+        lens = np.random.default_rng(seed).integers(30000, 170001, size=pool)
+        return int(sum((int(n) * 4 + 255) // 256 * 256 for n in lens))
+
     def close(self):
         (self.ctx.host_free if self.host else self.ctx.device_free)(self.base)
 
 
-def make_workload(name, L, ctx, host, seed, args):
-    if name == "speech":
-        return SpeechWorkload(L, ctx, pool=args.pool or 512, host=host, seed=seed)
-    if name == "rrc":
-        return RrcWorkload(L, ctx, pool=args.pool or 1024, host=host, seed=seed)
+def pool_size(workload: str, host: bool, pool_arg: int = 0) -> int:
+    if pool_arg:
+        return pool_arg
+    if workload == "speech":
+        return 512
+    if workload == "rrc":
+        return 1024
     # device pools: 48 volumes, so the touched crop windows (48 x 10.5 MB) exceed the
     # 126 MB L2; pinned-host pools stay at 12 (every window crosses PCIe anyway)
-    vols = args.pool or (12 if host else 48)
+    return 12 if host else 48
+
+
+def make_context(L, workload: str, device: int = 0, workers: int = 16, group: int = 0, seed: int = 1):
+    """The shard context bench.py measures: batch size and launch group of the
+    workload, `workers` in-flight launch groups, enough output slot buffers for every
+    in-flight group plus the batches being consumed.  Returns (ctx, B, group)."""
+    B = BATCH[workload][0]
+    group = group or BATCH[workload][1]
+    slots = max(8, -(-workers * group // B) + 4)
+    ctx = L.Context(device=device, batch_size=B, n_workers=workers, max_group=group,
+                    max_slot_buffers=slots, seed=seed)
+    return ctx, B, group
+
+
+def make_workload(name, L, ctx, host, seed, args):
+    pool = pool_size(name, host, args.pool)
+    if name == "speech":
+        return SpeechWorkload(L, ctx, pool=pool, host=host, seed=seed)
+    if name == "rrc":
+        return RrcWorkload(L, ctx, pool=pool, host=host, seed=seed)
     if name == "img3d":
-        return Img3dWorkload(L, ctx, pool=vols, host=host, seed=seed)
+        return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed)
     if name == "img3d_fg":   # MLPerf RandBalancedCrop: 40% of crops scan the label volume (K2)
-        return Img3dWorkload(L, ctx, pool=vols, host=host, seed=seed, p_fg=0.4)
+        return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed, p_fg=0.4)
     if name == "img3d_heavy":
-        return Img3dWorkload(L, ctx, pool=vols, host=host, seed=seed,
+        return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed,
                              heavy_frac=args.heavy_frac, time_scale_us_per_ms=args.time_scale)
     raise SystemExit(f"unknown workload {name}")
 
 
+WORKLOAD_NAMES = {
+    "rrc": "C2 ImageNet-shaped u8 3x(256..512)^2 -> RRC224+hflip+normalize",
+    "img3d": "C1 KiTS19-shaped 3D crop128^3+flip+brightness+noise+cast",
+    "img3d_fg": "C1 shapes, RandomCrop with MLPerf foreground oversampling 0.4 (K2 label scan + K1)",
+    "img3d_heavy": "C3 heavy-tailed 3D + synthetic trainer",
+    "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT + log-mel (tcgen05 3xTF32) + SpecAugment + splice, batch 64",
+}
+
+
+def bench_config(args, world: int) -> dict:
+    """The `config` object of the JSON line -- identical for both arms (--impl)."""
+    wl = args.workload
+    cls = {"rrc": RrcWorkload, "speech": SpeechWorkload}.get(wl, Img3dWorkload)
+    return {"workload": WORKLOAD_NAMES[wl], "batch": BATCH[wl][0],
+            "launch_group": args.group or BATCH[wl][1], "workers": args.workers,
+            "raw_pool_bytes": cls.pool_bytes_of(pool_size(wl, False, args.pool), args.seed),
+            "l2": "inputs > L2 (pool larger than 126 MB)",
+            "parallelism": f"dp{world} independent loader shards"}
+
+
 # ------------------------------------------------------------------ runs
 def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, policy=0,
-              t_out_us=0, d2h_probe=0):
+              t_out_us=0, d2h_probe=0, capture=None):
+    """Warm-up run, then the timed run (`ids_timed` through lfg_run_shard); the
+    delivered outputs of the feed positions in `capture` are copied out of their
+    batch tensors on the trainer stream (counted in d2h_bytes) for the oracle check."""
     B = wl.B
     rc_w = L.run_config(batch_size=B, t_out_us=t_out_us, policy=policy, trainer_us=trainer_us,
                         n_workers=args.workers, warmup_us=args.profiler_warmup_us,
@@ -331,12 +477,44 @@ def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, 
     c0 = ctx.counters()
     descs = wl.descs(ids_timed)
     t0 = time.perf_counter()
-    rep, ids, bsz, cls = ctx.run_shard(wl.chain, descs, rc_w)
+    rep, ids, bsz, cls = ctx.run_shard(wl.chain, descs, rc_w, capture=capture)
     ctx.synchronize()
     wall = time.perf_counter() - t0
     barrier(dist)
     c1 = ctx.counters()
-    return rep, ids, wall, {k: c1[k] - c0[k] for k in c1}
+    cap = dict(getattr(ctx, "last_capture", {})) if capture else {}
+    return rep, ids, wall, {k: c1[k] - c0[k] for k in c1}, cap
+
+
+def capture_positions(n_timed: int, k: int, seed: int) -> list[int]:
+    """k feed positions among the first 60% of the timed run (their batches are
+    delivered while the rest of the run is still in flight)."""
+    rng = np.random.default_rng(seed + 99)
+    hi = max(1, int(0.6 * n_timed))
+    return sorted(int(x) for x in rng.choice(hi, size=min(k, hi), replace=False))
+
+
+def oracle_check(wl, ids_timed, cap) -> dict:
+    """Verification leg (after the timed region): the captured delivered samples
+    against the CPU oracle (oracle/checks.py; the oracle is the checker only)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import checks
+    import lf_oracle as O
+    seed = wl.ctx.cfg.seed
+    worst, n = 0.0, 0
+    for pos, (raw, _) in sorted(cap.items()):
+        sid = int(ids_timed[pos])
+        src = wl.source(sid)
+        if wl.name == "rrc":
+            r = checks.check_rrc(O, O.cfg2d(), seed, sid, src[0], raw)
+        elif wl.name == "speech":
+            r = checks.check_speech(O, O.cfgsp(), seed, sid, src[0], raw)
+        else:
+            ocfg = O.cfg3d(has_fg=1 if wl.p_fg > 0 else 0, p_fg=wl.p_fg)
+            r = checks.check_img3d(O, ocfg, seed, sid, src[0], src[1], raw, (128, 128, 128))
+        worst = max(worst, r)
+        n += 1
+    return {"samples": n, "worst_err_over_bound": round(worst, 4), "ok": n > 0 and worst <= 1.0}
 
 
 def traffic_of(workload: str):
@@ -439,7 +617,8 @@ def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: i
 
 
 def reference_arm(args):
-    """--impl reference: the reference's own CPU loader on all host cores (rank 0 only)."""
+    """--impl reference: the reference's own CPU loader on all host cores (rank 0 only;
+    the other ranks of a torchrun launch exit 0 without work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -453,12 +632,79 @@ def reference_arm(args):
             "ms_per_step": round(1e3 * B / v, 3) if v else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": wl, "batch": B},
+            "config": bench_config(args, args.gpus),
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": base["cores"],
                              "kind": base["kind"], "sample": base["sample"]},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def measure(args, rank: int, local: int, world: int, dist) -> dict:
+    """One rank's shard: the resident-input run (value), the roofline pass, the
+    pinned-host run (e2e), and the oracle check of samples captured from both runs."""
+    from paper_2509_10712_b200 import lfgpu as L
+    hbm_peak, tf32_peak, peak_src = peaks()
+    ctx, B, group = make_context(L, args.workload, device=local, workers=args.workers,
+                                 group=args.group, seed=args.seed)
+    ids_all = shard_ids(args.warmup + args.steps, B, rank, world)
+    ids_warm, ids_timed = ids_all[: args.warmup * B], ids_all[args.warmup * B:]
+    heavy = args.workload == "img3d_heavy"
+    trainer_us = args.trainer_us if args.trainer_us else (2000 if heavy else 0)
+    cap_pos = capture_positions(len(ids_timed), args.check, args.seed + rank) if args.check else None
+    out = {"group": group}
+
+    # ---- value: inputs resident in HBM
+    wl = make_workload(args.workload, L, ctx, host=False, seed=args.seed, args=args)
+    with ClockSampler(local) as clk:
+        rep, ids, wall, dc, cap = run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local,
+                                            trainer_us=trainer_us, policy=1 if heavy else 0,
+                                            capture=cap_pos)
+    out["clocks"] = clk.summary()
+    if os.environ.get("LFG_BENCH_DIAG"):
+        print(json.dumps({"diag": {"elapsed_ms": rep.elapsed_ms, "wall_s": wall, "kernel_ms": rep.kernel_ms,
+                                   "launches": rep.launches, "batches": rep.batches,
+                                   "inplace": rep.inplace_batches}}), file=sys.stderr, flush=True)
+    out["check_value"] = oracle_check(wl, ids_timed, cap) if cap_pos and rank == 0 else None
+    out["roof"] = dict(kernel_roofline(L, ctx, wl, ids_timed[: min(len(ids_timed), 64 * B if B > 2 else 64)],
+                                       hbm_peak, tf32_peak), peak_source=peak_src)
+    out["pool_bytes"] = int(wl.pool_bytes)
+    wl.close()
+
+    # ---- e2e: inputs in pinned host memory, H2D + a D2H read of every delivered batch
+    wl_h = make_workload(args.workload, L, ctx, host=True, seed=args.seed, args=args)
+    rep_h, ids_h, wall_h, dc_h, cap_h = run_timed(L, ctx, wl_h, ids_warm, ids_timed, args, dist, local,
+                                                  trainer_us=trainer_us, policy=1 if heavy else 0,
+                                                  d2h_probe=1, capture=cap_pos)
+    out["check_e2e"] = oracle_check(wl_h, ids_timed, cap_h) if cap_pos and rank == 0 else None
+    wl_h.close()
+    ctx.close()
+    consumed = ids.tolist()
+    out.update(elapsed_ms=rep.elapsed_ms, timed_samples=rep.timed_samples, e2e_elapsed_ms=rep_h.elapsed_ms,
+               e2e_samples=rep_h.timed_samples, h2d=rep_h.h2d_bytes, d2h=rep_h.d2h_bytes,
+               launches=dc["launches"], idle=rep.consumer_idle_frac if trainer_us else None,
+               samples=rep.samples, fast=rep.fast, slow=rep.slow,
+               dups=int(len(consumed) - len(set(consumed))) + rep.duplicates,
+               digest=id_digest(consumed), digest_e2e=id_digest(ids_h.tolist()), wall=wall)
+    return out
+
+
+def fake_measure(args, rank: int, local: int, world: int, dist) -> dict:
+    """TEST HOOK (LFG_BENCH_FAKE_SHARD=1, CPU tests of the multi-rank plumbing only):
+    stands in for measure() without a GPU -- each rank "delivers" exactly its
+    partition's timed ids; the line it produces carries "fake_shard": true."""
+    B = BATCH[args.workload][0]
+    ids_all = shard_ids(args.warmup + args.steps, B, rank, world)
+    ids_timed = ids_all[args.warmup * B:]
+    if os.environ.get("LFG_BENCH_FAKE_SHARD") == "dup" and rank == world - 1:
+        ids_timed = ids_timed[:-1] + ids_timed[:1]      # one id lost, one delivered twice
+    return {"group": args.group or BATCH[args.workload][1], "clocks": {"sm_mhz": None, "reasons": ["fake"]},
+            "check_value": None, "check_e2e": None, "roof": None, "pool_bytes": 0,
+            "elapsed_ms": 1.0 + rank, "timed_samples": len(ids_timed), "e2e_elapsed_ms": 2.0 + rank,
+            "e2e_samples": len(ids_timed), "h2d": 0, "d2h": 0, "launches": 0, "idle": None,
+            "samples": len(ids_timed), "fast": len(ids_timed), "slow": 0,
+            "dups": len(ids_timed) - len(set(ids_timed)),
+            "digest": id_digest(ids_timed), "digest_e2e": id_digest(ids_timed), "wall": 0.0}
 
 
 def main():
@@ -475,6 +721,7 @@ def main():
     ap.add_argument("--time-scale", type=float, default=10.0, help="spin us per reference ms")
     ap.add_argument("--trainer-us", type=int, default=0)
     ap.add_argument("--profiler-warmup-us", type=int, default=20000)
+    ap.add_argument("--check", type=int, default=8, help="delivered samples checked against the oracle")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()
@@ -482,85 +729,59 @@ def main():
     if args.steps <= 0:
         args.steps = BATCH[args.workload][2]
 
+    rc = launch_ranks(args)          # --gpus N without a launcher: one process per GPU
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         reference_arm(args)
         return
 
-    from paper_2509_10712_b200 import lfgpu as L
     rank, local, world, dist = dist_setup(args.gpus)
-    hbm_peak, tf32_peak, peak_src = peaks()
+    fake = os.environ.get("LFG_BENCH_FAKE_SHARD") in ("1", "dup")
+    r = (fake_measure if fake else measure)(args, rank, local, world, dist)
     B = BATCH[args.workload][0]
-    group = args.group or BATCH[args.workload][1]
-    # enough output slot buffers for every in-flight launch group (+ batches being consumed)
-    slots = max(8, -(-args.workers * group // B) + 4)
-    ctx = L.Context(device=local, batch_size=B, n_workers=args.workers, max_group=group,
-                    max_slot_buffers=slots, seed=args.seed)
-    ids_all = shard_ids(args.warmup + args.steps, B, rank, world)
-    ids_warm, ids_timed = ids_all[: args.warmup * B], ids_all[args.warmup * B:]
-    heavy = args.workload == "img3d_heavy"
-    trainer_us = args.trainer_us if args.trainer_us else (2000 if heavy else 0)
 
-    # ---- value: inputs resident in HBM
-    wl = make_workload(args.workload, L, ctx, host=False, seed=args.seed, args=args)
-    with ClockSampler(local) as clk:
-        rep, ids, wall, dc = run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local,
-                                       trainer_us=trainer_us, policy=1 if heavy else 0)
-    clocks = clk.summary()
-    if os.environ.get("LFG_BENCH_DIAG"):
-        print(json.dumps({"diag": {"elapsed_ms": rep.elapsed_ms, "wall_s": wall, "kernel_ms": rep.kernel_ms,
-                                   "launches": rep.launches, "batches": rep.batches,
-                                   "inplace": rep.inplace_batches}}), file=sys.stderr, flush=True)
-    el_max = allreduce_max(dist, rep.elapsed_ms, local)
-    samples_total = allreduce_sum(dist, [rep.timed_samples], local)[0]
-    value = samples_total / (el_max / 1e3)
-    roof = kernel_roofline(L, ctx, wl, ids_timed[: min(len(ids_timed), 64 * B if B > 2 else 64)],
-                           hbm_peak, tf32_peak)
-    wl.close()
-
-    # ---- e2e: inputs in pinned host memory, H2D + a D2H read of every delivered batch
-    wl_h = make_workload(args.workload, L, ctx, host=True, seed=args.seed, args=args)
-    rep_h, ids_h, wall_h, dc_h = run_timed(L, ctx, wl_h, ids_warm, ids_timed, args, dist, local,
-                                           trainer_us=trainer_us, policy=1 if heavy else 0,
-                                           d2h_probe=1)
-    el_h = allreduce_max(dist, rep_h.elapsed_ms, local)
-    e2e_total = allreduce_sum(dist, [rep_h.timed_samples], local)[0]
-    e2e = e2e_total / (el_h / 1e3)
-    wl_h.close()
-
-    counters = allreduce_sum(dist, [rep.samples, rep.fast, rep.slow, rep.exactly_once,
-                                    rep.duplicates, rep.batches, rep.short_batches], local)
-    ctx.close()
+    # the run's only collectives: max of the device-timed spans, one counter reduce
+    el_max = allreduce_max(dist, r["elapsed_ms"], local)
+    el_h = allreduce_max(dist, r["e2e_elapsed_ms"], local)
+    cnt = allreduce_sum(dist, [r["timed_samples"], r["e2e_samples"], r["samples"], r["fast"], r["slow"],
+                               r["dups"], r["launches"], r["h2d"], r["d2h"]], local)
+    dig = allreduce_sum_i64(dist, r["digest"] + r["digest_e2e"], local)
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
-    cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
+    # exactly-once over the union of the shards (experiment.cpp:396-413): the timed
+    # ids of all ranks are batches warmup*world .. (warmup+steps)*world - 1
+    want = id_digest(range(args.warmup * world * B, (args.warmup + args.steps) * world * B))
+    exactly_once = dig[:4] == want and dig[4:] == want and cnt[5] == 0
+    value = cnt[0] / (el_max / 1e3)
+    e2e = cnt[1] / (el_h / 1e3)
+    cpu = None if (args.no_cpu_baseline or fake) else cpu_baseline(args.workload)
     steps = args.steps
+    checks = [c for c in (r["check_value"], r["check_e2e"]) if c is not None]
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
         "steps": steps, "warmup": args.warmup, "ms_per_step": round(el_max / steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (Philox(seed,id) images/volumes generated on device / pinned host)",
-        "config": {"workload": {"rrc": "C2 ImageNet-shaped u8 3x(256..512)^2 -> RRC224+hflip+normalize",
-                                "img3d": "C1 KiTS19-shaped 3D crop128^3+flip+brightness+noise+cast",
-                                "img3d_fg": "C1 shapes, RandomCrop with MLPerf foreground oversampling 0.4 (K2 label scan + K1)",
-                                "img3d_heavy": "C3 heavy-tailed 3D + synthetic trainer",
-                                "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT + log-mel (tcgen05 3xTF32) + SpecAugment + splice, batch 64"}[args.workload],
-                   "batch": B, "launch_group": group, "workers": args.workers,
-                   "raw_pool_bytes": int(wl.pool_bytes), "l2": "inputs > L2 (pool larger than 126 MB)",
-                   "parallelism": f"dp{world} independent loader shards"},
-        "roofline": dict(roof, peak_source=peak_src),
+        "config": bench_config(args, world),
+        "roofline": r["roof"],
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e, 1), "unit": "samples/s",
-                "h2d_bytes_per_step": int(rep_h.h2d_bytes / max(1, steps)),
-                "d2h_bytes_per_step": int(rep_h.d2h_bytes / max(1, steps))},
-        "clocks": clocks,
-        "gpu_launches": int(dc["launches"]),
-        "consumer_idle_pct": round(100 * rep.consumer_idle_frac, 2) if trainer_us else None,
-        "slow_frac": round(counters[2] / max(1, counters[0]), 4),
-        "exactly_once": bool(counters[3] == world and counters[4] == 0),
-        "wall_s": round(wall, 3),
+                "h2d_bytes_per_step": int(cnt[7] / max(1, steps)),     # whole job (all ranks)
+                "d2h_bytes_per_step": int(cnt[8] / max(1, steps))},
+        "clocks": r["clocks"],
+        "gpu_launches": int(cnt[6]),
+        "consumer_idle_pct": round(100 * r["idle"], 2) if r["idle"] is not None else None,
+        "slow_frac": round(cnt[4] / max(1, cnt[2]), 4),
+        "exactly_once": bool(exactly_once),
+        "checked": bool(checks) and all(c["ok"] for c in checks),
+        "check": {"value_run": r["check_value"], "e2e_run": r["check_e2e"]},
+        "wall_s": round(r["wall"], 3),
     }
+    if fake:
+        line["fake_shard"] = True
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

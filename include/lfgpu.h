@@ -30,8 +30,9 @@
 extern "C" {
 #endif
 
-#define LFG_ABI_VERSION 3   /* 2: run config percentile / scheduler fields, report scheduler fields, lfg_run_shard_source;
-                               3: run config prefetch_factor */
+#define LFG_ABI_VERSION 4   /* 2: run config percentile / scheduler fields, report scheduler fields, lfg_run_shard_source;
+                               3: run config prefetch_factor;
+                               4: run config output capture (capture_pos / capture_buf / ...) */
 
 #define LFG_OK 0
 #define LFG_ERR_INVALID -1
@@ -264,6 +265,20 @@ typedef struct {
     int32_t prefetch_factor;    /* policy 3: at most prefetch_factor x n_workers batches fed ahead of
                                    the oldest unsealed batch (SyncLoaderConfig::prefetch_factor,
                                    baselines.cpp:115-151, pipeline.prefetch_factor); 0 = unbounded */
+    /* Output capture (verification of delivered samples; ABI 4).  When a delivered
+     * batch holds the sample fed at position capture_pos[k] of `samples`, that
+     * sample's output -- exactly as it sits in the delivered batch tensor -- is
+     * copied on the trainer stream to capture_buf + k * capture_stride (pinned host
+     * memory, lfg_host_alloc): img_seg = f32 image then u8 label (the plane bytes
+     * of lfg_chain_info's out_bytes), obj_det = f32 [3, oh, ow], speech = its T'_i
+     * rows of the time-major batch, row-packed ([T'_i, stack * 80] f32).
+     * capture_done[k] (may be NULL) is set to the sample's batch index + 1. */
+    int32_t n_capture;
+    int32_t reserved1;
+    const int64_t* capture_pos;
+    void* capture_buf;
+    int64_t capture_stride;
+    int32_t* capture_done;
 } lfg_run_config;
 
 typedef struct {

@@ -28,14 +28,6 @@ struct lfg_chain {
 
 namespace {
 
-// Launch groups run on up to Context::kStreamPool concurrent streams; with the
-// default of 8 hardware connections, streams alias onto shared queues and a
-// parked slow sample would block unrelated fast ones.  Must precede the CUDA
-// context's creation (it is read once, at context init).
-__attribute__((constructor)) void lfg_set_connections() {
-    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
-}
-
 thread_local std::string g_last_error;
 
 template <typename F>

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace lfg {
@@ -210,11 +211,21 @@ Context::Context(const lfg_config& c) : cfg(c) {
     // Nothing that can implicitly synchronise the device (stream / event /
     // buffer creation) may run inside the shard loop: a blocked host loop
     // would push in-flight samples past t_out.  Pools are created up front.
-    // Stream pool = the hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS = 32,
-    // set when the library loads) minus the seal / aux / trainer streams, so no
-    // two launch groups ever share a queue: a parked (slow) group must not
-    // create a false dependency for the fast groups behind it.
-    for (int i = 0; i < kStreamPool; ++i) {
+    // Stream pool = the hardware work queues minus the seal / aux / trainer
+    // streams (and one spare), so no two launch groups share a queue: a parked
+    // (slow) group must not create a false dependency for the fast groups behind
+    // it.  The queue count is the process's CUDA_DEVICE_MAX_CONNECTIONS (CUDA's
+    // default 8 if unset), which CUDA reads when the device context is created;
+    // the library never sets it -- applications that want up to 28 concurrent
+    // launch groups export CUDA_DEVICE_MAX_CONNECTIONS=32 before their first CUDA
+    // call (bench.py, the tests and the CLI do).  The shard's in-flight group
+    // limit is capped at the pool size.
+    {
+        int conn = 8;
+        if (const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS")) conn = std::atoi(e);
+        stream_pool = std::clamp(conn - 4, 4, kMaxStreamPool);
+    }
+    for (int i = 0; i < stream_pool; ++i) {
         cudaStream_t s;
         cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
         streams_.push_back(s);
@@ -431,7 +442,10 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
         if (c->oh < 1 || c->ow < 2 || c->ow > 256 || (c->ow & 1) || c->oh > 4096)
             fail(LFG_ERR_UNSUPPORTED, "Resize output width must be even and <= 256");
         c->nplanes = 1;
-        c->plane_bytes[0] = int64_t(3) * c->oh * c->ow * 4;
+        // slot stride rounded up to 16 B: K12 gathers in 16-B words (3*oh*ow*4 is
+        // 8 mod 16 when oh is odd and ow = 2 mod 4); the 3 planes fill the first
+        // 3*oh*ow*4 bytes of each slot
+        c->plane_bytes[0] = (int64_t(3) * c->oh * c->ow * 4 + 15) / 16 * 16;
     } else {
         bool splice = false;
         for (int i = 0; i < n; ++i) splice |= ops[i].kind == LFG_OP_FRAME_SPLICING;
@@ -1411,6 +1425,30 @@ void Context::trainer_step(int64_t b, cudaStream_t s, int64_t us) {
         cuda_check(launch_trainer_spin(us * 1000, 1, s), "trainer step");
         counters.launches++;
     }
+}
+
+int64_t Context::capture_sample(int64_t b, int pos, char* dst, int64_t cap_bytes, cudaStream_t s) {
+    BatchRec& br = batch(b);
+    const Chain& c = *br.chain;
+    if (pos < 0 || pos >= br.n) fail(LFG_ERR_INVALID, "capture position out of range");
+    const SlotBuf& buf = bufs_[br.buf];
+    batch_wait_stream(b, s);
+    if (c.fam == FAM_SPEECH) {   // time-major [t_max, n, width]: the sample's rows, packed
+        const int64_t w = int64_t(c.stack) * c.n_mels * 4;
+        const int64_t rows = br.rows[pos];
+        if (rows * w > cap_bytes) fail(LFG_ERR_INVALID, "capture stride too small");
+        cuda_check(cudaMemcpy2DAsync(dst, w, buf.base + pos * w, w * br.n, w, rows, cudaMemcpyDeviceToHost, s),
+                   "capture D2H");
+        return rows * w;
+    }
+    const int64_t p0 = c.plane_bytes[0], p1 = c.nplanes > 1 ? c.plane_bytes[1] : 0;
+    if (p0 + p1 > cap_bytes) fail(LFG_ERR_INVALID, "capture stride too small");
+    cuda_check(cudaMemcpyAsync(dst, buf.base + pos * p0, p0, cudaMemcpyDeviceToHost, s), "capture D2H");
+    if (p1 > 0)
+        cuda_check(cudaMemcpyAsync(dst + p0, buf.base + int64_t(buf.cap) * p0 + pos * p1, p1,
+                                   cudaMemcpyDeviceToHost, s),
+                   "capture D2H");
+    return p0 + p1;
 }
 
 }  // namespace lfg

@@ -231,6 +231,10 @@ public:
     void batch_wait_stream(int64_t b, cudaStream_t s);
     void batch_release(int64_t b, cudaStream_t s, bool readers = true);
     void trainer_step(int64_t b, cudaStream_t s, int64_t us);
+    // Copies the sample at batch position `pos` out of the delivered batch tensor
+    // into pinned host memory on `s` (after the batch is resident there); returns
+    // the bytes copied (lfg_run_config capture layout).
+    int64_t capture_sample(int64_t b, int pos, char* dst, int64_t cap_bytes, cudaStream_t s);
     // samples assigned to slot buffer bi once it stopped accepting new ones; -1 otherwise
     int buf_closed_count(int bi) const {
         const SlotBuf& b = bufs_[bi];
@@ -251,7 +255,10 @@ public:
     // the next run reuses memory that is already faulted in.  Returns whether it did.
     bool recycle_tables();
 
-    static constexpr int kStreamPool = 28;
+    // Launch-group streams: one per hardware work queue the process configured
+    // (CUDA_DEVICE_MAX_CONNECTIONS, read at context creation; see Context()).
+    static constexpr int kMaxStreamPool = 28;
+    int stream_pool = kMaxStreamPool;
     int free_stream_count() const { return static_cast<int>(free_streams_.size()); }
     lfg_counters counters{};
     double prof_group_ns = 0, prof_launch_ns = 0;   // host time in launch_group / kernel launch calls

@@ -23,6 +23,7 @@
 // (img3d_tma_kernel below); the row kernel serves K0-staged windows (skewed
 // rows) and unaligned geometries.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -369,13 +370,16 @@ cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s) {
         const int cw = L.crop[2];
         if (cw % 16 != 0 || cw > 240) return cudaErrorInvalidValue;
         const int smem = tma_smem_bytes(cw);
-        static int occ[17] = {0};   // per cw / 16: resident CTAs per SM
-        int& o = occ[cw / 16];
+        // resident CTAs per SM, per cw / 16 (same on every B200; a benign race between
+        // shard threads: each computes the same value)
+        static std::atomic<int> occ[17];
+        int o = occ[cw / 16].load(std::memory_order_relaxed);
         if (o == 0) {
             int v = 0;
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, img3d_tma_kernel, kTmaThreads, smem);
             if (e != cudaSuccess) return e;
             o = v > 0 ? v : 1;
+            occ[cw / 16].store(o, std::memory_order_relaxed);
         }
         const int64_t total = int64_t(L.n) * L.crop[0] * ((L.crop[1] + kTR - 1) / kTR);
         const int grid = static_cast<int>(std::min<int64_t>(total, int64_t(sm_count()) * o));

@@ -132,6 +132,9 @@ cudaError_t launch_trainer_spin(int64_t ns, int ctas, cudaStream_t s) {
 
 cudaError_t launch_gather(const GatherLaunch& L, cudaStream_t s) {
     if (L.n <= 0) return cudaSuccess;
+    // planes are copied in 16-B words: slot strides are 16-B multiples (chain_create)
+    for (int p = 0; p < L.nplanes; ++p)
+        if (L.plane_bytes[p] & 15) return cudaErrorInvalidValue;
     int64_t words = L.plane_bytes[0] >> 4;
     int gx = (int)((words + 256 * 8 - 1) / (256 * 8));
     if (gx < 1) gx = 1;

@@ -38,6 +38,9 @@ namespace {
 constexpr int kRows = 8;        // 16 measured slower (larger windows cut occupancy)
 constexpr int kThreads = 128;
 constexpr int kMaxSmem = 64 * 1024;
+// load6 reads 12 bytes from (off & ~3): up to 5 bytes past the last staged
+// row's slot, so every window is allocated with this much slack behind it
+constexpr int kSmemSlack = 16;
 
 // PyTorch area_pixel_compute_source_index (align_corners=False, linear), fp64,
 // written with _rn intrinsics so nvcc cannot contract it into an FMA.
@@ -151,7 +154,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
         ylo = __shfl_sync(0xffffffffu, y0, 0);
         const int yhi = __shfl_sync(0xffffffffu, y1, n_rows_out - 1);
         const int nrows = yhi - ylo + 1;
-        staged = nrows * spitch <= smem_bytes;
+        staged = nrows * spitch + kSmemSlack <= smem_bytes;
         if (staged) {
             if (lane == 0) {
                 mbar_init(&stage_bar, 1);
@@ -280,26 +283,25 @@ int rrc2d_smem_bytes(const RrcLaunch& L) {
         const int spitch = ((d.w * 3 + 30) >> 4) << 4;
         need = max(need, rows * spitch);
     }
-    return min(need, kMaxSmem);
+    return min(need, kMaxSmem) + kSmemSlack;
 }
 
 cudaError_t launch_rrc2d(const RrcLaunch& L, cudaStream_t s) {
     if (L.n <= 0) return cudaSuccess;
     if (L.ow > 2 * kThreads || (L.ow & 1)) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(rrc2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kMaxSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    // (the raised shared-memory limit is set per device by warm_rrc2d at context creation)
     const int smem = rrc2d_smem_bytes(L);
     dim3 grid((L.oh + kRows - 1) / kRows, L.n);
     rrc2d_kernel<<<grid, kThreads, smem, s>>>(L, smem);
     return cudaGetLastError();
 }
 
+// Runs on every Context's device at creation: the dynamic shared-memory limit
+// is a per-device (per CUDA context) attribute of the kernel.
 cudaError_t warm_rrc2d() {
+    cudaError_t e = cudaFuncSetAttribute(rrc2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kMaxSmem + kSmemSlack);
+    if (e != cudaSuccess) return e;
     cudaFuncAttributes a;
     return cudaFuncGetAttributes(&a, rrc2d_kernel);
 }

@@ -136,13 +136,6 @@ cudaError_t launch_stage(const StageLaunch& L, cudaStream_t s) {
     }
     const bool bulk = bulk_env >= 0 ? bulk_env != 0 : bytes_all >= 640 * rows_all;
     if (bulk && fits) {
-        static bool attr = false;
-        if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(stage_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 kWarps * kBulkDepth * kBulkBuf);
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
         int64_t gb = (max_rows + kWarps * 4 - 1) / (kWarps * 4);   // ~4 rows per issuing thread
         int gxb = (int)(gb > 4096 ? 4096 : (gb < 1 ? 1 : gb));
         stage_bulk_kernel<<<dim3(gxb, L.n), 32 * kWarps, kWarps * kBulkDepth * kBulkBuf, s>>>(L);
@@ -155,7 +148,12 @@ cudaError_t launch_stage(const StageLaunch& L, cudaStream_t s) {
 }  // namespace lfg
 
 namespace lfg {
+// Runs on every Context's device at creation (the shared-memory limit is a
+// per-device kernel attribute).
 cudaError_t warm_stage() {
+    cudaError_t e = cudaFuncSetAttribute(stage_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kWarps * kBulkDepth * kBulkBuf);
+    if (e != cudaSuccess) return e;
     cudaFuncAttributes a;
     return cudaFuncGetAttributes(&a, stage_kernel);
 }

@@ -133,7 +133,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     // q = delivered batches the trainer has not finished, c = busy fraction of the
     // in-flight slots over the tick (time-integral of inflight / limit)
     const int max_workers = std::max(1, std::min(rc.max_workers > 0 ? rc.max_workers : 2 * n_workers,
-                                                 Context::kStreamPool));
+                                                 ctx.stream_pool));
     if (rc.scheduler) n_workers = std::min(n_workers, max_workers);
     const int64_t sched_tick = rc.sched_tick_us > 0 ? rc.sched_tick_us : 500;
     const double q_max = std::max(1, ctx.cfg.max_slot_buffers);
@@ -164,6 +164,19 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     char* probe = nullptr;
     if (rc.d2h_probe) cuda_check(cudaMallocHost(&probe, 16 * 1024), "probe buffer");
     int64_t probe_bytes = 0;
+    // output capture (verification): feed position -> capture slot
+    std::vector<int32_t> cap_slot;
+    if (rc.n_capture > 0) {
+        if (rc.capture_pos == nullptr || rc.capture_buf == nullptr || rc.capture_stride <= 0)
+            fail(LFG_ERR_INVALID, "capture needs capture_pos, capture_buf and capture_stride");
+        cap_slot.assign(static_cast<size_t>(std::max<int64_t>(n, 0)), -1);
+        for (int k = 0; k < rc.n_capture; ++k) {
+            const int64_t p = rc.capture_pos[k];
+            if (p < 0 || p >= n) fail(LFG_ERR_INVALID, "capture position out of range");
+            cap_slot[static_cast<size_t>(p)] = k;
+            if (rc.capture_done) rc.capture_done[k] = 0;
+        }
+    }
     cudaEvent_t t_start = mk();
     cuda_check(cudaEventRecord(t_start, trainer), "record");
     const auto setup_t0 = std::chrono::steady_clock::now();
@@ -479,6 +492,19 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             } else if (rc.trainer_us > 0 || probe) {
                 ctx.trainer_step(b, trainer, rc.trainer_us);
             }
+            bool captured = false;
+            if (!cap_slot.empty()) {
+                for (size_t q = 0; q < ts.size(); ++q) {
+                    const int k = cap_slot[static_cast<size_t>(ts[q] - tbase)];
+                    if (k < 0) continue;
+                    // batch position: the slot (zero-copy seal) or the seal order (collated)
+                    const int pos = br.in_place ? ctx.tickets[ts[q]].pos : static_cast<int>(q);
+                    probe_bytes += ctx.capture_sample(b, pos, static_cast<char*>(rc.capture_buf) + k * rc.capture_stride,
+                                                      rc.capture_stride, trainer);
+                    if (rc.capture_done) rc.capture_done[k] = static_cast<int32_t>(nbatches + 1);
+                    captured = true;
+                }
+            }
             if (probe) {
                 void* bp = nullptr;
                 int64_t bb = 0;
@@ -500,7 +526,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 cuda_check(cudaEventRecord(ce, trainer), "record consume");
                 consume_q.push_back(ce);
             }
-            ctx.batch_release(b, trainer, rc.trainer_us > 0 || probe != nullptr);
+            ctx.batch_release(b, trainer, rc.trainer_us > 0 || probe != nullptr || captured);
             for (int64_t t : ts) ctx.ticket_release(t);
             ++nbatches;
             if (nbatches == rc.warmup_batches) {

@@ -14,6 +14,7 @@
 // device-measured duration is charged to the virtual clock, exactly like a
 // synthetic cost model, so the reference's deterministic tests apply.
 #include <cmath>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -26,7 +27,11 @@ namespace {
 
 std::mutex g_mu;
 std::vector<lfg_ctx*> g_shards;
-std::map<std::pair<lfg_ctx*, const TransformChain*>, lfg_chain*> g_chains;
+// Compiled chains keyed by context and by the CONTENTS of the device op list
+// (kind, params, size factor, barrier, name), not by the TransformChain's
+// address: a chain destroyed and rebuilt at the same address, or edited after
+// its first use, must never reuse a stale compiled chain.
+std::map<std::pair<lfg_ctx*, std::string>, lfg_chain*> g_chains;
 
 void check(int rc) {
     if (rc == LFG_OK) return;
@@ -46,18 +51,22 @@ lfg_ctx* ctx_of(const Sample& s) {
 }
 
 lfg_chain* compiled(lfg_ctx* ctx, const TransformChain& chain) {
-    std::lock_guard<std::mutex> g(g_mu);
-    auto key = std::make_pair(ctx, &chain);
-    auto it = g_chains.find(key);
-    if (it != g_chains.end()) return it->second;
     std::vector<lfg_op> ops;
     for (const Transform& t : chain.transforms()) {
-        lfg_op o = t.device.op;
+        lfg_op o;
+        std::memset(&o, 0, sizeof(o));   // the key compares bytes: no padding garbage
+        o.kind = t.device.op.kind;
+        for (int k = 0; k < 8; ++k) o.param[k] = t.device.op.param[k];
         o.size_factor = t.size_factor;
         o.barrier = t.barrier;
         std::snprintf(o.name, sizeof(o.name), "%s", t.name.c_str());
         ops.push_back(o);
     }
+    std::lock_guard<std::mutex> g(g_mu);
+    auto key = std::make_pair(ctx, std::string(reinterpret_cast<const char*>(ops.data()),
+                                               ops.size() * sizeof(lfg_op)));
+    auto it = g_chains.find(key);
+    if (it != g_chains.end()) return it->second;
     lfg_chain* h = nullptr;
     check(lfg_chain_create(ctx, ops.data(), static_cast<int>(ops.size()), &h));
     g_chains[key] = h;

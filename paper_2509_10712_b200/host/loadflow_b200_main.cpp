@@ -22,6 +22,7 @@
 // time_scale per batch.  The report follows MetricsReport's fields
 // (metrics.hpp:29-69) with a "gpu" block.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -410,6 +411,9 @@ int usage() {
 }  // namespace
 
 int main(int argc, char** argv) {
+    // the application's choice (the library never sets it): one hardware queue per
+    // launch-group stream, before the first CUDA call creates the device context
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
     try {
         if (argc < 3) return usage();
         const std::string cmd = argv[1];

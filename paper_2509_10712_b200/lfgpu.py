@@ -69,6 +69,10 @@ class Counters(C.Structure):
         ("reserved", C.c_int64 * 4)]
 
 
+_P_i64 = C.POINTER(C.c_int64)
+_P_i32 = C.POINTER(C.c_int32)
+
+
 class RunConfig(C.Structure):
     _fields_ = [("batch_size", C.c_int32), ("policy", C.c_int32), ("t_out_us", C.c_int64),
                 ("warmup_us", C.c_int64), ("update_interval_us", C.c_int64),
@@ -76,7 +80,9 @@ class RunConfig(C.Structure):
                 ("trainer_priority", C.c_int32), ("warmup_batches", C.c_int32),
                 ("record_trace", C.c_int32), ("d2h_probe", C.c_int32), ("percentile", C.c_int32),
                 ("scheduler", C.c_int32), ("max_workers", C.c_int32), ("sched_tick_us", C.c_int64),
-                ("prefetch_factor", C.c_int32)]
+                ("prefetch_factor", C.c_int32), ("n_capture", C.c_int32), ("reserved1", C.c_int32),
+                ("capture_pos", _P_i64), ("capture_buf", C.c_void_p), ("capture_stride", C.c_int64),
+                ("capture_done", _P_i32)]
 
 
 class RunReport(C.Structure):
@@ -435,16 +441,37 @@ class Context:
 
     # whole shard
     def run_shard(self, ch: Chain, descs: Sequence[SampleDesc], rc: RunConfig,
-                  want_ids: bool = True):
+                  want_ids: bool = True, capture: Sequence[int] | None = None):
+        """lfg_run_shard.  ``capture``: feed positions whose delivered outputs are copied
+        out of their batch tensors (lfg_run_config capture); they are returned as
+        ``self.last_capture = {position: (uint8 array, batch index)}``."""
         n = len(descs)
         arr = (SampleDesc * n)(*descs)
         rep = RunReport()
         ids = (C.c_uint64 * max(n, 1))()
         bs = (C.c_int32 * max(n, 1))()
         cls = (C.c_int32 * max(n, 1))()
-        _check(_lib.lfg_run_shard(self.h, ch.handle, arr, n, C.byref(rc), C.byref(rep),
-                                  ids if want_ids else None, bs if want_ids else None,
-                                  cls if want_ids else None))
+        buf = None
+        if capture:
+            _, stride, _ = ch.info()
+            stride = (stride + 255) // 256 * 256
+            pos = (C.c_int64 * len(capture))(*capture)
+            done = (C.c_int32 * len(capture))()
+            buf = self.host_alloc(stride * len(capture))
+            rc.n_capture, rc.capture_pos, rc.capture_buf = len(capture), pos, buf
+            rc.capture_stride, rc.capture_done = stride, done
+        try:
+            _check(_lib.lfg_run_shard(self.h, ch.handle, arr, n, C.byref(rc), C.byref(rep),
+                                      ids if want_ids else None, bs if want_ids else None,
+                                      cls if want_ids else None))
+            if buf is not None:
+                raw = np.ctypeslib.as_array((C.c_uint8 * (stride * len(capture))).from_address(buf))
+                self.last_capture = {int(p): (raw[k * stride:(k + 1) * stride].copy(), int(done[k]) - 1)
+                                     for k, p in enumerate(capture) if done[k] > 0}
+        finally:
+            if buf is not None:
+                rc.n_capture, rc.capture_pos, rc.capture_buf, rc.capture_done = 0, None, None, None
+                self.host_free(buf)
         nb = rep.batches
         return rep, np.array(ids[:n], dtype=np.uint64), np.array(bs[:nb]), np.array(cls[:n])
 

@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# 28 concurrent launch-group streams need 32 hardware queues (read by CUDA at
+# context creation; the library itself never sets it -- engine.cpp Context())
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))

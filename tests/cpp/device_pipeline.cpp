@@ -10,6 +10,7 @@
 // Exit code 0 = exactly-once delivery, fast/slow split as expected, every
 // batch device-sealed.
 #include <cstdio>
+#include <cstdlib>
 #include <set>
 #include <vector>
 
@@ -30,6 +31,7 @@ using namespace loadflow;
     } while (0)
 
 int main() {
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);   // before the first CUDA call
     lfg_config cfg;
     lfg_config_default(&cfg);
     cfg.batch_size = 4;
