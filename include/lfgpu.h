@@ -157,6 +157,11 @@ int lfg_chain_stage(lfg_chain* chain, int s, int* first_op, int* last_op);
 int lfg_draw_params(lfg_chain* chain, uint64_t seed, const lfg_sample_desc* s, double* out,
                     int cap, int* n_out);
 
+/* The per-sample generator itself (host only, no GPU needed): the first n outputs
+ * of std::mt19937_64(seed ^ 0x9e3779b97f4a7c15*(id+1)) as the product draws them
+ * (a lazily seeded, bit-exact evaluation; checked against libstdc++ in the tests). */
+int lfg_rng_outputs(uint64_t seed, uint64_t id, int n, uint64_t* out);
+
 /* ---- submit / progress: replaces process_sample's transform loop
  * (balancer.cpp:42-77) and the worker slot (worker_pool.cpp:63-98).
  * lfg_submit draws the sample's parameters, assigns its output slot and adds
@@ -297,6 +302,8 @@ typedef struct {
     int32_t final_workers;      /* in-flight group limit at the end (scheduler) */
     int32_t sched_ticks;        /* scheduler decisions taken */
     double mean_workers;        /* time-average of the in-flight group limit */
+    int32_t pct_up, pct_down;   /* profiler p75 -> p90 escalations / p90 -> p75 de-escalations (ABI 4) */
+    int64_t profiled;           /* per-sample totals recorded into the profiler window (ABI 4) */
 } lfg_run_report;
 
 /* samples[i] are fed in order (the feeder, experiment.cpp:221-228).

@@ -270,6 +270,13 @@ int lfg_draw_params(lfg_chain* chain, uint64_t seed, const lfg_sample_desc* s, d
     });
 }
 
+int lfg_rng_outputs(uint64_t seed, uint64_t id, int n, uint64_t* out) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && !out)) fail(LFG_ERR_INVALID, "bad output buffer");
+        rng_outputs(seed, id, n, out);
+    });
+}
+
 int lfg_submit(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* s, lfg_ticket* out) {
     return guarded([&] {
         Context& c = C(ctx);
@@ -308,7 +315,8 @@ int lfg_wait(lfg_ctx* ctx, lfg_ticket t) {
         for (int spins = 0;; ++spins) {
             {
                 std::lock_guard<std::mutex> g(c.mu);
-                if (c.poll_group(c.group_of(t))) return;
+                c.group_of(t);   // validates the ticket
+                if (c.sample_ready(t)) return;   // its own stamp, or the whole group
             }
             if (spins < 64) std::this_thread::yield();
             else std::this_thread::sleep_for(std::chrono::microseconds(20));

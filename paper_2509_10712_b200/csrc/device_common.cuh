@@ -54,6 +54,25 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 // ------------------------------------------------------------------ mbarrier / bulk-copy PTX
+// Per-sample completion stamps (the shard classifies samples, not launch groups).
+// Each sample of a group's last stage has a slot: a device counter cnt[slot] and
+// a host-mapped stamp[slot] the host polls.  Every part of the sample's work (a
+// CTA, or a warp's tile) calls this once, from one thread, after its output
+// stores are ordered before it (__syncthreads / __syncwarp): the acq_rel count
+// publishes them device-wide; the part that completes the count resets it (for
+// the slot's next use) and writes %globaltimer | 1 to the host with release
+// semantics at system scope.
+__device__ __forceinline__ void sample_part_done(uint32_t* cnt, uint64_t* stamp, uint32_t parts) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+    if (old + 1 == parts) {
+        *cnt = 0u;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(stamp), "l"(t | 1ull) : "memory");
+    }
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

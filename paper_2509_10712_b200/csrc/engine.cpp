@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <optional>
 
 namespace lfg {
 
@@ -36,8 +37,51 @@ static int64_t rows_touched(int64_t h, int oh);
 // Per-sample generator: the reference's Rng (std::mt19937_64, sample.hpp:25)
 // seeded with experiment.cpp:163's mixing constant keyed by sample id.
 namespace {
+// std::mt19937_64, bit-exact, evaluated lazily.  A sample draws at most a few
+// dozen numbers, but std::mt19937_64 seeds all 312 state words and twists all of
+// them before its first output (~1.3 us).  Output k < 156 depends only on the
+// seeded words k, k + 1 and k + 156 (the twist reads x[k + 156] before it is
+// rewritten), so this generator seeds words on demand (157 + k of them) and
+// twists one word per output; from output 156 on it falls back to the library
+// generator advanced to the same position.
+class LazyMt64 {
+public:
+    explicit LazyMt64(uint64_t seed) : seeded_(1) { x_[0] = seed; }
+    uint64_t operator()() {
+        if (k_ >= kM) {
+            if (!full_) {
+                full_.emplace(x_[0]);
+                full_->discard(static_cast<unsigned long long>(k_));
+            }
+            ++k_;
+            return (*full_)();
+        }
+        const int need = k_ + kM + 1;
+        while (seeded_ < need) {
+            const uint64_t p = x_[seeded_ - 1];
+            x_[seeded_] = 6364136223846793005ULL * (p ^ (p >> 62)) + static_cast<uint64_t>(seeded_);
+            ++seeded_;
+        }
+        const uint64_t y = (x_[k_] & 0xFFFFFFFF80000000ULL) | (x_[k_ + 1] & 0x7FFFFFFFULL);
+        uint64_t z = x_[k_ + kM] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+        ++k_;
+        z ^= (z >> 29) & 0x5555555555555555ULL;
+        z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+        z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+        z ^= z >> 43;
+        return z;
+    }
+
+private:
+    static constexpr int kM = 156;
+    uint64_t x_[312];
+    int seeded_;
+    int k_ = 0;
+    std::optional<std::mt19937_64> full_;
+};
+
 struct SampleRng {
-    std::mt19937_64 g;
+    LazyMt64 g;
     SampleRng(uint64_t seed, uint64_t id) : g(seed ^ (0x9e3779b97f4a7c15ULL * (id + 1ULL))) {}
     double unif01() { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
     int64_t randint(int64_t lo, int64_t hi) {
@@ -194,6 +238,50 @@ int64_t Chain::algo_bytes_per_sample(const lfg_sample_desc& s) const {
     }
 }
 
+// ------------------------------------------------------------------ worker threads
+WorkerThreads::WorkerThreads(int n) {
+    for (int w = 0; w < n; ++w)
+        th_.emplace_back([this, w] {
+            uint64_t seen = 0;
+            for (;;) {
+                std::function<void(int)> f;
+                {
+                    std::unique_lock<std::mutex> l(m_);
+                    cv_.wait(l, [&] { return quit_ || gen_ != seen; });
+                    if (quit_) return;
+                    seen = gen_;
+                    f = job_;
+                }
+                f(w);
+                std::lock_guard<std::mutex> l(m_);
+                if (--busy_ == 0) idle_.notify_all();
+            }
+        });
+}
+
+WorkerThreads::~WorkerThreads() {
+    {
+        std::lock_guard<std::mutex> l(m_);
+        quit_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+}
+
+void WorkerThreads::run(std::function<void(int)> f) {
+    std::lock_guard<std::mutex> l(m_);
+    job_ = std::move(f);
+    busy_ = static_cast<int>(th_.size());
+    ++gen_;
+    cv_.notify_all();
+}
+
+void WorkerThreads::wait() {
+    std::unique_lock<std::mutex> l(m_);
+    idle_.wait(l, [&] { return busy_ == 0; });
+    job_ = nullptr;
+}
+
 // ------------------------------------------------------------------ context
 Context::Context(const lfg_config& c) : cfg(c) {
     if (cfg.n_workers < 1) fail(LFG_ERR_INVALID, "n_workers must be >= 1");
@@ -246,6 +334,17 @@ Context::Context(const lfg_config& c) : cfg(c) {
         cuda_check(cudaEventCreate(&e), "cudaEventCreate");
         free_events_.push_back(e);
     }
+    // per-sample completion stamps: host-mapped words the kernels write, device counters
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&stamp_host_), kStampSlots * sizeof(uint64_t),
+                             cudaHostAllocMapped | cudaHostAllocPortable),
+               "stamp words");
+    std::memset(stamp_host_, 0, kStampSlots * sizeof(uint64_t));
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&stamp_dev_), stamp_host_, 0), "stamp words");
+    cuda_check(cudaMalloc(&stamp_cnt_, kStampSlots * sizeof(uint32_t)), "stamp counters");
+    cuda_check(cudaMemset(stamp_cnt_, 0, kStampSlots * sizeof(uint32_t)), "stamp counters");
+    // draw workers: half the host threads (the shard loop and the trainer keep theirs), <= 16
+    workers = std::make_unique<WorkerThreads>(
+        static_cast<int>(std::clamp(std::thread::hardware_concurrency() / 2, 1u, 16u)));
 }
 
 Context::~Context() {
@@ -259,6 +358,8 @@ Context::~Context() {
         cudaFree(b.base);
     }
     for (auto& r : raws_) cudaFree(r.ptr);
+    if (stamp_host_) cudaFreeHost(stamp_host_);
+    if (stamp_cnt_) cudaFree(stamp_cnt_);
     if (csum_) cudaFree(csum_);
     if (fg_box_) cudaFree(fg_box_);
     if (fg_offs_) cudaFree(fg_offs_);
@@ -729,6 +830,12 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
     }
     // the ticket is built in place (submit runs once per sample)
     const int64_t ti = static_cast<int64_t>(tickets.size());
+    // its completion stamp slot (ticket index mod the ring) must be free: the ticket
+    // that used it last, kStampSlots earlier, has finished
+    if (ti >= kStampSlots && !groups[tickets[ti - kStampSlots].group].complete &&
+        !poll_group(groups[tickets[ti - kStampSlots].group]))
+        fail(LFG_ERR_AGAIN, "completion stamp ring full (a sample 2^20 submissions old is still running)");
+    stamp_host_[ti & (kStampSlots - 1)] = 0;
     tickets.emplace_back();
     Ticket& t = tickets.back();
     t.id = s.id;
@@ -973,10 +1080,20 @@ void Context::launch_group(Group& g) {
         }
     }
 
-    auto launch_spins = [&](int slot) {
+    // The group's last kernel carries the per-sample completion stamps.
+    const StampRef stamps{stamp_cnt_, stamp_dev_};
+    const auto slot_of = [&](int i) { return static_cast<int32_t>(g.tickets[i] & (kStampSlots - 1)); };
+    g.stamped = true;
+    g.got.assign(static_cast<size_t>(n), 0);
+    g.n_got = g.scan_from = 0;
+    auto launch_spins = [&](int slot, bool stamp) {
         SpinLaunch L{};
         L.n = n;
         for (int i = 0; i < n; ++i) L.ns[i] = tickets[g.tickets[i]].desc.spin_us[slot] * 1000;
+        if (stamp) {
+            L.st = stamps;
+            for (int i = 0; i < n; ++i) L.slot[i] = slot_of(i);
+        }
         start();
         cuda_check(launch_spin(L, st), "spin launch");
         counters.launches++;
@@ -984,10 +1101,13 @@ void Context::launch_group(Group& g) {
 
     for (int s = 0; s < nst; ++s) {
         const Stage& S = c.stages[s];
+        // this stage's transform kernel is the group's last kernel
+        const bool stamp_here = s == nst - 1 && S.spin_ops.empty();
         if (S.kind == ST_SPIN) {
-            launch_spins(S.spin_ops[0]);
+            launch_spins(S.spin_ops[0], s == nst - 1);
         } else if (S.kind == ST_IMG3D) {
             Img3dLaunch L{};
+            if (stamp_here) L.st = stamps;
             for (int a = 0; a < 3; ++a) L.crop[a] = c.crop[a];
             L.n = n;
             // TMA tile path: HBM-resident volumes with 16-B aligned rows
@@ -1032,6 +1152,7 @@ void Context::launch_group(Group& g) {
                 }
                 d.contrast = static_cast<float>(t.p3.contrast);
                 d.csum = nullptr;
+                d.slot = slot_of(i);
                 counters.kernel_bytes += img3d_algo_bytes(c, t);
             }
             // RandomCrop foreground oversampling: K2 scans the label volumes of the
@@ -1104,10 +1225,12 @@ void Context::launch_group(Group& g) {
                 L.b[k] = static_cast<float>(-c.mean[k] / c.std[k]);
             }
             L.n = n;
+            if (stamp_here) L.st = stamps;
             for (int i = 0; i < n; ++i) {
                 Ticket& t = tickets[g.tickets[i]];
                 const View& v = views[i];
                 RrcDesc& d = L.d[i];
+                d.slot = slot_of(i);
                 d.src = reinterpret_cast<const uint8_t*>(v.p[0]);
                 d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
                 d.pitch = static_cast<int32_t>(v.py[0]);   // < 2^31: image width <= 65535
@@ -1129,9 +1252,11 @@ void Context::launch_group(Group& g) {
             L.n_fmask = c.n_fmask;
             L.n_tmask = c.n_tmask;
             L.stack = c.stack;
+            if (stamp_here) L.st = stamps;
             for (int i = 0; i < n; ++i) {
                 Ticket& t = tickets[g.tickets[i]];
                 SpDesc& d = L.d[i];
+                d.slot = slot_of(i);
                 d.wav = reinterpret_cast<const float*>(views[i].p[0]);
                 d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
                 d.L = static_cast<int32_t>(t.desc.dims[0]);
@@ -1152,7 +1277,8 @@ void Context::launch_group(Group& g) {
             cuda_check(launch_speech(L, speech_, st), "speech launch");
             counters.launches++;
         }
-        for (int slot : S.spin_ops) launch_spins(slot);
+        for (size_t k = 0; k < S.spin_ops.size(); ++k)
+            launch_spins(S.spin_ops[k], s == nst - 1 && k + 1 == S.spin_ops.size());
         start();
         cuda_check(cudaEventRecord(g.ev[s + 1], st), "record stage end");
     }
@@ -1204,10 +1330,11 @@ void Context::finalize_group_timing(Group& g) {
 void Context::progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed_us) {
     Group& g = group_of(t);
     poll_group(g);
+    const bool done = sample_ready(t);   // its own stamp, or the whole group
     const auto& st = g.chain->stages;
     const int od = g.stages_done > 0 ? st[g.stages_done - 1].last_op : 0;
-    if (ops_done) *ops_done = g.complete ? static_cast<int>(g.chain->ops.size()) : od;
-    if (complete) *complete = g.complete ? 1 : 0;
+    if (ops_done) *ops_done = done ? static_cast<int>(g.chain->ops.size()) : od;
+    if (complete) *complete = done ? 1 : 0;
     if (elapsed_us) *elapsed_us = g.launched ? host_now_us() - g.t_launch_us : 0;
 }
 
@@ -1232,10 +1359,17 @@ void Context::wait(int64_t t) {
 
 int Context::exec_costs(int64_t t, double* out, int cap) {
     Group& g = group_of(t);
-    if (!g.complete) fail(LFG_ERR_STATE, "sample not complete");
+    if (!sample_ready(t)) fail(LFG_ERR_STATE, "sample not complete");
     const int nops = static_cast<int>(g.chain->ops.size());
     if (cap < nops) fail(LFG_ERR_INVALID, "cost buffer too small");
     for (int i = 0; i < nops; ++i) out[i] = 0.0;
+    if (!g.complete) {
+        // the sample finished before its group: no stage events yet, so its cost is
+        // the wall time from the group's launch to now (the realtime runtime's clock),
+        // attributed to the last op
+        out[nops - 1] = static_cast<double>(host_now_us() - g.t_launch_us);
+        return nops;
+    }
     for (size_t s = 0; s < g.stage_ms.size(); ++s)
         out[g.chain->stages[s].last_op - 1] = 1000.0 * g.stage_ms[s];
     return nops;
@@ -1244,7 +1378,7 @@ int Context::exec_costs(int64_t t, double* out, int cap) {
 void Context::ticket_output(int64_t t, void* dst, size_t bytes) {
     Group& g = group_of(t);
     Ticket& tk = tickets[t];
-    if (!g.complete) fail(LFG_ERR_STATE, "sample not complete");
+    if (!sample_ready(t)) fail(LFG_ERR_STATE, "sample not complete");
     if (tk.consumed) fail(LFG_ERR_STATE, "sample already sealed into a batch");
     const Chain& c = *g.chain;
     if (bytes < static_cast<size_t>(c.plane_bytes[0] + (c.nplanes > 1 ? c.plane_bytes[1] : 0)))
@@ -1262,7 +1396,7 @@ void Context::ticket_release(int64_t t) {
     Group& g = group_of(t);
     Ticket& tk = tickets[t];
     if (!tk.consumed) {
-        if (!g.complete) fail(LFG_ERR_STATE, "cannot release an in-flight sample");
+        if (!sample_ready(t)) fail(LFG_ERR_STATE, "cannot release an in-flight sample");
         bufs_[tk.buf].live--;
         tk.consumed = true;
     }
@@ -1281,7 +1415,7 @@ int64_t Context::seal(const int64_t* ts, int n) {
         Ticket& t = tickets[ts[i]];
         if (t.released || t.consumed) fail(LFG_ERR_INVALID, "ticket already sealed or released");
         Group& g = groups[t.group];
-        if (!poll_group(g)) fail(LFG_ERR_STATE, "cannot seal an incomplete sample");
+        if (!sample_ready(ts[i])) fail(LFG_ERR_STATE, "cannot seal an incomplete sample");
         if (c == nullptr) c = g.chain;
         if (g.chain != c) fail(LFG_ERR_INVALID, "batch mixes chains");
         if (t.buf != tickets[ts[0]].buf) same_buf = false;
@@ -1310,7 +1444,8 @@ int64_t Context::seal(const int64_t* ts, int n) {
     for (int i = 0; i < n; ++i) gs.push_back(tickets[ts[i]].group);
     std::sort(gs.begin(), gs.end());
     gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
-    (void)gs;  // all producing groups are complete (checked above): no device wait needed
+    (void)gs;  // every sample is complete (its stamp landed: its outputs are written and
+               // published device-wide) -- no device wait needed
 
     if (in_place) {
         SlotBuf& b = bufs_[b0];
@@ -1374,8 +1509,8 @@ int64_t Context::seal(const int64_t* ts, int n) {
         for (int i = 0; i < n; ++i) bufs_[tickets[ts[i]].buf].live--;
         counters.gathered_batches++;
     }
-    // An in-place batch is ready the moment it is sealed: every producing group
-    // was seen complete above, so there is nothing for a consumer stream to wait on.
+    // An in-place batch is ready the moment it is sealed: every sample was seen
+    // complete above, so there is nothing for a consumer stream to wait on.
     if (!in_place) {
         br.ready = get_event();
         cuda_check(cudaEventRecord(br.ready, seal_stream), "record batch ready");
@@ -1449,6 +1584,11 @@ int64_t Context::capture_sample(int64_t b, int pos, char* dst, int64_t cap_bytes
                                    cudaMemcpyDeviceToHost, s),
                    "capture D2H");
     return p0 + p1;
+}
+
+void rng_outputs(uint64_t seed, uint64_t id, int n, uint64_t* out) {
+    SampleRng r(seed, id);
+    for (int i = 0; i < n; ++i) out[i] = r.g();
 }
 
 }  // namespace lfg

@@ -13,7 +13,10 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <thread>
 #include <deque>
 #include <memory>
 #include <mutex>
@@ -138,6 +141,8 @@ struct PreDraw {
     PreDraw() {}
 };
 void draw_params(const Chain& c, uint64_t seed, const lfg_sample_desc& s, PreDraw& out);
+// the first n outputs of sample `id`'s generator (lfg_rng_outputs)
+void rng_outputs(uint64_t seed, uint64_t id, int n, uint64_t* out);
 int64_t rrc_algo_bytes(const Chain& c, const Params2D& p);
 
 struct SlotBuf {
@@ -173,6 +178,12 @@ struct Group {
     int64_t raw_idx = -1;
     int refs = 0;
     std::vector<float> stage_ms;   // filled once complete
+    // per-sample completion: the group's last kernel writes one stamp per sample
+    // (Context::sample_stamp); the shard delivers samples as their stamps land
+    bool stamped = false;
+    int n_got = 0;                 // samples handed on by the shard
+    int scan_from = 0;             // first sample not yet handed on (in order)
+    std::vector<uint8_t> got;      // per sample: handed on
 };
 
 struct Ticket {
@@ -204,6 +215,28 @@ struct BatchRec {
     bool released = false;
     int t_max = 0;               // speech: padded time length of the batch tensor
     std::vector<int> rows;       // speech: per-sample spliced lengths T'_i
+};
+
+// Host worker threads owned by a context (created once at lfg_open): the shard
+// runner hands them the per-sample parameter draws of each run, so no run pays
+// for spawning threads.  run(f) starts f on every worker; wait() returns once all
+// of them have finished it.
+class WorkerThreads {
+public:
+    explicit WorkerThreads(int n);
+    ~WorkerThreads();
+    int size() const { return static_cast<int>(th_.size()); }
+    void run(std::function<void(int)> f);
+    void wait();
+
+private:
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, idle_;
+    std::function<void(int)> job_;
+    uint64_t gen_ = 0;
+    int busy_ = 0;
+    bool quit_ = false;
 };
 
 class Context {
@@ -247,6 +280,17 @@ public:
 
     // group-level queries used by the shard runner
     Group& group_of(int64_t t);
+    // Per-sample completion stamps: %globaltimer (| 1) written to host-mapped memory
+    // by the group's last kernel when the sample's outputs are complete, else 0.
+    static constexpr int64_t kStampSlots = int64_t(1) << 20;   // ring, indexed by ticket
+    uint64_t sample_stamp(int64_t t) const {
+        return *static_cast<volatile const uint64_t*>(stamp_host_ + (t & (kStampSlots - 1)));
+    }
+    // the sample's outputs are complete (its stamp landed, or its whole group finished)
+    bool sample_ready(int64_t t) {
+        Group& g = groups[tickets[t].group];
+        return g.complete || (g.stamped && sample_stamp(t) != 0) || poll_group(g);
+    }
     bool poll_group(Group& g);          // updates stages_done/complete; true if complete
     void finalize_group_timing(Group& g);
     int64_t open_group_count() const;
@@ -267,6 +311,7 @@ public:
     void time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms, int64_t* launches,
                       int64_t* bytes, int64_t* flops);
     std::mutex mu;   // one lock per context (C ABI calls serialise on it)
+    std::unique_ptr<WorkerThreads> workers;   // parameter draws of shard runs
 
     cudaStream_t seal_stream = nullptr;
     cudaStream_t aux_stream = nullptr;
@@ -278,6 +323,9 @@ public:
 private:
     std::vector<std::unique_ptr<Chain>> chains_;
     SpeechTables* speech_ = nullptr;   // DFT basis + mel tables, created with the first speech chain
+    uint64_t* stamp_host_ = nullptr;   // [kStampSlots] host-mapped pinned completion stamps
+    uint64_t* stamp_dev_ = nullptr;    // the same words' device address
+    uint32_t* stamp_cnt_ = nullptr;    // [kStampSlots] device part counters (self-resetting)
     bool img3d_tma_ = true;            // LFG_IMG3D_TMA=0 forces the row kernel (A/B checks)
     static constexpr int kCsumSlots = 4096;   // RandomContrast crop sums (a ring; stream-ordered)
     double* csum_ = nullptr;

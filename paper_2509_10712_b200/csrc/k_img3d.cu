@@ -131,6 +131,11 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
             __stcs(reinterpret_cast<unsigned int*>(d.out_lbl + vox), l[r]);
         }
     }
+    if (L.st.cnt != nullptr) {   // this CTA's rows of the sample are written
+        __syncthreads();
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, gridDim.x * gridDim.y);
+    }
 }
 
 // ------------------------------------------------------------------ TMA tile path
@@ -179,7 +184,7 @@ struct __align__(16) TileRec {
     int32_t flags;           // bit 0 flip_y, bit 1 flip_w
     int32_t wl0, m;          // realignment: first label word inside the box row, element shift
     float bias;              // affine B (contrast; 0 otherwise)
-    int32_t pad;
+    int32_t slot;            // the sample's completion stamp slot
 };
 static_assert(sizeof(TileRec) == 64, "tile record is one 64-B slot");
 
@@ -248,7 +253,7 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
                 tr.flags = ((d.flip >> 1) & 1) | (((d.flip >> 2) & 1) << 1);
                 tr.wl0 = (d.off[2] & (kPadLbl - 1)) >> 2;
                 tr.m = d.off[2] & 3;
-                tr.pad = 0;
+                tr.slot = d.slot;
                 rec[s] = tr;
                 if (L.debug & 2) {   // profiling switch: no loads
                     mbar_arrive(full + s);
@@ -313,7 +318,11 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);
+        if (lane == 0) {
+            mbar_arrive(empty + s);
+            // one part of per = cd * nyb tiles of the sample is written
+            if (L.st.cnt != nullptr) sample_part_done(L.st.cnt + tr.slot, L.st.stamp + tr.slot, (uint32_t)per);
+        }
     }
 }
 

@@ -133,86 +133,92 @@ __global__ void __launch_bounds__(32 * kZRows, 4) img3d_zoom_kernel(const __grid
     __syncthreads();
 
     const int y = blockIdx.x * kZRows + threadIdx.y;
-    if (y >= ch) return;
-    const int wy = (d.flip & 2) ? ch - 1 - y : y;
-    int y0, y1;
-    double ly0d, ly1d;
-    taps(wy, d.win[1], d.zscale[1], y0, y1, ly0d, ly1d);
-    const float ly0 = (float)ly0d, ly1 = (float)ly1d;
-    const int ny = min(wy * d.win[1] / ch, d.win[1] - 1);
-    // the row part of img_row / lbl_row (-1: outside the source)
-    const int sy0 = off[1] + y0, sy1 = off[1] + y1, syn = off[1] + ny;
-    const int64_t yo0 = sy0 < d.sdim[1] ? sy0 * d.img_py : -1;
-    const int64_t yo1 = sy1 < d.sdim[1] ? sy1 * d.img_py : -1;
-    const int64_t ylo = syn < d.sdim[1] ? syn * d.lbl_py : -1;
-    const int yk0 = sy0 * d.img_sky, yk1 = sy1 * d.img_sky, ylk = syn * d.lbl_sky;
-    const int cw4 = cw >> 2;
-    for (int q = threadIdx.x; q < cw4; q += 32) {
-        float H0[4], H1[4];            // H of the even / odd source plane held
-        int held0 = -1, held1 = -1;
-        // the quad's column taps are re-read from shared memory (4 x 16 B) per build
-        // rather than held across the plane loop: registers decide the occupancy here
-        auto build = [&](int64_t io, int ik, float h[4]) {
-            const float* r0 = (io >= 0 && yo0 >= 0) ? d.img + io + yo0 + ((ik + yk0) & 3) : nullptr;
-            const float* r1 = (io >= 0 && yo1 >= 0) ? d.img + io + yo1 + ((ik + yk1) & 3) : nullptr;
-            const int4 ta = reinterpret_cast<const int4*>(sx_tap)[2 * q];
-            const int4 tb = reinterpret_cast<const int4*>(sx_tap)[2 * q + 1];
-            const float4 wa = reinterpret_cast<const float4*>(sx_w)[2 * q];
-            const float4 wb = reinterpret_cast<const float4*>(sx_w)[2 * q + 1];
-            const int2 t[4] = {make_int2(ta.x, ta.y), make_int2(ta.z, ta.w), make_int2(tb.x, tb.y),
-                               make_int2(tb.z, tb.w)};
-            const float2 w[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w), make_float2(wb.x, wb.y),
-                                 make_float2(wb.z, wb.w)};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float a = r0 ? fmaf(w[k].x, __ldg(r0 + t[k].x), w[k].y * __ldg(r0 + t[k].y)) : 0.0f;
-                const float b = r1 ? fmaf(w[k].x, __ldg(r1 + t[k].x), w[k].y * __ldg(r1 + t[k].y)) : 0.0f;
-                h[k] = fmaf(ly0, a, ly1 * b);
+    if (y < ch) {
+        const int wy = (d.flip & 2) ? ch - 1 - y : y;
+        int y0, y1;
+        double ly0d, ly1d;
+        taps(wy, d.win[1], d.zscale[1], y0, y1, ly0d, ly1d);
+        const float ly0 = (float)ly0d, ly1 = (float)ly1d;
+        const int ny = min(wy * d.win[1] / ch, d.win[1] - 1);
+        // the row part of img_row / lbl_row (-1: outside the source)
+        const int sy0 = off[1] + y0, sy1 = off[1] + y1, syn = off[1] + ny;
+        const int64_t yo0 = sy0 < d.sdim[1] ? sy0 * d.img_py : -1;
+        const int64_t yo1 = sy1 < d.sdim[1] ? sy1 * d.img_py : -1;
+        const int64_t ylo = syn < d.sdim[1] ? syn * d.lbl_py : -1;
+        const int yk0 = sy0 * d.img_sky, yk1 = sy1 * d.img_sky, ylk = syn * d.lbl_sky;
+        const int cw4 = cw >> 2;
+        for (int q = threadIdx.x; q < cw4; q += 32) {
+            float H0[4], H1[4];            // H of the even / odd source plane held
+            int held0 = -1, held1 = -1;
+            // the quad's column taps are re-read from shared memory (4 x 16 B) per build
+            // rather than held across the plane loop: registers decide the occupancy here
+            auto build = [&](int64_t io, int ik, float h[4]) {
+                const float* r0 = (io >= 0 && yo0 >= 0) ? d.img + io + yo0 + ((ik + yk0) & 3) : nullptr;
+                const float* r1 = (io >= 0 && yo1 >= 0) ? d.img + io + yo1 + ((ik + yk1) & 3) : nullptr;
+                const int4 ta = reinterpret_cast<const int4*>(sx_tap)[2 * q];
+                const int4 tb = reinterpret_cast<const int4*>(sx_tap)[2 * q + 1];
+                const float4 wa = reinterpret_cast<const float4*>(sx_w)[2 * q];
+                const float4 wb = reinterpret_cast<const float4*>(sx_w)[2 * q + 1];
+                const int2 t[4] = {make_int2(ta.x, ta.y), make_int2(ta.z, ta.w), make_int2(tb.x, tb.y),
+                                   make_int2(tb.z, tb.w)};
+                const float2 w[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w), make_float2(wb.x, wb.y),
+                                     make_float2(wb.z, wb.w)};
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float a = r0 ? fmaf(w[k].x, __ldg(r0 + t[k].x), w[k].y * __ldg(r0 + t[k].y)) : 0.0f;
+                    const float b = r1 ? fmaf(w[k].x, __ldg(r1 + t[k].x), w[k].y * __ldg(r1 + t[k].y)) : 0.0f;
+                    h[k] = fmaf(ly0, a, ly1 * b);
+                }
+            };
+            for (int z = z_begin; z < z_end; ++z) {
+                const ZPlane& e = sz_tab[z - z_begin];
+                const int z0 = e.z0, z1 = e.z1;
+                // the plane's nearest labels first, so their latency overlaps the builds'
+                const uint8_t* rl = (e.lo >= 0 && ylo >= 0) ? d.lbl + e.lo + ylo + ((e.lk + ylk) & 15) : nullptr;
+                const int4 n4 = reinterpret_cast<const int4*>(sx_near)[q];
+                const int nx[4] = {n4.x, n4.y, n4.z, n4.w};
+                uint32_t lbk[4];
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) lbk[k] = (rl != nullptr && nx[k] >= 0) ? (uint32_t)__ldg(rl + nx[k]) : 0u;
+                // warp-uniform: every lane of the warp is on the same (z, y)
+                if (z0 & 1) {
+                    if (held1 != z0) { build(e.io0, e.ik0, H1); held1 = z0; }
+                    if (z1 != z0 && held0 != z1) { build(e.io1, e.ik1, H0); held0 = z1; }
+                } else {
+                    if (held0 != z0) { build(e.io0, e.ik0, H0); held0 = z0; }
+                    if (z1 != z0 && held1 != z1) { build(e.io1, e.ik1, H1); held1 = z1; }
+                }
+                const bool odd0 = (z0 & 1) != 0, odd1 = (z1 & 1) != 0;
+                const float lz0 = e.lz0, lz1 = e.lz1;
+                float o[4];
+                const uint32_t lb = lbk[0] | (lbk[1] << 8) | (lbk[2] << 16) | (lbk[3] << 24);
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float a = odd0 ? H1[k] : H0[k];
+                    const float b = odd1 ? H1[k] : H0[k];
+                    o[k] = fmaf(A, fmaf(lz0, a, lz1 * b), B);
+                }
+                const int64_t vox = ((int64_t)z * ch + y) * cw + 4 * q;
+                if (noise) {
+                    const uint64_t g = (uint64_t)vox >> 2;
+                    const uint4 rnd =
+                        philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, 0u), d.key0, d.key1);
+                    const float2 z01 = box_muller(rnd.x, rnd.y);
+                    const float2 z23 = box_muller(rnd.z, rnd.w);
+                    o[0] = fmaf(d.sigma, z01.x, o[0]);
+                    o[1] = fmaf(d.sigma, z01.y, o[1]);
+                    o[2] = fmaf(d.sigma, z23.x, o[2]);
+                    o[3] = fmaf(d.sigma, z23.y, o[3]);
+                }
+                __stcs(reinterpret_cast<float4*>(d.out_img + vox), make_float4(o[0], o[1], o[2], o[3]));
+                __stcs(reinterpret_cast<unsigned int*>(d.out_lbl + vox), lb);
             }
-        };
-        for (int z = z_begin; z < z_end; ++z) {
-            const ZPlane& e = sz_tab[z - z_begin];
-            const int z0 = e.z0, z1 = e.z1;
-            // the plane's nearest labels first, so their latency overlaps the builds'
-            const uint8_t* rl = (e.lo >= 0 && ylo >= 0) ? d.lbl + e.lo + ylo + ((e.lk + ylk) & 15) : nullptr;
-            const int4 n4 = reinterpret_cast<const int4*>(sx_near)[q];
-            const int nx[4] = {n4.x, n4.y, n4.z, n4.w};
-            uint32_t lbk[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) lbk[k] = (rl != nullptr && nx[k] >= 0) ? (uint32_t)__ldg(rl + nx[k]) : 0u;
-            // warp-uniform: every lane of the warp is on the same (z, y)
-            if (z0 & 1) {
-                if (held1 != z0) { build(e.io0, e.ik0, H1); held1 = z0; }
-                if (z1 != z0 && held0 != z1) { build(e.io1, e.ik1, H0); held0 = z1; }
-            } else {
-                if (held0 != z0) { build(e.io0, e.ik0, H0); held0 = z0; }
-                if (z1 != z0 && held1 != z1) { build(e.io1, e.ik1, H1); held1 = z1; }
-            }
-            const bool odd0 = (z0 & 1) != 0, odd1 = (z1 & 1) != 0;
-            const float lz0 = e.lz0, lz1 = e.lz1;
-            float o[4];
-            const uint32_t lb = lbk[0] | (lbk[1] << 8) | (lbk[2] << 16) | (lbk[3] << 24);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float a = odd0 ? H1[k] : H0[k];
-                const float b = odd1 ? H1[k] : H0[k];
-                o[k] = fmaf(A, fmaf(lz0, a, lz1 * b), B);
-            }
-            const int64_t vox = ((int64_t)z * ch + y) * cw + 4 * q;
-            if (noise) {
-                const uint64_t g = (uint64_t)vox >> 2;
-                const uint4 rnd =
-                    philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0u, 0u), d.key0, d.key1);
-                const float2 z01 = box_muller(rnd.x, rnd.y);
-                const float2 z23 = box_muller(rnd.z, rnd.w);
-                o[0] = fmaf(d.sigma, z01.x, o[0]);
-                o[1] = fmaf(d.sigma, z01.y, o[1]);
-                o[2] = fmaf(d.sigma, z23.x, o[2]);
-                o[3] = fmaf(d.sigma, z23.y, o[3]);
-            }
-            __stcs(reinterpret_cast<float4*>(d.out_img + vox), make_float4(o[0], o[1], o[2], o[3]));
-            __stcs(reinterpret_cast<unsigned int*>(d.out_lbl + vox), lb);
         }
+    }
+    if (L.st.cnt != nullptr) {   // this CTA's rows of the sample are written
+        __syncthreads();
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, gridDim.x * gridDim.y);
     }
 }
 

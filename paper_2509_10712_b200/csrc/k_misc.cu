@@ -12,9 +12,13 @@ namespace {
 // ports so the spin models latency, not SM occupancy.
 __global__ void spin_kernel(const __grid_constant__ SpinLaunch L) {
     const int64_t ns = L.ns[blockIdx.x];
-    if (threadIdx.x != 0 || ns <= 0) return;
+    if (threadIdx.x != 0) return;
     const uint64_t t0 = globaltimer_ns();
-    while ((int64_t)(globaltimer_ns() - t0) < ns) __nanosleep(1000);
+    while (ns > 0 && (int64_t)(globaltimer_ns() - t0) < ns) __nanosleep(1000);
+    if (L.st.cnt != nullptr) {
+        const int sl = L.slot[blockIdx.x];
+        sample_part_done(L.st.cnt + sl, L.st.stamp + sl, 1u);
+    }
 }
 
 // K13: synthetic trainer step (trainer.cpp:50-51): `ctas` CTAs spin for ns.

@@ -120,6 +120,12 @@ __device__ __forceinline__ void blend_row_l2(const RrcDesc& d, int y, const ColP
     }
 }
 
+// the row loop of one CTA (defined below the kernel)
+__device__ __forceinline__ void blend_rows(const RrcLaunch& L, const RrcDesc& d, const ColPair& cp, int y_begin,
+                                           int n_rows_out, bool staged, int xa, const uint8_t* smem,
+                                           uint64_t* stage_bar, const int2* sched_rows,
+                                           const float (*sched_w)[6]);
+
 __global__ void __launch_bounds__(kThreads)
 rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -237,7 +243,18 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     }
     __syncthreads();   // schedule visible; the mbarrier was initialised before the copies
     staged = yspan[0] != 0;
-    if (xa >= ow) return;
+    if (xa < ow) blend_rows(L, d, cp, y_begin, n_rows_out, staged, xa, smem, &stage_bar, sched_rows, sched_w);
+    if (L.st.cnt != nullptr) {   // this CTA's rows of the sample are written
+        __syncthreads();
+        if (threadIdx.x == 0) sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, gridDim.x);
+    }
+}
+
+__device__ __forceinline__ void blend_rows(const RrcLaunch& L, const RrcDesc& d, const ColPair& cp, int y_begin,
+                                           int n_rows_out, bool staged, int xa, const uint8_t* smem,
+                                           uint64_t* stage_bar, const int2* sched_rows,
+                                           const float (*sched_w)[6]) {
+    const int oh = L.oh, ow = L.ow;
     const int64_t plane = (int64_t)oh * ow;
     float2* o = reinterpret_cast<float2*>(d.out + (int64_t)y_begin * ow + (d.flip ? ow - 2 - xa : xa));
     const int ow2 = ow >> 1;
@@ -249,7 +266,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     float2 E[3], O[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) E[k] = O[k] = make_float2(0.f, 0.f);
-    if (staged) mbar_wait(&stage_bar, 0);
+    if (staged) mbar_wait(stage_bar, 0);
     for (int j = 0; j < n_rows_out; ++j) {
         const int2 lr = sched_rows[j];   // CTA-uniform: no divergence
         if (lr.x >= 0) {

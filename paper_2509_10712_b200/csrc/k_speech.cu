@@ -142,7 +142,11 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
     const int tile = blockIdx.x - L.tile_start[u];
     const int T = d.T;
     const int f0 = tile * kFramesPerCta;
-    if (f0 >= T) return;                                  // CTA-uniform
+    const uint32_t parts = (uint32_t)(L.tile_start[u + 1] - L.tile_start[u]);   // the utterance's CTAs
+    if (f0 >= T) {                                        // CTA-uniform (never, with the launcher's tiling)
+        if (L.st.cnt != nullptr && threadIdx.x == 0) sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, parts);
+        return;
+    }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     uint64_t* full_a = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -385,6 +389,8 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    // this CTA's spliced rows of the utterance are written
+    if (L.st.cnt != nullptr && tid == 0) sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, parts);
 }
 
 // K11: PermuteAudio + Pad: per-sample [T'_i, W] slots -> batch [T'_max, n, W], zero-padded.

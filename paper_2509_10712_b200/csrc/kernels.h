@@ -13,7 +13,7 @@ namespace lfg {
 constexpr int kMax3D = 16;   // img_seg samples per launch group
 constexpr int kMax2D = 256;  // obj_det samples per launch group
 constexpr int kMaxSp = 64;   // speech utterances per launch group
-constexpr int kMaxSpin = 64;
+constexpr int kMaxSpin = 256;   // >= the largest launch group
 constexpr int kMaxGather = 256;
 constexpr int kTapsDft = 320;   // speech: non-zero window taps per frame (the DFT GEMM's K)
 
@@ -22,6 +22,15 @@ constexpr int kTapsDft = 320;   // speech: non-zero window taps per frame (the D
 // For HBM-resident payloads the skews are 0.  For payloads staged from pinned
 // host memory by K0 the skews re-create the source's 16-byte alignment phase,
 // which lets K0 move every row with aligned 16-byte loads and stores.
+
+// ---- per-sample completion stamps (device_common.cuh sample_part_done): the
+// launch of a group's LAST stage carries them; sample i of the launch owns slot
+// d[i].slot (stamp_cnt: device counters, stamp: host-mapped pinned words).
+// Null: no stamps (the group's completion event alone).
+struct StampRef {
+    uint32_t* cnt;
+    uint64_t* stamp;
+};
 
 // ---- K0: strided-box gather from pinned host memory (PCIe) into HBM staging
 struct StageDesc {
@@ -59,6 +68,8 @@ struct Img3dDesc {
     float contrast;          // RandomContrast factor (1 = not applied)
     const double* csum;      // contrast: sum of the (resampled) crop, written by K5 (null: none)
     double zscale[3];        // RandomZoom3D source-index scale win / crop (IEEE division, host)
+    int32_t slot;            // completion stamp slot
+    int32_t pad_;
 };
 // Contrast folded into one affine per sample: out = A * v + B (+ noise), with
 // A = scale * c and B = scale * (1 - c) * mean, mean = csum / crop voxels.
@@ -80,6 +91,7 @@ struct Img3dLaunch {
     const int4* offs;
     int32_t tma;             // 1: every sample has tm_img/tm_lbl (TMA tile path)
     int32_t debug;           // profiling switch (LFG_IMG3D_DEBUG): 1 no stores, 2 no loads
+    StampRef st;             // per-sample completion stamps (null cnt: none)
     Img3dDesc d[kMax3D];
     // TMA path: 3-D tiled maps over the whole source volume (dims W, H, D),
     // box (cw + 16, kImg3dTileRows, 1); out-of-bounds boxes fill zeros, which is
@@ -120,13 +132,15 @@ struct RrcDesc {
     uint16_t h, w;           // crop box size
     uint8_t sk0, sky;        // row skew (only the low 4 bits matter), see above
     uint8_t flip;
-    uint8_t pad[5];
+    uint8_t pad;
+    int32_t slot;            // completion stamp slot
 };
 static_assert(sizeof(RrcDesc) == 32, "RrcDesc layout");
 struct RrcLaunch {
     int32_t oh, ow;
     float a[3], b[3];        // out = v * a_c + b_c  (= (v/255 - mean_c) / std_c)
     int32_t n;
+    StampRef st;
     RrcDesc d[kMax2D];
 };
 
@@ -138,12 +152,15 @@ struct SpDesc {
     int32_t T;               // frames
     int32_t f_lo[2], f_w[2];
     int32_t t_lo[10], t_w[10];
+    int32_t slot;            // completion stamp slot
+    int32_t pad_;
 };
 struct SpLaunch {
     int32_t n;
     int32_t n_fmask, n_tmask;
     int32_t stack;
     int32_t debug;            // profiling switch: 1 builders skip loads, 2 skip MMAs
+    StampRef st;
     int32_t tile_start[kMaxSp + 1];   // CTA prefix sums (flattened grid), filled by the launcher
     SpDesc d[kMaxSp];
 };
@@ -161,7 +178,9 @@ struct SpCollate {
 // ---- K14: synthetic per-sample cost (LightStep / HeavyStep / step_costs)
 struct SpinLaunch {
     int32_t n;
+    StampRef st;
     int64_t ns[kMaxSpin];
+    int32_t slot[kMaxSpin];
 };
 
 // ---- K12: batch collation gather (planar: plane p of sample i -> dst + p*plane_stride + i*plane_bytes[p])

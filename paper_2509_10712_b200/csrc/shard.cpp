@@ -50,9 +50,12 @@ struct Profile {
     bool adaptive = true;   // false: a fixed percentile (policy 2, the C5 sweep)
     double escalate = 0.35, deescalate = 0.15;
 
+    int up = 0, down = 0;
+    int64_t recorded = 0;
     void record(int64_t total_us, bool slow) {
         window.emplace_back(total_us, slow);
         if (window.size() > cap) window.pop_front();
+        ++recorded;
     }
     // Profiler::update_timeout (profiler.cpp:47-72) with nearest-rank percentile (profiler.cpp:13-21)
     int64_t update() {
@@ -63,8 +66,13 @@ struct Profile {
             slow += w.second;
         }
         const double rate = double(slow) / double(window.size());
-        if (adaptive && pct == 75 && rate > escalate) pct = 90;
-        else if (adaptive && pct == 90 && window.size() == cap && rate < deescalate) pct = 75;
+        if (adaptive && pct == 75 && rate > escalate) {
+            pct = 90;
+            ++up;
+        } else if (adaptive && pct == 90 && window.size() == cap && rate < deescalate) {
+            pct = 75;   // only on a full window: hysteresis against flapping
+            ++down;
+        }
         std::sort(totals.begin(), totals.end());
         size_t rank = static_cast<size_t>(std::ceil(pct / 100.0 * double(totals.size())));
         if (rank == 0) rank = 1;
@@ -240,28 +248,91 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         for (float x : g.stage_ms) ms += x;
         return static_cast<int64_t>(std::llround(ms * 1000.0));
     };
-    auto classify = [&](const Group& g, bool is_slow) {
-        for (int64_t t : g.tickets)
-            if (sample_class) sample_class[t - tbase] = is_slow ? 2 : 1;
-        if (is_slow) rep.slow += static_cast<int64_t>(g.tickets.size());
-        else rep.fast += static_cast<int64_t>(g.tickets.size());
+    // Per-sample classification (balancer.cpp:42-77 decides per sample): a sample is
+    // handed on as soon as its completion stamp lands -- fast while its group is
+    // within budget, slow once the group was parked -- so the fast members of a
+    // launch group never wait for a slow one.
+    std::vector<uint8_t> cls(static_cast<size_t>(std::max<int64_t>(n, 0)), 0);   // 1 fast, 2 slow
+    auto hand_on = [&](Group& g, int i, bool is_slow) {
+        g.got[static_cast<size_t>(i)] = is_slow ? 2 : 1;
+        ++g.n_got;
+        const int64_t t = g.tickets[static_cast<size_t>(i)];
+        cls[static_cast<size_t>(t - tbase)] = is_slow ? 2 : 1;
+        if (sample_class) sample_class[t - tbase] = is_slow ? 2 : 1;
+        if (is_slow) ++rep.slow;
+        else ++rep.fast;
+        if (sync) ready_pos[static_cast<size_t>(t - tbase)] = 1;
+        else if (is_slow) slow.push_back(t);
+        else fast_add(t, false);
+    };
+    // stamps in sample order from scan_from; `all` also looks past the first pending one
+    auto scan_stamps = [&](Group& g, bool all, bool is_slow) {
+        const int sz = static_cast<int>(g.tickets.size());
+        const int before = g.n_got;
+        while (g.scan_from < sz &&
+               (g.got[static_cast<size_t>(g.scan_from)] || ctx.sample_stamp(g.tickets[g.scan_from]) != 0)) {
+            if (!g.got[static_cast<size_t>(g.scan_from)]) hand_on(g, g.scan_from, is_slow);
+            ++g.scan_from;
+        }
+        for (int i = g.scan_from + 1; all && i < sz; ++i)
+            if (!g.got[static_cast<size_t>(i)] && ctx.sample_stamp(g.tickets[i]) != 0) hand_on(g, i, is_slow);
+        return g.n_got != before;
+    };
+    const bool profiled = rc.policy == 1 || rc.policy == 2;
+    // the group's last event completed: hand on the rest; per-sample device-timed
+    // totals (the group's event-timed span less the time from the sample's stamp to
+    // the group's last stamp) go to the profiler window, one record per sample as
+    // profiler.cpp:40-45
+    auto finish_group = [&](Group& g, bool parked_group) {
+        const int sz = static_cast<int>(g.tickets.size());
+        const int64_t tot = total_us(g);
+        const bool per = g.stamped && (profiled || t_out < kNoTimeoutUs);
+        uint64_t last = 0;
+        for (int i = 0; per && i < sz; ++i) last = std::max(last, ctx.sample_stamp(g.tickets[i]));
+        for (int i = 0; i < sz; ++i) {
+            int64_t us = tot;
+            if (per) {
+                const uint64_t st = ctx.sample_stamp(g.tickets[i]);
+                if (st != 0 && last >= st) us = std::max<int64_t>(0, tot - static_cast<int64_t>((last - st) / 1000));
+            }
+            if (!g.got[static_cast<size_t>(i)]) hand_on(g, i, parked_group || us > t_out);   // inclusive budget, balancer.cpp:17
+            if (profiled) prof.record(us, g.got[static_cast<size_t>(i)] == 2);
+        }
+        if (nbatches >= rc.warmup_batches) kernel_ms += tot / 1000.0;
+        release_group(g);
     };
 
-    // Parameter prefetch: the per-sample draws (std::mt19937_64 seeding + twist,
-    // ~2 us each) are a pure function of (seed, id, dims), so a host thread pool
-    // draws them ahead of the submit loop, chunk by chunk.
-    constexpr int64_t kChunk = 64;
+    // Parameter prefetch: the per-sample draws (mt19937_64 keyed by id, ~0.5 us each
+    // with the lazily seeded generator) are a pure function of (seed, id, dims), so
+    // the context's worker threads draw them ahead of the submit loop, chunk by
+    // chunk; the first chunks are small so the first launch group is ready soon.
+    // One worker first has the kernel populate the run's fresh ticket storage
+    // (MADV_POPULATE_WRITE leaves contents untouched, so it may run while submit
+    // constructs tickets) instead of the submitting thread taking one page fault
+    // per ~15 tickets.
+    constexpr int64_t kChunk = 32;
     const int64_t n_chunks = (n + kChunk - 1) / kChunk;
     std::vector<PreDraw> pre(static_cast<size_t>(n));
     std::unique_ptr<std::atomic<uint8_t>[]> ready(new std::atomic<uint8_t>[std::max<int64_t>(n_chunks, 1)]);
     for (int64_t i = 0; i < n_chunks; ++i) ready[i].store(0, std::memory_order_relaxed);
     std::atomic<int64_t> next_chunk{0};
     std::atomic<bool> stop_draw{false};
-    const int n_threads = src != nullptr ? 0 : static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>({8, std::max(1u, std::thread::hardware_concurrency()) / 2, n_chunks})));
-    std::vector<std::thread> drawers;
-    for (int t = 0; t < n_threads; ++t) {
-        drawers.emplace_back([&] {
+    uintptr_t pop_lo = 0, pop_hi = 0;
+    if (!std::getenv("LFG_NO_POPULATE")) {   // (A/B switch)
+        const uintptr_t pg = 4096;
+        pop_lo = (reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase) + pg - 1) & ~(pg - 1);
+        pop_hi = reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase + n) & ~(pg - 1);
+        if (pop_hi <= pop_lo + (1u << 20)) pop_lo = pop_hi = 0;
+    }
+    const bool draw = src == nullptr && n > 0;
+    if (draw || pop_hi > pop_lo) {
+        ctx.workers->run([&, draw](int w) {
+            if (w == ctx.workers->size() - 1 && pop_hi > pop_lo) {
+                for (uintptr_t p = pop_lo; p < pop_hi && !stop_draw.load(std::memory_order_relaxed);
+                     p += (1u << 20))   // in 1 MB steps, front first
+                    madvise(reinterpret_cast<void*>(p), std::min<uintptr_t>(1u << 20, pop_hi - p), kMadvPopulateWrite);
+            }
+            if (!draw) return;
             for (;;) {
                 const int64_t ck = next_chunk.fetch_add(1);
                 if (ck >= n_chunks || stop_draw.load(std::memory_order_relaxed)) return;
@@ -271,33 +342,16 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             }
         });
     }
-    struct Joiner {
-        std::vector<std::thread>& th;
+    struct Joiner {   // the workers reference this run's tables: wait for them on every exit path
+        WorkerThreads& w;
         std::atomic<bool>& stop;
+        bool on;
         ~Joiner() {
+            if (!on) return;
             stop.store(true);
-            for (auto& t : th) t.join();
+            w.wait();
         }
-    } joiner{drawers, stop_draw};
-    // (spawned after the draw threads: its page-table work holds the mm lock that
-    // thread creation needs)
-    std::thread populate;
-    if (!std::getenv("LFG_NO_POPULATE")) {   // (A/B switch)
-        const uintptr_t pg = 4096;
-        const uintptr_t lo = (reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase) + pg - 1) & ~(pg - 1);
-        const uintptr_t hi = reinterpret_cast<uintptr_t>(ctx.tickets.data() + tbase + n) & ~(pg - 1);
-        if (hi > lo + (1u << 20))
-            populate = std::thread([lo, hi] {
-                for (uintptr_t p = lo; p < hi; p += (1u << 20))   // in 1 MB steps, front first
-                    madvise(reinterpret_cast<void*>(p), std::min<uintptr_t>(1u << 20, hi - p), kMadvPopulateWrite);
-            });
-    }
-    struct PopulateJoin {
-        std::thread& t;
-        ~PopulateJoin() {
-            if (t.joinable()) t.join();
-        }
-    } populate_join{populate};
+    } joiner{*ctx.workers, stop_draw, draw || pop_hi > pop_lo};
 
     Phases ph;
     const double g_ns0 = ctx.prof_group_ns, l_ns0 = ctx.prof_launch_ns;
@@ -310,36 +364,29 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         bool progressed = false;
         const int64_t now = host_now_us();
 
-        // (1) in-flight groups: finished in budget -> fast; over budget -> slow (parked).
-        // An event query costs ~0.5 us with 32 hardware queues, so the groups are
-        // queried in launch order up to the first unfinished one, and all of them
-        // only every kScanUs (out-of-order finishers are picked up within that);
-        // a group is always queried before it is parked for its timeout.
+        // (1) in-flight groups.  Samples whose completion stamp landed are handed on
+        // (fast: the group is within budget).  A group finished in budget hands on the
+        // rest; over budget, its unfinished samples are slow and the group is parked.
+        // An event query costs ~0.5 us with 32 hardware queues, so groups are queried
+        // in launch order up to the first unfinished one, and all of them only every
+        // kScanUs (out-of-order finishers are picked up within that); a group is
+        // always queried before it is parked for its timeout.  Stamps are plain reads.
         const bool full_scan = now - last_scan_us >= kScanUs;
         if (full_scan) last_scan_us = now;
         bool query = true;
         for (size_t k = 0; k < inflight.size();) {
             Group& g = ctx.groups[inflight[k]];
             const bool over = now - g.t_launch_us > t_out;
-            const bool done = (query || full_scan || over) && ctx.poll_group(g);
+            const int sz = static_cast<int>(g.tickets.size());
+            if (g.stamped && g.n_got < sz && scan_stamps(g, full_scan || over, false)) progressed = true;
+            const bool done = (query || full_scan || over || g.n_got == sz) && ctx.poll_group(g);
             if (!done) query = false;
             bool remove = false;
             if (done) {
-                const int64_t dev_us = total_us(g);
-                const bool is_slow = dev_us > t_out;   // inclusive budget, balancer.cpp:17
-                classify(g, is_slow);
-                for (int64_t t : g.tickets) {
-                    if (sync) ready_pos[static_cast<size_t>(t - tbase)] = 1;
-                    else if (is_slow) slow.push_back(t);
-                    else fast_add(t, false);
-                }
-                prof.record(dev_us, is_slow);
-                if (nbatches >= rc.warmup_batches) kernel_ms += dev_us / 1000.0;
-                release_group(g);
+                finish_group(g, false);
                 remove = true;
             } else if (over) {
-                classify(g, true);
-                parked.push_back(inflight[k]);
+                parked.push_back(inflight[k]);   // its unfinished samples are slow
                 remove = true;
             }
             if (remove) {
@@ -350,16 +397,14 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             }
         }
         ph.lap(Phases::POLL);
-        // (2) parked (slow) groups finishing in the background -> slow list
-        for (size_t k = 0; k < parked.size() && full_scan;) {
+        // (2) parked groups finishing in the background (resume_slow, balancer.cpp:96-113):
+        // their remaining samples reach the slow list as their stamps land
+        for (size_t k = 0; k < parked.size();) {
             Group& g = ctx.groups[parked[k]];
-            if (ctx.poll_group(g)) {
-                for (int64_t t : g.tickets) {
-                    if (sync) ready_pos[static_cast<size_t>(t - tbase)] = 1;
-                    else slow.push_back(t);
-                }
-                prof.record(total_us(g), true);
-                release_group(g);
+            const int sz = static_cast<int>(g.tickets.size());
+            if (g.stamped && g.n_got < sz && scan_stamps(g, full_scan, true)) progressed = true;
+            if ((full_scan || g.n_got == sz) && ctx.poll_group(g)) {
+                finish_group(g, true);
                 parked.erase(parked.begin() + static_cast<long>(k));
                 progressed = true;
             } else {
@@ -473,8 +518,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 if (e.code != LFG_ERR_AGAIN) throw;
                 if (sync) break;   // the batch stays ready; retried next pass
                 for (auto it = ts.rbegin(); it != ts.rend(); ++it) {
-                    const int cls = sample_class ? sample_class[*it - tbase] : 1;
-                    if (cls == 2) slow.push_front(*it);
+                    if (cls[static_cast<size_t>(*it - tbase)] == 2) slow.push_front(*it);
                     else fast_add(*it, true);
                 }
                 break;
@@ -612,6 +656,9 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     rep.consumer_idle_frac = (rc.trainer_us > 0 && el > 0) ? 1.0 - busy / el : 1.0;
     rep.final_t_out_us = static_cast<double>(t_out >= kNoTimeoutUs ? -1 : t_out);
     rep.final_percentile = prof.pct;
+    rep.pct_up = prof.up;
+    rep.pct_down = prof.down;
+    rep.profiled = prof.recorded;
     rep.exactly_once = (all_ids == want && dups == 0) ? 1 : 0;
     rep.duplicates = dups;
     rep.kernel_ms = kernel_ms;

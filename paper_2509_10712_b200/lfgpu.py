@@ -94,7 +94,8 @@ class RunReport(C.Structure):
                 ("final_t_out_us", C.c_double), ("final_percentile", C.c_int32),
                 ("exactly_once", C.c_int32), ("duplicates", C.c_int64), ("kernel_ms", C.c_double),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("launches", C.c_int64),
-                ("final_workers", C.c_int32), ("sched_ticks", C.c_int32), ("mean_workers", C.c_double)]
+                ("final_workers", C.c_int32), ("sched_ticks", C.c_int32), ("mean_workers", C.c_double),
+                ("pct_up", C.c_int32), ("pct_down", C.c_int32), ("profiled", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -122,6 +123,7 @@ _sig = {
     "lfg_chain_stage": ([_vp, C.c_int, _P(C.c_int), _P(C.c_int)], C.c_int),
     "lfg_draw_params": ([_vp, C.c_uint64, _P(SampleDesc), _P(C.c_double), C.c_int,
                          _P(C.c_int)], C.c_int),
+    "lfg_rng_outputs": ([C.c_uint64, C.c_uint64, C.c_int, _P(C.c_uint64)], C.c_int),
     "lfg_submit": ([_vp, _vp, _P(SampleDesc), _P(C.c_int64)], C.c_int),
     "lfg_flush": ([_vp], C.c_int),
     "lfg_progress": ([_vp, C.c_int64, _P(C.c_int), _P(C.c_int), _P(C.c_int64)], C.c_int),
@@ -161,6 +163,13 @@ EXPORTED = tuple(_sig)
 def _check(rc: int):
     if rc != LFG_OK:
         raise LfgError(rc, _lib.lfg_last_error().decode(errors="replace"))
+
+
+def rng_outputs(seed: int, sid: int, n: int) -> np.ndarray:
+    """First n outputs of sample `sid`'s generator (host only)."""
+    out = (C.c_uint64 * max(n, 1))()
+    _check(_lib.lfg_rng_outputs(seed, sid, n, out))
+    return np.array(out[:n], dtype=np.uint64)
 
 
 def device_count() -> int:

@@ -549,6 +549,78 @@ def test_shard_exactly_once_fast_first(lfgpu):
     ctx.close()
 
 
+def test_shard_classifies_per_sample_inside_wide_groups(lfgpu, oracle):
+    """balancer.cpp:42-77 classifies each sample; here 16 samples share one launch
+    group (one kernel per stage) and each sample's last kernel part stamps its own
+    completion, so a group holding a slow sample (a 30 ms HeavyStep, t_out 8 ms)
+    hands its fast members on as soon as they finish: the slow set is exactly the
+    heavy samples, every fast member of a group is delivered before its slow one,
+    and the delivered outputs still match the oracle."""
+    ctx = lfgpu.Context(batch_size=2, n_workers=4, max_group=16, max_slot_buffers=48, seed=SEED)
+    crop = (8, 8, 16)
+    ops = lfgpu.img_seg_ops(crop=crop, p_flip=0.5, p_bright=1.0, p_noise=1.0) + [
+        lfgpu.op(lfgpu.OP_SPIN, "HeavyStep")]
+    ch = ctx.chain(ops)
+    ocfg = oracle.cfg3d(crop=crop, p_flip=0.5, p_bright=1.0, p_noise=1.0)
+    dims = (10, 12, 20)
+    rng = np.random.default_rng(41)
+    img = rng.standard_normal(dims).astype(np.float32)
+    lbl = rng.integers(0, 3, dims, dtype=np.uint8)
+    pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+    n = 64
+    heavy = {3, 9, 14, 21, 40, 47, 50}
+    descs = [lfgpu.sample_desc(i, dims, pi, pl, spin_us=[30_000 if i in heavy else 200]) for i in range(n)]
+    rc = lfgpu.run_config(batch_size=2, t_out_us=8_000, policy=0, n_workers=4)
+    rep, ids, bsz, cls = ctx.run_shard(ch, descs, rc, capture=list(range(n)))
+    assert rep.exactly_once == 1 and sorted(ids.tolist()) == list(range(n))
+    assert {i for i in range(n) if cls[i] == 2} == heavy and rep.slow == len(heavy)
+    pos = {int(s): k for k, s in enumerate(ids)}
+    for h in heavy:
+        mates = [i for i in range(16 * (h // 16), 16 * (h // 16) + 16) if i not in heavy]
+        assert all(pos[m] < pos[h] for m in mates), f"a fast member of {h}'s group waited for it"
+    vox = int(np.prod(crop))
+    for p_, (raw, _) in ctx.last_capture.items():
+        (e_img, e_lbl), _ = oracle.chain3d(ocfg, SEED, p_, img, lbl)
+        assert np.array_equal(raw[vox * 4: vox * 5].reshape(crop), e_lbl)
+        _assert_close(raw[: vox * 4].view(np.float32).reshape(crop), e_img, atol=1e-6)
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
+def test_device_profiler_escalates_and_deescalates(lfgpu):
+    """The device profiler (policy 1) on per-sample device-timed totals, as the
+    reference Profiler (test_profiler.cpp:83-115, profiler.cpp:47-72): with 60% of
+    samples over the initial budget the slow rate exceeds 0.35 and t_out escalates
+    from p75 to p90; once a full window of fast records follows, it falls back to
+    p75.  One record per sample."""
+    ctx = lfgpu.Context(batch_size=4, n_workers=8, max_group=4, max_slot_buffers=40, seed=SEED)
+    crop = (8, 8, 16)
+    ch = ctx.chain(lfgpu.img_seg_ops(crop=crop) + [lfgpu.op(lfgpu.OP_SPIN, "HeavyStep")])
+    dims = (10, 10, 20)
+    rng = np.random.default_rng(43)
+    pi = _upload(ctx, rng.standard_normal(dims).astype(np.float32))
+    pl = _upload(ctx, rng.integers(0, 3, dims, dtype=np.uint8))
+    rc = lfgpu.run_config(batch_size=4, policy=1, t_out_us=1_000, warmup_us=0, update_interval_us=1_000,
+                          window=40, n_workers=8)
+    # (a) 60% heavy throughout: escalation
+    descs = [lfgpu.sample_desc(i, dims, pi, pl, spin_us=[3_000 if i % 5 < 3 else 100]) for i in range(200)]
+    rep, ids, _, _ = ctx.run_shard(ch, descs, rc)
+    assert rep.exactly_once == 1 and rep.profiled == 200
+    assert rep.pct_up >= 1, rep.as_dict()
+    # (b) a heavy phase, then a long light phase that refills the window with fast records
+    descs = [lfgpu.sample_desc(1000 + i, dims, pi, pl, spin_us=[3_000 if (i < 40 and i % 5 < 3) else 150])
+             for i in range(1240)]
+    rep, ids, _, _ = ctx.run_shard(ch, descs, rc)
+    assert rep.exactly_once == 1 and rep.profiled == 1240
+    assert rep.pct_up >= 1 and rep.pct_down >= 1 and rep.final_percentile == 75, rep.as_dict()
+    ctx.device_free(pi)
+    ctx.device_free(pl)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
 # ------------------------------------------------------------------ reference-shaped C++ API
 def test_cpp_api_device_pipeline():
     """process_sample / resume_slow / build_batches / run_consumer (the reference
