@@ -279,7 +279,10 @@ typedef struct {
      * rows of the time-major batch, row-packed ([T'_i, stack * 80] f32).
      * capture_done[k] (may be NULL) is set to the sample's batch index + 1. */
     int32_t n_capture;
-    int32_t reserved1;
+    int32_t sample_stamps;      /* 1: the transform kernels stamp each sample's completion, so the shard
+                                   classifies and hands on per sample inside a launch group (costs a
+                                   release fence per kernel part); 0: per sample only where the group's
+                                   last kernel is a synthetic cost (always) or per sub-launch */
     const int64_t* capture_pos;
     void* capture_buf;
     int64_t capture_stride;

@@ -582,8 +582,16 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
 }
 
 void Context::chain_destroy(Chain* c) {
-    for (auto& g : groups)
-        if (g.chain == c && !g.complete) fail(LFG_ERR_STATE, "chain has samples in flight");
+    for (auto& g : groups) {
+        if (g.chain != c || g.complete || poll_group(g)) continue;
+        // a group whose samples all completed (stamps) may still be retiring its last
+        // kernel: wait for it; a group with unfinished samples is a caller error
+        bool ready = g.launched;
+        for (int64_t t : g.tickets) ready = ready && sample_ready(t);
+        if (!ready) fail(LFG_ERR_STATE, "chain has samples in flight");
+        cuda_check(cudaEventSynchronize(g.ev.back()), "group completion");
+        poll_group(g);
+    }
     for (size_t i = 0; i < chains_.size(); ++i) {
         if (chains_[i].get() == c) {
             open_buf_.erase(c);
@@ -1083,7 +1091,10 @@ void Context::launch_group(Group& g) {
     // The group's last kernel carries the per-sample completion stamps.
     const StampRef stamps{stamp_cnt_, stamp_dev_};
     const auto slot_of = [&](int i) { return static_cast<int32_t>(g.tickets[i] & (kStampSlots - 1)); };
-    g.stamped = true;
+    {
+        const Stage& last = c.stages.back();
+        g.stamped = last.kind == ST_SPIN || !last.spin_ops.empty() || stamp_transforms;
+    }
     g.got.assign(static_cast<size_t>(n), 0);
     g.n_got = g.scan_from = 0;
     auto launch_spins = [&](int slot, bool stamp) {
@@ -1101,8 +1112,8 @@ void Context::launch_group(Group& g) {
 
     for (int s = 0; s < nst; ++s) {
         const Stage& S = c.stages[s];
-        // this stage's transform kernel is the group's last kernel
-        const bool stamp_here = s == nst - 1 && S.spin_ops.empty();
+        // this stage's transform kernel is the group's last kernel (and stamps)
+        const bool stamp_here = s == nst - 1 && S.spin_ops.empty() && stamp_transforms;
         if (S.kind == ST_SPIN) {
             launch_spins(S.spin_ops[0], s == nst - 1);
         } else if (S.kind == ST_IMG3D) {

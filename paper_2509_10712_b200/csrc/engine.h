@@ -308,6 +308,14 @@ public:
     double prof_group_ns = 0, prof_launch_ns = 0;   // host time in launch_group / kernel launch calls
     bool serial = false;
     bool defer_launch = false;
+    // Per-sample completion stamps.  A group whose last kernel is a synthetic cost
+    // (K14 spin: LightStep / HeavyStep, workloads.cpp:109-110) always stamps its
+    // samples (one CTA per sample, nothing to fence).  The transform kernels stamp
+    // only when this is set (lfg_run_config.sample_stamps): there every kernel part
+    // pays a release fence (its output stores acknowledged before the count),
+    // ~30% of K1 / K3 time, so by default a transform-last group completes as a
+    // whole -- or per sub-launch, as the foreground-crop split does (see launch_group).
+    bool stamp_transforms = false;
     void time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms, int64_t* launches,
                       int64_t* bytes, int64_t* flops);
     std::mutex mu;   // one lock per context (C ABI calls serialise on it)

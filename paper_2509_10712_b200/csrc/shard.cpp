@@ -205,6 +205,13 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     const bool sync = rc.policy == 3;
     int64_t t_out = (rc.t_out_us > 0 && !sync) ? rc.t_out_us : kNoTimeoutUs;
     std::vector<char> ready_pos(sync ? static_cast<size_t>(n) : 0, 0);
+    // per-sample completion stamps from the transform kernels too (sample_stamps = 1)
+    struct StampMode {
+        Context& c;
+        bool saved;
+        ~StampMode() { c.stamp_transforms = saved; }
+    } stamp_mode{ctx, ctx.stamp_transforms};
+    ctx.stamp_transforms = rc.sample_stamps == 1;
     int64_t sync_next = 0;   // first position of the next batch to seal
     const int64_t run_t0 = host_now_us();
     int64_t last_update = run_t0;
@@ -615,6 +622,22 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             std::this_thread::yield();
         }
         ph.lap(Phases::IDLE);
+    }
+    // every sample is consumed; groups whose samples were all handed on by their
+    // stamps may still be finishing their last kernel: complete them
+    while (!inflight.empty() || !parked.empty()) {
+        for (auto* lst : {&inflight, &parked}) {
+            for (size_t k = 0; k < lst->size();) {
+                Group& g = ctx.groups[(*lst)[k]];
+                if (ctx.poll_group(g)) {
+                    finish_group(g, lst == &parked);
+                    lst->erase(lst->begin() + static_cast<long>(k));
+                } else {
+                    ++k;
+                }
+            }
+        }
+        if (!inflight.empty() || !parked.empty()) std::this_thread::yield();
     }
     ph.print(n, ctx.prof_group_ns - g_ns0, ctx.prof_launch_ns - l_ns0,
              static_cast<int64_t>(ctx.groups.size() - groups0));

@@ -80,7 +80,7 @@ class RunConfig(C.Structure):
                 ("trainer_priority", C.c_int32), ("warmup_batches", C.c_int32),
                 ("record_trace", C.c_int32), ("d2h_probe", C.c_int32), ("percentile", C.c_int32),
                 ("scheduler", C.c_int32), ("max_workers", C.c_int32), ("sched_tick_us", C.c_int64),
-                ("prefetch_factor", C.c_int32), ("n_capture", C.c_int32), ("reserved1", C.c_int32),
+                ("prefetch_factor", C.c_int32), ("n_capture", C.c_int32), ("sample_stamps", C.c_int32),
                 ("capture_pos", _P_i64), ("capture_buf", C.c_void_p), ("capture_stride", C.c_int64),
                 ("capture_done", _P_i32)]
 
@@ -564,7 +564,7 @@ def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: 
                update_interval_us: int = 1000, window: int = 1024,
                trainer_priority: int = 1, d2h_probe: int = 0, percentile: int = 75,
                scheduler: int = 0, max_workers: int = 0, sched_tick_us: int = 0,
-               prefetch_factor: int = 0) -> RunConfig:
+               prefetch_factor: int = 0, sample_stamps: int = 0) -> RunConfig:
     rc = RunConfig()
     rc.batch_size = batch_size
     rc.policy = policy
@@ -582,4 +582,5 @@ def run_config(batch_size: int, t_out_us: int = 0, policy: int = 0, trainer_us: 
     rc.max_workers = max_workers
     rc.sched_tick_us = sched_tick_us
     rc.prefetch_factor = prefetch_factor
+    rc.sample_stamps = sample_stamps
     return rc

@@ -589,6 +589,67 @@ def test_shard_classifies_per_sample_inside_wide_groups(lfgpu, oracle):
     ctx.close()
 
 
+@pytest.mark.parametrize("family", ["img3d_tma", "img3d_rows", "rrc", "speech"])
+def test_transform_kernel_stamps(lfgpu, oracle, family):
+    """lfg_run_config.sample_stamps = 1: the transform kernels themselves stamp every
+    sample (per-CTA / per-tile release + count) inside launch groups of 16; the shard
+    hands samples on one by one, and every delivered output still matches the oracle."""
+    B = 2 if family.startswith("img3d") else 4
+    ctx = lfgpu.Context(batch_size=B, n_workers=4, max_group=16, max_slot_buffers=48, seed=SEED)
+    rng = np.random.default_rng(47)
+    bufs, descs, check = [], [], {}
+    if family.startswith("img3d"):
+        crop = (16, 16, 32)
+        ch = ctx.chain(lfgpu.img_seg_ops(crop=crop, p_flip=0.5, p_bright=1.0, p_noise=1.0))
+        ocfg = oracle.cfg3d(crop=crop, p_flip=0.5, p_bright=1.0, p_noise=1.0)
+        dims = (20, 24, 48) if family == "img3d_tma" else (20, 24, 40)
+        img = rng.standard_normal(dims).astype(np.float32)
+        lbl = rng.integers(0, 3, dims, dtype=np.uint8)
+        pi, pl = _upload(ctx, img), _upload(ctx, lbl)
+        bufs += [pi, pl]
+        vox = int(np.prod(crop))
+        descs = [lfgpu.sample_desc(i, dims, pi, pl) for i in range(48)]
+
+        def check(i, raw):
+            (e_img, e_lbl), _ = oracle.chain3d(ocfg, SEED, i, img, lbl)
+            assert np.array_equal(raw[vox * 4: vox * 5].reshape(crop), e_lbl)
+            _assert_close(raw[: vox * 4].view(np.float32).reshape(crop), e_img, atol=1e-6)
+    elif family == "rrc":
+        ch = ctx.chain(lfgpu.obj_det_ops())
+        ocfg = oracle.cfg2d()
+        imgs = [rng.integers(0, 256, (int(h), int(w), 3), dtype=np.uint8)
+                for h, w in rng.integers(200, 400, (48, 2))]
+        for i, im in enumerate(imgs):
+            p = _upload(ctx, im)
+            bufs.append(p)
+            descs.append(lfgpu.sample_desc(i, im.shape, p))
+
+        def check(i, raw):
+            e, _ = oracle.chain2d(ocfg, SEED, i, imgs[i])
+            _assert_close(raw[: 3 * 224 * 224 * 4].view(np.float32).reshape(3, 224, 224), e, atol=1e-5)
+    else:
+        import checks
+        ch = ctx.chain(lfgpu.speech_ops(max_len=40000))
+        ocfg = oracle.cfgsp()
+        waves = [(0.3 * rng.standard_normal(int(L))).astype(np.float32) for L in rng.integers(1000, 40000, 48)]
+        for i, w in enumerate(waves):
+            p = _upload(ctx, w)
+            bufs.append(p)
+            descs.append(lfgpu.sample_desc(i, w.shape, p))
+
+        def check(i, raw):
+            assert checks.check_speech(oracle, ocfg, SEED, i, waves[i], raw) <= 1.0
+    rc = lfgpu.run_config(batch_size=B, n_workers=4, sample_stamps=1)
+    rep, ids, _, _ = ctx.run_shard(ch, descs, rc, capture=list(range(len(descs))))
+    assert rep.exactly_once == 1 and len(ctx.last_capture) == len(descs)
+    for i, (raw, _) in ctx.last_capture.items():
+        check(i, raw)
+    for p in bufs:
+        ctx.device_free(p)
+    ctx.destroy_chain(ch)
+    ctx.close()
+
+
 def test_device_profiler_escalates_and_deescalates(lfgpu):
     """The device profiler (policy 1) on per-sample device-timed totals, as the
     reference Profiler (test_profiler.cpp:83-115, profiler.cpp:47-72): with 60% of
