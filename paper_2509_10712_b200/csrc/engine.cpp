@@ -746,6 +746,7 @@ struct Box {
     const char* src;
     int64_t src_py, src_pz;
     int32_t row_bytes, ny, nz;
+    int plane;               // 0: image / primary payload, 1: label
     int64_t dst_py() const { return 16 * ((static_cast<int64_t>(row_bytes) + 30) / 16); }
     int64_t bytes() const { return dst_py() * ny * nz; }
 };
@@ -755,26 +756,38 @@ static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) 
     wd[0] = wd[1] = wd[2] = 0;
     if (c.fam == FAM_IMG3D) {
         const int64_t H = s.dims[1], W = s.dims[2];
-        // a foreground-biased crop's window depends on the label scan: stage the whole volume
-        const bool whole = c.has_fg && t.p3.fg;
-        for (int a = 0; a < 3; ++a)
-            wd[a] = whole ? s.dims[a] : std::min<int64_t>(t.p3.win[a], s.dims[a] - t.p3.off[a]);
-        const int64_t first = whole ? 0 : (t.p3.off[0] * H + t.p3.off[1]) * W + t.p3.off[2];
+        if (c.has_fg && t.p3.fg) {
+            // a foreground-biased crop's window depends on the label scan: stage the
+            // label volume only; K0w pulls the image window once K2 resolved it
+            for (int a = 0; a < 3; ++a) wd[a] = s.dims[a];
+            out[0] = Box{static_cast<const char*>(s.aux), W, H * W, static_cast<int32_t>(W),
+                         static_cast<int32_t>(H), static_cast<int32_t>(s.dims[0]), 1};
+            return 1;
+        }
+        for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(t.p3.win[a], s.dims[a] - t.p3.off[a]);
+        const int64_t first = (t.p3.off[0] * H + t.p3.off[1]) * W + t.p3.off[2];
         out[0] = Box{static_cast<const char*>(s.data) + first * 4, W * 4, H * W * 4,
                      static_cast<int32_t>(wd[2] * 4), static_cast<int32_t>(wd[1]),
-                     static_cast<int32_t>(wd[0])};
+                     static_cast<int32_t>(wd[0]), 0};
         out[1] = Box{static_cast<const char*>(s.aux) + first, W, H * W, static_cast<int32_t>(wd[2]),
-                     static_cast<int32_t>(wd[1]), static_cast<int32_t>(wd[0])};
+                     static_cast<int32_t>(wd[1]), static_cast<int32_t>(wd[0]), 1};
         return 2;
     }
     if (c.fam == FAM_RRC2D) {
         const int64_t W = s.dims[1];
         out[0] = Box{static_cast<const char*>(s.data) + (t.p2.top * W + t.p2.left) * 3, W * 3, 0,
-                     static_cast<int32_t>(t.p2.w * 3), static_cast<int32_t>(t.p2.h), 1};
+                     static_cast<int32_t>(t.p2.w * 3), static_cast<int32_t>(t.p2.h), 1, 0};
         return 1;
     }
-    out[0] = Box{static_cast<const char*>(s.data), 0, 0, static_cast<int32_t>(s.dims[0] * 4), 1, 1};
+    out[0] = Box{static_cast<const char*>(s.data), 0, 0, static_cast<int32_t>(s.dims[0] * 4), 1, 1, 0};
     return 1;
+}
+
+// a foreground-crop sample's compact window (K0w): image rows padded to 4 floats,
+// label rows to 16 bytes
+static int64_t fg_window_bytes(const Params3D& p) {
+    const int64_t rows = p.win[0] * p.win[1];
+    return align256(4 * rows * ((p.win[2] + 3) / 4 * 4)) + align256(rows * ((p.win[2] + 15) / 16 * 16));
 }
 
 int64_t Context::stage_raw_bytes(const Chain& c, const Ticket& t) const {
@@ -783,6 +796,7 @@ int64_t Context::stage_raw_bytes(const Chain& c, const Ticket& t) const {
     const int nb = boxes_of(c, t, b, wd);
     int64_t total = 0;
     for (int i = 0; i < nb; ++i) total += align256(b[i].bytes());
+    if (c.fam == FAM_IMG3D && c.has_fg && t.p3.fg) total += fg_window_bytes(t.p3);
     return total;
 }
 
@@ -1019,7 +1033,9 @@ void Context::launch_group(Group& g) {
             Box b[2];
             int64_t wd[3];
             const int nb = boxes_of(c, t, b, wd);
+            v.p[0] = v.p[1] = nullptr;
             for (int k = 0; k < nb; ++k) {
+                const int pl = b[k].plane;
                 StageDesc& d = SL.d[SL.n++];
                 d.src = b[k].src;
                 d.dst = dst;
@@ -1031,17 +1047,23 @@ void Context::launch_group(Group& g) {
                 d.ny = b[k].ny;
                 d.nz = b[k].nz;
                 const uintptr_t sa = reinterpret_cast<uintptr_t>(b[k].src);
-                const int esz = (c.fam == FAM_IMG3D && k == 0) ? 4 : 1;  // skew unit
-                v.p[k] = dst;
-                v.py[k] = d.dst_py / esz;
-                v.pz[k] = d.dst_pz / esz;
-                v.sk0[k] = static_cast<int32_t>((sa & 15) / esz);
-                v.sky[k] = static_cast<int32_t>((b[k].src_py & 15) / esz);
-                v.skz[k] = static_cast<int32_t>((b[k].src_pz & 15) / esz);
+                const int esz = (c.fam == FAM_IMG3D && pl == 0) ? 4 : 1;  // skew unit
+                v.p[pl] = dst;
+                v.py[pl] = d.dst_py / esz;
+                v.pz[pl] = d.dst_pz / esz;
+                v.sk0[pl] = static_cast<int32_t>((sa & 15) / esz);
+                v.sky[pl] = static_cast<int32_t>((b[k].src_py & 15) / esz);
+                v.skz[pl] = static_cast<int32_t>((b[k].src_pz & 15) / esz);
                 counters.h2d_bytes += static_cast<int64_t>(b[k].row_bytes) * b[k].ny * b[k].nz;
                 dst += align256(b[k].bytes());
             }
             const bool whole = c.fam == FAM_IMG3D && c.has_fg && t.p3.fg;   // see boxes_of
+            if (whole) {   // the K0w compact window follows the staged label volume
+                v.p[0] = dst;
+                v.py[0] = v.pz[0] = 0;
+                v.sk0[0] = v.sky[0] = v.skz[0] = 0;
+                dst += fg_window_bytes(t.p3);
+            }
             for (int a = 0; a < 3; ++a) {
                 v.sdim[a] = wd[a];
                 v.off[a] = whole ? t.p3.off[a] : 0;
@@ -1097,6 +1119,10 @@ void Context::launch_group(Group& g) {
     }
     g.got.assign(static_cast<size_t>(n), 0);
     g.n_got = g.scan_from = 0;
+    g.part_ev = nullptr;
+    g.part_idx.clear();
+    g.part_done = g.part_handed = false;
+    g.part_ms = 0.0f;
     auto launch_spins = [&](int slot, bool stamp) {
         SpinLaunch L{};
         L.n = n;
@@ -1163,69 +1189,141 @@ void Context::launch_group(Group& g) {
                 }
                 d.contrast = static_cast<float>(t.p3.contrast);
                 d.csum = nullptr;
+                d.contrast_on = t.p3.contrast != 1.0;
                 d.slot = slot_of(i);
                 counters.kernel_bytes += img3d_algo_bytes(c, t);
             }
-            // RandomCrop foreground oversampling: K2 scans the label volumes of the
-            // samples that drew it, then resolves every window origin (same stream)
-            if (c.has_fg) {
-                FgLaunch F{};
-                int n_fg = 0;
-                for (int i = 0; i < n; ++i) {
-                    const Params3D& p3 = tickets[g.tickets[i]].p3;
-                    F.d[i].fg = p3.fg;
-                    F.d[i].u_cls = p3.u_cls;
-                    for (int a = 0; a < 3; ++a) F.d[i].u_adj[a] = p3.u_adj[a];
-                    if (p3.fg) {
-                        ++n_fg;
-                        counters.kernel_bytes += L.d[i].lbl_pz * L.d[i].sdim[0];   // the label volume, once
+            // RandomContrast (K5 sums each contrasted sample's crop first) then K1 / K4
+            // over the launch `Lx` (the whole group, or one part of a split group)
+            auto contrast_and_transform = [&](Img3dLaunch& Lx) {
+                if (c.has_contrast) {
+                    int n_c = 0;
+                    for (int i = 0; i < Lx.n; ++i) {
+                        Img3dDesc& d = Lx.d[i];
+                        if (!d.contrast_on) continue;
+                        d.csum = csum_ + csum_next_;
+                        csum_next_ = (csum_next_ + 1) % kCsumSlots;
+                        ++n_c;
+                        counters.kernel_bytes += int64_t(4) * std::min(d.win[0], d.sdim[0] - d.off[0]) *
+                                                 std::min(d.win[1], d.sdim[1] - d.off[1]) *
+                                                 std::min(d.win[2], d.sdim[2] - d.off[2]);
+                    }
+                    if (n_c > 0) {
+                        start();
+                        for (int i = 0; i < Lx.n; ++i)
+                            if (Lx.d[i].csum != nullptr)
+                                cuda_check(cudaMemsetAsync(const_cast<double*>(Lx.d[i].csum), 0, sizeof(double), st),
+                                           "csum reset");
+                        cuda_check(launch_img3d_mean(Lx, st), "img3d mean launch");
+                        counters.launches++;
                     }
                 }
-                if (n_fg > 0) {
-                    const int slot = fg_next_;
-                    fg_next_ = (fg_next_ + 1) % kFgSlots;
-                    int32_t* box = fg_box_ + size_t(slot) * kMax3D * 48;
-                    int4* offs = fg_offs_ + size_t(slot) * kMax3D;
-                    start();
-                    // mins ([kMax3D][8][3]) preset large, maxs (the next block) to -1
-                    cuda_check(cudaMemsetAsync(box, 0x7f, kMax3D * 24 * sizeof(int32_t), st), "fg box reset");
-                    cuda_check(cudaMemsetAsync(box + kMax3D * 24, 0xff, kMax3D * 24 * sizeof(int32_t), st),
-                               "fg box reset");
-                    cuda_check(launch_fg_scan(L, F, box, st), "fg scan launch");
-                    cuda_check(launch_fg_offsets(L, F, box, offs, st), "fg offsets launch");
-                    counters.launches += 2;
-                    L.offs = offs;
+                start();
+                if (c.has_zoom) cuda_check(launch_img3d_zoom(Lx, st), "img3d zoom launch");
+                else cuda_check(launch_img3d(Lx, st), "img3d launch");
+                counters.launches++;
+            };
+            int n_fg = 0;
+            for (int i = 0; i < n && c.has_fg; ++i) n_fg += tickets[g.tickets[i]].p3.fg != 0;
+            if (n_fg == 0) {
+                contrast_and_transform(L);
+            } else {
+                // RandomCrop foreground oversampling (K2).  The group splits: its plain
+                // samples run first and complete at a sub-launch event, so they never
+                // wait for the label scans; then K2 scans the label volumes of the
+                // samples that drew it, resolves their window origins, and K1 / K4
+                // crops them (from pinned memory K0w first pulls just those windows).
+                std::vector<int> plain, fgi;
+                for (int i = 0; i < n; ++i) (tickets[g.tickets[i]].p3.fg ? fgi : plain).push_back(i);
+                auto subset = [&](const std::vector<int>& idx) {
+                    std::unique_ptr<Img3dLaunch> X(new Img3dLaunch(L));
+                    X->n = static_cast<int32_t>(idx.size());
+                    for (size_t j = 0; j < idx.size(); ++j) {
+                        X->d[j] = L.d[idx[j]];
+                        X->tm_img[j] = L.tm_img[idx[j]];
+                        X->tm_lbl[j] = L.tm_lbl[idx[j]];
+                    }
+                    return X;
+                };
+                if (!plain.empty()) {
+                    auto Lp = subset(plain);
+                    contrast_and_transform(*Lp);
+                    g.part_ev = get_event();
+                    cuda_check(cudaEventRecord(g.part_ev, st), "record plain part");
+                    g.part_idx = plain;
                 }
-            }
-            // RandomContrast: K5 sums each contrasted sample's crop first (same stream);
-            // it runs over the whole group and skips the samples without contrast
-            if (c.has_contrast) {
-                int n_c = 0;
-                for (int i = 0; i < n; ++i) {
-                    if (tickets[g.tickets[i]].p3.contrast == 1.0) continue;
-                    L.d[i].csum = csum_ + csum_next_;
-                    csum_next_ = (csum_next_ + 1) % kCsumSlots;
-                    ++n_c;
-                    const Img3dDesc& d = L.d[i];
-                    counters.kernel_bytes += int64_t(4) * std::min(d.win[0], d.sdim[0] - d.off[0]) *
-                                             std::min(d.win[1], d.sdim[1] - d.off[1]) *
-                                             std::min(d.win[2], d.sdim[2] - d.off[2]);
+                auto Lf = subset(fgi);
+                FgLaunch F{};
+                for (size_t j = 0; j < fgi.size(); ++j) {
+                    const Params3D& p3 = tickets[g.tickets[fgi[j]]].p3;
+                    F.d[j].fg = 1;
+                    F.d[j].u_cls = p3.u_cls;
+                    for (int a = 0; a < 3; ++a) F.d[j].u_adj[a] = p3.u_adj[a];
+                    counters.kernel_bytes += Lf->d[j].lbl_pz * Lf->d[j].sdim[0];   // the label volume, once
                 }
-                if (n_c > 0) {
-                    start();
-                    for (int i = 0; i < n; ++i)
-                        if (L.d[i].csum != nullptr)
-                            cuda_check(cudaMemsetAsync(const_cast<double*>(L.d[i].csum), 0, sizeof(double), st),
-                                       "csum reset");
-                    cuda_check(launch_img3d_mean(L, st), "img3d mean launch");
+                const int slot = fg_next_;
+                fg_next_ = (fg_next_ + 1) % kFgSlots;
+                int32_t* box = fg_box_ + size_t(slot) * kMax3D * 48;
+                int4* offs = fg_offs_ + size_t(slot) * kMax3D;
+                start();
+                // mins ([kMax3D][8][3]) preset large, maxs (the next block) to -1
+                cuda_check(cudaMemsetAsync(box, 0x7f, kMax3D * 24 * sizeof(int32_t), st), "fg box reset");
+                cuda_check(cudaMemsetAsync(box + kMax3D * 24, 0xff, kMax3D * 24 * sizeof(int32_t), st),
+                           "fg box reset");
+                cuda_check(launch_fg_scan(*Lf, F, box, st), "fg scan launch");
+                cuda_check(launch_fg_offsets(*Lf, F, box, offs, st), "fg offsets launch");
+                counters.launches += 2;
+                if (staged) {
+                    // K0w: the windows at the resolved origins, from pinned host memory
+                    // (image) and the staged label volume (label), into compact windows
+                    WindowLaunch W{};
+                    W.n = Lf->n;
+                    W.offs = offs;
+                    for (int j = 0; j < Lf->n; ++j) {
+                        const Ticket& t = tickets[g.tickets[fgi[j]]];
+                        const View& v = views[fgi[j]];
+                        WindowDesc& w = W.d[j];
+                        Img3dDesc& d = Lf->d[j];
+                        w.img_host = static_cast<const float*>(t.desc.data);
+                        w.lbl = d.lbl;
+                        w.lbl_py = d.lbl_py;
+                        w.lbl_pz = d.lbl_pz;
+                        w.lbl_sk0 = d.lbl_sk0;
+                        w.lbl_sky = d.lbl_sky;
+                        w.lbl_skz = d.lbl_skz;
+                        for (int a = 0; a < 3; ++a) {
+                            w.dims[a] = static_cast<int32_t>(t.desc.dims[a]);
+                            w.win[a] = d.win[a];
+                        }
+                        w.img_pitch = (d.win[2] + 3) / 4 * 4;
+                        w.lbl_pitch = (d.win[2] + 15) / 16 * 16;
+                        w.dst_img = reinterpret_cast<float*>(const_cast<char*>(v.p[0]));
+                        w.dst_lbl = reinterpret_cast<uint8_t*>(const_cast<char*>(v.p[0])) +
+                                    align256(int64_t(4) * w.img_pitch * d.win[1] * d.win[0]);
+                        counters.h2d_bytes += int64_t(4) * d.win[0] * d.win[1] *
+                                              std::max<int64_t>(0, std::min<int64_t>(d.win[2], t.desc.dims[2]));
+                        // K1 / K4 read the compact window: origin 0, all of it valid
+                        d.img = w.dst_img;
+                        d.lbl = w.dst_lbl;
+                        d.img_py = w.img_pitch;
+                        d.img_pz = int64_t(w.img_pitch) * d.win[1];
+                        d.lbl_py = w.lbl_pitch;
+                        d.lbl_pz = int64_t(w.lbl_pitch) * d.win[1];
+                        d.img_sk0 = d.img_sky = d.img_skz = d.lbl_sk0 = d.lbl_sky = d.lbl_skz = 0;
+                        for (int a = 0; a < 3; ++a) {
+                            d.sdim[a] = d.win[a];
+                            d.off[a] = 0;
+                        }
+                    }
+                    cuda_check(launch_stage_window(W, st), "window stage launch");
                     counters.launches++;
+                    Lf->offs = nullptr;
+                } else {
+                    Lf->offs = offs;
                 }
+                contrast_and_transform(*Lf);
             }
-            start();
-            if (c.has_zoom) cuda_check(launch_img3d_zoom(L, st), "img3d zoom launch");
-            else cuda_check(launch_img3d(L, st), "img3d launch");
             prof_launch_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_l).count();
-            counters.launches++;
         } else if (S.kind == ST_RRC2D) {
             RrcLaunch L{};
             L.oh = c.oh;
@@ -1333,6 +1431,12 @@ void Context::finalize_group_timing(Group& g) {
         float ms = 0;
         cuda_check(cudaEventElapsedTime(&ms, g.ev[s], g.ev[s + 1]), "stage time");
         g.stage_ms[s] = ms;
+    }
+    if (g.part_ev != nullptr) {
+        cuda_check(cudaEventElapsedTime(&g.part_ms, g.ev[0], g.part_ev), "part time");
+        put_event(g.part_ev);
+        g.part_ev = nullptr;
+        g.part_done = true;
     }
     for (auto e : g.ev) put_event(e);
     g.ev.clear();

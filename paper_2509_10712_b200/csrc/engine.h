@@ -13,6 +13,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstdint>
 #include <functional>
@@ -184,6 +185,17 @@ struct Group {
     int n_got = 0;                 // samples handed on by the shard
     int scan_from = 0;             // first sample not yet handed on (in order)
     std::vector<uint8_t> got;      // per sample: handed on
+    // a sub-launch that completes some samples early (the plain samples of a group
+    // split around foreground-crop label scans): its event and the samples it covers
+    cudaEvent_t part_ev = nullptr;
+    std::vector<int> part_idx;
+    bool part_done = false;        // the part event completed
+    bool part_handed = false;      // (shard) the part's samples were handed on
+    float part_ms = 0.0f;          // device time from the group's start to the part event
+    bool part_ready() {
+        if (!part_done && part_ev != nullptr) part_done = cudaEventQuery(part_ev) == cudaSuccess;
+        return part_done;
+    }
 };
 
 struct Ticket {
@@ -289,7 +301,11 @@ public:
     // the sample's outputs are complete (its stamp landed, or its whole group finished)
     bool sample_ready(int64_t t) {
         Group& g = groups[tickets[t].group];
-        return g.complete || (g.stamped && sample_stamp(t) != 0) || poll_group(g);
+        if (g.complete || (g.stamped && sample_stamp(t) != 0)) return true;
+        if (!g.part_idx.empty() && g.part_ready() &&
+            std::find(g.part_idx.begin(), g.part_idx.end(), tickets[t].idx) != g.part_idx.end())
+            return true;
+        return poll_group(g);
     }
     bool poll_group(Group& g);          // updates stages_done/complete; true if complete
     void finalize_group_timing(Group& g);

@@ -109,7 +109,82 @@ __global__ void __launch_bounds__(32 * kWarps) stage_bulk_kernel(const __grid_co
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// K0w: one CTA per (window plane z, sample); a warp per window row.  Image rows
+// come from host memory as 16-B aligned chunks (lane l holds chunk q0 + l, lane
+// 31 also the next group's first chunk) and are realigned to the window's first
+// float with a shuffle; label rows come from the staged volume in HBM.
+__device__ __forceinline__ float4 shift4w(float4 a, float4 b, int m) {
+    switch (m) {   // warp-uniform
+        case 0: return a;
+        case 1: return make_float4(a.y, a.z, a.w, b.x);
+        case 2: return make_float4(a.z, a.w, b.x, b.y);
+        default: return make_float4(a.w, b.x, b.y, b.z);
+    }
+}
+
+__global__ void __launch_bounds__(32 * kWarps) stage_window_kernel(const __grid_constant__ WindowLaunch L) {
+    const WindowDesc& d = L.d[blockIdx.y];
+    const int z = blockIdx.x;
+    if (z >= d.win[0]) return;
+    const int4 o = L.offs[blockIdx.y];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int D = d.dims[0], H = d.dims[1], W = d.dims[2];
+    const int sz = o.x + z;
+    const int w2 = d.win[2];
+    const int vw = max(0, min(w2, W - o.z));            // window columns inside the volume
+    const int nq = (w2 + 3) >> 2;                         // output quads per row
+    for (int y = warp; y < d.win[1]; y += kWarps) {
+        const int sy = o.y + y;
+        float4* out = reinterpret_cast<float4*>(d.dst_img + ((int64_t)z * d.win[1] + y) * d.img_pitch);
+        uint8_t* lout = d.dst_lbl + ((int64_t)z * d.win[1] + y) * d.lbl_pitch;
+        const bool row_ok = sz < D && sy < H && vw > 0;
+        if (!row_ok) {
+            for (int q = lane; q < nq; q += 32) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int x = lane; x < w2; x += 32) lout[x] = 0;
+            continue;
+        }
+        const float* a = d.img_host + ((int64_t)sz * H + sy) * W + o.z;   // first window float
+        const uintptr_t ab = reinterpret_cast<uintptr_t>(a);
+        const int m = (int)((ab & 15) >> 2);                               // warp-uniform
+        const float4* c0 = reinterpret_cast<const float4*>(ab & ~uintptr_t(15));
+        const int nch = (m + vw + 3) >> 2;                                 // chunks holding window data
+        for (int q0 = 0; q0 < nq; q0 += 32) {
+            const int c = q0 + lane;
+            const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 v = c < nch ? c0[c] : zero;
+            float4 nx = make_float4(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1),
+                                    __shfl_down_sync(0xffffffffu, v.z, 1), __shfl_down_sync(0xffffffffu, v.w, 1));
+            if (lane == 31) nx = (q0 + 32 < nch) ? c0[q0 + 32] : zero;
+            if (c < nq) {
+                float4 x = shift4w(v, nx, m);
+                const int keep = vw - 4 * c;                                // valid floats of this quad
+                if (keep < 4) x.w = 0.f;
+                if (keep < 3) x.z = 0.f;
+                if (keep < 2) x.y = 0.f;
+                if (keep < 1) x.x = 0.f;
+                out[c] = x;
+            }
+        }
+        const uint8_t* lrow = d.lbl + (int64_t)sz * d.lbl_pz + (int64_t)sy * d.lbl_py +
+                              ((d.lbl_sk0 + sz * d.lbl_skz + sy * d.lbl_sky) & 15) + o.z;
+        for (int x = lane; x < w2; x += 32) lout[x] = x < vw ? lrow[x] : (uint8_t)0;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_stage_window(const WindowLaunch& L, cudaStream_t s) {
+    if (L.n <= 0) return cudaSuccess;
+    int planes = 1;
+    for (int i = 0; i < L.n; ++i) {
+        if ((L.d[i].img_pitch & 3) || (L.d[i].lbl_pitch & 15) || L.d[i].img_pitch < L.d[i].win[2] ||
+            L.d[i].lbl_pitch < L.d[i].win[2])
+            return cudaErrorInvalidValue;
+        planes = planes > L.d[i].win[0] ? planes : L.d[i].win[0];
+    }
+    stage_window_kernel<<<dim3(planes, L.n), 32 * kWarps, 0, s>>>(L);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_stage(const StageLaunch& L, cudaStream_t s) {
     if (L.n <= 0) return cudaSuccess;

@@ -48,6 +48,30 @@ struct StageLaunch {
 };
 static_assert(kMaxStage >= 2 * 16 && kMaxStage >= 256, "K0 must hold a whole launch group");
 
+// ---- K0w: the crop windows of foreground-oversampled samples from pinned host
+// memory.  Their origin is resolved on the device (K2 over the staged label
+// volume), so the window cannot be a host-described K0 box: this kernel reads the
+// origin from offs[i], pulls the image window rows over PCIe (16-B aligned reads,
+// realigned by warp shuffles) and the label window rows from the staged label
+// volume in HBM, into compact windows (skew 0, zero outside the volume).
+struct WindowDesc {
+    const float* img_host;   // UVA pointer of the pinned D x H x W f32 image volume
+    const uint8_t* lbl;      // the staged label volume (K0 layout: pitches + skews)
+    int64_t lbl_py, lbl_pz;
+    int32_t lbl_sk0, lbl_sky, lbl_skz;
+    int32_t dims[3];         // D, H, W of the source volume
+    int32_t win[3];          // window edge (crop, or the RandomZoom3D window)
+    int32_t img_pitch;       // floats per compact window row (multiple of 4)
+    int32_t lbl_pitch;       // bytes per compact label row (multiple of 16)
+    float* dst_img;          // [win0][win1][img_pitch]
+    uint8_t* dst_lbl;        // [win0][win1][lbl_pitch]
+};
+struct WindowLaunch {
+    int32_t n;
+    const int4* offs;        // K2's window origins (d, h, w), one per sample
+    WindowDesc d[16];
+};
+
 // ---- K1: RandomCrop + RandomFlip + RandomBrightness + GaussianNoise + Cast
 struct Img3dDesc {
     const float* img;        // source: full volume (HBM) or staged crop window
@@ -69,7 +93,7 @@ struct Img3dDesc {
     const double* csum;      // contrast: sum of the (resampled) crop, written by K5 (null: none)
     double zscale[3];        // RandomZoom3D source-index scale win / crop (IEEE division, host)
     int32_t slot;            // completion stamp slot
-    int32_t pad_;
+    int32_t contrast_on;     // (host) RandomContrast drawn: K5 sums the crop first
 };
 // Contrast folded into one affine per sample: out = A * v + B (+ noise), with
 // A = scale * c and B = scale * (1 - c) * mean, mean = csum / crop voxels.
@@ -195,6 +219,7 @@ struct GatherLaunch {
 };
 
 cudaError_t launch_stage(const StageLaunch& L, cudaStream_t s);
+cudaError_t launch_stage_window(const WindowLaunch& L, cudaStream_t s);
 cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s);
 // K4: RandomZoom3D chains (trilinear image / nearest label resample of the window)
 cudaError_t launch_img3d_zoom(const Img3dLaunch& L, cudaStream_t s);

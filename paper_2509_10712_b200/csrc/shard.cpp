@@ -285,6 +285,15 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             if (!g.got[static_cast<size_t>(i)] && ctx.sample_stamp(g.tickets[i]) != 0) hand_on(g, i, is_slow);
         return g.n_got != before;
     };
+    // a sub-launch that finished part of the group (the plain samples of a split
+    // foreground-crop group) hands that part on
+    auto check_part = [&](Group& g, bool is_slow) {
+        if (g.part_idx.empty() || g.part_handed || !g.part_ready()) return false;
+        for (int i : g.part_idx)
+            if (!g.got[static_cast<size_t>(i)]) hand_on(g, i, is_slow);
+        g.part_handed = true;
+        return true;
+    };
     const bool profiled = rc.policy == 1 || rc.policy == 2;
     // the group's last event completed: hand on the rest; per-sample device-timed
     // totals (the group's event-timed span less the time from the sample's stamp to
@@ -296,8 +305,10 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         const bool per = g.stamped && (profiled || t_out < kNoTimeoutUs);
         uint64_t last = 0;
         for (int i = 0; per && i < sz; ++i) last = std::max(last, ctx.sample_stamp(g.tickets[i]));
+        std::vector<uint8_t> in_part(static_cast<size_t>(sz), 0);
+        for (int i : g.part_idx) in_part[static_cast<size_t>(i)] = 1;
         for (int i = 0; i < sz; ++i) {
-            int64_t us = tot;
+            int64_t us = in_part[static_cast<size_t>(i)] ? static_cast<int64_t>(std::llround(g.part_ms * 1000.0)) : tot;
             if (per) {
                 const uint64_t st = ctx.sample_stamp(g.tickets[i]);
                 if (st != 0 && last >= st) us = std::max<int64_t>(0, tot - static_cast<int64_t>((last - st) / 1000));
@@ -386,6 +397,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             const bool over = now - g.t_launch_us > t_out;
             const int sz = static_cast<int>(g.tickets.size());
             if (g.stamped && g.n_got < sz && scan_stamps(g, full_scan || over, false)) progressed = true;
+            if ((query || full_scan || over) && check_part(g, false)) progressed = true;
             const bool done = (query || full_scan || over || g.n_got == sz) && ctx.poll_group(g);
             if (!done) query = false;
             bool remove = false;
@@ -410,6 +422,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             Group& g = ctx.groups[parked[k]];
             const int sz = static_cast<int>(g.tickets.size());
             if (g.stamped && g.n_got < sz && scan_stamps(g, full_scan, true)) progressed = true;
+            if (full_scan && check_part(g, true)) progressed = true;
             if ((full_scan || g.n_got == sz) && ctx.poll_group(g)) {
                 finish_group(g, true);
                 parked.erase(parked.begin() + static_cast<long>(k));
