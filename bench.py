@@ -653,6 +653,8 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
     trainer_us = args.trainer_us if args.trainer_us else (2000 if heavy else 0)
     cap_pos = capture_positions(len(ids_timed), args.check, args.seed + rank) if args.check else None
     out = {"group": group}
+    if args.serial:
+        ctx.set_serial(True)
 
     # ---- value: inputs resident in HBM
     wl = make_workload(args.workload, L, ctx, host=False, seed=args.seed, args=args)
@@ -722,6 +724,7 @@ def main():
     ap.add_argument("--trainer-us", type=int, default=0)
     ap.add_argument("--profiler-warmup-us", type=int, default=20000)
     ap.add_argument("--check", type=int, default=8, help="delivered samples checked against the oracle")
+    ap.add_argument("--serial", action="store_true", help="(experiment) all launch groups on one stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()

@@ -576,6 +576,7 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
             i = last_tf;
         }
     }
+    c->spin_last = c->stages.back().kind == ST_SPIN || !c->stages.back().spin_ops.empty();
     chains_.push_back(std::move(c));
     reserve_bufs(chains_.back().get());
     return chains_.back().get();
@@ -733,10 +734,10 @@ static int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 // source, read once (f32 + u8), and the crop written (f32 + u8).  Without
 // RandomZoom3D the window is the crop: 128^3 * 10 B.
 int64_t img3d_algo_bytes(const Chain& c, const Ticket& t) {
-    if (!c.has_zoom) return c.algo_bytes_per_sample(t.desc);
+    if (!c.has_zoom) return c.algo_bytes_per_sample(t.desc());
     int64_t in = 5;
     for (int a = 0; a < 3; ++a)
-        in *= std::max<int64_t>(0, std::min<int64_t>(t.p3.win[a], t.desc.dims[a] - t.p3.off[a]));
+        in *= std::max<int64_t>(0, std::min<int64_t>(t.p3().win[a], t.desc().dims[a] - t.p3().off[a]));
     return in + int64_t(c.crop[0]) * c.crop[1] * c.crop[2] * 5;
 }
 
@@ -752,11 +753,11 @@ struct Box {
 };
 
 static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) {
-    const lfg_sample_desc& s = t.desc;
+    const lfg_sample_desc& s = t.desc();
     wd[0] = wd[1] = wd[2] = 0;
     if (c.fam == FAM_IMG3D) {
         const int64_t H = s.dims[1], W = s.dims[2];
-        if (c.has_fg && t.p3.fg) {
+        if (c.has_fg && t.p3().fg) {
             // a foreground-biased crop's window depends on the label scan: stage the
             // label volume only; K0w pulls the image window once K2 resolved it
             for (int a = 0; a < 3; ++a) wd[a] = s.dims[a];
@@ -764,8 +765,8 @@ static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) 
                          static_cast<int32_t>(H), static_cast<int32_t>(s.dims[0]), 1};
             return 1;
         }
-        for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(t.p3.win[a], s.dims[a] - t.p3.off[a]);
-        const int64_t first = (t.p3.off[0] * H + t.p3.off[1]) * W + t.p3.off[2];
+        for (int a = 0; a < 3; ++a) wd[a] = std::min<int64_t>(t.p3().win[a], s.dims[a] - t.p3().off[a]);
+        const int64_t first = (t.p3().off[0] * H + t.p3().off[1]) * W + t.p3().off[2];
         out[0] = Box{static_cast<const char*>(s.data) + first * 4, W * 4, H * W * 4,
                      static_cast<int32_t>(wd[2] * 4), static_cast<int32_t>(wd[1]),
                      static_cast<int32_t>(wd[0]), 0};
@@ -775,8 +776,8 @@ static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) 
     }
     if (c.fam == FAM_RRC2D) {
         const int64_t W = s.dims[1];
-        out[0] = Box{static_cast<const char*>(s.data) + (t.p2.top * W + t.p2.left) * 3, W * 3, 0,
-                     static_cast<int32_t>(t.p2.w * 3), static_cast<int32_t>(t.p2.h), 1, 0};
+        out[0] = Box{static_cast<const char*>(s.data) + (t.p2().top * W + t.p2().left) * 3, W * 3, 0,
+                     static_cast<int32_t>(t.p2().w * 3), static_cast<int32_t>(t.p2().h), 1, 0};
         return 1;
     }
     out[0] = Box{static_cast<const char*>(s.data), 0, 0, static_cast<int32_t>(s.dims[0] * 4), 1, 1, 0};
@@ -796,7 +797,7 @@ int64_t Context::stage_raw_bytes(const Chain& c, const Ticket& t) const {
     const int nb = boxes_of(c, t, b, wd);
     int64_t total = 0;
     for (int i = 0; i < nb; ++i) total += align256(b[i].bytes());
-    if (c.fam == FAM_IMG3D && c.has_fg && t.p3.fg) total += fg_window_bytes(t.p3);
+    if (c.fam == FAM_IMG3D && c.has_fg && t.p3().fg) total += fg_window_bytes(t.p3());
     return total;
 }
 
@@ -845,10 +846,18 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
     }
     for (int k = 0; k < c->n_spin; ++k)
         if (s.spin_us[k] < 0) fail(LFG_ERR_STATE, "negative transform cost");  // balancer.cpp:16
-    PreDraw local;
+    // Tickets point at the sample's descriptor and drawn parameters.  The shard
+    // runner passes its run arrays (they outlive the run's tickets); a sample
+    // submitted through the ABI is copied into context-owned storage.
+    const lfg_sample_desc* sp = &s;
+    bool owned = false;
     if (pre == nullptr) {
-        draw_params(*c, cfg.seed, s, local);
-        pre = &local;
+        owned_.emplace_back();
+        owned_.back().first = s;
+        draw_params(*c, cfg.seed, s, owned_.back().second);
+        sp = &owned_.back().first;
+        pre = &owned_.back().second;
+        owned = true;
     }
     // the ticket is built in place (submit runs once per sample)
     const int64_t ti = static_cast<int64_t>(tickets.size());
@@ -857,18 +866,17 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
     if (ti >= kStampSlots && !groups[tickets[ti - kStampSlots].group].complete &&
         !poll_group(groups[tickets[ti - kStampSlots].group]))
         fail(LFG_ERR_AGAIN, "completion stamp ring full (a sample 2^20 submissions old is still running)");
-    stamp_host_[ti & (kStampSlots - 1)] = 0;
+    if (c->spin_last || stamp_transforms) stamp_host_[ti & (kStampSlots - 1)] = 0;
     tickets.emplace_back();
     Ticket& t = tickets.back();
     t.id = s.id;
-    t.desc = s;
-    if (c->fam == FAM_IMG3D) t.p3 = pre->p3;
-    else if (c->fam == FAM_RRC2D) t.p2 = pre->p2;
-    else t.ps = pre->ps;
+    t.dp = sp;
+    t.pp = pre;
     try {
         assign_slot(t, c);
     } catch (...) {
         tickets.pop_back();
+        if (owned) owned_.pop_back();
         throw;
     }
     auto& og = open_group_[s.src_kind == LFG_SRC_DEVICE ? 0 : 1];
@@ -913,6 +921,7 @@ bool Context::recycle_tables() {
         if (!t.released) return false;
     tickets.clear();
     groups.clear();
+    owned_.clear();
     return true;
 }
 
@@ -997,6 +1006,13 @@ void Context::launch_group(Group& g) {
     };
     const int n = static_cast<int>(g.tickets.size());
     const bool staged = g.src_kind == LFG_SRC_HOST_PINNED;
+    auto lap = [&](double& acc, std::chrono::steady_clock::time_point& t0) {
+        if (!prof_on) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        acc += std::chrono::duration<double, std::nano>(t1 - t0).count();
+        t0 = t1;
+    };
+    auto t_lap = std::chrono::steady_clock::now();
 
     // Host-pinned payloads: K0 pulls exactly the boxes the chain reads over
     // PCIe into one staging buffer (part of the group's first stage).
@@ -1006,7 +1022,9 @@ void Context::launch_group(Group& g) {
         int32_t sk0[2], sky[2], skz[2];
         int64_t sdim[3], off[3];
     };
-    std::vector<View> views(n);
+    // per-thread scratch: no allocation or clearing per group
+    static thread_local std::vector<View> views;
+    if (static_cast<int>(views.size()) < n) views.resize(static_cast<size_t>(n));
     if (staged) {
         int64_t total = 0;
         for (int i = 0; i < n; ++i) total += stage_raw_bytes(c, tickets[g.tickets[i]]);
@@ -1021,9 +1039,9 @@ void Context::launch_group(Group& g) {
             if (c.fam == FAM_SPEECH) {
                 // a waveform is one contiguous block: the copy engines move it at full
                 // PCIe rate; the group's copies go out as one batched DMA call below
-                const int64_t bytes = t.desc.dims[0] * 4;
+                const int64_t bytes = t.desc().dims[0] * 4;
                 wav_dst.push_back(dst);
-                wav_src.push_back(const_cast<void*>(t.desc.data));
+                wav_src.push_back(const_cast<void*>(t.desc().data));
                 wav_bytes.push_back(static_cast<size_t>(bytes));
                 v.p[0] = dst;
                 counters.h2d_bytes += bytes;
@@ -1057,16 +1075,16 @@ void Context::launch_group(Group& g) {
                 counters.h2d_bytes += static_cast<int64_t>(b[k].row_bytes) * b[k].ny * b[k].nz;
                 dst += align256(b[k].bytes());
             }
-            const bool whole = c.fam == FAM_IMG3D && c.has_fg && t.p3.fg;   // see boxes_of
+            const bool whole = c.fam == FAM_IMG3D && c.has_fg && t.p3().fg;   // see boxes_of
             if (whole) {   // the K0w compact window follows the staged label volume
                 v.p[0] = dst;
                 v.py[0] = v.pz[0] = 0;
                 v.sk0[0] = v.sky[0] = v.skz[0] = 0;
-                dst += fg_window_bytes(t.p3);
+                dst += fg_window_bytes(t.p3());
             }
             for (int a = 0; a < 3; ++a) {
                 v.sdim[a] = wd[a];
-                v.off[a] = whole ? t.p3.off[a] : 0;
+                v.off[a] = whole ? t.p3().off[a] : 0;
             }
         }
         if (!wav_dst.empty()) {
@@ -1086,12 +1104,12 @@ void Context::launch_group(Group& g) {
             cuda_check(launch_stage(SL, st), "stage launch");
             counters.launches++;
         }
-    } else {
+    } else if (c.fam != FAM_RRC2D) {   // (obj_det reads its HBM-resident boxes straight from the tickets)
         for (int i = 0; i < n; ++i) {
             Ticket& t = tickets[g.tickets[i]];
             View& v = views[i];
             std::memset(&v, 0, sizeof(v));
-            const lfg_sample_desc& s = t.desc;
+            const lfg_sample_desc& s = t.desc();
             if (c.fam == FAM_IMG3D) {
                 v.p[0] = static_cast<const char*>(s.data);
                 v.p[1] = static_cast<const char*>(s.aux);
@@ -1099,11 +1117,8 @@ void Context::launch_group(Group& g) {
                 v.pz[0] = v.pz[1] = s.dims[1] * s.dims[2];
                 for (int a = 0; a < 3; ++a) {
                     v.sdim[a] = s.dims[a];
-                    v.off[a] = t.p3.off[a];
+                    v.off[a] = t.p3().off[a];
                 }
-            } else if (c.fam == FAM_RRC2D) {
-                v.p[0] = static_cast<const char*>(s.data) + (t.p2.top * s.dims[1] + t.p2.left) * 3;
-                v.py[0] = s.dims[1] * 3;
             } else {
                 v.p[0] = static_cast<const char*>(s.data);
             }
@@ -1113,20 +1128,18 @@ void Context::launch_group(Group& g) {
     // The group's last kernel carries the per-sample completion stamps.
     const StampRef stamps{stamp_cnt_, stamp_dev_};
     const auto slot_of = [&](int i) { return static_cast<int32_t>(g.tickets[i] & (kStampSlots - 1)); };
-    {
-        const Stage& last = c.stages.back();
-        g.stamped = last.kind == ST_SPIN || !last.spin_ops.empty() || stamp_transforms;
-    }
+    g.stamped = c.spin_last || stamp_transforms;
     g.got.assign(static_cast<size_t>(n), 0);
     g.n_got = g.scan_from = 0;
     g.part_ev = nullptr;
     g.part_idx.clear();
     g.part_done = g.part_handed = false;
     g.part_ms = 0.0f;
+    lap(prof_views_ns, t_lap);
     auto launch_spins = [&](int slot, bool stamp) {
         SpinLaunch L{};
         L.n = n;
-        for (int i = 0; i < n; ++i) L.ns[i] = tickets[g.tickets[i]].desc.spin_us[slot] * 1000;
+        for (int i = 0; i < n; ++i) L.ns[i] = tickets[g.tickets[i]].desc().spin_us[slot] * 1000;
         if (stamp) {
             L.st = stamps;
             for (int i = 0; i < n; ++i) L.slot[i] = slot_of(i);
@@ -1150,7 +1163,7 @@ void Context::launch_group(Group& g) {
             // TMA tile path: HBM-resident volumes with 16-B aligned rows
             bool tma = !staged && img3d_tma_ && !c.has_zoom;
             for (int i = 0; i < n && tma; ++i) {
-                const lfg_sample_desc& sd = tickets[g.tickets[i]].desc;
+                const lfg_sample_desc& sd = tickets[g.tickets[i]].desc();
                 tma = img3d_tma_ok(sd.data, sd.aux, sd.dims, c.crop) &&
                       img3d_encode_maps(L, i, sd.data, sd.aux, sd.dims) == cudaSuccess;
             }
@@ -1178,18 +1191,18 @@ void Context::launch_group(Group& g) {
                     d.sdim[a] = static_cast<int32_t>(v.sdim[a]);
                     d.off[a] = static_cast<int32_t>(v.off[a]);
                 }
-                d.flip = t.p3.flip[0] | (t.p3.flip[1] << 1) | (t.p3.flip[2] << 2);
-                d.scale = static_cast<float>(t.p3.scale);
-                d.sigma = static_cast<float>(t.p3.sigma);
-                d.key0 = t.p3.key[0];
-                d.key1 = t.p3.key[1];
+                d.flip = t.p3().flip[0] | (t.p3().flip[1] << 1) | (t.p3().flip[2] << 2);
+                d.scale = static_cast<float>(t.p3().scale);
+                d.sigma = static_cast<float>(t.p3().sigma);
+                d.key0 = t.p3().key[0];
+                d.key1 = t.p3().key[1];
                 for (int a = 0; a < 3; ++a) {
-                    d.win[a] = static_cast<int32_t>(t.p3.win[a]);
-                    d.zscale[a] = static_cast<double>(t.p3.win[a]) / static_cast<double>(c.crop[a]);
+                    d.win[a] = static_cast<int32_t>(t.p3().win[a]);
+                    d.zscale[a] = static_cast<double>(t.p3().win[a]) / static_cast<double>(c.crop[a]);
                 }
-                d.contrast = static_cast<float>(t.p3.contrast);
+                d.contrast = static_cast<float>(t.p3().contrast);
                 d.csum = nullptr;
-                d.contrast_on = t.p3.contrast != 1.0;
+                d.contrast_on = t.p3().contrast != 1.0;
                 d.slot = slot_of(i);
                 counters.kernel_bytes += img3d_algo_bytes(c, t);
             }
@@ -1224,7 +1237,7 @@ void Context::launch_group(Group& g) {
                 counters.launches++;
             };
             int n_fg = 0;
-            for (int i = 0; i < n && c.has_fg; ++i) n_fg += tickets[g.tickets[i]].p3.fg != 0;
+            for (int i = 0; i < n && c.has_fg; ++i) n_fg += tickets[g.tickets[i]].p3().fg != 0;
             if (n_fg == 0) {
                 contrast_and_transform(L);
             } else {
@@ -1234,7 +1247,7 @@ void Context::launch_group(Group& g) {
                 // samples that drew it, resolves their window origins, and K1 / K4
                 // crops them (from pinned memory K0w first pulls just those windows).
                 std::vector<int> plain, fgi;
-                for (int i = 0; i < n; ++i) (tickets[g.tickets[i]].p3.fg ? fgi : plain).push_back(i);
+                for (int i = 0; i < n; ++i) (tickets[g.tickets[i]].p3().fg ? fgi : plain).push_back(i);
                 auto subset = [&](const std::vector<int>& idx) {
                     std::unique_ptr<Img3dLaunch> X(new Img3dLaunch(L));
                     X->n = static_cast<int32_t>(idx.size());
@@ -1255,7 +1268,7 @@ void Context::launch_group(Group& g) {
                 auto Lf = subset(fgi);
                 FgLaunch F{};
                 for (size_t j = 0; j < fgi.size(); ++j) {
-                    const Params3D& p3 = tickets[g.tickets[fgi[j]]].p3;
+                    const Params3D& p3 = tickets[g.tickets[fgi[j]]].p3();
                     F.d[j].fg = 1;
                     F.d[j].u_cls = p3.u_cls;
                     for (int a = 0; a < 3; ++a) F.d[j].u_adj[a] = p3.u_adj[a];
@@ -1284,7 +1297,7 @@ void Context::launch_group(Group& g) {
                         const View& v = views[fgi[j]];
                         WindowDesc& w = W.d[j];
                         Img3dDesc& d = Lf->d[j];
-                        w.img_host = static_cast<const float*>(t.desc.data);
+                        w.img_host = static_cast<const float*>(t.desc().data);
                         w.lbl = d.lbl;
                         w.lbl_py = d.lbl_py;
                         w.lbl_pz = d.lbl_pz;
@@ -1292,7 +1305,7 @@ void Context::launch_group(Group& g) {
                         w.lbl_sky = d.lbl_sky;
                         w.lbl_skz = d.lbl_skz;
                         for (int a = 0; a < 3; ++a) {
-                            w.dims[a] = static_cast<int32_t>(t.desc.dims[a]);
+                            w.dims[a] = static_cast<int32_t>(t.desc().dims[a]);
                             w.win[a] = d.win[a];
                         }
                         w.img_pitch = (d.win[2] + 3) / 4 * 4;
@@ -1301,7 +1314,7 @@ void Context::launch_group(Group& g) {
                         w.dst_lbl = reinterpret_cast<uint8_t*>(const_cast<char*>(v.p[0])) +
                                     align256(int64_t(4) * w.img_pitch * d.win[1] * d.win[0]);
                         counters.h2d_bytes += int64_t(4) * d.win[0] * d.win[1] *
-                                              std::max<int64_t>(0, std::min<int64_t>(d.win[2], t.desc.dims[2]));
+                                              std::max<int64_t>(0, std::min<int64_t>(d.win[2], t.desc().dims[2]));
                         // K1 / K4 read the compact window: origin 0, all of it valid
                         d.img = w.dst_img;
                         d.lbl = w.dst_lbl;
@@ -1337,19 +1350,27 @@ void Context::launch_group(Group& g) {
             if (stamp_here) L.st = stamps;
             for (int i = 0; i < n; ++i) {
                 Ticket& t = tickets[g.tickets[i]];
-                const View& v = views[i];
                 RrcDesc& d = L.d[i];
                 d.slot = slot_of(i);
-                d.src = reinterpret_cast<const uint8_t*>(v.p[0]);
+                if (staged) {   // the K0-staged box (skewed rows)
+                    const View& v = views[i];
+                    d.src = reinterpret_cast<const uint8_t*>(v.p[0]);
+                    d.pitch = static_cast<int32_t>(v.py[0]);
+                    d.sk0 = static_cast<uint8_t>(v.sk0[0] & 15);
+                    d.sky = static_cast<uint8_t>(v.sky[0] & 15);
+                } else {        // the crop box inside the HBM-resident HWC image
+                    const lfg_sample_desc& sd = t.desc();
+                    d.src = static_cast<const uint8_t*>(sd.data) + (t.p2().top * sd.dims[1] + t.p2().left) * 3;
+                    d.pitch = static_cast<int32_t>(sd.dims[1] * 3);   // < 2^31: image width <= 65535
+                    d.sk0 = d.sky = 0;
+                }
                 d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
-                d.pitch = static_cast<int32_t>(v.py[0]);   // < 2^31: image width <= 65535
-                d.sk0 = static_cast<uint8_t>(v.sk0[0] & 15);
-                d.sky = static_cast<uint8_t>(v.sky[0] & 15);
-                d.h = static_cast<uint16_t>(t.p2.h);
-                d.w = static_cast<uint16_t>(t.p2.w);
-                d.flip = static_cast<uint8_t>(t.p2.flip);
-                counters.kernel_bytes += rrc_algo_bytes(c, t.p2);
+                d.h = static_cast<uint16_t>(t.p2().h);
+                d.w = static_cast<uint16_t>(t.p2().w);
+                d.flip = static_cast<uint8_t>(t.p2().flip);
+                counters.kernel_bytes += rrc_algo_bytes(c, t.p2());
             }
+            lap(prof_desc_ns, t_lap);
             const auto t_l = std::chrono::steady_clock::now();
             start();
             cuda_check(launch_rrc2d(L, st), "rrc2d launch");
@@ -1368,19 +1389,19 @@ void Context::launch_group(Group& g) {
                 d.slot = slot_of(i);
                 d.wav = reinterpret_cast<const float*>(views[i].p[0]);
                 d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
-                d.L = static_cast<int32_t>(t.desc.dims[0]);
-                d.T = t.ps.T;
+                d.L = static_cast<int32_t>(t.desc().dims[0]);
+                d.T = t.ps().T;
                 for (int k = 0; k < c.n_fmask; ++k) {
-                    d.f_lo[k] = t.ps.f_lo[k];
-                    d.f_w[k] = t.ps.f_w[k];
+                    d.f_lo[k] = t.ps().f_lo[k];
+                    d.f_w[k] = t.ps().f_w[k];
                 }
                 for (int k = 0; k < c.n_tmask; ++k) {
-                    d.t_lo[k] = t.ps.t_lo[k];
-                    d.t_w[k] = t.ps.t_w[k];
+                    d.t_lo[k] = t.ps().t_lo[k];
+                    d.t_w[k] = t.ps().t_w[k];
                 }
-                counters.kernel_bytes += 4 * t.desc.dims[0] +
-                                         4 * int64_t((t.ps.T + c.stack - 1) / c.stack) * c.stack * c.n_mels;
-                counters.reserved[1] += int64_t(t.ps.T) * 2 * kTapsDft * 512 * 3;   // tensor FLOPs
+                counters.kernel_bytes += 4 * t.desc().dims[0] +
+                                         4 * int64_t((t.ps().T + c.stack - 1) / c.stack) * c.stack * c.n_mels;
+                counters.reserved[1] += int64_t(t.ps().T) * 2 * kTapsDft * 512 * 3;   // tensor FLOPs
             }
             start();
             cuda_check(launch_speech(L, speech_, st), "speech launch");
@@ -1600,7 +1621,7 @@ int64_t Context::seal(const int64_t* ts, int n) {
             SC.width = c->stack * c->n_mels;
             for (int i = 0; i < n; ++i) {
                 const Ticket& t = tickets[ts[i]];
-                SC.rows[i] = (t.ps.T + c->stack - 1) / c->stack;
+                SC.rows[i] = (t.ps().T + c->stack - 1) / c->stack;
                 SC.src[i] = reinterpret_cast<const float*>(L.src[i]);
                 SC.t_max = std::max(SC.t_max, SC.rows[i]);
             }

@@ -102,6 +102,7 @@ struct Chain {
     double tmask_frac = 0;
     int64_t max_L = 170000;
     // output slot layout (planar)
+    bool spin_last = false;        // the last stage ends in a synthetic-cost spin (stamps)
     int nplanes = 1;
     int64_t plane_bytes[2] = {0, 0};
     int64_t out_bytes = 0;
@@ -201,20 +202,20 @@ struct Group {
 struct Ticket {
     uint64_t id = 0;
     int64_t group = -1;
+    // the sample's descriptor and drawn parameters: the shard runner's run arrays
+    // (alive until the run's tickets are released) or context-owned copies (lfg_submit);
+    // a ticket is one cache line, so the per-sample submit writes ~48 B
+    const lfg_sample_desc* dp = nullptr;
+    const PreDraw* pp = nullptr;
     int idx = 0;
     int buf = -1, pos = -1;
     bool released = false;
     bool consumed = false;   // sealed into a batch
     bool in_seal = false;    // scratch mark for seal's duplicate check
-    lfg_sample_desc desc;
-    // the drawn parameters of the chain's family (a ticket belongs to one chain);
-    // a union keeps the per-sample record small -- submit writes ~250 B, not ~400
-    union {
-        Params3D p3;
-        Params2D p2;
-        ParamsSp ps;
-    };
-    Ticket() {}   // submit assigns desc and the chain's params member (no clearing per sample)
+    const lfg_sample_desc& desc() const { return *dp; }
+    const Params3D& p3() const { return pp->p3; }
+    const Params2D& p2() const { return pp->p2; }
+    const ParamsSp& ps() const { return pp->ps; }
 };
 
 struct BatchRec {
@@ -322,6 +323,8 @@ public:
     int free_stream_count() const { return static_cast<int>(free_streams_.size()); }
     lfg_counters counters{};
     double prof_group_ns = 0, prof_launch_ns = 0;   // host time in launch_group / kernel launch calls
+    double prof_views_ns = 0, prof_desc_ns = 0;     // launch_group: payload views / descriptor fill (LFG_SHARD_PROF)
+    bool prof_on = false;
     bool serial = false;
     bool defer_launch = false;
     // Per-sample completion stamps.  A group whose last kernel is a synthetic cost
@@ -341,6 +344,7 @@ public:
     cudaStream_t aux_stream = nullptr;
 
     std::vector<Ticket> tickets;
+    std::deque<std::pair<lfg_sample_desc, PreDraw>> owned_;   // samples submitted through the ABI
     std::vector<Group> groups;
     std::vector<BatchRec> batches;
 
