@@ -331,8 +331,10 @@ Context::Context(const lfg_config& c) : cfg(c) {
     if (const char* e = std::getenv("LFG_IMG3D_TMA")) img3d_tma_ = std::atoi(e) != 0;
     for (int i = 0; i < 512; ++i) {
         cudaEvent_t e;
-        cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
         free_events_.push_back(e);
+        cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        free_tevents_.push_back(e);
     }
     // per-sample completion stamps: host-mapped words the kernels write, device counters
     cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&stamp_host_), kStampSlots * sizeof(uint64_t),
@@ -353,6 +355,7 @@ Context::~Context() {
     for (auto& g : groups) for (auto e : g.ev) if (e) cudaEventDestroy(e);
     for (auto& b : batches) if (b.ready) cudaEventDestroy(b.ready);
     for (auto e : free_events_) cudaEventDestroy(e);
+    for (auto e : free_tevents_) cudaEventDestroy(e);
     for (auto& b : bufs_) {
         for (auto e : b.pending) cudaEventDestroy(e);
         cudaFree(b.base);
@@ -363,24 +366,27 @@ Context::~Context() {
     if (csum_) cudaFree(csum_);
     if (fg_box_) cudaFree(fg_box_);
     if (fg_offs_) cudaFree(fg_offs_);
+    if (out_tab_) cudaFree(out_tab_);
     for (auto s : streams_) cudaStreamDestroy(s);
     cudaStreamDestroy(seal_stream);
     cudaStreamDestroy(aux_stream);
     speech_tables_destroy(speech_);
 }
 
-cudaEvent_t Context::get_event() {
-    if (!free_events_.empty()) {
-        cudaEvent_t e = free_events_.back();
-        free_events_.pop_back();
+cudaEvent_t Context::get_event(bool timed) {
+    auto& pool = timed ? free_tevents_ : free_events_;
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
         return e;
     }
     cudaEvent_t e;
-    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    cuda_check(timed ? cudaEventCreate(&e) : cudaEventCreateWithFlags(&e, cudaEventDisableTiming),
+               "cudaEventCreate");
     return e;
 }
 
-void Context::put_event(cudaEvent_t e) { free_events_.push_back(e); }
+void Context::put_event(cudaEvent_t e, bool timed) { (timed ? free_tevents_ : free_events_).push_back(e); }
 
 int Context::get_stream() {
     if (serial) return 0;   // stream 0 is reserved for serial (roofline) mode
@@ -661,6 +667,21 @@ void Context::reserve_bufs(const Chain* c) {
             bufs_.push_back(b);
         }
     }
+    sync_out_tab();
+}
+
+// The device table of slot-buffer bases (K3's packed descriptors name a buffer by
+// its index); rewritten whenever buffers are created -- at chain creation, never
+// inside the shard loop.
+void Context::sync_out_tab() {
+    if (bufs_.size() > static_cast<size_t>(kMaxRrcBufs))
+        fail(LFG_ERR_UNSUPPORTED, "more than 4096 output buffers in one context");
+    if (out_tab_ == nullptr)
+        cuda_check(cudaMalloc(&out_tab_, kMaxRrcBufs * sizeof(float*)), "output buffer table");
+    std::vector<float*> h(bufs_.size());
+    for (size_t i = 0; i < bufs_.size(); ++i) h[i] = reinterpret_cast<float*>(bufs_[i].base);
+    cuda_check(cudaMemcpy(out_tab_, h.data(), h.size() * sizeof(float*), cudaMemcpyHostToDevice),
+               "output buffer table");
 }
 
 // Round-robin from the buffer after the last one handed out: the oldest
@@ -945,6 +966,8 @@ void Context::time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* me
     if (n > fit) n = static_cast<int>(fit);
     cuda_check(cudaDeviceSynchronize(), "sync");
     const lfg_counters c0 = counters;
+    const bool timed0 = time_groups;
+    time_groups = true;
     serial = true;
     defer_launch = true;
     std::vector<int64_t> ts;
@@ -959,9 +982,11 @@ void Context::time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* me
         flush();
     } catch (...) {
         serial = defer_launch = false;
+        time_groups = timed0;
         throw;
     }
     serial = false;
+    time_groups = timed0;
     cuda_check(cudaDeviceSynchronize(), "sync");
     double ms = 0;
     int64_t nl = 0;
@@ -991,7 +1016,8 @@ void Context::launch_group(Group& g) {
     g.stream = streams_[g.stream_idx];
     const int nst = static_cast<int>(c.stages.size());
     g.ev.resize(nst + 1);
-    for (auto& e : g.ev) e = get_event();
+    g.timed = time_groups;
+    for (auto& e : g.ev) e = get_event(g.timed);
     cudaStream_t st = g.stream;
     // The start event goes in immediately before the group's first device
     // operation, after the host has built that operation's parameters: stage
@@ -1000,7 +1026,7 @@ void Context::launch_group(Group& g) {
     bool started = false;
     auto start = [&] {
         if (!started) {
-            cuda_check(cudaEventRecord(g.ev[0], st), "record start");
+            if (g.timed) cuda_check(cudaEventRecord(g.ev[0], st), "record start");
             started = true;
         }
     };
@@ -1261,7 +1287,7 @@ void Context::launch_group(Group& g) {
                 if (!plain.empty()) {
                     auto Lp = subset(plain);
                     contrast_and_transform(*Lp);
-                    g.part_ev = get_event();
+                    g.part_ev = get_event(g.timed);
                     cuda_check(cudaEventRecord(g.part_ev, st), "record plain part");
                     g.part_idx = plain;
                 }
@@ -1347,28 +1373,31 @@ void Context::launch_group(Group& g) {
                 L.b[k] = static_cast<float>(-c.mean[k] / c.std[k]);
             }
             L.n = n;
-            if (stamp_here) L.st = stamps;
+            L.out_tab = out_tab_;
+            L.out_stride = c.plane_bytes[0] / 4;
+            L.slot_base = slot_of(0);
+            if (stamp_here) {   // image i stamps slot_base + i: the group's tickets must be consecutive
+                bool consecutive = true;
+                for (int i = 1; i < n && consecutive; ++i) consecutive = slot_of(i) == L.slot_base + i;
+                if (consecutive) L.st = stamps;
+                else g.stamped = false;   // (the group completes as a whole)
+            }
             for (int i = 0; i < n; ++i) {
-                Ticket& t = tickets[g.tickets[i]];
-                RrcDesc& d = L.d[i];
-                d.slot = slot_of(i);
+                const Ticket& t = tickets[g.tickets[i]];
+                const Params2D& p = t.p2();
+                bool ok;
                 if (staged) {   // the K0-staged box (skewed rows)
                     const View& v = views[i];
-                    d.src = reinterpret_cast<const uint8_t*>(v.p[0]);
-                    d.pitch = static_cast<int32_t>(v.py[0]);
-                    d.sk0 = static_cast<uint8_t>(v.sk0[0] & 15);
-                    d.sky = static_cast<uint8_t>(v.sky[0] & 15);
+                    ok = rrc_pack(L.d[i], v.p[0], v.sk0[0], v.sky[0], static_cast<int>(v.py[0]), static_cast<int>(p.h),
+                                  static_cast<int>(p.w), p.flip, t.pos, t.buf);
                 } else {        // the crop box inside the HBM-resident HWC image
                     const lfg_sample_desc& sd = t.desc();
-                    d.src = static_cast<const uint8_t*>(sd.data) + (t.p2().top * sd.dims[1] + t.p2().left) * 3;
-                    d.pitch = static_cast<int32_t>(sd.dims[1] * 3);   // < 2^31: image width <= 65535
-                    d.sk0 = d.sky = 0;
+                    ok = rrc_pack(L.d[i], static_cast<const uint8_t*>(sd.data) + (p.top * sd.dims[1] + p.left) * 3, 0, 0,
+                                  static_cast<int>(sd.dims[1] * 3), static_cast<int>(p.h), static_cast<int>(p.w), p.flip,
+                                  t.pos, t.buf);
                 }
-                d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
-                d.h = static_cast<uint16_t>(t.p2().h);
-                d.w = static_cast<uint16_t>(t.p2().w);
-                d.flip = static_cast<uint8_t>(t.p2().flip);
-                counters.kernel_bytes += rrc_algo_bytes(c, t.p2());
+                if (!ok) fail(LFG_ERR_UNSUPPORTED, "obj_det sample does not fit the packed K3 descriptor");
+                counters.kernel_bytes += rrc_algo_bytes(c, p);
             }
             lap(prof_desc_ns, t_lap);
             const auto t_l = std::chrono::steady_clock::now();
@@ -1429,13 +1458,22 @@ bool Context::poll_group(Group& g) {
     if (!g.launched) return false;
     const int nst = static_cast<int>(g.chain->stages.size());
     while (g.stages_done < nst) {
+        std::chrono::steady_clock::time_point t0;
+        if (prof_on) t0 = std::chrono::steady_clock::now();
         cudaError_t q = cudaEventQuery(g.ev[g.stages_done + 1]);
+        if (prof_on) {
+            prof_query_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+            ++prof_queries;
+        }
         if (q == cudaErrorNotReady) return false;
         cuda_check(q, "stage event");
         g.stages_done++;
     }
     g.complete = true;
+    std::chrono::steady_clock::time_point t1;
+    if (prof_on) t1 = std::chrono::steady_clock::now();
     finalize_group_timing(g);
+    if (prof_on) prof_final_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t1).count();
     counters.completed += static_cast<int64_t>(g.tickets.size());
     if (g.stream_idx != 0) free_streams_.push_back(g.stream_idx);
     if (g.raw_idx >= 0) {
@@ -1448,18 +1486,18 @@ bool Context::poll_group(Group& g) {
 void Context::finalize_group_timing(Group& g) {
     const int nst = static_cast<int>(g.chain->stages.size());
     g.stage_ms.assign(nst, 0.0f);
-    for (int s = 0; s < nst; ++s) {
+    for (int s = 0; s < nst && g.timed; ++s) {
         float ms = 0;
         cuda_check(cudaEventElapsedTime(&ms, g.ev[s], g.ev[s + 1]), "stage time");
         g.stage_ms[s] = ms;
     }
     if (g.part_ev != nullptr) {
-        cuda_check(cudaEventElapsedTime(&g.part_ms, g.ev[0], g.part_ev), "part time");
-        put_event(g.part_ev);
+        if (g.timed) cuda_check(cudaEventElapsedTime(&g.part_ms, g.ev[0], g.part_ev), "part time");
+        put_event(g.part_ev, g.timed);
         g.part_ev = nullptr;
         g.part_done = true;
     }
-    for (auto e : g.ev) put_event(e);
+    for (auto e : g.ev) put_event(e, g.timed);
     g.ev.clear();
 }
 

@@ -179,7 +179,8 @@ struct Group {
     int64_t t_launch_us = 0;
     int64_t raw_idx = -1;
     int refs = 0;
-    std::vector<float> stage_ms;   // filled once complete
+    bool timed = true;             // stage events carry timing (Context::time_groups at launch)
+    std::vector<float> stage_ms;   // filled once complete (zeros when untimed)
     // per-sample completion: the group's last kernel writes one stamp per sample
     // (Context::sample_stamp); the shard delivers samples as their stamps land
     bool stamped = false;
@@ -325,6 +326,8 @@ public:
     double prof_group_ns = 0, prof_launch_ns = 0;   // host time in launch_group / kernel launch calls
     double prof_views_ns = 0, prof_desc_ns = 0;     // launch_group: payload views / descriptor fill (LFG_SHARD_PROF)
     bool prof_on = false;
+    double prof_query_ns = 0, prof_final_ns = 0;    // event queries / completed-group timing reads
+    int64_t prof_queries = 0;
     bool serial = false;
     bool defer_launch = false;
     // Per-sample completion stamps.  A group whose last kernel is a synthetic cost
@@ -335,6 +338,12 @@ public:
     // ~30% of K1 / K3 time, so by default a transform-last group completes as a
     // whole -- or per sub-launch, as the foreground-crop split does (see launch_group).
     bool stamp_transforms = false;
+    // Launch groups carry timed stage events (device-timed stage / sample costs:
+    // the profiler, device-timed timeout classification, lfg_exec_costs, the
+    // roofline).  A query + elapsed-time read of timed events costs the submitting
+    // thread ~8 us per group, so shard runs without a profiler or timeout use
+    // untimed events (run_shard sets this).
+    bool time_groups = true;
     void time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms, int64_t* launches,
                       int64_t* bytes, int64_t* flops);
     std::mutex mu;   // one lock per context (C ABI calls serialise on it)
@@ -345,6 +354,7 @@ public:
 
     std::vector<Ticket> tickets;
     std::deque<std::pair<lfg_sample_desc, PreDraw>> owned_;   // samples submitted through the ABI
+    std::vector<PreDraw> pre_store;   // the shard runner's per-sample draws (reused between runs)
     std::vector<Group> groups;
     std::vector<BatchRec> batches;
 
@@ -364,8 +374,10 @@ private:
     int fg_next_ = 0;
     std::vector<cudaStream_t> streams_;
     std::vector<int> free_streams_;
-    std::vector<cudaEvent_t> free_events_;
+    std::vector<cudaEvent_t> free_events_, free_tevents_;   // untimed / timed
     std::vector<SlotBuf> bufs_;
+    float** out_tab_ = nullptr;         // device copy of the slot-buffer bases (K3 descriptors index it)
+    void sync_out_tab();
     size_t alloc_cursor_[2] = {0, 0};   // [for_batch] last buffer handed out
     std::vector<RawBuf> raws_;
     std::vector<int64_t> free_raws_;
@@ -373,8 +385,10 @@ private:
     std::vector<int64_t> deferred_;          // full groups awaiting launch (timing mode)
     SmallMap<int64_t> open_group_[2];        // [src_kind] chain -> group
 
-    cudaEvent_t get_event();
-    void put_event(cudaEvent_t e);
+    // events: untimed (cudaEventDisableTiming: ordering and completion only; cheap to
+    // record and query) unless `timed` (stage timing of a launch group)
+    cudaEvent_t get_event(bool timed = false);
+    void put_event(cudaEvent_t e, bool timed = false);
     int get_stream();
     int alloc_buf(const Chain* c, bool for_batch);
     void reserve_bufs(const Chain* c);

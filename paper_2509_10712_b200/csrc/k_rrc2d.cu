@@ -57,13 +57,34 @@ __device__ __forceinline__ void src_index(int dst, int in, double scale, int& i0
     l0 = (float)__dadd_rn(1.0, -w1);
 }
 
-__device__ __forceinline__ const uint8_t* row_ptr(const RrcDesc& d, int y) {
+// an image's descriptor, unpacked once per CTA
+struct RrcView {
+    const uint8_t* src;
+    float* out;
+    int pitch, h, w, sk0, sky, flip, slot;
+};
+__device__ __forceinline__ RrcView unpack(const RrcLaunch& L, int i) {
+    const RrcDesc p = L.d[i];
+    RrcView v;
+    v.src = rrc_src(p);
+    v.sk0 = rrc_sk0(p);
+    v.sky = rrc_sky(p);
+    v.pitch = rrc_pitch(p);
+    v.h = rrc_h(p);
+    v.w = rrc_w(p);
+    v.flip = rrc_flip(p);
+    v.out = L.out_tab[rrc_buf(p)] + (int64_t)rrc_pos(p) * L.out_stride;
+    v.slot = L.slot_base + i;
+    return v;
+}
+
+__device__ __forceinline__ const uint8_t* row_ptr(const RrcView& d, int y) {
     return d.src + (int64_t)y * d.pitch + ((d.sk0 + y * d.sky) & 15);
 }
 
 // byte offset of staged row y's first pixel: the row sits at (y - ylo) * spitch
 // with its 16-byte alignment phase preserved (only the low 4 address bits matter)
-__device__ __forceinline__ int staged_off(const RrcDesc& d, int y, int ylo, int spitch) {
+__device__ __forceinline__ int staged_off(const RrcView& d, int y, int ylo, int spitch) {
     const uint32_t lo = (uint32_t)reinterpret_cast<uintptr_t>(d.src) + (uint32_t)y * (uint32_t)d.pitch +
                         (uint32_t)((d.sk0 + y * d.sky) & 15);
     return (y - ylo) * spitch + (int)(lo & 15u);
@@ -109,7 +130,7 @@ __device__ __forceinline__ void blend_row(const uint8_t* smem, int row_off, cons
     h[2] = __ffma2_rn(c.w0, ubyte2(la, lb, 2), __fmul2_rn(c.w1, ubyte2(ha, hb, 1)));
 }
 
-__device__ __forceinline__ void blend_row_l2(const RrcDesc& d, int y, const ColPair& c, float2 h[3]) {
+__device__ __forceinline__ void blend_row_l2(const RrcView& d, int y, const ColPair& c, float2 h[3]) {
     const uint8_t* row = row_ptr(d, y);
     const int x1a = min(c.x0_a + 1, d.w - 1), x1b = min(c.x0_b + 1, d.w - 1);
 #pragma unroll
@@ -121,12 +142,12 @@ __device__ __forceinline__ void blend_row_l2(const RrcDesc& d, int y, const ColP
 }
 
 // the row loop of one CTA (defined below the kernel)
-__device__ __forceinline__ void blend_rows(const RrcLaunch& L, const RrcDesc& d, const ColPair& cp, int y_begin,
+__device__ __forceinline__ void blend_rows(const RrcLaunch& L, const RrcView& d, const ColPair& cp, int y_begin,
                                            int n_rows_out, bool staged, int xa, const uint8_t* smem,
                                            uint64_t* stage_bar, const int2* sched_rows,
                                            const float (*sched_w)[6]);
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 12)   // 40 registers (one 8-B spill): shared memory, not registers, sets the CTAs / SM
 rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t stage_bar;   // staged rows landed
@@ -138,7 +159,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
                                                   // staged byte offset (or a row index, unstaged)
     __shared__ float sched_w[kRows][6];           // {wE * a_c (c = 0..2), wO * a_c}
     __shared__ int yspan[2];                      // [0]: the block's rows are staged
-    const RrcDesc& d = L.d[blockIdx.y];
+    const RrcView d = unpack(L, blockIdx.y);
     const int oh = L.oh, ow = L.ow;
     const int y_begin = blockIdx.x * kRows;
     const int n_rows_out = min(kRows, oh - y_begin);
@@ -250,7 +271,7 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
     }
 }
 
-__device__ __forceinline__ void blend_rows(const RrcLaunch& L, const RrcDesc& d, const ColPair& cp, int y_begin,
+__device__ __forceinline__ void blend_rows(const RrcLaunch& L, const RrcView& d, const ColPair& cp, int y_begin,
                                            int n_rows_out, bool staged, int xa, const uint8_t* smem,
                                            uint64_t* stage_bar, const int2* sched_rows,
                                            const float (*sched_w)[6]) {
@@ -296,8 +317,8 @@ int rrc2d_smem_bytes(const RrcLaunch& L) {
     int need = 0;
     for (int i = 0; i < L.n; ++i) {
         const RrcDesc& d = L.d[i];
-        const int rows = (int)((double)(kRows - 1) * d.h / L.oh) + 4;
-        const int spitch = ((d.w * 3 + 30) >> 4) << 4;
+        const int rows = (int)((double)(kRows - 1) * rrc_h(d) / L.oh) + 4;
+        const int spitch = ((rrc_w(d) * 3 + 30) >> 4) << 4;
         need = max(need, rows * spitch);
     }
     return min(need, kMaxSmem) + kSmemSlack;

@@ -146,25 +146,52 @@ inline bool img3d_tma_ok(const void* img, const void* lbl, const int64_t dims[3]
 }
 
 // ---- K3: RandomResizedCrop (bilinear) + RandomHorizontalFlip + ToTensor + Normalize
-// 32 B per image: the launch passes 256 of these as kernel parameters, and the
-// launch call's cost grows with the parameter block (h / oh and w / ow are divided
-// on the device, IEEE-rounded like the host / oracle)
+// 16 B per image, packed: the launch passes up to 256 of these as kernel
+// parameters, and the launch call's host cost grows with the parameter block
+// (8 KB of 32-B descriptors: ~12 us per call; 4 KB: ~8 us).  h / oh and w / ow
+// are divided on the device, IEEE-rounded like the host / oracle.
+//   a: bits  0-47 src (crop-box origin, row 0 column 0, of an HWC u8 image; UVA)
+//           48-51 sk0, 52-55 sky (row skew, see above), 56-63 output buffer (low 8 bits)
+//   b: bits  0-17 pitch (bytes per source row), 18-33 h, 34-49 w (crop box),
+//           50 flip, 51-59 position in the output buffer, 60-63 output buffer (high 4 bits)
+// The output of image i is out_tab[buffer] + position * out_stride floats; the
+// buffer index is the context's slot-buffer index (out_tab: device table).
 struct RrcDesc {
-    const uint8_t* src;      // crop-box origin (row 0, column 0) of an HWC u8 image
-    float* out;              // [3, oh, ow] f32
-    int32_t pitch;           // bytes per source row
-    uint16_t h, w;           // crop box size
-    uint8_t sk0, sky;        // row skew (only the low 4 bits matter), see above
-    uint8_t flip;
-    uint8_t pad;
-    int32_t slot;            // completion stamp slot
+    uint64_t a, b;
 };
-static_assert(sizeof(RrcDesc) == 32, "RrcDesc layout");
+static_assert(sizeof(RrcDesc) == 16, "RrcDesc layout");
+__host__ __device__ inline const uint8_t* rrc_src(const RrcDesc& d) {
+    return reinterpret_cast<const uint8_t*>(d.a & 0xFFFFFFFFFFFFull);
+}
+__host__ __device__ inline int rrc_sk0(const RrcDesc& d) { return (int)((d.a >> 48) & 15); }
+__host__ __device__ inline int rrc_sky(const RrcDesc& d) { return (int)((d.a >> 52) & 15); }
+__host__ __device__ inline int rrc_pitch(const RrcDesc& d) { return (int)(d.b & 0x3FFFF); }
+__host__ __device__ inline int rrc_h(const RrcDesc& d) { return (int)((d.b >> 18) & 0xFFFF); }
+__host__ __device__ inline int rrc_w(const RrcDesc& d) { return (int)((d.b >> 34) & 0xFFFF); }
+__host__ __device__ inline int rrc_flip(const RrcDesc& d) { return (int)((d.b >> 50) & 1); }
+__host__ __device__ inline int rrc_pos(const RrcDesc& d) { return (int)((d.b >> 51) & 0x1FF); }
+__host__ __device__ inline int rrc_buf(const RrcDesc& d) { return (int)(((d.a >> 56) & 0xFF) | (((d.b >> 60) & 0xF) << 8)); }
+// false if a field does not fit (src >= 2^48, pitch >= 2^18, position >= 512, buffer >= 4096)
+inline bool rrc_pack(RrcDesc& d, const void* src, int sk0, int sky, int pitch, int h, int w, int flip, int pos,
+                     int buf) {
+    const uint64_t p = reinterpret_cast<uint64_t>(src);
+    if ((p >> 48) || pitch < 0 || pitch >= (1 << 18) || h < 1 || h > 0xFFFF || w < 1 || w > 0xFFFF || pos < 0 ||
+        pos >= 512 || buf < 0 || buf >= 4096)
+        return false;
+    d.a = p | (uint64_t(sk0 & 15) << 48) | (uint64_t(sky & 15) << 52) | (uint64_t(buf & 0xFF) << 56);
+    d.b = uint64_t(pitch) | (uint64_t(h) << 18) | (uint64_t(w) << 34) | (uint64_t(flip & 1) << 50) |
+          (uint64_t(pos) << 51) | (uint64_t(buf >> 8) << 60);
+    return true;
+}
+constexpr int kMaxRrcBufs = 4096;
 struct RrcLaunch {
     int32_t oh, ow;
     float a[3], b[3];        // out = v * a_c + b_c  (= (v/255 - mean_c) / std_c)
     int32_t n;
+    int32_t slot_base;       // completion stamp slot of image i: slot_base + i
     StampRef st;
+    float* const* out_tab;   // device table: slot-buffer index -> base
+    int64_t out_stride;      // floats per output slot
     RrcDesc d[kMax2D];
 };
 

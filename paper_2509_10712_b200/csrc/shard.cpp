@@ -212,6 +212,13 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         ~StampMode() { c.stamp_transforms = saved; }
     } stamp_mode{ctx, ctx.stamp_transforms};
     ctx.stamp_transforms = rc.sample_stamps == 1;
+    // device-timed stage events only where the run uses device time (Context::time_groups)
+    struct TimeMode {
+        Context& c;
+        bool saved;
+        ~TimeMode() { c.time_groups = saved; }
+    } time_mode{ctx, ctx.time_groups};
+    ctx.time_groups = t_out < kNoTimeoutUs || rc.policy == 1 || rc.policy == 2 || std::getenv("LFG_SHARD_TIMED");
     int64_t sync_next = 0;   // first position of the next batch to seal
     const int64_t run_t0 = host_now_us();
     int64_t last_update = run_t0;
@@ -295,6 +302,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         return true;
     };
     const bool profiled = rc.policy == 1 || rc.policy == 2;
+    int64_t est_group_us = 0;   // ~70% of the recent groups' device time (query throttle)
     // the group's last event completed: hand on the rest; per-sample device-timed
     // totals (the group's event-timed span less the time from the sample's stamp to
     // the group's last stamp) go to the profiler window, one record per sample as
@@ -305,6 +313,35 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         const bool per = g.stamped && (profiled || t_out < kNoTimeoutUs);
         uint64_t last = 0;
         for (int i = 0; per && i < sz; ++i) last = std::max(last, ctx.sample_stamp(g.tickets[i]));
+        if (!per && g.n_got == 0 && g.part_idx.empty()) {
+            // the common case -- a whole group finishing together: hand it on in bulk
+            const bool slow_all = parked_group || tot > t_out;   // inclusive budget, balancer.cpp:17
+            const uint8_t cv = slow_all ? 2 : 1;
+            std::fill(g.got.begin(), g.got.end(), cv);
+            g.n_got = sz;
+            for (int64_t t : g.tickets) {
+                cls[static_cast<size_t>(t - tbase)] = cv;
+                if (sample_class) sample_class[t - tbase] = cv;
+            }
+            (slow_all ? rep.slow : rep.fast) += sz;
+            if (sync) {
+                for (int64_t t : g.tickets) ready_pos[static_cast<size_t>(t - tbase)] = 1;
+            } else if (slow_all) {
+                slow.insert(slow.end(), g.tickets.begin(), g.tickets.end());
+            } else {
+                fast.insert(fast.end(), g.tickets.begin(), g.tickets.end());
+                for (int64_t t : g.tickets) {
+                    const int b = ctx.tickets[t].buf;
+                    if (b >= static_cast<int>(fast_cnt.size())) fast_cnt.resize(static_cast<size_t>(b) + 1, 0);
+                    if (++fast_cnt[b] == B && ctx.buf_closed_count(b) == B) full_bufs.push_back(b);
+                }
+            }
+            for (int i = 0; profiled && i < sz; ++i) prof.record(tot, slow_all);
+            if (nbatches >= rc.warmup_batches) kernel_ms += tot / 1000.0;
+            est_group_us = static_cast<int64_t>(0.8 * est_group_us + 0.2 * 0.7 * tot);
+            release_group(g);
+            return;
+        }
         std::vector<uint8_t> in_part(static_cast<size_t>(sz), 0);
         for (int i : g.part_idx) in_part[static_cast<size_t>(i)] = 1;
         for (int i = 0; i < sz; ++i) {
@@ -317,6 +354,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             if (profiled) prof.record(us, g.got[static_cast<size_t>(i)] == 2);
         }
         if (nbatches >= rc.warmup_batches) kernel_ms += tot / 1000.0;
+        est_group_us = static_cast<int64_t>(0.8 * est_group_us + 0.2 * 0.7 * tot);
         release_group(g);
     };
 
@@ -330,7 +368,9 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     // per ~15 tickets.
     constexpr int64_t kChunk = 32;
     const int64_t n_chunks = (n + kChunk - 1) / kChunk;
-    std::vector<PreDraw> pre(static_cast<size_t>(n));
+    // (the context keeps this table between runs: its pages stay mapped and warm)
+    std::vector<PreDraw>& pre = ctx.pre_store;
+    if (pre.size() < static_cast<size_t>(n)) pre.resize(static_cast<size_t>(n));
     std::unique_ptr<std::atomic<uint8_t>[]> ready(new std::atomic<uint8_t>[std::max<int64_t>(n_chunks, 1)]);
     for (int64_t i = 0; i < n_chunks; ++i) ready[i].store(0, std::memory_order_relaxed);
     std::atomic<int64_t> next_chunk{0};
@@ -375,16 +415,22 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     ctx.prof_on = ph.on;
     const double g_ns0 = ctx.prof_group_ns, l_ns0 = ctx.prof_launch_ns;
     const double v_ns0 = ctx.prof_views_ns, d_ns0 = ctx.prof_desc_ns;
+    const double q_ns0 = ctx.prof_query_ns, f_ns0 = ctx.prof_final_ns;
+    const int64_t nq0 = ctx.prof_queries;
+    int64_t iters = 0;
     const size_t groups0 = ctx.groups.size();
-    // full scans (every in-flight group's event queried) every 10 us when timeouts
-    // or the profiler need prompt completions, else every 50 us: each query costs
-    // ~0.5 us of the submitting thread
-    const int64_t kScanUs = (t_out < kNoTimeoutUs || profiled) ? 10 : 50;
+    // Full scans (every in-flight group's event queried) every 10 us when timeouts
+    // or the profiler need prompt completions.  Without them a group's samples only
+    // matter once sealable, and the groups complete nearly in launch order, so the
+    // oldest group is queried each pass and a full scan (~0.7 us per event query on
+    // the submitting thread) runs every 500 us.
+    const int64_t kScanUs = (t_out < kNoTimeoutUs || profiled) ? 10 : 500;
     int64_t last_scan_us = 0;
     ph.start();
     ph.setup_ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - setup_t0).count();
     while (consumed < n) {
         bool progressed = false;
+        ++iters;
         const int64_t now = host_now_us();
 
         // (1) in-flight groups.  Samples whose completion stamp landed are handed on
@@ -403,7 +449,10 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             const int sz = static_cast<int>(g.tickets.size());
             if (g.stamped && g.n_got < sz && scan_stamps(g, full_scan || over, false)) progressed = true;
             if ((query || full_scan || over) && check_part(g, false)) progressed = true;
-            const bool done = (query || full_scan || over || g.n_got == sz) && ctx.poll_group(g);
+            // a group is not queried before ~70% of the recent groups' device time has
+            // passed since its launch (the query would only cost the submitting thread)
+            const bool due = now - g.t_launch_us >= est_group_us;
+            const bool done = ((query && due) || full_scan || over || g.n_got == sz) && ctx.poll_group(g);
             if (!done) query = false;
             bool remove = false;
             if (done) {
@@ -512,8 +561,10 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 bool at_front = true;   // common case: the buffer's samples lead the fast list
                 for (int64_t i = 0; i < B && at_front; ++i)
                     at_front = ctx.tickets[fast[static_cast<size_t>(i)]].buf == pick;
-                if (at_front) {
-                    for (int64_t i = 0; i < B; ++i) ts.push_back(fast_take());
+                if (at_front) {   // (bulk: the first B entries are exactly buffer `pick`)
+                    ts.assign(fast.begin(), fast.begin() + B);
+                    fast.erase(fast.begin(), fast.begin() + B);
+                    fast_cnt[pick] -= static_cast<int>(B);
                 } else {
                     for (auto it = fast.begin(); it != fast.end();) {
                         if (ctx.tickets[*it].buf == pick) {
@@ -660,9 +711,13 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     ph.print(n, ctx.prof_group_ns - g_ns0, ctx.prof_launch_ns - l_ns0,
              static_cast<int64_t>(ctx.groups.size() - groups0));
     if (ph.on)
-        std::fprintf(stderr, "[lfg shard] per group: views=%.0f desc=%.0f ns\n",
+        std::fprintf(stderr, "[lfg shard] per group: views=%.0f desc=%.0f query=%.0f (%.1f queries) final=%.0f ns; %.1f loop passes\n",
                      (ctx.prof_views_ns - v_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
-                     (ctx.prof_desc_ns - d_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)));
+                     (ctx.prof_desc_ns - d_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
+                     (ctx.prof_query_ns - q_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
+                     double(ctx.prof_queries - nq0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
+                     (ctx.prof_final_ns - f_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
+                     double(iters) / double(std::max<size_t>(1, ctx.groups.size() - groups0)));
     cudaEvent_t t_end = mk();
     cuda_check(cudaEventRecord(t_end, trainer), "record");
     cuda_check(cudaEventSynchronize(t_end), "sync");
