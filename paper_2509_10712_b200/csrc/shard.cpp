@@ -511,7 +511,18 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                         }
                     } else if (!ready[i / kChunk].load(std::memory_order_acquire)) {
                         ph.lap(Phases::SUBMIT);
-                        while (!ready[i / kChunk].load(std::memory_order_acquire)) std::this_thread::yield();
+                        // help rather than wait: draw the next unclaimed chunk (the
+                        // workers may still be waking up at the start of a run)
+                        while (!ready[i / kChunk].load(std::memory_order_acquire)) {
+                            const int64_t ck = next_chunk.fetch_add(1);
+                            if (ck >= n_chunks) {
+                                std::this_thread::yield();
+                                continue;
+                            }
+                            for (int64_t q = ck * kChunk; q < std::min(n, (ck + 1) * kChunk); ++q)
+                                draw_params(*chain, ctx.cfg.seed, samples[q], pre[q]);
+                            ready[ck].store(1, std::memory_order_release);
+                        }
                         ph.lap(Phases::DRAW);
                     }
                     const int64_t t = ctx.submit(chain, samples[i], &pre[i]);
