@@ -1057,23 +1057,9 @@ void Context::launch_group(Group& g) {
         g.raw_idx = get_raw(total);
         char* dst = raws_[g.raw_idx].ptr;
         StageLaunch SL{};
-        std::vector<void*> wav_dst, wav_src;
-        std::vector<size_t> wav_bytes;
         for (int i = 0; i < n; ++i) {
             Ticket& t = tickets[g.tickets[i]];
             View& v = views[i];
-            if (c.fam == FAM_SPEECH) {
-                // a waveform is one contiguous block: the copy engines move it at full
-                // PCIe rate; the group's copies go out as one batched DMA call below
-                const int64_t bytes = t.desc().dims[0] * 4;
-                wav_dst.push_back(dst);
-                wav_src.push_back(const_cast<void*>(t.desc().data));
-                wav_bytes.push_back(static_cast<size_t>(bytes));
-                v.p[0] = dst;
-                counters.h2d_bytes += bytes;
-                dst += align256(bytes);
-                continue;
-            }
             Box b[2];
             int64_t wd[3];
             const int nb = boxes_of(c, t, b, wd);
@@ -1101,6 +1087,12 @@ void Context::launch_group(Group& g) {
                 counters.h2d_bytes += static_cast<int64_t>(b[k].row_bytes) * b[k].ny * b[k].nz;
                 dst += align256(b[k].bytes());
             }
+            if (c.fam == FAM_SPEECH) {
+                // a waveform is one K0 row (read over PCIe with the group's other
+                // boxes in the same launch); the kernel reads it at its skew
+                v.p[0] += v.sk0[0];
+                continue;
+            }
             const bool whole = c.fam == FAM_IMG3D && c.has_fg && t.p3().fg;   // see boxes_of
             if (whole) {   // the K0w compact window follows the staged label volume
                 v.p[0] = dst;
@@ -1112,18 +1104,6 @@ void Context::launch_group(Group& g) {
                 v.sdim[a] = wd[a];
                 v.off[a] = whole ? t.p3().off[a] : 0;
             }
-        }
-        if (!wav_dst.empty()) {
-            start();
-            cudaMemcpyAttributes attr{};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            attr.srcLocHint.type = cudaMemLocationTypeHost;
-            attr.dstLocHint.type = cudaMemLocationTypeDevice;
-            attr.dstLocHint.id = cfg.device;
-            size_t attr_idx = 0, fail_idx = 0;
-            cuda_check(cudaMemcpyBatchAsync(wav_dst.data(), wav_src.data(), wav_bytes.data(), wav_dst.size(),
-                                            &attr, &attr_idx, 1, &fail_idx, st),
-                       "H2D waveforms (batched)");
         }
         if (SL.n > 0) {
             start();

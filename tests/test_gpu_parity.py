@@ -717,8 +717,8 @@ def _splice(logmel, stack=3):
 
 
 def test_speech_pinned_host_source_matches_device(lfgpu, oracle):
-    """Speech from pinned host memory (the e2e path: one batched DMA call per launch
-    group, cudaMemcpyBatchAsync) produces bit-identical outputs to HBM-resident input."""
+    """Speech from pinned host memory (the e2e path: every waveform of the launch
+    group is one K0 row read over PCIe) produces bit-identical outputs to HBM-resident input."""
     ctx = lfgpu.Context(batch_size=8, n_workers=4, max_group=8, max_slot_buffers=8, seed=SEED)
     ch = ctx.chain(lfgpu.speech_ops(max_len=40000))
     rng = np.random.default_rng(22)
