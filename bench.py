@@ -23,7 +23,10 @@ value      : whole-job samples/s with raw inputs resident in HBM (device events 
              each rank's trainer stream, max over ranks)
 e2e        : same metric with raw inputs in pinned host memory (H2D of each sample's
              crop box / window inside the timed region) plus a 16-byte D2H read of every
-             delivered batch
+             delivered batch, consumed through the public streaming API (lfg_shard_start /
+             lfg_shard_next_batch / lfg_batch_release: this process is the trainer)
+dropin     : (rrc) the drop-in C++ path -- the reference's own realtime Minato wiring over our
+             headers, process_sample worker threads submitting through the C ABI
 roofline   : the dominant kernel timed alone (serial mode) with CUDA events:
              algorithmic bytes per launch / mean launch time, against MEASURED_PEAKS.json
 """
@@ -462,7 +465,7 @@ def bench_config(args, world: int) -> dict:
 
 # ------------------------------------------------------------------ runs
 def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, policy=0,
-              t_out_us=0, d2h_probe=0, capture=None):
+              t_out_us=0, d2h_probe=0, capture=None, stream=False):
     """Warm-up run, then the timed run (`ids_timed` through lfg_run_shard); the
     delivered outputs of the feed positions in `capture` are copied out of their
     batch tensors on the trainer stream (counted in d2h_bytes) for the oracle check."""
@@ -477,7 +480,15 @@ def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, 
     c0 = ctx.counters()
     descs = wl.descs(ids_timed)
     t0 = time.perf_counter()
-    rep, ids, bsz, cls = ctx.run_shard(wl.chain, descs, rc_w, capture=capture)
+    if stream:
+        # through the public streaming API: this loop is the trainer -- it receives
+        # each sealed batch (lfg_shard_next_batch) and hands it back (lfg_batch_release)
+        st = ctx.shard_stream(wl.chain, descs, rc_w, capture=capture)
+        for b, _ in st:
+            ctx.batch_release(b)
+        rep, ids, bsz, cls = st.finish()
+    else:
+        rep, ids, bsz, cls = ctx.run_shard(wl.chain, descs, rc_w, capture=capture)
     ctx.synchronize()
     wall = time.perf_counter() - t0
     barrier(dist)
@@ -677,7 +688,7 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
     wl_h = make_workload(args.workload, L, ctx, host=True, seed=args.seed, args=args)
     rep_h, ids_h, wall_h, dc_h, cap_h = run_timed(L, ctx, wl_h, ids_warm, ids_timed, args, dist, local,
                                                   trainer_us=trainer_us, policy=1 if heavy else 0,
-                                                  d2h_probe=1, capture=cap_pos)
+                                                  d2h_probe=1, capture=cap_pos, stream=trainer_us == 0)
     out["check_e2e"] = oracle_check(wl_h, ids_timed, cap_h) if cap_pos and rank == 0 else None
     wl_h.close()
     ctx.close()
@@ -709,6 +720,24 @@ def fake_measure(args, rank: int, local: int, world: int, dist) -> dict:
             "digest": id_digest(ids_timed), "digest_e2e": id_digest(ids_timed), "wall": 0.0}
 
 
+def dropin_arm():
+    """Throughput of the DROP-IN C++ path on the same C2 workload: the reference's own
+    realtime Minato wiring (process_sample worker threads, resume, build_batches,
+    run_consumer) over our headers, every process_sample submitting through the C ABI,
+    concurrent workers' samples coalesced into shared launch groups
+    (`loadflow_b200 dropin`, host/lf_dropin.cpp).  Host clock over the whole run."""
+    exe = os.path.join(ROOT, "paper_2509_10712_b200", "loadflow_b200")
+    try:
+        r = subprocess.run([exe, "dropin", "--workers", "16", "--coalesce-us", "60", "--samples", "20480",
+                            "--batch", "256", "--group", "64", "--max-seconds", "60"],
+                           capture_output=True, text=True, timeout=90)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:   # reported, never fatal for the headline line
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    return {k: d[k] for k in ("path", "value", "unit", "workers", "coalesce_us", "max_group", "samples",
+                              "samples_per_launch", "exactly_once")}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -726,6 +755,7 @@ def main():
     ap.add_argument("--check", type=int, default=8, help="delivered samples checked against the oracle")
     ap.add_argument("--serial", action="store_true", help="(experiment) all launch groups on one stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in C++ path measurement")
     ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -761,6 +791,7 @@ def main():
     value = cnt[0] / (el_max / 1e3)
     e2e = cnt[1] / (el_h / 1e3)
     cpu = None if (args.no_cpu_baseline or fake) else cpu_baseline(args.workload)
+    dropin = dropin_arm() if (args.workload == "rrc" and not fake and not args.no_dropin) else None
     steps = args.steps
     checks = [c for c in (r["check_value"], r["check_e2e"]) if c is not None]
     line = {
@@ -783,6 +814,8 @@ def main():
         "check": {"value_run": r["check_value"], "e2e_run": r["check_e2e"]},
         "wall_s": round(r["wall"], 3),
     }
+    if dropin is not None:
+        line["dropin"] = dropin
     if fake:
         line["fake_shard"] = True
     print(json.dumps(line), flush=True)

@@ -30,9 +30,11 @@
 extern "C" {
 #endif
 
-#define LFG_ABI_VERSION 4   /* 2: run config percentile / scheduler fields, report scheduler fields, lfg_run_shard_source;
+#define LFG_ABI_VERSION 5   /* 2: run config percentile / scheduler fields, report scheduler fields, lfg_run_shard_source;
                                3: run config prefetch_factor;
-                               4: run config output capture (capture_pos / capture_buf / ...) */
+                               4: run config output capture (capture_pos / capture_buf / ...);
+                               5: streaming shard runs (lfg_shard_start / lfg_shard_next_batch / lfg_shard_finish),
+                                  lfg_config.coalesce_us (was reserved0) */
 
 #define LFG_OK 0
 #define LFG_ERR_INVALID -1
@@ -114,7 +116,11 @@ typedef struct {
     int32_t max_group;          /* samples per launch group (multi-sample launch), default 1 */
     int32_t batch_size;         /* slot-buffer capacity = batch size */
     int32_t max_slot_buffers;   /* bound on live output batch buffers (HBM budget) */
-    int32_t reserved0;
+    int32_t coalesce_us;        /* ABI 5: > 0 = lfg_flush launches an open launch group only once
+                                   it is full (max_group) or its first sample has waited this
+                                   long; lfg_progress launches a due group, lfg_wait at once.
+                                   Per-sample submitters (process_sample workers) then share
+                                   launches instead of one launch per sample.  0 = flush launches */
     uint64_t seed;              /* per-sample Rng: mt19937_64(seed ^ 0x9e3779b97f4a7c15*(id+1)) */
     int64_t max_raw_bytes;      /* bound on one group's raw staging (0 = auto) */
 } lfg_config;
@@ -334,6 +340,34 @@ typedef struct {
 int lfg_run_shard_source(lfg_ctx* ctx, lfg_chain* chain, const lfg_source* src, int64_t n,
                          const lfg_run_config* cfg, lfg_run_report* report, uint64_t* consumed_ids,
                          int32_t* batch_sizes, int32_t* sample_class);
+
+/* ---- streaming consumer (ABI 5): the shard loop runs on a library thread and each
+ * sealed batch is handed to the caller, who is the trainer -- build_batches' output
+ * queue and run_consumer's next_batch (batcher.cpp:50-58, trainer.cpp:7-18).  The
+ * context lock is not held across the run: between loop passes the consumer's
+ * lfg_batch_info / lfg_batch_wait_stream / lfg_batch_copy_to_host / lfg_batch_lengths
+ * / lfg_batch_release calls interleave with sealing.  A batch stays the consumer's
+ * until lfg_batch_release; the loop waits for a free batch buffer when all of
+ * max_slot_buffers are held (back-pressure, BoundedQueue::put, queue.hpp:57-59).
+ * While a run is active, lfg_submit / lfg_seal_batch / lfg_run_shard* /
+ * lfg_time_kernels / lfg_chain_destroy / lfg_close on the context fail with
+ * LFG_ERR_STATE.  cfg->trainer_us is ignored (the caller is the trainer);
+ * captures and the d2h probe still run, ordered before the batch's ready event. */
+typedef struct lfg_shard lfg_shard;
+/* samples are copied; the payloads they point at must stay valid until finish */
+int lfg_shard_start(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples, int64_t n,
+                    const lfg_run_config* cfg, lfg_shard** out);
+/* The next sealed batch in delivery order.  timeout_us < 0 waits indefinitely.
+ * LFG_OK: *out (and *n, may be NULL) set; LFG_ERR_AGAIN: none within the timeout;
+ * LFG_ERR_CLOSED: end of stream (every sample delivered; QueueClosedError,
+ * queue.hpp:29-33); another code: the run failed (lfg_last_error). */
+int lfg_shard_next_batch(lfg_shard* sh, int64_t timeout_us, lfg_batch* out, int* n);
+/* Waits for the run to end, releasing batches the consumer did not take, fills
+ * the report (consumer_busy/span/idle from the caller's time blocked in
+ * lfg_shard_next_batch, as ConsumerStats, trainer.hpp:30-47) and the optional
+ * arrays as lfg_run_shard does, and frees the handle (also on error). */
+int lfg_shard_finish(lfg_shard* sh, lfg_run_report* report, uint64_t* consumed_ids, int32_t* batch_sizes,
+                     int32_t* sample_class);
 
 #ifdef __cplusplus
 }

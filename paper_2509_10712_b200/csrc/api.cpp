@@ -1,7 +1,10 @@
 // api.cpp -- extern "C" entry points (include/lfgpu.h).  Every call takes the
 // context lock, converts engine exceptions into LFG_ERR_* codes and records a
 // thread-local message for lfg_last_error().
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -13,7 +16,8 @@
 namespace lfg {
 int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_t n,
               const lfg_run_config& rc, lfg_run_report& rep, uint64_t* consumed_ids,
-              int32_t* batch_sizes, int32_t* sample_class, const lfg_source* src = nullptr);
+              int32_t* batch_sizes, int32_t* sample_class, const lfg_source* src = nullptr,
+              const ShardStream* ss = nullptr);
 }
 
 using namespace lfg;
@@ -24,6 +28,29 @@ struct lfg_ctx {
 struct lfg_chain {
     Chain* impl;
     lfg_ctx* ctx;
+};
+// A streaming shard run: the Algorithm-1 loop on its own thread, sealed batches
+// queued for the consumer (the reference's BatchQueue between build_batches and
+// run_consumer, batcher.cpp:50-58 / trainer.cpp:7-18).
+struct lfg_shard {
+    lfg_ctx* ctx = nullptr;
+    std::vector<lfg_sample_desc> samples;
+    lfg_run_config cfg{};
+    std::thread th;
+    std::mutex qm;
+    std::condition_variable cv;
+    std::deque<std::pair<int64_t, int>> q;   // (batch, samples), delivery order
+    bool ended = false;
+    int rc = LFG_OK;
+    std::string err;
+    lfg_run_report rep{};
+    std::vector<uint64_t> ids;
+    std::vector<int32_t> sizes, cls;
+    // consumer-side ConsumerStats (trainer.hpp:30-47): host time blocked in next_batch
+    std::chrono::steady_clock::time_point t_first, t_last;
+    bool started = false;
+    double wait_us = 0;
+    int64_t taken = 0;
 };
 
 namespace {
@@ -45,6 +72,10 @@ int guarded(F&& f) {
         g_last_error = e.what();
         return LFG_ERR_STATE;
     }
+}
+
+void refuse_while_streaming(const Context& c) {
+    if (c.streaming) fail(LFG_ERR_STATE, "a streaming shard run owns this context (lfg_shard_finish first)");
 }
 
 Context& C(lfg_ctx* ctx) {
@@ -140,6 +171,10 @@ int lfg_open(const lfg_config* cfg, lfg_ctx** out) {
 int lfg_close(lfg_ctx* ctx) {
     return guarded([&] {
         if (!ctx) fail(LFG_ERR_INVALID, "null context");
+        {
+            std::lock_guard<std::mutex> g(ctx->impl->mu);
+            refuse_while_streaming(*ctx->impl);
+        }
         cudaSetDevice(ctx->impl->cfg.device);
         delete ctx->impl;
         delete ctx;
@@ -208,6 +243,7 @@ int lfg_chain_destroy(lfg_ctx* ctx, lfg_chain* chain) {
         Context& c = C(ctx);
         if (!chain) fail(LFG_ERR_INVALID, "null chain");
         std::lock_guard<std::mutex> g(c.mu);
+        refuse_while_streaming(c);
         c.chain_destroy(chain->impl);
         delete chain;
     });
@@ -282,6 +318,7 @@ int lfg_submit(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* s, lfg_tic
         Context& c = C(ctx);
         if (!chain || !s || !out) fail(LFG_ERR_INVALID, "null argument");
         std::lock_guard<std::mutex> g(c.mu);
+        refuse_while_streaming(c);
         *out = c.submit(chain->impl, *s);
     });
 }
@@ -290,7 +327,7 @@ int lfg_flush(lfg_ctx* ctx) {
     return guarded([&] {
         Context& c = C(ctx);
         std::lock_guard<std::mutex> g(c.mu);
-        c.flush();
+        c.flush_due();
     });
 }
 
@@ -356,6 +393,7 @@ int lfg_seal_batch(lfg_ctx* ctx, const lfg_ticket* tickets, int n, lfg_batch* ou
         Context& c = C(ctx);
         if (!tickets || !out) fail(LFG_ERR_INVALID, "null argument");
         std::lock_guard<std::mutex> g(c.mu);
+        refuse_while_streaming(c);
         *out = c.seal(tickets, n);
     });
 }
@@ -558,6 +596,7 @@ int lfg_time_kernels(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samp
         Context& c = C(ctx);
         if (!chain || !samples || !mean_ms || !launches || !bytes || !flops) fail(LFG_ERR_INVALID, "null argument");
         std::lock_guard<std::mutex> g(c.mu);
+        refuse_while_streaming(c);
         c.time_kernels(chain->impl, samples, n, mean_ms, launches, bytes, flops);
     });
 }
@@ -577,6 +616,7 @@ int lfg_run_shard(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples
         Context& c = C(ctx);
         if (!chain || !cfg || !report) fail(LFG_ERR_INVALID, "null argument");
         std::lock_guard<std::mutex> g(c.mu);
+        refuse_while_streaming(c);
         run_shard(c, chain->impl, samples, n, *cfg, *report, consumed_ids, batch_sizes,
                   sample_class);
     });
@@ -589,8 +629,150 @@ int lfg_run_shard_source(lfg_ctx* ctx, lfg_chain* chain, const lfg_source* src, 
         Context& c = C(ctx);
         if (!chain || !cfg || !report || !src) fail(LFG_ERR_INVALID, "null argument");
         std::lock_guard<std::mutex> g(c.mu);
+        refuse_while_streaming(c);
         run_shard(c, chain->impl, nullptr, n, *cfg, *report, consumed_ids, batch_sizes, sample_class, src);
     });
+}
+
+namespace {
+void shard_deliver(void* user, int64_t b, int n) {
+    auto* sh = static_cast<lfg_shard*>(user);
+    {
+        std::lock_guard<std::mutex> g(sh->qm);
+        sh->q.emplace_back(b, n);
+    }
+    sh->cv.notify_one();
+}
+}  // namespace
+
+int lfg_shard_start(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* samples, int64_t n,
+                    const lfg_run_config* cfg, lfg_shard** out) {
+    return guarded([&] {
+        Context& c = C(ctx);
+        if (!chain || !cfg || !out || n < 0 || (n > 0 && !samples)) fail(LFG_ERR_INVALID, "null argument");
+        *out = nullptr;
+        {
+            std::lock_guard<std::mutex> g(c.mu);
+            if (c.streaming) fail(LFG_ERR_STATE, "a streaming shard run is already active on this context");
+            c.streaming = true;
+        }
+        auto sh = std::make_unique<lfg_shard>();
+        sh->ctx = ctx;
+        sh->samples.assign(samples, samples + n);
+        sh->cfg = *cfg;
+        sh->cfg.trainer_us = 0;   // the caller is the trainer
+        sh->ids.resize(static_cast<size_t>(n));
+        sh->sizes.resize(static_cast<size_t>(n));
+        sh->cls.resize(static_cast<size_t>(n));
+        lfg_shard* p = sh.get();
+        Chain* ch = chain->impl;
+        p->th = std::thread([p, ch, n] {
+            Context& cx = *p->ctx->impl;
+            int rc = LFG_OK;
+            std::string err;
+            try {
+                cuda_check(cudaSetDevice(cx.cfg.device), "cudaSetDevice");
+                ShardStream ss;
+                ss.lock = &cx.mu;
+                ss.deliver = shard_deliver;
+                ss.user = p;
+                run_shard(cx, ch, p->samples.data(), n, p->cfg, p->rep, p->ids.data(), p->sizes.data(),
+                          p->cls.data(), nullptr, &ss);
+            } catch (const Error& e) {
+                rc = e.code;
+                err = e.msg;
+            } catch (const std::exception& e) {
+                rc = LFG_ERR_STATE;
+                err = e.what();
+            }
+            {
+                std::lock_guard<std::mutex> g(cx.mu);
+                cx.streaming = false;
+            }
+            {
+                std::lock_guard<std::mutex> g(p->qm);
+                p->rc = rc;
+                p->err = err;
+                p->ended = true;
+            }
+            p->cv.notify_all();
+        });
+        *out = sh.release();
+    });
+}
+
+int lfg_shard_next_batch(lfg_shard* sh, int64_t timeout_us, lfg_batch* out, int* n) {
+    return guarded([&] {
+        if (!sh || !out) fail(LFG_ERR_INVALID, "null argument");
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!sh->started) {
+            sh->started = true;
+            sh->t_first = t0;
+        }
+        std::unique_lock<std::mutex> lk(sh->qm);
+        auto have = [&] { return !sh->q.empty() || sh->ended; };
+        if (timeout_us < 0) sh->cv.wait(lk, have);
+        else sh->cv.wait_for(lk, std::chrono::microseconds(timeout_us), have);
+        const auto t1 = std::chrono::steady_clock::now();
+        sh->wait_us += std::chrono::duration<double, std::micro>(t1 - t0).count();
+        sh->t_last = t1;
+        if (!sh->q.empty()) {
+            *out = sh->q.front().first;
+            if (n) *n = sh->q.front().second;
+            sh->q.pop_front();
+            ++sh->taken;
+            return;
+        }
+        if (!sh->ended) fail(LFG_ERR_AGAIN, "no batch sealed within the timeout");
+        if (sh->rc != LFG_OK) fail(sh->rc, "shard run failed: " + sh->err);
+        fail(LFG_ERR_CLOSED, "end of stream: every sample was delivered");
+    });
+}
+
+int lfg_shard_finish(lfg_shard* sh, lfg_run_report* report, uint64_t* consumed_ids, int32_t* batch_sizes,
+                     int32_t* sample_class) {
+    if (!sh) {
+        g_last_error = "null shard";
+        return LFG_ERR_INVALID;
+    }
+    // drain: batches the consumer never took go back to the pool as they arrive
+    for (;;) {
+        std::pair<int64_t, int> b{-1, 0};
+        bool end = false;
+        {
+            std::unique_lock<std::mutex> lk(sh->qm);
+            sh->cv.wait(lk, [&] { return !sh->q.empty() || sh->ended; });
+            if (!sh->q.empty()) {
+                b = sh->q.front();
+                sh->q.pop_front();
+            } else {
+                end = true;
+            }
+        }
+        if (end) break;
+        lfg_batch_release(sh->ctx, b.first, nullptr);
+    }
+    if (sh->th.joinable()) sh->th.join();
+    const int rc = sh->rc;
+    if (rc == LFG_OK) {
+        const int64_t n = static_cast<int64_t>(sh->samples.size());
+        if (report) {
+            *report = sh->rep;
+            // consumer idle as ConsumerStats counts it: time blocked waiting for a batch
+            // over the consumer's span (first next_batch call .. last return)
+            const double span = sh->started ? std::chrono::duration<double, std::micro>(sh->t_last - sh->t_first).count() : 0.0;
+            report->consumer_span_ms = span / 1000.0;
+            report->consumer_busy_ms = std::max(0.0, span - sh->wait_us) / 1000.0;
+            report->consumer_idle_frac = span > 0 ? std::min(1.0, sh->wait_us / span) : 1.0;
+        }
+        if (consumed_ids) std::copy(sh->ids.begin(), sh->ids.begin() + std::min<int64_t>(n, sh->rep.samples), consumed_ids);
+        if (batch_sizes) std::copy(sh->sizes.begin(), sh->sizes.begin() + std::min<int64_t>(n, sh->rep.batches), batch_sizes);
+        if (sample_class) std::copy(sh->cls.begin(), sh->cls.end(), sample_class);
+    } else {
+        g_last_error = "shard run failed: " + sh->err;
+    }
+    delete sh;
+    return rc;
 }
 
 }  // extern "C"

@@ -911,6 +911,7 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
         ng.chain = c;
         ng.src_kind = s.src_kind;
         ng.tickets.reserve(static_cast<size_t>(std::max(1, cfg.max_group)));
+        if (cfg.coalesce_us > 0) ng.t_open_us = host_now_us();
         og[c] = gi;
     } else {
         gi = it->second;
@@ -952,6 +953,26 @@ void Context::flush() {
     for (auto& og : open_group_) {
         for (auto& kv : og) launch_group(groups[kv.second]);
         og.clear();
+    }
+}
+
+void Context::flush_due() {
+    if (cfg.coalesce_us <= 0) {
+        flush();
+        return;
+    }
+    for (int64_t gi : deferred_) launch_group(groups[gi]);
+    deferred_.clear();
+    const int64_t now = host_now_us();
+    for (auto& og : open_group_) {
+        std::vector<const Chain*> due;
+        for (auto& kv : og)
+            if (now - groups[kv.second].t_open_us >= cfg.coalesce_us) due.push_back(kv.first);
+        for (const Chain* c : due) {
+            const int64_t gi = og.find(c)->second;
+            og.erase(c);
+            launch_group(groups[gi]);
+        }
     }
 }
 
@@ -1483,6 +1504,9 @@ void Context::finalize_group_timing(Group& g) {
 
 void Context::progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed_us) {
     Group& g = group_of(t);
+    // a coalescing group still open launches once its deadline passed
+    if (!g.launched && !g.complete && cfg.coalesce_us > 0 && host_now_us() - g.t_open_us >= cfg.coalesce_us)
+        launch_if_pending(t);
     poll_group(g);
     const bool done = sample_ready(t);   // its own stamp, or the whole group
     const auto& st = g.chain->stages;
@@ -1704,7 +1728,9 @@ void Context::batch_release(int64_t b, cudaStream_t s, bool readers) {
     buf.in_batch = false;
     if (br.in_place) buf.live -= br.n;
     br.released = true;
-    if (br.ready) put_event(br.ready);
+    // the ready event also covers work queued before it on the delivering stream (a
+    // streaming run's captures / probe): the buffer is reused only after it, too
+    if (br.ready) buf.pending.push_back(br.ready);
     br.ready = nullptr;
 }
 

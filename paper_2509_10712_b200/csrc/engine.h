@@ -177,6 +177,7 @@ struct Group {
     bool complete = false;
     int stages_done = 0;
     int64_t t_launch_us = 0;
+    int64_t t_open_us = 0;       // first submit (coalescing deadline, lfg_config.coalesce_us)
     int64_t raw_idx = -1;
     int refs = 0;
     bool timed = true;             // stage events carry timing (Context::time_groups at launch)
@@ -253,6 +254,16 @@ private:
     bool quit_ = false;
 };
 
+// Streaming delivery (lfg_shard_start / lfg_shard_next_batch): the shard loop holds
+// `lock` (the context lock) except between passes, so the consumer's batch calls
+// (info / wait / release) interleave with it, and each sealed batch goes to
+// deliver() instead of the internal trainer -- the consumer releases it.
+struct ShardStream {
+    std::mutex* lock = nullptr;
+    void (*deliver)(void* user, int64_t batch, int n) = nullptr;
+    void* user = nullptr;
+};
+
 class Context {
 public:
     explicit Context(const lfg_config& cfg);
@@ -266,6 +277,8 @@ public:
 
     int64_t submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre = nullptr);
     void flush();
+    // lfg_flush: with coalesce_us > 0 only groups open that long (or full) launch
+    void flush_due();
     void progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed_us);
     void wait(int64_t t);                 // blocking; callers must not hold `mu` (see lfg_wait)
     bool launch_if_pending(int64_t t);    // launches t's open group if needed; true if complete
@@ -309,6 +322,7 @@ public:
             return true;
         return poll_group(g);
     }
+    cudaEvent_t make_ready_event() { return get_event(); }   // a batch's pooled ready event
     bool poll_group(Group& g);          // updates stages_done/complete; true if complete
     void finalize_group_timing(Group& g);
     int64_t open_group_count() const;
@@ -347,6 +361,9 @@ public:
     void time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms, int64_t* launches,
                       int64_t* bytes, int64_t* flops);
     std::mutex mu;   // one lock per context (C ABI calls serialise on it)
+    // a streaming shard run (lfg_shard_start) is active: its loop takes `mu` per pass;
+    // calls that submit or run another shard are refused until it ends
+    bool streaming = false;
     std::unique_ptr<WorkerThreads> workers;   // parameter draws of shard runs
 
     cudaStream_t seal_stream = nullptr;

@@ -120,7 +120,11 @@ struct Phases {
 
 int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_t n,
               const lfg_run_config& rc, lfg_run_report& rep, uint64_t* consumed_ids,
-              int32_t* batch_sizes, int32_t* sample_class, const lfg_source* src) {
+              int32_t* batch_sizes, int32_t* sample_class, const lfg_source* src,
+              const ShardStream* ss) {
+    // streaming delivery: the context lock is held except between loop passes
+    std::unique_lock<std::mutex> lk;
+    if (ss != nullptr) lk = std::unique_lock<std::mutex>(*ss->lock);
     if (src != nullptr && src->next == nullptr) fail(LFG_ERR_INVALID, "source without next()");
     // streaming input: descriptors arrive through src->next, in feed order
     std::vector<lfg_sample_desc> src_descs;
@@ -417,7 +421,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     const double v_ns0 = ctx.prof_views_ns, d_ns0 = ctx.prof_desc_ns;
     const double q_ns0 = ctx.prof_query_ns, f_ns0 = ctx.prof_final_ns;
     const int64_t nq0 = ctx.prof_queries;
-    int64_t iters = 0;
+    int64_t iters = 0, idle_passes = 0;
     const size_t groups0 = ctx.groups.size();
     // Full scans (every in-flight group's event queried) every 10 us when timeouts
     // or the profiler need prompt completions.  Without them a group's samples only
@@ -613,7 +617,11 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             BatchRec& br = ctx.batch(b);
             if (sync) sync_next += k;
             const bool timed = nbatches >= rc.warmup_batches;
-            if (timed && rc.trainer_us > 0) {
+            if (ss != nullptr) {
+                // the consumer owns the batch: the trainer stream only marks its delivery
+                // (the run's device-timed span) and carries the captures / probe
+                ctx.batch_wait_stream(b, trainer);
+            } else if (timed && rc.trainer_us > 0) {
                 cudaEvent_t s0 = mk(), s1 = mk();
                 ctx.batch_wait_stream(b, trainer);
                 cuda_check(cudaEventRecord(s0, trainer), "record");
@@ -657,8 +665,16 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 cuda_check(cudaEventRecord(ce, trainer), "record consume");
                 consume_q.push_back(ce);
             }
-            ctx.batch_release(b, trainer, rc.trainer_us > 0 || probe != nullptr || captured);
+            if (ss != nullptr) {
+                if (captured || probe != nullptr) {   // the consumer's wait also covers the reads queued here
+                    if (br.ready == nullptr) br.ready = ctx.make_ready_event();
+                    cuda_check(cudaEventRecord(br.ready, trainer), "record delivery");
+                }
+            } else {
+                ctx.batch_release(b, trainer, rc.trainer_us > 0 || probe != nullptr || captured);
+            }
             for (int64_t t : ts) ctx.ticket_release(t);
+            if (ss != nullptr) ss->deliver(ss->user, b, br.n);
             ++nbatches;
             if (nbatches == rc.warmup_batches) {
                 t_timed = mk();
@@ -699,6 +715,16 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             if (inflight.empty() && parked.empty() && fed == n && fast.empty() && slow.empty() &&
                 !(sync && sync_next < n))
                 fail(LFG_ERR_STATE, "shard stalled with samples unaccounted for");
+        }
+        idle_passes = progressed ? 0 : idle_passes + 1;
+        if (lk.owns_lock()) {
+            // between passes the consumer's batch calls take the context lock; a loop
+            // that has waited a while (the consumer holds every batch buffer) naps
+            lk.unlock();
+            if (idle_passes > 256) std::this_thread::sleep_for(std::chrono::microseconds(20));
+            else if (idle_passes > 0) std::this_thread::yield();
+            lk.lock();
+        } else if (!progressed) {
             std::this_thread::yield();
         }
         ph.lap(Phases::IDLE);
@@ -717,7 +743,11 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                 }
             }
         }
-        if (!inflight.empty() || !parked.empty()) std::this_thread::yield();
+        if (!inflight.empty() || !parked.empty()) {
+            if (lk.owns_lock()) lk.unlock();
+            std::this_thread::yield();
+            if (ss != nullptr) lk.lock();
+        }
     }
     ph.print(n, ctx.prof_group_ns - g_ns0, ctx.prof_launch_ns - l_ns0,
              static_cast<int64_t>(ctx.groups.size() - groups0));

@@ -19,6 +19,8 @@
 #include <mutex>
 #include <thread>
 
+#include <sys/prctl.h>
+
 #include "loadflow/api.hpp"
 
 namespace loadflow {
@@ -42,6 +44,31 @@ void check(int rc) {
         case LFG_ERR_CLOSED: throw QueueClosedError(msg);
         default: throw std::runtime_error("lfgpu error " + std::to_string(rc) + ": " + msg);
     }
+}
+
+// A full output pool (LFG_ERR_AGAIN: every slot / batch buffer holds samples the
+// batcher or consumer has not released yet) is back-pressure: the caller waits, as
+// BoundedQueue::put blocks on a full queue (queue.hpp:57-59), instead of failing.
+template <typename F>
+void retry_full(F&& call) {
+    for (int k = 0;; ++k) {
+        const int rc = call();
+        if (rc != LFG_ERR_AGAIN) {
+            check(rc);
+            return;
+        }
+        if (k < 64) std::this_thread::yield();
+        else std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
+void poll_pause() {
+    thread_local bool slack = [] {
+        prctl(PR_SET_TIMERSLACK, 1000UL, 0, 0, 0);   // 1 us: short sleeps stay short
+        return true;
+    }();
+    (void)slack;
+    std::this_thread::sleep_for(std::chrono::microseconds(4));
 }
 
 lfg_ctx* ctx_of(const Sample& s) {
@@ -155,7 +182,7 @@ void seal_device_batch(Batch& b) {
     std::vector<lfg_ticket> ts;
     for (const Sample& s : b.samples) ts.push_back(s.device.ticket);
     lfg_batch h = -1;
-    check(lfg_seal_batch(ctx, ts.data(), static_cast<int>(ts.size()), &h));
+    retry_full([&] { return lfg_seal_batch(ctx, ts.data(), static_cast<int>(ts.size()), &h); });
     for (lfg_ticket t : ts) check(lfg_ticket_release(ctx, t));
     b.device_batch = h;
 }
@@ -170,7 +197,7 @@ RouteResult process_on_device(Sample s, DurationMs t_out, SampleQueue& fast_q, T
     lfg_chain* chain = compiled(ctx, *s.chain);
     const std::size_t n = s.chain->size();
     s.device.desc.id = s.id;
-    check(lfg_submit(ctx, chain, &s.device.desc, &s.device.ticket));
+    retry_full([&] { return lfg_submit(ctx, chain, &s.device.desc, &s.device.ticket); });
     check(lfg_flush(ctx));
     RouteResult res;
     const TimeMs t0 = rt.now();
@@ -216,7 +243,10 @@ RouteResult process_on_device(Sample s, DurationMs t_out, SampleQueue& fast_q, T
                 break;
             }
             if (el > t_out) return park(static_cast<std::size_t>(ops_done), el);
-            std::this_thread::yield();
+            // every worker thread polls its own sample: sleep between polls (1 us timer
+            // slack) rather than spin, so the pollers do not keep the context lock and
+            // the host cores busy that the submitting workers need
+            poll_pause();
         }
     }
     advance_to(s, n);

@@ -4,6 +4,7 @@
 //
 //   loadflow_b200 run <config.ini> [--loader minato-gpu|sync-gpu] [--seed N] [--out DIR]
 //   loadflow_b200 compare <report.json>... [--csv FILE]
+//   loadflow_b200 dropin [...]   (lf_dropin.cpp: throughput of the drop-in C++ path)
 //
 // The config file uses the reference's flat `[section] key = value` format and key
 // names (experiment.cpp:64-116): workload.name / n_samples / seed,
@@ -404,17 +405,22 @@ int cmd_compare(const std::vector<std::string>& paths, const std::string& csv_ou
 
 int usage() {
     std::cerr << "usage: loadflow_b200 run <config.ini> [--loader minato-gpu|sync-gpu] [--seed N] [--out DIR]\n"
-                 "       loadflow_b200 compare <report.json>... [--csv FILE]\n";
+                 "       loadflow_b200 compare <report.json>... [--csv FILE]\n"
+                 "       loadflow_b200 dropin [--workers N] [--samples N] [--batch B] [--group G]\n"
+                 "                            [--coalesce-us U] [--t-out-us T] [--pool P] [--seed S] [--max-seconds M]\n";
     return 1;
 }
 
 }  // namespace
+
+int cmd_dropin(int argc, char** argv);   // lf_dropin.cpp
 
 int main(int argc, char** argv) {
     // the application's choice (the library never sets it): one hardware queue per
     // launch-group stream, before the first CUDA call creates the device context
     setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
     try {
+        if (argc >= 2 && std::string(argv[1]) == "dropin") return cmd_dropin(argc, argv);
         if (argc < 3) return usage();
         const std::string cmd = argv[1];
         if (cmd == "run") {

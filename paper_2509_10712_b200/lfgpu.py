@@ -59,7 +59,7 @@ class SampleDesc(C.Structure):
 class Config(C.Structure):
     _fields_ = [("device", C.c_int32), ("n_workers", C.c_int32), ("max_group", C.c_int32),
                 ("batch_size", C.c_int32), ("max_slot_buffers", C.c_int32),
-                ("reserved0", C.c_int32), ("seed", C.c_uint64), ("max_raw_bytes", C.c_int64)]
+                ("coalesce_us", C.c_int32), ("seed", C.c_uint64), ("max_raw_bytes", C.c_int64)]
 
 
 class Counters(C.Structure):
@@ -151,6 +151,9 @@ _sig = {
                        _P(C.c_uint64), _P(C.c_int32), _P(C.c_int32)], C.c_int),
     "lfg_run_shard_source": ([_vp, _vp, _vp, C.c_int64, _P(RunConfig), _P(RunReport),
                               _P(C.c_uint64), _P(C.c_int32), _P(C.c_int32)], C.c_int),
+    "lfg_shard_start": ([_vp, _vp, _P(SampleDesc), C.c_int64, _P(RunConfig), _P(_vp)], C.c_int),
+    "lfg_shard_next_batch": ([_vp, C.c_int64, _P(C.c_int64), _P(C.c_int)], C.c_int),
+    "lfg_shard_finish": ([_vp, _P(RunReport), _P(C.c_uint64), _P(C.c_int32), _P(C.c_int32)], C.c_int),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
@@ -300,11 +303,12 @@ class Context:
     """One GPU shard (lfg_ctx)."""
 
     def __init__(self, device=0, batch_size=24, n_workers=12, max_group=1, max_slot_buffers=8,
-                 seed=1):
+                 seed=1, coalesce_us=0):
         cfg = Config()
         _lib.lfg_config_default(C.byref(cfg))
         cfg.device, cfg.batch_size, cfg.n_workers = device, batch_size, n_workers
         cfg.max_group, cfg.max_slot_buffers, cfg.seed = max_group, max_slot_buffers, seed
+        cfg.coalesce_us = coalesce_us
         self.cfg = cfg
         h = _vp()
         _check(_lib.lfg_open(C.byref(cfg), C.byref(h)))
@@ -460,29 +464,50 @@ class Context:
         ids = (C.c_uint64 * max(n, 1))()
         bs = (C.c_int32 * max(n, 1))()
         cls = (C.c_int32 * max(n, 1))()
-        buf = None
-        if capture:
-            _, stride, _ = ch.info()
-            stride = (stride + 255) // 256 * 256
-            pos = (C.c_int64 * len(capture))(*capture)
-            done = (C.c_int32 * len(capture))()
-            buf = self.host_alloc(stride * len(capture))
-            rc.n_capture, rc.capture_pos, rc.capture_buf = len(capture), pos, buf
-            rc.capture_stride, rc.capture_done = stride, done
+        cap = self._capture_begin(ch, rc, capture)
         try:
             _check(_lib.lfg_run_shard(self.h, ch.handle, arr, n, C.byref(rc), C.byref(rep),
                                       ids if want_ids else None, bs if want_ids else None,
                                       cls if want_ids else None))
-            if buf is not None:
-                raw = np.ctypeslib.as_array((C.c_uint8 * (stride * len(capture))).from_address(buf))
-                self.last_capture = {int(p): (raw[k * stride:(k + 1) * stride].copy(), int(done[k]) - 1)
-                                     for k, p in enumerate(capture) if done[k] > 0}
+            self._capture_collect(cap)
         finally:
-            if buf is not None:
-                rc.n_capture, rc.capture_pos, rc.capture_buf, rc.capture_done = 0, None, None, None
-                self.host_free(buf)
+            self._capture_end(rc, cap)
         nb = rep.batches
         return rep, np.array(ids[:n], dtype=np.uint64), np.array(bs[:nb]), np.array(cls[:n])
+
+    # output capture of delivered samples (lfg_run_config capture fields)
+    def _capture_begin(self, ch: Chain, rc: RunConfig, capture):
+        if not capture:
+            return None
+        _, stride, _ = ch.info()
+        stride = (stride + 255) // 256 * 256
+        pos = (C.c_int64 * len(capture))(*capture)
+        done = (C.c_int32 * len(capture))()
+        buf = self.host_alloc(stride * len(capture))
+        rc.n_capture, rc.capture_pos, rc.capture_buf = len(capture), pos, buf
+        rc.capture_stride, rc.capture_done = stride, done
+        return (list(capture), stride, pos, done, buf)
+
+    def _capture_collect(self, cap):
+        if cap is None:
+            return
+        capture, stride, _, done, buf = cap
+        raw = np.ctypeslib.as_array((C.c_uint8 * (stride * len(capture))).from_address(buf))
+        self.last_capture = {int(p): (raw[k * stride:(k + 1) * stride].copy(), int(done[k]) - 1)
+                             for k, p in enumerate(capture) if done[k] > 0}
+
+    def _capture_end(self, rc: RunConfig, cap):
+        if cap is None:
+            return
+        rc.n_capture, rc.capture_pos, rc.capture_buf, rc.capture_done = 0, None, None, None
+        self.host_free(cap[4])
+
+    def shard_stream(self, ch: Chain, descs: Sequence[SampleDesc], rc: RunConfig,
+                     capture: Sequence[int] | None = None) -> "ShardStream":
+        """lfg_shard_start: the shard loop on a library thread; iterate the returned
+        stream for sealed batches (the caller is the trainer and releases each one).
+        ``capture`` as in run_shard (collected into ``last_capture`` by finish())."""
+        return ShardStream(self, ch, descs, rc, capture)
 
     def run_shard_source(self, ch: Chain, src: "FileSource", rc: RunConfig):
         """lfg_run_shard_source: the shard pulls samples from a streaming source."""
@@ -494,6 +519,59 @@ class Context:
         _check(_lib.lfg_run_shard_source(self.h, ch.handle, C.addressof(src.src), n, C.byref(rc), C.byref(rep),
                                          ids, bs, cls))
         return rep, np.array(ids[:n], dtype=np.uint64), np.array(bs[:rep.batches]), np.array(cls[:n])
+
+
+class ShardStream:
+    """A streaming shard run (lfg_shard_start / lfg_shard_next_batch / lfg_shard_finish):
+    ``next_batch()`` returns ``(batch, n)``, ``None`` at the end of the stream; the batch
+    is the caller's until ``ctx.batch_release(batch, stream)``.  ``finish()`` returns
+    ``(report, consumed ids, batch sizes, sample classes)`` as ``Context.run_shard``."""
+
+    def __init__(self, ctx: Context, ch: Chain, descs: Sequence[SampleDesc], rc: RunConfig, capture=None):
+        self.ctx = ctx
+        self.n = len(descs)
+        arr = (SampleDesc * max(self.n, 1))(*descs)
+        self.h = _vp()
+        self.rc = rc
+        self.cap = ctx._capture_begin(ch, rc, capture)   # kept alive until finish()
+        try:
+            _check(_lib.lfg_shard_start(ctx.h, ch.handle, arr, self.n, C.byref(rc), C.byref(self.h)))
+        except Exception:
+            ctx._capture_end(rc, self.cap)
+            raise
+
+    def next_batch(self, timeout_us: int = -1):
+        b, n = C.c_int64(-1), C.c_int(0)
+        rc = _lib.lfg_shard_next_batch(self.h, timeout_us, C.byref(b), C.byref(n))
+        if rc == ERR_CLOSED:
+            return None
+        if rc == ERR_AGAIN:
+            raise TimeoutError(_lib.lfg_last_error().decode(errors="replace"))
+        _check(rc)
+        return b.value, n.value
+
+    def __iter__(self):
+        while True:
+            r = self.next_batch()
+            if r is None:
+                return
+            yield r
+
+    def finish(self):
+        if not self.h:
+            raise LfgError(ERR_STATE, "stream already finished")
+        n = max(self.n, 1)
+        rep = RunReport()
+        ids = (C.c_uint64 * n)()
+        bs = (C.c_int32 * n)()
+        cls = (C.c_int32 * n)()
+        h, self.h = self.h, _vp()
+        try:
+            _check(_lib.lfg_shard_finish(h, C.byref(rep), ids, bs, cls))
+            self.ctx._capture_collect(self.cap)
+        finally:
+            self.ctx._capture_end(self.rc, self.cap)
+        return rep, np.array(ids[:self.n], dtype=np.uint64), np.array(bs[:rep.batches]), np.array(cls[:self.n])
 
 
 # ---- raw sample files + reader-thread source (include/lfgpu_files.h, host library) ----

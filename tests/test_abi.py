@@ -37,7 +37,7 @@ def test_library_is_sm100a(lfgpu):
 
 
 def test_abi_version_and_defaults(lfgpu):
-    assert lfgpu._lib.lfg_abi_version() == 4
+    assert lfgpu._lib.lfg_abi_version() == 5
     cfg = lfgpu.Config()
     lfgpu._lib.lfg_config_default(ctypes.byref(cfg))
     assert cfg.n_workers == 12 and cfg.batch_size == 24 and cfg.seed == 1

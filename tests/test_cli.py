@@ -52,3 +52,26 @@ def test_cli_run_and_compare_on_gpu(cli, tmp_path):
                         str(tmp_path / "minato-gpu" / "report.json"), "--csv", str(tmp_path / "cmp.csv")],
                        capture_output=True, text=True)
     assert r.returncode == 0 and "minato-gpu" in r.stdout and (tmp_path / "cmp.csv").exists()
+
+
+def test_cli_dropin_usage(cli):
+    r = subprocess.run([cli, "dropin", "--bogus", "1"], capture_output=True, text=True)
+    assert r.returncode == 2 and "unknown option" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_dropin_coalesces_per_sample_submissions(cli):
+    """The drop-in C++ path (run_minato_pipeline wiring, one process_sample per worker
+    thread) delivers every sample exactly once; with coalescing its workers' samples
+    share launch groups instead of one launch per sample."""
+    res = {}
+    for co in (0, 40):
+        r = subprocess.run([cli, "dropin", "--samples", "4096", "--workers", "16", "--batch", "64",
+                            "--group", "16", "--coalesce-us", str(co), "--max-seconds", "100"],
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        res[co] = json.loads(r.stdout.strip().splitlines()[-1])
+        assert res[co]["exactly_once"] is True and res[co]["samples"] == 4096
+    assert res[0]["samples_per_launch"] < 1.5
+    assert res[40]["samples_per_launch"] > 2.0
+    print(res)
