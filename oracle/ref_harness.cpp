@@ -235,6 +235,7 @@ int main(int argc, char** argv) {
     const int warmup = arg_int(argc, argv, "--warmup", 2);
     const int cores = arg_int(argc, argv, "--workers", (int)std::max(1u, std::thread::hardware_concurrency()));
     const int max_s = arg_int(argc, argv, "--max-seconds", 150);
+    const int feeders = std::max(1, arg_int(argc, argv, "--feeders", 4));
     // C5 sweep knobs: a heavy-tailed fraction of samples gets an
     // extra synthetic cost (a leading "SampleCost" transform that sleeps), the
     // consumer computes for trainer_ms per batch (trainer.hpp:15), and the
@@ -373,34 +374,44 @@ int main(int argc, char** argv) {
             fast[slot]->close();
             temp[slot]->close();
         });
-    // a sample with its fp64 payload [id, dims..., data...] (one of the pool's inputs)
+    // The pool's inputs as fp64 payloads [id, dims..., data...], built once before the
+    // clock starts; a fed sample copies its template (the feeder loads, the workers
+    // transform -- experiment.cpp:221-228), so the feeders never bound the loader.
+    std::vector<std::vector<double>> tmpl(static_cast<size_t>(pool));
+    for (int q = 0; q < pool; ++q) {
+        auto& t = tmpl[static_cast<size_t>(q)];
+        if (rrc) {
+            const auto& im = images[q];
+            const auto [h, w] = hw[q];
+            t.resize(kHdr2d + im.size());
+            t[1] = h;
+            t[2] = w;
+            for (size_t k = 0; k < im.size(); ++k) t[kHdr2d + k] = im[k];
+        } else {
+            const auto& v = vols[q];
+            const auto& l = lbls[q];
+            t.resize(kHdr3d + 2 * v.size());
+            t[1] = D;
+            t[2] = H3;
+            t[3] = W3;
+            for (size_t k = 0; k < v.size(); ++k) t[kHdr3d + k] = v[k];
+            for (size_t k = 0; k < l.size(); ++k) t[kHdr3d + v.size() + k] = l[k];
+        }
+    }
     auto make_payload_sample = [&](int64_t i) {
         Sample s;
         s.id = (uint64_t)i;
         s.chain = &chain;
-        if (rrc) {
-            const auto& im = images[i % pool];
-            const auto [h, w] = hw[i % pool];
-            s.payload.resize(kHdr2d + im.size());
-            s.payload[0] = (double)i;
-            s.payload[1] = h;
-            s.payload[2] = w;
-            for (size_t k = 0; k < im.size(); ++k) s.payload[kHdr2d + k] = im[k];
-        } else {
-            const auto& v = vols[i % pool];
-            const auto& l = lbls[i % pool];
-            s.payload.resize(kHdr3d + 2 * v.size());
-            s.payload[0] = (double)i;
-            s.payload[1] = D;
-            s.payload[2] = H3;
-            s.payload[3] = W3;
-            for (size_t k = 0; k < v.size(); ++k) s.payload[kHdr3d + k] = v[k];
-            for (size_t k = 0; k < l.size(); ++k) s.payload[kHdr3d + v.size() + k] = l[k];
-        }
+        s.payload = tmpl[static_cast<size_t>(i % pool)];
+        s.payload[0] = (double)i;
         s.bytes_in = s.size_bytes = (double)s.payload.size() * 8;
         s.t_enqueue = rt->now();
         return s;
     };
+    // F feeder threads claim ids in order (one copy of a multi-MB payload each), the
+    // last one to finish closes the input
+    std::atomic<int64_t> next_id{0};
+    std::atomic<int> feeders_left{feeders};
     if (!sync) {
     for (int i = 0; i < cores; ++i) {
         rt->spawn("resume." + std::to_string(i), [&, i] {
@@ -413,17 +424,20 @@ int main(int argc, char** argv) {
             slow[i]->close();
         });
     }
-    rt->spawn("feeder", [&] {
-        for (int64_t i = 0; i < n; ++i) {
-            const auto el = std::chrono::steady_clock::now() - wall0;
-            if (std::chrono::duration_cast<std::chrono::seconds>(el).count() > max_s) {
-                give_up = true;
-                break;
+    for (int f = 0; f < feeders; ++f)
+        rt->spawn("feeder." + std::to_string(f), [&] {
+            for (;;) {
+                const int64_t i = next_id.fetch_add(1);
+                if (i >= n) break;
+                const auto el = std::chrono::steady_clock::now() - wall0;
+                if (std::chrono::duration_cast<std::chrono::seconds>(el).count() > max_s) {
+                    give_up = true;
+                    break;
+                }
+                input.put(make_payload_sample(i));
             }
-            input.put(make_payload_sample(i));
-        }
-        input.close();
-    });
+            if (feeders_left.fetch_sub(1) == 1) input.close();
+        });
     }
     if (sync) {
         // all samples up front (start_sync_loader takes the stream by value)
@@ -474,11 +488,12 @@ int main(int argc, char** argv) {
                 "\"idle_frac\": %.4f, \"final_t_out_ms\": %lld, "
                 "\"samples\": %.0f, \"span_ms\": %.0f, \"slow\": %lld, \"truncated\": %s, "
                 "\"sample\": \"reference libloadflow (proj/src, realtime Minato wiring) with oracle "
-                "transforms over fp64 Payload: %s, %lld samples fed, batch %d, %d workers\"}\n",
+                "transforms over fp64 Payload: %s, %lld samples fed (payloads pre-built, %d feeder threads), "
+                "batch %d, %d workers\"}\n",
                 value, cores, cs.idle_fraction(), (long long)policy.timeout(), timed, span_ms,
                 (long long)n_slow.load(), give_up ? "true" : "false",
                 rrc ? "RRC224+flip+ToTensor+Normalize on u8 3x(256..512)^2"
                     : "crop128^3+flip+brightness+noise+cast on 128x384x384",
-                (long long)cs.samples, B, cores);
+                (long long)cs.samples, feeders, B, cores);
     return 0;
 }
