@@ -16,8 +16,11 @@ Workloads:
                img_seg sizes) -> crop 128^3 + flip + brightness + noise, batch 2
   img3d_fg     C1 shapes with RandomCrop's MLPerf foreground oversampling (p 0.4): those
                samples scan their whole label volume (K2) -- a real heavy tail
-  img3d_heavy  C3: as img3d with a heavy-tailed per-sample cost (spin) on a fraction
-               of samples and a synthetic trainer: reports consumer idle %
+  img3d_heavy  C3: img3d_fg's REAL heavy tail (40% of crops scan their label volume;
+               from pinned memory that whole volume crosses PCIe) in launch groups of 16,
+               4 in-flight groups, a synthetic trainer step calibrated to 90% of the
+               loader's measured capacity; Minato (adaptive p75/p90 timeout) reports
+               consumer idle %, and the synchronous head-of-line loader runs beside it
 
 value      : whole-job samples/s with raw inputs resident in HBM (device events on
              each rank's trainer stream, max over ranks)
@@ -54,7 +57,7 @@ METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform H
 
 # workload -> (batch size, samples per launch group, default timed steps)
 BATCH = {"rrc": (256, 256, 1000), "img3d": (2, 16, 4000), "img3d_fg": (2, 16, 2000),
-         "img3d_heavy": (2, 1, 400),
+         "img3d_heavy": (2, 16, 400),
          "speech": (64, 64, 500)}
 
 
@@ -437,8 +440,8 @@ def make_workload(name, L, ctx, host, seed, args):
         return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed)
     if name == "img3d_fg":   # MLPerf RandBalancedCrop: 40% of crops scan the label volume (K2)
         return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed, p_fg=0.4)
-    if name == "img3d_heavy":
-        return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed,
+    if name == "img3d_heavy":   # the real tail (foreground oversampling); optional spin tail on top
+        return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed, p_fg=args.fg,
                              heavy_frac=args.heavy_frac, time_scale_us_per_ms=args.time_scale)
     raise SystemExit(f"unknown workload {name}")
 
@@ -447,9 +450,16 @@ WORKLOAD_NAMES = {
     "rrc": "C2 ImageNet-shaped u8 3x(256..512)^2 -> RRC224+hflip+normalize",
     "img3d": "C1 KiTS19-shaped 3D crop128^3+flip+brightness+noise+cast",
     "img3d_fg": "C1 shapes, RandomCrop with MLPerf foreground oversampling 0.4 (K2 label scan + K1)",
-    "img3d_heavy": "C3 heavy-tailed 3D + synthetic trainer",
+    "img3d_heavy": "C3 heavy-tailed 3D (MLPerf foreground oversampling 0.4 as the tail) + synthetic "
+                   "trainer at 90% of loader capacity",
     "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT + log-mel (tcgen05 3xTF32) + SpecAugment + splice, batch 64",
 }
+
+
+def workers_of(args) -> int:
+    """In-flight launch groups: 16, or 4 for C3 (64 samples in flight, so head-of-line
+    blocking is not hidden behind a deep window)."""
+    return args.workers or (4 if args.workload == "img3d_heavy" else 16)
 
 
 def bench_config(args, world: int) -> dict:
@@ -457,10 +467,13 @@ def bench_config(args, world: int) -> dict:
     wl = args.workload
     cls = {"rrc": RrcWorkload, "speech": SpeechWorkload}.get(wl, Img3dWorkload)
     return {"workload": WORKLOAD_NAMES[wl], "batch": BATCH[wl][0],
-            "launch_group": args.group or BATCH[wl][1], "workers": args.workers,
+            "launch_group": args.group or BATCH[wl][1], "workers": workers_of(args),
             "raw_pool_bytes": cls.pool_bytes_of(pool_size(wl, False, args.pool), args.seed),
             "l2": "inputs > L2 (pool larger than 126 MB)",
-            "parallelism": f"dp{world} independent loader shards"}
+            "parallelism": f"dp{world} independent loader shards",
+            **({"trainer": "synthetic step per batch calibrated to 90% of the loader capacity measured "
+                           "in a drain run (trainer.hpp:14-21 consumer model)",
+                "fg": args.fg} if wl == "img3d_heavy" else {})}
 
 
 # ------------------------------------------------------------------ runs
@@ -471,7 +484,7 @@ def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, 
     batch tensors on the trainer stream (counted in d2h_bytes) for the oracle check."""
     B = wl.B
     rc_w = L.run_config(batch_size=B, t_out_us=t_out_us, policy=policy, trainer_us=trainer_us,
-                        n_workers=args.workers, warmup_us=args.profiler_warmup_us,
+                        n_workers=workers_of(args), warmup_us=args.profiler_warmup_us,
                         update_interval_us=1000, d2h_probe=d2h_probe)
     if ids_warm:
         ctx.run_shard(wl.chain, wl.descs(ids_warm), rc_w, want_ids=False)
@@ -495,6 +508,16 @@ def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, 
     c1 = ctx.counters()
     cap = dict(getattr(ctx, "last_capture", {})) if capture else {}
     return rep, ids, wall, {k: c1[k] - c0[k] for k in c1}, cap
+
+
+def calibrated_trainer_us(L, ctx, wl, ids, args, util: float = 0.9) -> int:
+    """C3's consumer: the loader's capacity R (samples/s) from a drain run (no trainer
+    step, no timeout) over `ids`; the synthetic step per batch of B is B / (util * R),
+    so the loader runs at `util` of its capacity (trainer.hpp:14-21 consumer model)."""
+    rc = L.run_config(batch_size=wl.B, n_workers=workers_of(args))
+    rep, *_ = ctx.run_shard(wl.chain, wl.descs(ids), rc, want_ids=False)
+    ctx.synchronize()
+    return max(1, int(round(wl.B / (util * rep.samples_per_s) * 1e6)))
 
 
 def capture_positions(n_timed: int, k: int, seed: int) -> list[int]:
@@ -656,12 +679,12 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
     pinned-host run (e2e), and the oracle check of samples captured from both runs."""
     from paper_2509_10712_b200 import lfgpu as L
     hbm_peak, tf32_peak, peak_src = peaks()
-    ctx, B, group = make_context(L, args.workload, device=local, workers=args.workers,
+    ctx, B, group = make_context(L, args.workload, device=local, workers=workers_of(args),
                                  group=args.group, seed=args.seed)
     ids_all = shard_ids(args.warmup + args.steps, B, rank, world)
     ids_warm, ids_timed = ids_all[: args.warmup * B], ids_all[args.warmup * B:]
     heavy = args.workload == "img3d_heavy"
-    trainer_us = args.trainer_us if args.trainer_us else (2000 if heavy else 0)
+    trainer_us = args.trainer_us
     cap_pos = capture_positions(len(ids_timed), args.check, args.seed + rank) if args.check else None
     out = {"group": group}
     if args.serial:
@@ -669,6 +692,9 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
 
     # ---- value: inputs resident in HBM
     wl = make_workload(args.workload, L, ctx, host=False, seed=args.seed, args=args)
+    if heavy and not args.trainer_us:
+        trainer_us = calibrated_trainer_us(L, ctx, wl, ids_all, args)
+    out["trainer_us"] = {"value": trainer_us}
     with ClockSampler(local) as clk:
         rep, ids, wall, dc, cap = run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local,
                                             trainer_us=trainer_us, policy=1 if heavy else 0,
@@ -686,10 +712,23 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
 
     # ---- e2e: inputs in pinned host memory, H2D + a D2H read of every delivered batch
     wl_h = make_workload(args.workload, L, ctx, host=True, seed=args.seed, args=args)
+    trainer_h = trainer_us
+    if heavy and not args.trainer_us:
+        trainer_h = calibrated_trainer_us(L, ctx, wl_h, ids_all, args)
+    out["trainer_us"]["e2e"] = trainer_h
     rep_h, ids_h, wall_h, dc_h, cap_h = run_timed(L, ctx, wl_h, ids_warm, ids_timed, args, dist, local,
-                                                  trainer_us=trainer_us, policy=1 if heavy else 0,
-                                                  d2h_probe=1, capture=cap_pos, stream=trainer_us == 0)
+                                                  trainer_us=trainer_h, policy=1 if heavy else 0,
+                                                  d2h_probe=1, capture=cap_pos, stream=trainer_h == 0)
     out["check_e2e"] = oracle_check(wl_h, ids_timed, cap_h) if cap_pos and rank == 0 else None
+    out["e2e_idle"] = rep_h.consumer_idle_frac if trainer_h else None
+    out["e2e_slow"] = rep_h.slow / max(1, rep_h.samples)
+    if heavy:
+        # the synchronous head-of-line loader on the same stream, trainer and workers
+        # (start_sync_loader, baselines.cpp:12-151; lfg_run_config.policy 3)
+        rep_s, *_ = run_timed(L, ctx, wl_h, ids_warm, ids_timed, args, dist, local,
+                              trainer_us=trainer_h, policy=3, d2h_probe=1)
+        out["sync_e2e_idle"] = rep_s.consumer_idle_frac
+        out["sync_e2e_value"] = rep_s.timed_samples / (rep_s.elapsed_ms / 1e3)
     wl_h.close()
     ctx.close()
     consumed = ids.tolist()
@@ -746,9 +785,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="rrc", choices=list(BATCH))
     ap.add_argument("--pool", type=int, default=0)
-    ap.add_argument("--workers", type=int, default=16)
+    ap.add_argument("--workers", type=int, default=0, help="in-flight launch groups (0 = 16; C3: 4)")
+    ap.add_argument("--fg", type=float, default=0.4, help="img3d_heavy: foreground oversampling probability")
     ap.add_argument("--group", type=int, default=0, help="samples per launch group (0 = auto)")
-    ap.add_argument("--heavy-frac", type=float, default=0.2)
+    ap.add_argument("--heavy-frac", type=float, default=0.0, help="img3d_heavy: extra synthetic spin tail")
     ap.add_argument("--time-scale", type=float, default=10.0, help="spin us per reference ms")
     ap.add_argument("--trainer-us", type=int, default=0)
     ap.add_argument("--profiler-warmup-us", type=int, default=20000)
@@ -808,6 +848,11 @@ def main():
         "clocks": r["clocks"],
         "gpu_launches": int(cnt[6]),
         "consumer_idle_pct": round(100 * r["idle"], 2) if r["idle"] is not None else None,
+        **({"e2e_consumer_idle_pct": round(100 * r["e2e_idle"], 2),
+            "sync_e2e_consumer_idle_pct": round(100 * r["sync_e2e_idle"], 2),
+            "sync_e2e_value": round(r["sync_e2e_value"], 1),
+            "e2e_slow_frac": round(r["e2e_slow"], 4),
+            "trainer_us_per_batch": r["trainer_us"]} if r.get("sync_e2e_idle") is not None else {}),
         "slow_frac": round(cnt[4] / max(1, cnt[2]), 4),
         "exactly_once": bool(exactly_once),
         "checked": bool(checks) and all(c["ok"] for c in checks),

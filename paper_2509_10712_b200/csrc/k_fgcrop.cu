@@ -54,9 +54,12 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
     __syncthreads();
     const int H = d.sdim[1], W = d.sdim[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t xmin[kClasses], xmax[kClasses], ymin[kClasses], ymax[kClasses];
+    // per lane: the class x extents of its chunks; the y extents are warp-uniform per
+    // row, so lane c keeps class c's (ylo, yhi + 1) for the whole warp (2 registers, not 14)
+    uint32_t xmin[kClasses], xmax[kClasses];
 #pragma unroll
-    for (int c = 0; c < kClasses; ++c) xmin[c] = ymin[c] = kNone, xmax[c] = ymax[c] = kNone;
+    for (int c = 0; c < kClasses; ++c) xmin[c] = xmax[c] = kNone;
+    uint32_t ylo = kNone, yhi1 = 0;
     uint32_t seen_all = 0;
     // one 16-B chunk of a label row against the per-class extents
     auto chunk = [&](const uint4 v, int q, uint32_t& seen) {
@@ -108,20 +111,17 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
         // row start (K0-staged volumes keep the source's 16-B alignment phase: skews)
         return plane + (int64_t)y * d.lbl_py + ((zsk + y * d.lbl_sky) & 15);
     };
+    // (warp-uniform call: every lane passes its chunks' classes of row y)
     auto close_row = [&](int y, uint32_t seen) {
-        if (seen == 0u) return;   // all-background row segment (most of a volume)
-        const int top = 31 - __clz(seen);
-#pragma unroll
-        for (int c = 1; c < kClasses; ++c) {
-            if (c > top) break;
-            if (seen & (1u << c)) {
-                ymin[c] = min(ymin[c], (uint32_t)y);
-                ymax[c] = (ymax[c] == kNone) ? (uint32_t)y : max(ymax[c], (uint32_t)y);
-            }
+        const uint32_t w = __reduce_or_sync(0xFFFFFFFFu, seen);
+        if (w == 0u) return;   // all-background row (most of a volume)
+        if ((w >> lane) & 1u) {
+            ylo = min(ylo, (uint32_t)y);
+            yhi1 = max(yhi1, (uint32_t)y + 1u);
         }
         seen_all |= seen;
     };
-    constexpr int kRowsInFlight = 4;    // rows per warp with their loads issued together
+    constexpr int kRowsInFlight = 8;    // rows per warp with their loads issued together
     constexpr int kWarps = kScanThreads / 32;
     const bool vec = (reinterpret_cast<uintptr_t>(row_ptr(0)) & 15) == 0 && (d.lbl_py & 15) == 0 &&
                      (d.lbl_pz & 15) == 0 && (W & 15) == 0;
@@ -167,15 +167,15 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
         if (!(seen_all & (1u << c))) continue;   // warp-uniform
         const uint32_t a = __reduce_min_sync(0xFFFFFFFFu, xmin[c]);
         const uint32_t b = __reduce_max_sync(0xFFFFFFFFu, xmax[c] == kNone ? 0u : xmax[c] + 1u);
-        const uint32_t e = __reduce_min_sync(0xFFFFFFFFu, ymin[c]);
-        const uint32_t f = __reduce_max_sync(0xFFFFFFFFu, ymax[c] == kNone ? 0u : ymax[c] + 1u);
         if (lane == 0) {
             atomicMin(&s_min[c][2], a);
             atomicMax(&s_max[c][2], b);
-            atomicMin(&s_min[c][1], e);
-            atomicMax(&s_max[c][1], f);
             atomicOr(&s_seen, 1u << c);
         }
+    }
+    if (lane >= 1 && lane < kClasses && yhi1 != 0u) {   // lane c: class c's rows
+        atomicMin(&s_min[lane][1], ylo);
+        atomicMax(&s_max[lane][1], yhi1);
     }
     __syncthreads();
     if (threadIdx.x < kClasses && (s_seen & (1u << threadIdx.x))) {

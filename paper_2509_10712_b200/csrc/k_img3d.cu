@@ -235,7 +235,9 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
             for (int k = lane, use = 0; k < ntiles; k += kTmaStages, ++use) {
                 if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
                 const int t = (int)blockIdx.x + k * (int)gridDim.x;
-                const int i = t / per, rr = t - i * per;
+                // (debug bit 4: samples interleaved tile by tile instead of one after another)
+                const int i = (L.debug & 4) ? t % L.n : t / per;
+                const int rr = (L.debug & 4) ? t / L.n : t - i * per;
                 const int z = rr / nyb, y0 = (rr - z * nyb) * kTR;
                 const Img3dDesc& d = sdesc[i];
                 const int fz = (d.flip & 1) ? cd - 1 - z : z;

@@ -1,24 +1,31 @@
 #!/usr/bin/env python
-"""C5: timeout / slow-ratio sweep of the heavy-tailed 3D-UNet loader,
-B200 shard vs the reference CPU loader on the host cores.
+"""C5: timeout-policy / tail-fraction sweep of the heavy-tailed 3D-UNet
+loader, B200 shard vs the reference CPU loader on the host cores, both with the REAL
+heavy tail and both at the same relative load.
 
-For every slow fraction f in {0.1, 0.2, 0.3} and timeout policy t_out in {p50, p75, p90,
-none} (nearest-rank percentile of the per-sample totals window, fixed -- no p75->p90
-escalation -- after a warm-up; "none" = kNoTimeout):
+Tail: RandomCrop's MLPerf foreground oversampling (RandBalancedCrop) with probability
+p_fg in {0.2, 0.4, 0.6}: an oversampled crop must scan its whole label volume for
+foreground boxes before it can cut its window -- on the GPU from pinned host memory
+that whole volume crosses PCIe (K0) and K2 scans it; on the CPU the oracle transform
+scans it in fp64.  Everything else is the plain img_seg chain (crop 128^3 + flip +
+brightness + noise + cast) on KiTS19-shaped D x 384 x 384 volumes.
 
-  gpu : bench.py's img3d_heavy workload (KiTS19-shaped volumes, crop 128^3 chain, a
-        fraction f of samples carries a synthetic cost of cost_ms x time_scale us on the
-        device (K14 spin) and a 2 ms synthetic trainer step per batch of 2 on a
-        high-priority stream).  Reports delivered samples/s, consumer idle % (CUDA
-        events, trainer.hpp:41-46 formula), slow fraction and the final t_out.
-  cpu : oracle/_ref/minato_cpu -- the reference libloadflow realtime Minato pipeline
-        with the oracle transforms, a leading SampleCost transform sleeping heavy_ms for
-        a fraction f of samples, run_consumer at 200 ms per batch (trainer.hpp:15) and
-        the same percentile policy.  Bounded sample per point.
+Consumer: a synthetic trainer step per batch of 2 (trainer.hpp:14-21), calibrated on
+each side to 90% of that side's own measured loader capacity at that p_fg (a drain
+run: no trainer step, no timeout) -- the same relative time scale on both sides.
 
-  python tools/sweep.py [--out profiles/r1_c5_sweep.md] [--no-cpu]
-Multi-GPU: launch under torchrun like bench.py; rank 0 prints (max over ranks of the
-device time, sum of samples; one all-reduce of counters at the end of each point).
+Policies (lfg_run_config.policy on the GPU, minato_cpu --pct / --loader on the CPU):
+  minato  the Profiler's adaptive p75 -> p90 timeout (profiler.cpp:47-72)
+  p50/p90 a fixed nearest-rank percentile of the per-sample totals window
+  none    no timeout (every sample fast; batches still sealed eagerly, FIFO)
+  sync    the synchronous head-of-line loader (start_sync_loader, baselines.cpp:12-151:
+          batch k = ids [kB, (k+1)B), sealed only when complete, in order)
+
+GPU: pinned-host inputs (the e2e storage path), launch groups of 16, 4 in-flight
+groups.  CPU: oracle/_ref/minato_cpu (the reference libloadflow realtime pipeline with
+the oracle transforms) on all host cores, bounded sample per point.
+
+  python tools/sweep.py [--out profiles/r2_c5_sweep.md] [--no-cpu]
 """
 from __future__ import annotations
 
@@ -33,59 +40,85 @@ sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402
 
-FRACS = (0.1, 0.2, 0.3)
-# (name, percentile): 0 = no timeout; -1 = the synchronous head-of-line baseline
-# (start_sync_loader, baselines.cpp:12-151; GPU: lfg_run_config.policy 3)
-POLICIES = (("p50", 50), ("p75", 75), ("p90", 90), ("none", 0), ("sync", -1))
+FRACS = (0.2, 0.4, 0.6)
+# (name, run_config policy, percentile): policy 1 adaptive, 2 fixed, 0 none, 3 sync
+POLICIES = (("minato", 1, 75), ("p50", 2, 50), ("p90", 2, 90), ("none", 0, 75), ("sync", 3, 75))
+GROUP, UTIL = 16, 0.9
+WORKERS = (4, 1)   # in-flight launch groups: 64 samples in flight, then a single group
 
 
 class _Args:
     pool = 0
-    workers = 16
+    workers = WORKERS
+    workload = "img3d_heavy"
     time_scale = 10.0
-    heavy_frac = 0.2
+    heavy_frac = 0.0
+    fg = 0.4
 
 
-def gpu_point(L, wl, frac, pct, steps, warmup, rank, world, dist, local):
-    ctx = wl.ctx
-    wl.heavy_frac = frac
-    B = wl.B
-    a = _Args()
+def gpu_sweep(L, steps, warmup, rank, world, dist, local, workers):
+    ctx = L.Context(device=local, batch_size=2, n_workers=workers, max_group=GROUP,
+                    max_slot_buffers=max(8, workers * GROUP // 2 + 4), seed=1)
+    B = 2
     ids = bench.shard_ids(warmup + steps, B, rank, world)
     warm, timed = ids[: warmup * B], ids[warmup * B:]
-    rc = L.run_config(batch_size=B, policy=3 if pct < 0 else (2 if pct else 0), percentile=pct if pct > 0 else 75,
-                      t_out_us=0,
-                      trainer_us=2000, n_workers=a.workers, warmup_us=20000, update_interval_us=1000)
-    ctx.run_shard(wl.chain, wl.descs(warm), rc, want_ids=False)
-    ctx.synchronize()
-    bench.barrier(dist)
-    rep, _, _, _ = ctx.run_shard(wl.chain, wl.descs(timed), rc)
-    ctx.synchronize()
-    bench.barrier(dist)
-    el = bench.allreduce_max(dist, rep.elapsed_ms, local)
-    tot = bench.allreduce_sum(dist, [rep.timed_samples, rep.slow, rep.samples,
-                                     rep.consumer_busy_ms, rep.consumer_span_ms], local)
-    return {"samples_per_s": round(tot[0] / (el / 1e3), 1),
-            "idle_pct": round(100 * (1 - tot[3] / tot[4]), 2) if tot[4] > 0 else None,
-            "slow_frac": round(tot[1] / max(1, tot[2]), 3),
-            "final_t_out_us": round(rep.final_t_out_us, 1) if pct > 0 else None}
+    rows = {}
+    for frac in FRACS:
+        a = _Args()
+        a.fg = frac
+        a.workers = workers
+        wl = bench.make_workload("img3d_heavy", L, ctx, True, 1, a)
+        trainer_us = bench.calibrated_trainer_us(L, ctx, wl, warm + timed, a, util=UTIL)
+        for name, policy, pct in POLICIES:
+            rc = L.run_config(batch_size=B, policy=policy, percentile=pct, t_out_us=0,
+                              trainer_us=trainer_us, n_workers=workers, warmup_us=20000,
+                              update_interval_us=1000, prefetch_factor=0)
+            ctx.run_shard(wl.chain, wl.descs(warm), rc, want_ids=False)
+            ctx.synchronize()
+            bench.barrier(dist)
+            rep, _, _, _ = ctx.run_shard(wl.chain, wl.descs(timed), rc)
+            ctx.synchronize()
+            bench.barrier(dist)
+            el = bench.allreduce_max(dist, rep.elapsed_ms, local)
+            tot = bench.allreduce_sum(dist, [rep.timed_samples, rep.slow, rep.samples,
+                                             rep.consumer_busy_ms, rep.consumer_span_ms], local)
+            rows[(frac, name)] = {
+                "samples_per_s": round(tot[0] / (el / 1e3), 1),
+                "idle_pct": round(100 * (1 - tot[3] / tot[4]), 2) if tot[4] > 0 else None,
+                "slow_frac": round(tot[1] / max(1, tot[2]), 3),
+                "final_t_out_us": round(rep.final_t_out_us, 1) if policy in (1, 2) else None,
+                "trainer_us": trainer_us}
+        wl.close()
+    ctx.close()
+    return rows
 
 
-def cpu_point(frac, pct, steps):
+def cpu_run(frac, extra, steps, trainer_ms):
     h = bench.ref_harness()
-    if h is None:
-        return None
     cores = os.cpu_count() or 1
-    extra = ["--loader", "sync", "--pct", "0"] if pct < 0 else ["--pct", str(pct)]
-    out = subprocess.run([h, "--workload", "img3d", "--steps", str(steps if pct >= 0 else min(steps, 6)),
-                          "--warmup", "2", "--workers", str(cores), "--heavy-frac", str(frac),
-                          "--heavy-ms", "470", "--trainer-ms", "200", "--profiler-warmup-ms", "1500",
-                          "--max-seconds", "40"] + extra,
-                         capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
-    b = json.loads(out)
-    return {"samples_per_s": b["value"], "idle_pct": round(100 * b["idle_frac"], 2),
-            "slow_frac": round(b["slow"] / max(1.0, b["samples"] + 4), 3),
-            "final_t_out_ms": b["final_t_out_ms"] if pct > 0 else None, "cores": b["cores"]}
+    out = subprocess.run([h, "--workload", "img3d", "--steps", str(steps), "--warmup", "2",
+                          "--workers", str(cores), "--fg", str(frac), "--trainer-ms", str(trainer_ms),
+                          "--profiler-warmup-ms", "300", "--max-seconds", "60"] + extra,
+                         capture_output=True, text=True, timeout=200, check=True).stdout.strip().splitlines()[-1]
+    return json.loads(out)
+
+
+def cpu_sweep(steps):
+    if bench.ref_harness() is None:
+        return {}
+    rows = {}
+    for frac in FRACS:
+        cap = cpu_run(frac, ["--pct", "0"], steps, 0)            # drain run: loader capacity
+        trainer_ms = max(1, int(round(2 / (UTIL * cap["value"]) * 1e3)))
+        for name, policy, pct in POLICIES:
+            extra = {"minato": ["--pct", "-1"], "none": ["--pct", "0"],
+                     "sync": ["--loader", "sync", "--pct", "0"]}.get(name, ["--pct", str(pct)])
+            b = cpu_run(frac, extra, steps, trainer_ms)
+            rows[(frac, name)] = {"samples_per_s": b["value"], "idle_pct": round(100 * b["idle_frac"], 2),
+                                  "slow_frac": round(b["slow"] / max(1.0, b["samples"] + 4), 3),
+                                  "final_t_out_ms": b["final_t_out_ms"] if policy in (1, 2) else None,
+                                  "trainer_ms": trainer_ms, "cores": b["cores"]}
+    return rows
 
 
 def main():
@@ -93,44 +126,43 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400, help="timed batches per GPU point")
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--cpu-steps", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     from paper_2509_10712_b200 import lfgpu as L
     rank, local, world, dist = bench.dist_setup(args.gpus)
-    ctx = L.Context(device=local, batch_size=2, n_workers=16, max_group=1, max_slot_buffers=24, seed=1)
-    wl = bench.make_workload("img3d_heavy", L, ctx, False, 1, _Args())
-    rows = []
-    for frac in FRACS:
-        for name, pct in POLICIES:
-            g = gpu_point(L, wl, frac, pct, args.steps, args.warmup, rank, world, dist, local)
-            c = None if (args.no_cpu or rank != 0) else cpu_point(frac, pct, args.cpu_steps)
-            rows.append({"slow_frac_target": frac, "t_out": name, "gpu": g, "cpu": c})
-            if rank == 0:
-                print(json.dumps(rows[-1]), flush=True)
-    wl.close()
-    ctx.close()
+    g = {w: gpu_sweep(L, args.steps, args.warmup, rank, world, dist, local, w) for w in WORKERS}
     if rank != 0:
         return
-    lines = [f"# C5 timeout / slow-ratio sweep ({world} x B200 shard(s) vs reference CPU loader)",
+    c = {} if args.no_cpu else cpu_sweep(args.cpu_steps)
+    cores = next(iter(c.values()))["cores"] if c else None
+    lines = [f"# C5 timeout-policy / tail sweep ({world} x B200 shard(s) vs reference CPU loader)",
              "",
-             "GPU: img3d_heavy (crop 128^3 chain; heavy samples spin cost_ms x 10 us; 2 ms trainer "
-             "step per batch of 2). CPU: reference libloadflow Minato pipeline + oracle transforms, "
-             "heavy samples sleep 470 ms, 200 ms trainer step per batch of 2.",
-             "t_out = fixed nearest-rank percentile of the per-sample totals window after warm-up "
-             "(none = kNoTimeout); sync = the synchronous head-of-line loader (batch k = ids "
-             "[kB, (k+1)B), sealed when complete, in order: start_sync_loader on the CPU, "
-             "lfg_run_config.policy 3 on the GPU).",
+             "Tail: MLPerf foreground oversampling p_fg (an oversampled crop scans its whole label volume; "
+             "GPU: from pinned host memory the volume crosses PCIe, then K2). Trainer step per batch of 2 "
+             f"calibrated on each side to {UTIL:.0%} of that side's drain-run loader capacity at that p_fg. "
+             f"GPU: launch groups of {GROUP}, W in-flight groups, pinned-host inputs. "
+             f"CPU: reference libloadflow realtime Minato / sync loader + oracle transforms, {cores} host cores.",
+             "minato = adaptive p75 -> p90 timeout; p50 / p90 = fixed percentile; none = no timeout; "
+             "sync = head-of-line loader (batch k = ids [kB, (k+1)B), sealed complete and in order).",
              "",
-             "| slow frac | t_out | GPU samples/s | GPU idle % | GPU slow | GPU t_out (us) | "
-             "CPU samples/s | CPU idle % | CPU slow | CPU t_out (ms) |",
-             "|---|---|---|---|---|---|---|---|---|---|"]
-    for r in rows:
-        g, c = r["gpu"], r["cpu"] or {}
-        lines.append(f"| {r['slow_frac_target']} | {r['t_out']} | {g['samples_per_s']} | {g['idle_pct']} | "
-                     f"{g['slow_frac']} | {g['final_t_out_us']} | {c.get('samples_per_s')} | "
-                     f"{c.get('idle_pct')} | {c.get('slow_frac')} | {c.get('final_t_out_ms')} |")
+             "| p_fg | policy | " + " | ".join(f"GPU W={w} samples/s | GPU W={w} idle % | GPU W={w} slow | "
+                                               f"GPU W={w} t_out (us) | GPU W={w} trainer (us)" for w in WORKERS) +
+             " | CPU samples/s | CPU idle % | CPU slow | CPU t_out (ms) | CPU trainer (ms) |",
+             "|---|---|" + "---|" * (5 * len(WORKERS) + 5)]
+    for frac in FRACS:
+        for name, _, _ in POLICIES:
+            b = c.get((frac, name), {})
+            cells = []
+            for w in WORKERS:
+                a = g[w][(frac, name)]
+                cells.append(f"{a['samples_per_s']} | {a['idle_pct']} | {a['slow_frac']} | "
+                             f"{a['final_t_out_us']} | {a['trainer_us']}")
+            t_out = b.get("final_t_out_ms")
+            t_out = None if t_out is not None and t_out > 10**15 else t_out   # kNoTimeout: never set
+            lines.append(f"| {frac} | {name} | " + " | ".join(cells) + f" | {b.get('samples_per_s')} | "
+                         f"{b.get('idle_pct')} | {b.get('slow_frac')} | {t_out} | {b.get('trainer_ms')} |")
     text = "\n".join(lines) + "\n"
     print(text)
     if args.out:
