@@ -567,6 +567,7 @@ def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
     every launch (the group's stage events); achieved = algorithmic bytes (or tensor
     FLOPs) / summed launch time."""
     chain = getattr(wl, "roof_chain", None) or wl.chain     # no synthetic spin stages
+    ctx.time_kernels(chain, wl.descs(ids[: max(1, len(ids) // 4)]))   # warm-up pass (untimed)
     t = ctx.time_kernels(chain, wl.descs(ids))              # launches back to back, CUDA events
     launches = t["launches"]
     ms = t["mean_ms"] * launches                            # total transform-kernel time

@@ -36,14 +36,25 @@ __device__ __forceinline__ void note(int v, uint32_t x, uint32_t xmin[kClasses],
     }
 }
 
+// bytes of q equal to the byte replicated in rep, as a 16-bit mask (byte k -> bit k):
+// per word, the match bytes' low bits (0, 8, 16, 24) times 0x10204080 land on bits
+// 28..31 with no carries
+__device__ __forceinline__ uint32_t byte_mask16(const uint4 q, uint32_t rep) {
+    const uint32_t m0 = (__vcmpeq4(q.x, rep) & 0x01010101u) * 0x10204080u;
+    const uint32_t m1 = (__vcmpeq4(q.y, rep) & 0x01010101u) * 0x10204080u;
+    const uint32_t m2 = (__vcmpeq4(q.z, rep) & 0x01010101u) * 0x10204080u;
+    const uint32_t m3 = (__vcmpeq4(q.w, rep) & 0x01010101u) * 0x10204080u;
+    return (m0 >> 28) | ((m1 >> 24) & 0xF0u) | ((m2 >> 20) & 0xF00u) | ((m3 >> 16) & 0xF000u);
+}
+
 __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_constant__ Img3dLaunch L,
                                                                const __grid_constant__ FgLaunch F,
                                                                int32_t* __restrict__ box) {
-    const int i = blockIdx.y;
-    if (!F.d[i].fg) return;
+    int k = 0;
+    while (k + 1 < F.n_scan && (int)blockIdx.x >= F.scan_start[k + 1]) ++k;
+    const int i = F.scan_i[k];
     const Img3dDesc& d = L.d[i];
-    const int z = blockIdx.x;
-    if (z >= d.sdim[0]) return;
+    const int z = (int)blockIdx.x - F.scan_start[k];
     __shared__ uint32_t s_min[kClasses][3], s_max[kClasses][3];
     __shared__ uint32_t s_seen;
     if (threadIdx.x < kClasses * 3) {
@@ -60,6 +71,7 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
 #pragma unroll
     for (int c = 0; c < kClasses; ++c) xmin[c] = xmax[c] = kNone;
     uint32_t ylo = kNone, yhi1 = 0;
+    uint32_t acc[(kClasses) / 2] = {0u, 0u, 0u, 0u};   // (row-vector path) per-class byte masks, 2 per word
     uint32_t seen_all = 0;
     // one 16-B chunk of a label row against the per-class extents
     auto chunk = [&](const uint4 v, int q, uint32_t& seen) {
@@ -124,25 +136,67 @@ __global__ void __launch_bounds__(kScanThreads) fg_scan_kernel(const __grid_cons
     constexpr int kRowsInFlight = 8;    // rows per warp with their loads issued together
     constexpr int kWarps = kScanThreads / 32;
     const bool vec = (reinterpret_cast<uintptr_t>(row_ptr(0)) & 15) == 0 && (d.lbl_py & 15) == 0 &&
-                     (d.lbl_pz & 15) == 0 && (W & 15) == 0;
+                     (d.lbl_pz & 15) == 0 && (W & 15) == 0 && (d.lbl_sky & 15) == 0;
     if (vec && (W >> 4) <= 32) {
-        // rows of <= 512 B: a lane per 16-B chunk, kRowsInFlight rows per warp at once
+        // rows of <= 512 B: lane q holds the row's 16-B chunk q, kRowsInFlight rows per
+        // warp with their loads issued together.  A row's class extents are found at
+        // warp level: ballot of the lanes whose chunk holds class c, then the first /
+        // last such lane's byte offsets by shuffle -- O(1) warp instructions per class
+        // present, no per-lane extent registers (occupancy, bytes in flight).  Lane c
+        // keeps class c's x / y extents for the warp.
         const bool lane_live = lane < (W >> 4);
+        const int64_t py = d.lbl_py;
+        const uint8_t* base = plane + (zsk & 15);   // aligned rows: no per-row skew
         for (int y0 = warp; y0 < H; y0 += kWarps * kRowsInFlight) {
             uint4 v[kRowsInFlight];
 #pragma unroll
             for (int r = 0; r < kRowsInFlight; ++r) {
                 const int y = y0 + r * kWarps;
-                v[r] = (lane_live && y < H) ? __ldcs(reinterpret_cast<const uint4*>(row_ptr(y)) + lane)
+                v[r] = (lane_live && y < H) ? __ldcs(reinterpret_cast<const uint4*>(base + (int64_t)y * py) + lane)
                                             : make_uint4(0u, 0u, 0u, 0u);
             }
+            // which of the 8 rows hold any foreground byte: one warp OR for all of them,
+            // so an all-background batch of rows (most of a volume) costs no per-row work
+            uint32_t anym = 0;
+#pragma unroll
+            for (int r = 0; r < kRowsInFlight; ++r)
+                anym |= ((v[r].x | v[r].y | v[r].z | v[r].w) != 0u ? 1u : 0u) << r;
+            const uint32_t rows = __reduce_or_sync(0xFFFFFFFFu, anym);
+            if (rows == 0u) continue;
 #pragma unroll
             for (int r = 0; r < kRowsInFlight; ++r) {
-                const int y = y0 + r * kWarps;
-                if (y >= H) break;
-                uint32_t seen = 0;
-                chunk(v[r], lane, seen);
-                close_row(y, seen);
+                if (!((rows >> r) & 1u)) continue;   // warp-uniform
+                const uint4 q = v[r];
+                uint32_t mx = __vmaxu4(__vmaxu4(q.x, q.y), __vmaxu4(q.z, q.w));
+                mx = __vmaxu4(mx, mx >> 16);
+                mx = max(mx & 0xFFu, (mx >> 8) & 0xFFu);
+                const uint32_t top = __reduce_max_sync(0xFFFFFFFFu, mx);
+                const uint32_t y = (uint32_t)(y0 + r * kWarps);
+#pragma unroll
+                for (int c = 1; c < kClasses; ++c) {
+                    if ((uint32_t)c > top) break;   // warp-uniform
+                    // the chunk's bytes equal to c as a 16-bit mask (byte k -> bit k), OR-ed
+                    // into the lane's per-class accumulator; the row's y once per class
+                    const uint32_t bm = (uint32_t)c <= mx ? byte_mask16(q, 0x01010101u * (uint32_t)c) : 0u;
+                    acc[(c - 1) >> 1] |= bm << (16 * ((c - 1) & 1));
+                    if (__any_sync(0xFFFFFFFFu, bm != 0u) && lane == c) {
+                        ylo = min(ylo, y);
+                        yhi1 = max(yhi1, y + 1u);
+                    }
+                }
+            }
+        }
+        // x extents: lane q's accumulated byte masks cover bytes 16q .. 16q + 15
+#pragma unroll
+        for (int c = 1; c < kClasses; ++c) {
+            const uint32_t m = (acc[(c - 1) >> 1] >> (16 * ((c - 1) & 1))) & 0xFFFFu;
+            if (__ballot_sync(0xFFFFFFFFu, m != 0u) == 0u) continue;   // warp-uniform
+            const uint32_t a = __reduce_min_sync(0xFFFFFFFFu, m ? 16u * lane + __ffs(m) - 1u : kNone);
+            const uint32_t b = __reduce_max_sync(0xFFFFFFFFu, m ? 16u * lane + 32u - __clz(m) : 0u);
+            if (lane == 0) {
+                atomicMin(&s_min[c][2], a);
+                atomicMax(&s_max[c][2], b);
+                atomicOr(&s_seen, 1u << c);
             }
         }
     } else {
@@ -239,9 +293,18 @@ __global__ void fg_offsets_kernel(const __grid_constant__ Img3dLaunch L, const _
 
 cudaError_t launch_fg_scan(const Img3dLaunch& L, const FgLaunch& F, int32_t* box, cudaStream_t s) {
     if (L.n <= 0) return cudaSuccess;
-    int planes = 1;
-    for (int i = 0; i < L.n; ++i) planes = planes > L.d[i].sdim[0] ? planes : L.d[i].sdim[0];
-    fg_scan_kernel<<<dim3(planes, L.n), kScanThreads, 0, s>>>(L, F, box);
+    FgLaunch G = F;   // one CTA per plane of each scanned sample (no empty CTAs)
+    G.n_scan = 0;
+    int planes = 0;
+    for (int i = 0; i < L.n; ++i) {
+        if (!F.d[i].fg) continue;
+        G.scan_i[G.n_scan] = i;
+        G.scan_start[G.n_scan++] = planes;
+        planes += L.d[i].sdim[0];
+    }
+    G.scan_start[G.n_scan] = planes;
+    if (planes == 0) return cudaSuccess;
+    fg_scan_kernel<<<planes, kScanThreads, 0, s>>>(L, G, box);
     return cudaGetLastError();
 }
 

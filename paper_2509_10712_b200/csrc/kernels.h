@@ -264,6 +264,11 @@ struct FgDraw {
 };
 struct FgLaunch {
     FgDraw d[kMax3D];        // per sample of the Img3dLaunch
+    // (filled by launch_fg_scan) the scanned samples' planes as one flat grid: CTA x
+    // scans plane x - scan_start[k] of sample scan_i[k]; no CTA for unscanned samples
+    int32_t n_scan;
+    int32_t scan_i[kMax3D];
+    int32_t scan_start[kMax3D + 1];
 };
 cudaError_t launch_fg_scan(const Img3dLaunch& L, const FgLaunch& F, int32_t* box, cudaStream_t s);
 cudaError_t launch_fg_offsets(const Img3dLaunch& L, const FgLaunch& F, const int32_t* box, int4* offs,

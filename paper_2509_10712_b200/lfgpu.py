@@ -13,7 +13,8 @@ from typing import Iterable, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblfgpu.so")
+# LFG_LIB: an alternative build of the same library (A/B experiments: tools/kernel_sweep.py)
+LIB_PATH = os.environ.get("LFG_LIB") or os.path.join(_PKG, "liblfgpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "lfgpu.h")
 
 if not os.path.exists(LIB_PATH):

@@ -49,7 +49,7 @@ WORKERS = (4, 1)   # in-flight launch groups: 64 samples in flight, then a singl
 
 class _Args:
     pool = 0
-    workers = WORKERS
+    workers = 4
     workload = "img3d_heavy"
     time_scale = 10.0
     heavy_frac = 0.0
