@@ -292,6 +292,13 @@ Context::Context(const lfg_config& c) : cfg(c) {
     cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
     cuda_check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, cfg.device),
                "sm count");
+    // (A/B experiment) L2 -> DRAM fetch granularity hint in bytes (LFG_L2_FETCH=32|64|128)
+    if (const char* e = std::getenv("LFG_L2_FETCH")) {
+        size_t v = 0;
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(e)));
+        cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+        std::fprintf(stderr, "[lfg] L2 fetch granularity %zu\n", v);
+    }
     int lo = 0, hi = 0;
     cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     cuda_check(cudaStreamCreateWithPriority(&seal_stream, cudaStreamNonBlocking, hi), "seal stream");

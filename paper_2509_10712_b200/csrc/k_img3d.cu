@@ -156,7 +156,10 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
 // shared loads, stores -- measured as the bottleneck when all 8 warps shared
 // every tile).  Flip = reversed row / quad order; 16-B streaming stores.
 constexpr int kTR = kImg3dTileRows;
-constexpr int kTmaStages = 16;
+#ifndef LFG_IMG3D_STAGES
+#define LFG_IMG3D_STAGES 16   // (build-time A/B switch)
+#endif
+constexpr int kTmaStages = LFG_IMG3D_STAGES;
 constexpr int kTmaWarps = 8;                       // consumer warps
 constexpr int kTmaThreads = 32 * (kTmaWarps + 1);  // + producer warp
 // header: full / empty barriers, tile records, the launch's sample descriptors
@@ -188,6 +191,9 @@ struct __align__(16) TileRec {
 };
 static_assert(sizeof(TileRec) == 64, "tile record is one 64-B slot");
 
+// kDebug: the LFG_IMG3D_DEBUG profiling switches are compiled in (debug launches only),
+// so the production tile loop carries no switch tests
+template <bool kDebug>
 __global__ void __launch_bounds__(kTmaThreads)
 img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -236,10 +242,11 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
                 if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
                 const int t = (int)blockIdx.x + k * (int)gridDim.x;
                 // (debug bit 4: samples interleaved tile by tile instead of one after another)
-                const int i = (L.debug & 4) ? t % L.n : t / per;
-                const int rr = (L.debug & 4) ? t / L.n : t - i * per;
+                const int i = (kDebug && (L.debug & 4)) ? t % L.n : t / per;
+                const int rr = (kDebug && (L.debug & 4)) ? t / L.n : t - i * per;
                 const int z = rr / nyb, y0 = (rr - z * nyb) * kTR;
-                const Img3dDesc& d = sdesc[i];
+                Img3dDesc& d = sdesc[i];
+                if (kDebug && (L.debug & 8)) d.off[2] &= ~31;   // (profiling switch: 128-B aligned crop rows; wrong output)
                 const int fz = (d.flip & 1) ? cd - 1 - z : z;
                 const int fy0 = (d.flip & 2) ? ch - kTR - y0 : y0;   // may be < 0: zero rows, never stored
                 const int64_t v0 = ((int64_t)z * ch + y0) * cw;
@@ -257,7 +264,7 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
                 tr.m = d.off[2] & 3;
                 tr.slot = d.slot;
                 rec[s] = tr;
-                if (L.debug & 2) {   // profiling switch: no loads
+                if (kDebug && (L.debug & 2)) {   // profiling switch: no loads
                     mbar_arrive(full + s);
                 } else {
                     uint8_t* st = tiles + s * stage_bytes;
@@ -311,7 +318,7 @@ img3d_tma_kernel(const __grid_constant__ Img3dLaunch L) {
                     o[2] = fmaf(tr.sigma, z23.x, o[2]);
                     o[3] = fmaf(tr.sigma, z23.y, o[3]);
                 }
-                if (L.debug & 1) {   // profiling switch: no stores
+                if (kDebug && (L.debug & 1)) {   // profiling switch: no stores
                     if (o[0] == 123.f && lb == 7u) tr.out_img[0] = o[1];
                     continue;
                 }
@@ -387,7 +394,7 @@ cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s) {
         int o = occ[cw / 16].load(std::memory_order_relaxed);
         if (o == 0) {
             int v = 0;
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, img3d_tma_kernel, kTmaThreads, smem);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, img3d_tma_kernel<false>, kTmaThreads, smem);
             if (e != cudaSuccess) return e;
             o = v > 0 ? v : 1;
             occ[cw / 16].store(o, std::memory_order_relaxed);
@@ -397,12 +404,12 @@ cudaError_t launch_img3d(const Img3dLaunch& L, cudaStream_t s) {
         static const int dbg = getenv("LFG_IMG3D_DEBUG") ? atoi(getenv("LFG_IMG3D_DEBUG")) : 0;
         static const int ctas = getenv("LFG_IMG3D_CTAS") ? atoi(getenv("LFG_IMG3D_CTAS")) : 0;
         if (dbg == 0 && ctas == 0) {
-            img3d_tma_kernel<<<grid, kTmaThreads, smem, s>>>(L);
+            img3d_tma_kernel<false><<<grid, kTmaThreads, smem, s>>>(L);
         } else {
             Img3dLaunch L2 = L;
             L2.debug = dbg;
             const int g2 = ctas ? static_cast<int>(std::min<int64_t>(total, int64_t(sm_count()) * ctas)) : grid;
-            img3d_tma_kernel<<<g2, kTmaThreads, smem, s>>>(L2);
+            img3d_tma_kernel<true><<<g2, kTmaThreads, smem, s>>>(L2);
         }
         return cudaGetLastError();
     }
@@ -416,11 +423,13 @@ cudaError_t warm_img3d() {
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, img3d_kernel);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(img3d_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem_bytes(240));
+    e = cudaFuncSetAttribute(img3d_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem_bytes(240));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(img3d_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem_bytes(240));
     if (e != cudaSuccess) return e;
     sm_count();
     encode_fn();
-    return cudaFuncGetAttributes(&a, img3d_tma_kernel);
+    return cudaFuncGetAttributes(&a, img3d_tma_kernel<false>);
 }
 
 }  // namespace lfg

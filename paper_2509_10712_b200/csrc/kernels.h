@@ -137,7 +137,10 @@ __device__ __forceinline__ void img3d_offsets(const Img3dLaunch& L, int i, int o
         }
     }
 }
-constexpr int kImg3dTileRows = 8;
+#ifndef LFG_IMG3D_TILE_ROWS
+#define LFG_IMG3D_TILE_ROWS 8   // (build-time A/B switch)
+#endif
+constexpr int kImg3dTileRows = LFG_IMG3D_TILE_ROWS;
 // TMA path preconditions on the sample / crop geometry (else the row kernel runs)
 inline bool img3d_tma_ok(const void* img, const void* lbl, const int64_t dims[3], const int crop[3]) {
     return (reinterpret_cast<uintptr_t>(img) & 15) == 0 && (reinterpret_cast<uintptr_t>(lbl) & 15) == 0 &&

@@ -7,9 +7,15 @@
 // resume_slow waits on completion events, build_batches seals device batches,
 // run_consumer releases them.  Some samples get a long synthetic device cost
 // (a spin op in front of the chain) so the timeout path is exercised.
+// Then four more samples go through process_sample's fast path, are sealed on the
+// device (gpu::seal_device_batch), read back and compared with the CPU oracle
+// (oracle/lf_oracle.c: labels bit-exact, image within 1e-5 relative + 1e-6).
 // Exit code 0 = exactly-once delivery, fast/slow split as expected, every
-// batch device-sealed.
+// batch device-sealed, delivered outputs equal to the oracle's.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <set>
 #include <vector>
@@ -19,6 +25,7 @@
 #include "loadflow/runtime.hpp"
 #include "loadflow/trainer.hpp"
 #include "loadflow/worker_pool.hpp"
+#include "../../oracle/lf_oracle.h"   // the checker (test infrastructure)
 
 using namespace loadflow;
 
@@ -150,6 +157,72 @@ int main() {
     EXPECT(c.batches == st.batches);          // every batch was sealed on the device
     std::printf("device batches %lld (in place %lld, gathered %lld)\n", (long long)c.batches,
                 (long long)c.inplace_batches, (long long)c.gathered_batches);
+
+    // ---- delivered outputs against the oracle
+    {
+        const int64_t vox_in = D * H * W, vox = 32 * 32 * 32;
+        std::vector<float> himg(static_cast<size_t>(vox_in));
+        std::vector<uint8_t> hlbl(static_cast<size_t>(vox_in));
+        EXPECT(lfg_memcpy_d2h(ctx, himg.data(), img, vox_in * 4) == LFG_OK);
+        EXPECT(lfg_memcpy_d2h(ctx, hlbl.data(), lbl, vox_in) == LFG_OK);
+        SampleQueue fq(*rt, 16, QueueRole::fast);
+        TempQueue tq(*rt, 16, QueueRole::temp);
+        Batch b;
+        for (uint64_t id = 1000; id < 1004; ++id) {
+            Sample s;
+            s.id = id;
+            s.chain = &chain;
+            s.bytes_in = s.size_bytes = double(vox_in * 5);
+            s.bytes_out = double(vox * 5);
+            s.device.shard = shard;
+            s.device.desc.src_kind = LFG_SRC_DEVICE;
+            s.device.desc.ndim = 3;
+            s.device.desc.dims[0] = D;
+            s.device.desc.dims[1] = H;
+            s.device.desc.dims[2] = W;
+            s.device.desc.data = img;
+            s.device.desc.aux = lbl;
+            s.device.desc.spin_us[0] = 10;
+            Rng rng(id);
+            RouteResult r = process_sample(std::move(s), kNoTimeout, fq, tq, *rt, rng);
+            EXPECT(r.route == Route::fast);
+            auto got = fq.try_get();
+            EXPECT(got.has_value());
+            b.samples.push_back(std::move(*got));
+        }
+        gpu::seal_device_batch(b);
+        EXPECT(b.device_batch >= 0);
+        void* dp = nullptr;
+        int64_t bytes = 0;
+        int nb = 0, inplace = 0;
+        uint64_t ids[4] = {};
+        EXPECT(lfg_batch_info(ctx, b.device_batch, &dp, &bytes, &nb, ids, &inplace) == LFG_OK);
+        EXPECT(nb == 4 && bytes >= 4 * vox * 5);
+        std::vector<uint8_t> host(static_cast<size_t>(bytes));
+        EXPECT(lfg_batch_copy_to_host(ctx, b.device_batch, host.data(), static_cast<size_t>(bytes)) == LFG_OK);
+        const int64_t dims[3] = {D, H, W};
+        double worst = 0.0;
+        for (int k = 0; k < nb; ++k) {   // planar batch: [f32 image x 4][u8 label x 4]
+            lfo_cfg3d oc;
+            lfo_cfg3d_default(&oc);
+            oc.crop[0] = oc.crop[1] = oc.crop[2] = 32;
+            lfo_params3d op;
+            lfo_draw3d(&oc, cfg.seed, ids[k], dims, &op);
+            std::vector<double> e_img(static_cast<size_t>(vox));
+            std::vector<uint8_t> e_lbl(static_cast<size_t>(vox));
+            lfo_apply3d(&oc, &op, himg.data(), hlbl.data(), dims, e_img.data(), e_lbl.data());
+            const float* g_img = reinterpret_cast<const float*>(host.data()) + k * vox;
+            const uint8_t* g_lbl = host.data() + 4 * vox * 4 + k * vox;
+            EXPECT(std::memcmp(g_lbl, e_lbl.data(), static_cast<size_t>(vox)) == 0);
+            for (int64_t v = 0; v < vox; ++v) {
+                const double err = std::fabs(g_img[v] - e_img[v]);
+                worst = std::max(worst, err / (1e-5 * std::fabs(e_img[v]) + 1e-6));
+            }
+        }
+        std::printf("delivered outputs vs oracle: worst err/bound %.3f\n", worst);
+        EXPECT(worst <= 1.0);
+        EXPECT(lfg_batch_release(ctx, b.device_batch, nullptr) == LFG_OK);
+    }
     gpu::unbind_all();
     lfg_device_free(ctx, img);
     lfg_device_free(ctx, lbl);

@@ -687,17 +687,19 @@ def test_device_profiler_escalates_and_deescalates(lfgpu):
 # ------------------------------------------------------------------ reference-shaped C++ API
 def test_cpp_api_device_pipeline():
     """process_sample / resume_slow / build_batches / run_consumer (the reference
-    signatures, include/loadflow) drive the GPU path end to end."""
+    signatures, include/loadflow) drive the GPU path end to end; delivered outputs
+    of the C++ path are compared with the oracle (lf_oracle.c) inside the program."""
     import os
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     pkg = os.path.join(root, "paper_2509_10712_b200")
     exe = os.path.join(root, "tests", "cpp", "device_pipeline")
-    if not os.path.exists(exe):
-        subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"),
-                               os.path.join(root, "tests", "cpp", "device_pipeline.cpp"), "-o", exe,
+    src = os.path.join(root, "tests", "cpp", "device_pipeline.cpp")
+    ora = os.path.join(root, "oracle")
+    if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+        subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"), src, "-o", exe,
                                "-L", pkg, "-lloadflow_b200", "-llfgpu", f"-Wl,-rpath,{pkg}",
-                               "-lpthread"])
+                               "-L", ora, "-llf_oracle", f"-Wl,-rpath,{ora}", "-lpthread"])
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr
