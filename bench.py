@@ -577,12 +577,21 @@ def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
         kernel = "fg_scan_kernel + img3d_tma_kernel (one stage)"
     out = {"kernel": kernel, "launches": int(launches), "mean_launch_us": round(1e3 * t["mean_ms"], 2),
            "traffic": traffic_of(wl.name), "algo_bytes_per_launch": int(t["bytes"] / max(launches, 1))}
-    if wl.name == "speech":
+    if wl.name == "speech" and os.environ.get("LFG_SPEECH_KERNEL") == "tc":
+        # the tcgen05 3xTF32 DFT-GEMM kernel (A/B switch): tensor-bound
         tf = t["flops"] / (ms / 1e3) / 1e12 if ms > 0 else 0.0
         out.update({"bound": "tensor", "achieved": round(tf, 1), "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": round(tf / tf32_peak, 4),
                     "flops_per_launch": int(t["flops"] / max(launches, 1)),
                     "hbm_gbs": round(t["bytes"] / (ms / 1e3) / 1e9, 1) if ms > 0 else 0.0})
+    elif wl.name == "speech":
+        # the FFT kernel (default): waveform read + spliced log-mel written, against HBM;
+        # it is issue-bound (~12 k CUDA-core FLOPs per frame), so the HBM fraction is low.
+        # dft_equiv: the 3xTF32 DFT-GEMM FLOPs the same work costs on the tensor cores
+        gbs = t["bytes"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        out.update({"kernel": "speech_fft_kernel", "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
+                    "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
+                    "dft_equiv_tflops": round(t["flops"] / (ms / 1e3) / 1e12, 1) if ms > 0 else 0.0})
     else:
         gbs = t["bytes"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0
         out.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",

@@ -393,6 +393,214 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
     if (L.st.cnt != nullptr && tid == 0) sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, parts);
 }
 
+// ------------------------------------------------------------------ K8'-K10' (default)
+// The same FilterBank + SpecAugment + FrameSplicing as speech_kernel, with the STFT as a
+// real 512-point FFT on the CUDA cores instead of a DFT GEMM: ~12 k FLOPs per frame
+// instead of 2 x 320 x 512 x 3 tensor FLOPs (3xTF32), so the kernel is bound by issue and
+// HBM rather than by the tensor pipe.  Per frame (one warp):
+//   z_n = a_2n + i a_2n+1 (a = windowed taps, 160 non-zero of 256); Z = FFT256(z) as
+//   256 = 8 x 32: lane l holds z[32 n1 + l] -> 8-point DFT over n1, twiddle W256^(l k1);
+//   a shared-memory transpose gives lane (k1, b) = 4 k1 + b the values of lanes 4a + b ->
+//   8-point DFT over a, twiddle W32^(b c); a 4-point DFT across the lane quad (two
+//   shuffle stages) -> lane (k1, b') holds Z[k1 + 8 c + 64 bitrev2(b')], c = 0..7;
+//   one shuffle per c fetches Z[256 - k]; X_k = E_k + W512^k O_k (E, O the even / odd
+//   sample spectra), P_k = |X_k|^2 for k = 0..256 (X_256 = E_0 - O_0).
+// Mel: each lane sums its filters' (bin, weight) lists from the warp's power row in
+// shared memory; then log(x + 2^-24), SpecAugment masks and the stack-3 splice layout
+// (frame f's 80 values at out + 80 f) as the tensor-core kernel.  Index mapping and
+// pairing are checked against numpy in tests (test_speech_* vs the oracle).
+constexpr int kFftFrames = 96;                                   // per CTA (multiple of 3)
+constexpr int kFftWarps = 8;
+constexpr int kTrPitch = 36;                                     // transpose row pitch (float2)
+// mel filters as dense taps: filter m = lane + 32 g reads kMelW[g] consecutive bins from
+// mel_b0[m] (the slaney bank's widest filters per lane group: 3, 10, 18 bins)
+constexpr int kMelW0 = 3, kMelW1 = 10, kMelW2 = 18;
+constexpr int kPwPitch = 260;
+
+struct __align__(16) FftTables {
+    float win[kTaps];                 // periodic Hann(320)
+    float2 tw256[8 * 32];             // [k1][l] W256^(l k1)
+    float2 tw32[4 * 8];               // [b][c] W32^(b c)
+    float2 tw512[kBins];              // W512^k
+    int32_t mel_b0[kMels];            // filter m's first bin
+    float mel_wd[kMelW2 * kMels];     // [tap][filter] weights (0 past the filter's span)
+};
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }   // a * (-i)
+// in-place 8-point DFT, natural order in and out
+__device__ __forceinline__ void dft8(float2 x[8]) {
+    constexpr float r = 0.70710678118654752f;
+    // even / odd 4-point DFTs
+    const float2 e0 = cadd(x[0], x[4]), e1 = csub(x[0], x[4]), e2 = cadd(x[2], x[6]), e3 = mul_mi(csub(x[2], x[6]));
+    const float2 E0 = cadd(e0, e2), E2 = csub(e0, e2), E1 = cadd(e1, e3), E3 = csub(e1, e3);
+    const float2 o0 = cadd(x[1], x[5]), o1 = csub(x[1], x[5]), o2 = cadd(x[3], x[7]), o3 = mul_mi(csub(x[3], x[7]));
+    float2 O0 = cadd(o0, o2), O2 = csub(o0, o2), O1 = cadd(o1, o3), O3 = csub(o1, o3);
+    O1 = make_float2(r * (O1.x + O1.y), r * (O1.y - O1.x));      // * W8^1 = (1 - i) / sqrt 2
+    O2 = mul_mi(O2);                                               // * W8^2 = -i
+    O3 = make_float2(r * (O3.y - O3.x), -r * (O3.x + O3.y));     // * W8^3 = -(1 + i) / sqrt 2
+    x[0] = cadd(E0, O0);
+    x[4] = csub(E0, O0);
+    x[1] = cadd(E1, O1);
+    x[5] = csub(E1, O1);
+    x[2] = cadd(E2, O2);
+    x[6] = csub(E2, O2);
+    x[3] = cadd(E3, O3);
+    x[7] = csub(E3, O3);
+}
+__device__ __forceinline__ float2 shfl2(float2 v, int src) {
+    return make_float2(__shfl_sync(0xFFFFFFFFu, v.x, src), __shfl_sync(0xFFFFFFFFu, v.y, src));
+}
+__device__ __forceinline__ int bitrev2(int x) { return ((x & 1) << 1) | ((x >> 1) & 1); }
+
+// Frames are dealt to warps round-robin over the launch's flattened frame space
+// (L.tile_start holds per-utterance frame prefix sums for this kernel), so every SM
+// works until the last few frames: no CTA-granular tail.  A frame's 320 taps are read
+// straight from the waveform (L1 / L2: neighbouring frames, on neighbouring warps of
+// the same CTA, share half of them); only the first frame of an utterance and the last
+// ones need the reflect padding.
+__global__ void __launch_bounds__(32 * kFftWarps, 3)
+speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restrict__ g) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    FftTables* tb = reinterpret_cast<FftTables*>(smem);
+    float2* tr_all = reinterpret_cast<float2*>(smem + sizeof(FftTables));
+    float* pw_all = reinterpret_cast<float*>(tr_all + kFftWarps * 8 * kTrPitch);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {
+        const float4* src = reinterpret_cast<const float4*>(g);
+        float4* dst = reinterpret_cast<float4*>(tb);
+#pragma unroll 4
+        for (int q = tid; q < (int)(sizeof(FftTables) / 16); q += blockDim.x) dst[q] = __ldg(src + q);
+    }
+    __syncthreads();
+    float2* tr = tr_all + warp * 8 * kTrPitch;
+    float* pw = pw_all + warp * kPwPitch;
+    const int qk1 = lane >> 2, qb = lane & 3;          // (k1, b) after the transpose
+    const int qd = bitrev2(qb);
+    const int total = L.tile_start[L.n];
+    const int stride = gridDim.x * kFftWarps;
+    // the raw taps x[(f - 1) * 160 + 2 n .. + 1], n = 32 n1 + lane (n1 < 5), of frame gf,
+    // loaded one frame ahead so their latency hides behind the current frame's FFT
+    auto load_taps = [&](int gfx, int& ux, float2 xv[5]) {
+        while (gfx >= L.tile_start[ux + 1]) ++ux;      // warp-uniform, monotone
+        const SpDesc& dx = L.d[ux];
+        const int f = gfx - L.tile_start[ux];
+        const int base = (f - 1) * kHop, Lw = dx.L;
+        if (f >= dx.T) return;                          // splice padding: no taps
+        const bool interior = base >= 0 && base + kTaps <= Lw && ((reinterpret_cast<uintptr_t>(dx.wav) & 7) == 0);
+#pragma unroll
+        for (int n1 = 0; n1 < 5; ++n1) {
+            const int j = 2 * (32 * n1 + lane);
+            if (interior) {
+                xv[n1] = __ldg(reinterpret_cast<const float2*>(dx.wav + base + j));
+            } else {
+                int i0 = base + j, i1 = base + j + 1;
+                i0 = i0 < 0 ? -i0 : (i0 >= Lw ? 2 * (Lw - 1) - i0 : i0);
+                i1 = i1 < 0 ? -i1 : (i1 >= Lw ? 2 * (Lw - 1) - i1 : i1);
+                xv[n1] = make_float2(__ldg(dx.wav + i0), __ldg(dx.wav + i1));
+            }
+        }
+    };
+    int u = 0, un = 0;
+    float2 cur[5], nxt[5];
+    const int gf0 = blockIdx.x * kFftWarps + warp;
+    if (gf0 < total) load_taps(gf0, un, cur);
+    for (int gf = gf0; gf < total; gf += stride) {
+        u = un;
+        if (gf + stride < total) load_taps(gf + stride, un, nxt);
+        const SpDesc& d = L.d[u];
+        const int f = gf - L.tile_start[u];
+        const int T = d.T;
+        float* out = d.out + (int64_t)f * kMels;
+        bool tmask = f >= T;                            // splice padding frames are zero
+        for (int q = 0; q < L.n_tmask; ++q) tmask |= f >= d.t_lo[q] && f < d.t_lo[q] + d.t_w[q];
+        if (tmask) {
+            for (int m = lane; m < kMels; m += 32) out[m] = 0.0f;
+        } else {
+            // stage 1: z[32 n1 + l] = a(2n) + i a(2n + 1), windowed taps
+            float2 v[8];
+#pragma unroll
+            for (int n1 = 0; n1 < 8; ++n1) {
+                if (n1 < 5) {
+                    const int j = 2 * (32 * n1 + lane);
+                    const float2 ww = *reinterpret_cast<const float2*>(tb->win + j);
+                    v[n1] = make_float2(cur[n1].x * ww.x, cur[n1].y * ww.y);
+                } else {
+                    v[n1] = make_float2(0.f, 0.f);
+                }
+            }
+            dft8(v);
+#pragma unroll
+            for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], tb->tw256[k1 * 32 + lane]);
+#pragma unroll
+            for (int k1 = 0; k1 < 8; ++k1) tr[k1 * kTrPitch + lane] = v[k1];
+            __syncwarp();
+            // stage 2: lane (k1, b) takes the values of lanes 4a + b; 8-point DFT over a
+#pragma unroll
+            for (int a = 0; a < 8; ++a) v[a] = tr[qk1 * kTrPitch + 4 * a + qb];
+            dft8(v);
+#pragma unroll
+            for (int c = 1; c < 8; ++c) v[c] = cmul(v[c], tb->tw32[qb * 8 + c]);
+            // stage 3: 4-point DFT across the lane quad (decimation in frequency)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float2 p2 = shfl2(v[c], lane ^ 2);
+                v[c] = (qb & 2) ? csub(p2, v[c]) : cadd(v[c], p2);
+                if ((qb & 2) && (qb & 1)) v[c] = mul_mi(v[c]);     // W4^1 on the upper half, j = 1
+                const float2 p1 = shfl2(v[c], lane ^ 1);
+                v[c] = (qb & 1) ? csub(p1, v[c]) : cadd(v[c], p1);
+            }
+            // lane (k1, b') holds Z[k1 + 8 c + 64 d], d = bitrev2(b').  Real-FFT split:
+            // Z[256 - k] lives at lane 4 (8 - k1) + 3 - b', element 7 - c (k1 >= 1), or in
+            // the k1 = 0 quad: lane 3 - b', element 8 - c (c >= 1) / lane bitrev2(4 - d), element 0
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float2 give = qk1 >= 1 ? v[7 - c] : v[(8 - c) & 7];
+                int src;
+                if (qk1 >= 1) src = 4 * (8 - qk1) + 3 - qb;
+                else if (c >= 1) src = 3 - qb;
+                else src = bitrev2((4 - qd) & 3);
+                const float2 zp = shfl2(give, src);
+                const int k = qk1 + 8 * c + 64 * qd;
+                const float2 zk = v[c];
+                const float2 e = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
+                const float2 o = make_float2(0.5f * (zk.y + zp.y), -0.5f * (zk.x - zp.x));   // -i/2 (zk - conj zp)
+                const float2 xk = cadd(e, cmul(tb->tw512[k], o));
+                pw[k] = fmaf(xk.x, xk.x, xk.y * xk.y);
+                if (k == 0) {
+                    const float ny = e.x - o.x;              // X_256 = E_0 - O_0 (both real)
+                    pw[kBins] = ny * ny;
+                }
+            }
+            __syncwarp();
+            // mel filters m = lane, lane + 32, lane + 64, log, frequency masks, store
+            const int fl0 = L.n_fmask > 0 ? d.f_lo[0] : 0, fh0 = L.n_fmask > 0 ? d.f_lo[0] + d.f_w[0] : 0;
+            const int fl1 = L.n_fmask > 1 ? d.f_lo[1] : 0, fh1 = L.n_fmask > 1 ? d.f_lo[1] + d.f_w[1] : 0;
+            auto mel_out = [&](auto W, int m) {
+                const int b0 = tb->mel_b0[m];
+                float acc = 0.0f;
+#pragma unroll
+                for (int q = 0; q < decltype(W)::value; ++q) acc = fmaf(tb->mel_wd[q * kMels + m], pw[b0 + q], acc);
+                const bool masked = (m >= fl0 && m < fh0) || (m >= fl1 && m < fh1);
+                out[m] = masked ? 0.0f : logf(acc + 5.9604644775390625e-8f);   // + 2^-24
+            };
+            mel_out(std::integral_constant<int, kMelW0>{}, lane);
+            mel_out(std::integral_constant<int, kMelW1>{}, lane + 32);
+            if (lane + 64 < kMels) mel_out(std::integral_constant<int, kMelW2>{}, lane + 64);
+        }
+        __syncwarp();   // (tr / pw are reused by the next frame; the frame's stores precede the count)
+        if (L.st.cnt != nullptr && lane == 0)
+            sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, (uint32_t)(L.tile_start[u + 1] - L.tile_start[u]));
+#pragma unroll
+        for (int n1 = 0; n1 < 5; ++n1) cur[n1] = nxt[n1];
+    }
+}
+constexpr int kFftSmem = (int)sizeof(FftTables) + kFftWarps * 8 * kTrPitch * 8 + kFftWarps * kPwPitch * 4;
+
 // K11: PermuteAudio + Pad: per-sample [T'_i, W] slots -> batch [T'_max, n, W], zero-padded.
 // Grid (t_max, ceil(n / 4)): a CTA moves one time row of 4 samples, 64 threads per
 // sample row (16-B loads / stores), so a batch is ~t_max * n / 4 small CTAs rather
@@ -426,8 +634,17 @@ float as_f(uint32_t u) {
 }  // namespace
 
 struct SpeechTables {
-    char* basis = nullptr;   // kChunks x 64 KB, the per-stage smem image of B
+    char* basis = nullptr;   // kChunks x 64 KB, the per-stage smem image of B (tensor-core kernel)
+    FftTables* fft = nullptr;   // window, twiddles and mel (bin, weight) lists (FFT kernel)
 };
+
+namespace {
+// LFG_SPEECH_KERNEL=tc: the tcgen05 DFT-GEMM kernel (A/B); default: the FFT kernel
+bool speech_use_tc() {
+    static const bool tc = getenv("LFG_SPEECH_KERNEL") && std::strcmp(getenv("LFG_SPEECH_KERNEL"), "tc") == 0;
+    return tc;
+}
+}  // namespace
 
 cudaError_t speech_tables_create(SpeechTables** out) {
     // B: column col of N half h is bin 128 h + (col mod 128), cos (col < 128) or
@@ -494,6 +711,32 @@ cudaError_t speech_tables_create(SpeechTables** out) {
         for (int m = first + 2; first >= 0 && m < kMels; ++m)
             if (fb[(size_t)m * nf + k] != 0.0) return cudaErrorInvalidValue;   // > 2 filters per bin
     }
+    // FFT kernel tables (fp64 -> fp32)
+    FftTables ft;
+    std::memset(&ft, 0, sizeof(ft));
+    for (int j = 0; j < kTaps; ++j) ft.win[j] = (float)win[j];
+    auto tw = [](int num, int den) {   // exp(-2 pi i num / den)
+        const double a = -2.0 * M_PI * (double)(num % den) / (double)den;
+        return make_float2((float)std::cos(a), (float)std::sin(a));
+    };
+    for (int k1 = 0; k1 < 8; ++k1)
+        for (int l = 0; l < 32; ++l) ft.tw256[k1 * 32 + l] = tw(l * k1, 256);
+    for (int b = 0; b < 4; ++b)
+        for (int c = 0; c < 8; ++c) ft.tw32[b * 8 + c] = tw(b * c, 32);
+    for (int k = 0; k < kBins; ++k) ft.tw512[k] = tw(k, 512);
+    for (int m = 0; m < kMels; ++m) {
+        int lo = -1, hi = -1;
+        for (int k = 0; k < nf; ++k)
+            if (fb[(size_t)m * nf + k] != 0.0) {
+                if (lo < 0) lo = k;
+                hi = k;
+            }
+        const int width = m < 32 ? kMelW0 : (m < 64 ? kMelW1 : kMelW2);
+        if (lo < 0) lo = hi = 0;
+        if (hi - lo + 1 > width || lo + width > nf) return cudaErrorInvalidValue;   // bank wider than the taps
+        ft.mel_b0[m] = lo;
+        for (int q = 0; q < width; ++q) ft.mel_wd[q * kMels + m] = (float)fb[(size_t)m * nf + lo + q];
+    }
     cudaError_t e;
     if ((e = cudaMemcpyToSymbol(c_win_nyq, nyq, sizeof(nyq))) != cudaSuccess) return e;
     if ((e = cudaMemcpyToSymbol(c_mel_m, mel_m, sizeof(mel_m))) != cudaSuccess) return e;
@@ -512,6 +755,11 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     if ((e = cudaFuncSetAttribute(speech_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBytes)) != cudaSuccess)
         return e;
+    if ((e = cudaMalloc(&t->fft, sizeof(FftTables))) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(t->fft, &ft, sizeof(FftTables), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(speech_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kFftSmem)) != cudaSuccess)
+        return e;
     *out = t;
     return cudaSuccess;
 }
@@ -519,10 +767,11 @@ cudaError_t speech_tables_create(SpeechTables** out) {
 void speech_tables_destroy(SpeechTables* t) {
     if (!t) return;
     cudaFree(t->basis);
+    cudaFree(t->fft);
     delete t;
 }
 
-int speech_frames_per_cta() { return kFramesPerCta; }
+int speech_frames_per_cta() { return speech_use_tc() ? kFramesPerCta : kFftFrames; }   // (stack must divide it)
 
 cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, cudaStream_t s) {
     if (L0.n <= 0) return cudaSuccess;
@@ -530,9 +779,24 @@ cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, cudaStream_
     SpLaunch L = L0;
     L.debug = dbg;
     L.tile_start[0] = 0;
+    if (speech_use_tc()) {   // CTA tiles of kFramesPerCta frames
+        for (int i = 0; i < L.n; ++i)
+            L.tile_start[i + 1] = L.tile_start[i] + (L.d[i].T + kFramesPerCta - 1) / kFramesPerCta;
+        speech_kernel<<<L.tile_start[L.n], kThreads, kSmemBytes, s>>>(L, t->basis);
+        return cudaGetLastError();
+    }
+    // FFT kernel: frame prefix sums (splice-padded frame counts); 3 CTAs per SM
     for (int i = 0; i < L.n; ++i)
-        L.tile_start[i + 1] = L.tile_start[i] + (L.d[i].T + kFramesPerCta - 1) / kFramesPerCta;
-    speech_kernel<<<L.tile_start[L.n], kThreads, kSmemBytes, s>>>(L, t->basis);
+        L.tile_start[i + 1] = L.tile_start[i] + (L.d[i].T + L.stack - 1) / L.stack * L.stack;
+    static int sms = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    const int need = (L.tile_start[L.n] + kFftWarps - 1) / kFftWarps;
+    const int grid = need < 3 * sms ? need : 3 * sms;
+    speech_fft_kernel<<<grid > 0 ? grid : 1, 32 * kFftWarps, kFftSmem, s>>>(L, t->fft);
     return cudaGetLastError();
 }
 
@@ -545,6 +809,7 @@ cudaError_t launch_speech_collate(const SpCollate& C, cudaStream_t s) {
 cudaError_t warm_speech() {
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, speech_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, speech_fft_kernel);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, speech_collate_kernel);
     return e;
 }
