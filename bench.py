@@ -553,9 +553,9 @@ def oracle_check(wl, ids_timed, cap) -> dict:
 
 def traffic_of(workload: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture
-    (profiles/r1_traffic.json), or None when there is no capture for this workload."""
+    (profiles/r2_traffic.json), or None when there is no capture for this workload."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             t = json.load(f).get(workload)
         return int(t["dram_read"] + t["dram_write"]) if t else None
     except Exception:

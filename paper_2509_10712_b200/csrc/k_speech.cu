@@ -463,7 +463,10 @@ __device__ __forceinline__ int bitrev2(int x) { return ((x & 1) << 1) | ((x >> 1
 // straight from the waveform (L1 / L2: neighbouring frames, on neighbouring warps of
 // the same CTA, share half of them); only the first frame of an utterance and the last
 // ones need the reflect padding.
-__global__ void __launch_bounds__(32 * kFftWarps, 3)
+#ifndef LFG_FFT_REG_TW
+#define LFG_FFT_REG_TW 0   // (build-time A/B) lane twiddles held in registers, 2 CTAs / SM
+#endif
+__global__ void __launch_bounds__(32 * kFftWarps, LFG_FFT_REG_TW ? 2 : 3)
 speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restrict__ g) {
     extern __shared__ __align__(16) uint8_t smem[];
     FftTables* tb = reinterpret_cast<FftTables*>(smem);
@@ -481,6 +484,19 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
     float* pw = pw_all + warp * kPwPitch;
     const int qk1 = lane >> 2, qb = lane & 3;          // (k1, b) after the transpose
     const int qd = bitrev2(qb);
+#if LFG_FFT_REG_TW
+    float2 rtw256[8], rtw32[8];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        rtw256[k] = tb->tw256[k * 32 + lane];
+        rtw32[k] = tb->tw32[qb * 8 + k];
+    }
+#define TW256(k1) rtw256[k1]
+#define TW32(c) rtw32[c]
+#else
+#define TW256(k1) tb->tw256[(k1) * 32 + lane]
+#define TW32(c) tb->tw32[qb * 8 + (c)]
+#endif
     const int total = L.tile_start[L.n];
     const int stride = gridDim.x * kFftWarps;
     // the raw taps x[(f - 1) * 160 + 2 n .. + 1], n = 32 n1 + lane (n1 < 5), of frame gf,
@@ -535,7 +551,7 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             }
             dft8(v);
 #pragma unroll
-            for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], tb->tw256[k1 * 32 + lane]);
+            for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], TW256(k1));
 #pragma unroll
             for (int k1 = 0; k1 < 8; ++k1) tr[k1 * kTrPitch + lane] = v[k1];
             __syncwarp();
@@ -544,7 +560,7 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             for (int a = 0; a < 8; ++a) v[a] = tr[qk1 * kTrPitch + 4 * a + qb];
             dft8(v);
 #pragma unroll
-            for (int c = 1; c < 8; ++c) v[c] = cmul(v[c], tb->tw32[qb * 8 + c]);
+            for (int c = 1; c < 8; ++c) v[c] = cmul(v[c], TW32(c));
             // stage 3: 4-point DFT across the lane quad (decimation in frequency)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
