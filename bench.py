@@ -715,6 +715,14 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
                                    "launches": rep.launches, "batches": rep.batches,
                                    "inplace": rep.inplace_batches}}), file=sys.stderr, flush=True)
     out["check_value"] = oracle_check(wl, ids_timed, cap) if cap_pos and rank == 0 else None
+    if not heavy:
+        # the same resident run with MinatoLoader's timeout machinery live: the Profiler's
+        # adaptive p75 / p90 budget over device-timed per-sample totals (policy 1), stage
+        # events timed -- what the fast / slow classification costs the headline path
+        rep_t, *_ = run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, policy=1)
+        out["value_timeouts"] = rep_t.timed_samples / (rep_t.elapsed_ms / 1e3) if rep_t.elapsed_ms > 0 else None
+        out["timeouts_slow"] = rep_t.slow / max(1, rep_t.samples)
+        out["timeouts_t_out_us"] = rep_t.final_t_out_us
     out["roof"] = dict(kernel_roofline(L, ctx, wl, ids_timed[: min(len(ids_timed), 64 * B if B > 2 else 64)],
                                        hbm_peak, tf32_peak), peak_source=peak_src)
     out["pool_bytes"] = int(wl.pool_bytes)
@@ -869,6 +877,12 @@ def main():
         "check": {"value_run": r["check_value"], "e2e_run": r["check_e2e"]},
         "wall_s": round(r["wall"], 3),
     }
+    if r.get("value_timeouts") is not None:
+        # rank-local figures of the extra run (rank 0's shard)
+        line["value_with_timeouts"] = {"value": round(r["value_timeouts"] * world, 1), "unit": "samples/s",
+                                       "policy": "profiler p75 -> p90 (adaptive)",
+                                       "slow_frac": round(r["timeouts_slow"], 4),
+                                       "final_t_out_us": round(r["timeouts_t_out_us"], 1)}
     if dropin is not None:
         line["dropin"] = dropin
     if fake:
