@@ -351,6 +351,16 @@ Context::Context(const lfg_config& c) : cfg(c) {
     cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&stamp_dev_), stamp_host_, 0), "stamp words");
     cuda_check(cudaMalloc(&stamp_cnt_, kStampSlots * sizeof(uint32_t)), "stamp counters");
     cuda_check(cudaMemset(stamp_cnt_, 0, kStampSlots * sizeof(uint32_t)), "stamp counters");
+    // Host tables of shard runs, faulted in once here (a run of up to kPrefault samples
+    // then takes no page fault on its ticket or parameter tables; larger runs grow them)
+    {
+        constexpr size_t kPrefault = size_t(1) << 16;
+        tickets.resize(kPrefault);
+        tickets.clear();
+        pre_store.resize(kPrefault);
+        std::memset(static_cast<void*>(pre_store.data()), 0, kPrefault * sizeof(PreDraw));
+        groups.reserve(kPrefault / 8);
+    }
     // draw workers: half the host threads (the shard loop and the trainer keep theirs), <= 16
     workers = std::make_unique<WorkerThreads>(
         static_cast<int>(std::clamp(std::thread::hardware_concurrency() / 2, 1u, 16u)));

@@ -226,6 +226,14 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     int64_t sync_next = 0;   // first position of the next batch to seal
     const int64_t run_t0 = host_now_us();
     int64_t last_update = run_t0;
+    // LFG_SHARD_TRACE=1: host timeline of the run (group fed / group finished / batch sealed), on stderr
+    const bool trace_on = std::getenv("LFG_SHARD_TRACE") != nullptr;
+    struct TraceEv {
+        int64_t t_us;
+        int kind;
+        int64_t id;
+    };
+    std::vector<TraceEv> trace;
 
     ctx.recycle_tables();   // a previous run's finished tickets: reuse their storage
     const int64_t tbase = static_cast<int64_t>(ctx.tickets.size());
@@ -306,12 +314,14 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         return true;
     };
     const bool profiled = rc.policy == 1 || rc.policy == 2;
-    int64_t est_group_us = 0;   // ~70% of the recent groups' device time (query throttle)
+    int64_t est_group_us = 0;   // ~70% of the recent groups' device time, or host-observed time when
+                                // the groups are untimed (query throttle)
     // the group's last event completed: hand on the rest; per-sample device-timed
     // totals (the group's event-timed span less the time from the sample's stamp to
     // the group's last stamp) go to the profiler window, one record per sample as
     // profiler.cpp:40-45
     auto finish_group = [&](Group& g, bool parked_group) {
+        if (trace_on) trace.push_back({host_now_us() - run_t0, 1, g.id});
         const int sz = static_cast<int>(g.tickets.size());
         const int64_t tot = total_us(g);
         const bool per = g.stamped && (profiled || t_out < kNoTimeoutUs);
@@ -342,7 +352,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             }
             for (int i = 0; profiled && i < sz; ++i) prof.record(tot, slow_all);
             if (nbatches >= rc.warmup_batches) kernel_ms += tot / 1000.0;
-            est_group_us = static_cast<int64_t>(0.8 * est_group_us + 0.2 * 0.7 * tot);
+            est_group_us = static_cast<int64_t>(0.8 * est_group_us + 0.2 * 0.7 * (tot > 0 ? tot : host_now_us() - g.t_launch_us));
             release_group(g);
             return;
         }
@@ -358,7 +368,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             if (profiled) prof.record(us, g.got[static_cast<size_t>(i)] == 2);
         }
         if (nbatches >= rc.warmup_batches) kernel_ms += tot / 1000.0;
-        est_group_us = static_cast<int64_t>(0.8 * est_group_us + 0.2 * 0.7 * tot);
+        est_group_us = static_cast<int64_t>(0.8 * est_group_us + 0.2 * 0.7 * (tot > 0 ? tot : host_now_us() - g.t_launch_us));
         release_group(g);
     };
 
@@ -374,7 +384,10 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
     const int64_t n_chunks = (n + kChunk - 1) / kChunk;
     // (the context keeps this table between runs: its pages stay mapped and warm)
     std::vector<PreDraw>& pre = ctx.pre_store;
-    if (pre.size() < static_cast<size_t>(n)) pre.resize(static_cast<size_t>(n));
+    if (pre.size() < static_cast<size_t>(n)) {   // grow without copying the old (scratch) entries
+        std::vector<PreDraw> fresh(static_cast<size_t>(n));
+        pre.swap(fresh);
+    }
     std::unique_ptr<std::atomic<uint8_t>[]> ready(new std::atomic<uint8_t>[std::max<int64_t>(n_chunks, 1)]);
     for (int64_t i = 0; i < n_chunks; ++i) ready[i].store(0, std::memory_order_relaxed);
     std::atomic<int64_t> next_chunk{0};
@@ -541,8 +554,16 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             ph.lap(Phases::FLUSH);
             fed += got;
             inflight.push_back(gid);
+            if (trace_on) trace.push_back({host_now_us() - run_t0, 0, gid});
             progressed = true;
             if (got < take) break;
+            // keep feeding while the oldest in-flight group is still running; once it has
+            // finished, go poll and seal first, so the first batches are not held back
+            // behind the whole feed (one event query, only once the group is due)
+            if (inflight.size() > 1) {
+                Group& og = ctx.groups[inflight.front()];
+                if (host_now_us() - og.t_launch_us >= est_group_us && ctx.poll_group(og)) break;
+            }
         }
         // (4) batcher: seal eagerly, fast first
         const bool tail = fed == n && inflight.empty() && parked.empty();
@@ -616,6 +637,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
             }
             BatchRec& br = ctx.batch(b);
             if (sync) sync_next += k;
+            if (trace_on) trace.push_back({host_now_us() - run_t0, 2, nbatches});
             const bool timed = nbatches >= rc.warmup_batches;
             if (ss != nullptr) {
                 // the consumer owns the batch: the trainer stream only marks its delivery
@@ -759,6 +781,12 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                      double(ctx.prof_queries - nq0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
                      (ctx.prof_final_ns - f_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
                      double(iters) / double(std::max<size_t>(1, ctx.groups.size() - groups0)));
+    if (trace_on) {
+        static const char* kinds[3] = {"fed", "done", "sealed"};
+        std::fprintf(stderr, "[lfg trace] n=%lld:", static_cast<long long>(n));
+        for (const auto& e : trace) std::fprintf(stderr, " %s%lld@%lld", kinds[e.kind], static_cast<long long>(e.id), static_cast<long long>(e.t_us));
+        std::fprintf(stderr, " end@%lld\n", static_cast<long long>(host_now_us() - run_t0));
+    }
     cudaEvent_t t_end = mk();
     cuda_check(cudaEventRecord(t_end, trainer), "record");
     cuda_check(cudaEventSynchronize(t_end), "sync");
