@@ -81,6 +81,7 @@ struct Stage {
 
 struct Chain {
     std::vector<lfg_op> ops;
+    int64_t est_group_us = 0;   // shard runs: the group-time estimate of the query throttle, kept across runs
     Family fam = FAM_NONE;
     std::vector<Stage> stages;
     int n_spin = 0;

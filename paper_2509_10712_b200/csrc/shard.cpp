@@ -314,8 +314,9 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
         return true;
     };
     const bool profiled = rc.policy == 1 || rc.policy == 2;
-    int64_t est_group_us = 0;   // ~70% of the recent groups' device time, or host-observed time when
-                                // the groups are untimed (query throttle)
+    // ~70% of the recent groups' device time, or host-observed time when the groups are
+    // untimed (query throttle); starts from the chain's previous runs
+    int64_t est_group_us = chain->est_group_us;
     // the group's last event completed: hand on the rest; per-sample device-timed
     // totals (the group's event-timed span less the time from the sample's stamp to
     // the group's last stamp) go to the profiler window, one record per sample as
@@ -781,6 +782,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                      double(ctx.prof_queries - nq0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
                      (ctx.prof_final_ns - f_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
                      double(iters) / double(std::max<size_t>(1, ctx.groups.size() - groups0)));
+    chain->est_group_us = est_group_us;
     if (trace_on) {
         static const char* kinds[3] = {"fed", "done", "sealed"};
         std::fprintf(stderr, "[lfg trace] n=%lld:", static_cast<long long>(n));
