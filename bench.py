@@ -30,6 +30,8 @@ e2e        : same metric with raw inputs in pinned host memory (H2D of each samp
              lfg_shard_next_batch / lfg_batch_release: this process is the trainer)
 dropin     : (rrc) the drop-in C++ path -- the reference's own realtime Minato wiring over our
              headers, process_sample worker threads submitting through the C ABI
+others     : (rrc at N=1) C1 / C1-fg / C3 / C4 each measured by this script in a sub-process
+             after the headline run ("other_workloads"; --no-others skips them)
 roofline   : the dominant kernel timed alone (serial mode) with CUDA events:
              algorithmic bytes per launch / mean launch time, against MEASURED_PEAKS.json
 """
@@ -705,6 +707,10 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
     if heavy and not args.trainer_us:
         trainer_us = calibrated_trainer_us(L, ctx, wl, ids_all, args)
     out["trainer_us"] = {"value": trainer_us}
+    # the dominant kernel alone first (untimed for the value; it also brings the GPU and
+    # the host path up to speed before the timed runs)
+    out["roof"] = dict(kernel_roofline(L, ctx, wl, ids_timed[: min(len(ids_timed), 64 * B if B > 2 else 64)],
+                                       hbm_peak, tf32_peak), peak_source=peak_src)
     with ClockSampler(local) as clk:
         rep, ids, wall, dc, cap = run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local,
                                             trainer_us=trainer_us, policy=1 if heavy else 0,
@@ -723,8 +729,6 @@ def measure(args, rank: int, local: int, world: int, dist) -> dict:
         out["value_timeouts"] = rep_t.timed_samples / (rep_t.elapsed_ms / 1e3) if rep_t.elapsed_ms > 0 else None
         out["timeouts_slow"] = rep_t.slow / max(1, rep_t.samples)
         out["timeouts_t_out_us"] = rep_t.final_t_out_us
-    out["roof"] = dict(kernel_roofline(L, ctx, wl, ids_timed[: min(len(ids_timed), 64 * B if B > 2 else 64)],
-                                       hbm_peak, tf32_peak), peak_source=peak_src)
     out["pool_bytes"] = int(wl.pool_bytes)
     wl.close()
 
@@ -777,6 +781,31 @@ def fake_measure(args, rank: int, local: int, world: int, dist) -> dict:
             "digest": id_digest(ids_timed), "digest_e2e": id_digest(ids_timed), "wall": 0.0}
 
 
+def other_workloads(args) -> dict:
+    """The other SURVEY 8(d) configurations, each measured by this same script in its own
+    process (default steps, oracle check of 8 delivered samples) after the headline run,
+    so the driver's N=1 record carries C1, C1-fg, C3 and C4 next to C2."""
+    out = {}
+    for wl in ("img3d", "img3d_fg", "img3d_heavy", "speech"):
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload", wl, "--no-cpu-baseline",
+                                "--no-dropin", "--no-others", "--seed", str(args.seed)],
+                               capture_output=True, text=True, timeout=240)
+            d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+            roof = d.get("roofline") or {}
+            out[wl] = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+                       "steps": d["steps"], "ms_per_step": d["ms_per_step"], "e2e": d["e2e"]["value"],
+                       "roofline": {k: roof.get(k) for k in ("kernel", "bound", "mean_launch_us", "achieved", "unit", "frac")},
+                       "checked": d.get("checked"), "exactly_once": d.get("exactly_once"),
+                       "clocks": d.get("clocks")}
+            for k in ("consumer_idle_pct", "e2e_consumer_idle_pct", "sync_e2e_consumer_idle_pct", "trainer_us_per_batch"):
+                if d.get(k) is not None:
+                    out[wl][k] = d[k]
+        except Exception as e:   # reported, never fatal for the headline line
+            out[wl] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    return out
+
+
 def dropin_arm():
     """Throughput of the DROP-IN C++ path on the same C2 workload: the reference's own
     realtime Minato wiring (process_sample worker threads, resume, build_batches,
@@ -814,6 +843,7 @@ def main():
     ap.add_argument("--serial", action="store_true", help="(experiment) all launch groups on one stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in C++ path measurement")
+    ap.add_argument("--no-others", action="store_true", help="(rrc, N=1) skip the other workloads' sub-runs")
     ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -885,6 +915,11 @@ def main():
                                        "final_t_out_us": round(r["timeouts_t_out_us"], 1)}
     if dropin is not None:
         line["dropin"] = dropin
+    if args.workload == "rrc" and world == 1 and not fake and not args.no_others:
+        if dist is not None:
+            dist.destroy_process_group()
+            dist = None
+        line["other_workloads"] = other_workloads(args)
     if fake:
         line["fake_shard"] = True
     print(json.dumps(line), flush=True)

@@ -198,7 +198,11 @@ int lfg_host_alloc(lfg_ctx* ctx, size_t bytes, void** out) {
 }
 int lfg_host_free(lfg_ctx* ctx, void* p) {
     return guarded([&] {
-        C(ctx);
+        Context& c = C(ctx);
+        {
+            std::lock_guard<std::mutex> g(c.mu);
+            c.forget_pinned();   // its pages may be reused for pageable memory
+        }
         cuda_check(cudaFreeHost(p), "cudaFreeHost");
     });
 }

@@ -749,7 +749,11 @@ char* Context::slot_ptr(const Ticket& t, int plane) const {
 }
 
 // ------------------------------------------------------------------ raw staging
-int64_t Context::get_raw(int64_t bytes) {
+// Raw staging buffers (pinned-host groups) are pooled.  A new buffer is stream-ordered
+// (cudaMallocAsync on the group's stream: unlike cudaMalloc it never synchronises the
+// device, which would stall every in-flight group) and sized with headroom, so groups a
+// little larger than the pooled buffers do not allocate again.
+int64_t Context::get_raw(int64_t bytes, cudaStream_t st) {
     int64_t best = -1;
     for (size_t k = 0; k < free_raws_.size(); ++k) {
         const int64_t i = free_raws_[k];
@@ -760,8 +764,31 @@ int64_t Context::get_raw(int64_t bytes) {
         return best;
     }
     RawBuf r;
-    r.cap = std::max<int64_t>(bytes, 1 << 20);
-    cuda_check(cudaMalloc(&r.ptr, static_cast<size_t>(r.cap)), "cudaMalloc(raw staging)");
+    constexpr int64_t kRound = int64_t(4) << 20;
+    r.cap = (std::max<int64_t>(bytes + bytes / 4, int64_t(8) << 20) + kRound - 1) / kRound * kRound;
+    static const bool trace = std::getenv("LFG_SHARD_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!raw_pool_primed_) {
+        // Growing the stream-ordered pool maps physical memory (~1 ms per 64 MB): at the
+        // first staged group, grow it once for every launch-group stream and keep it
+        // (release threshold: never), so later groups -- inside a timed run -- carve their
+        // buffers from memory the pool already holds
+        cudaMemPool_t pool;
+        cuda_check(cudaDeviceGetDefaultMemPool(&pool, cfg.device), "default mem pool");
+        uint64_t keep = UINT64_MAX;
+        cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool threshold");
+        void* prime = nullptr;
+        const size_t total = static_cast<size_t>(r.cap) * static_cast<size_t>(std::min(stream_pool, 32));
+        if (cudaMallocAsync(&prime, total, st) == cudaSuccess) cudaFreeAsync(prime, st);
+        else cudaGetLastError();   // (not enough free HBM to hold it all: grow on demand)
+        raw_pool_primed_ = true;
+    }
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&r.ptr), static_cast<size_t>(r.cap), st),
+               "cudaMallocAsync(raw staging)");
+    if (trace)
+        std::fprintf(stderr, "[lfg trace] raw staging +%lld MB (pool %zu) in %.0f us\n",
+                     static_cast<long long>(r.cap >> 20), raws_.size() + 1,
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     raws_.push_back(r);
     return static_cast<int64_t>(raws_.size()) - 1;
 }
@@ -875,11 +902,17 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
         // K0 reads the payload over PCIe through its UVA mapping: it must be pinned
         for (const void* p : {s.data, s.aux}) {
             if (p == nullptr) continue;
+            // a page that held a validated pinned address stays pinned while the caller's
+            // buffer lives (allocations are page-granular): one driver query per page
+            const uintptr_t page = reinterpret_cast<uintptr_t>(p) >> 12;
+            if (pinned_pages_.count(page)) continue;
             cudaPointerAttributes at{};
             if (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeHost) {
                 cudaGetLastError();
                 fail(LFG_ERR_INVALID, "LFG_SRC_HOST_PINNED payload is not pinned host memory");
             }
+            if (pinned_pages_.size() > (size_t(1) << 20)) pinned_pages_.clear();
+            pinned_pages_.insert(page);
         }
     }
     for (int k = 0; k < c->n_spin; ++k)
@@ -1092,7 +1125,7 @@ void Context::launch_group(Group& g) {
     if (staged) {
         int64_t total = 0;
         for (int i = 0; i < n; ++i) total += stage_raw_bytes(c, tickets[g.tickets[i]]);
-        g.raw_idx = get_raw(total);
+        g.raw_idx = get_raw(total, st);
         char* dst = raws_[g.raw_idx].ptr;
         StageLaunch SL{};
         for (int i = 0; i < n; ++i) {

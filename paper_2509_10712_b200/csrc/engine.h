@@ -24,6 +24,7 @@
 #include <random>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/lfgpu.h"
@@ -323,7 +324,8 @@ public:
             return true;
         return poll_group(g);
     }
-    cudaEvent_t make_ready_event() { return get_event(); }   // a batch's pooled ready event
+    cudaEvent_t make_ready_event() { return get_event(); }
+    void forget_pinned() { pinned_pages_.clear(); }   // (a pinned buffer was freed)   // a batch's pooled ready event
     bool poll_group(Group& g);          // updates stages_done/complete; true if complete
     void finalize_group_timing(Group& g);
     int64_t open_group_count() const;
@@ -398,6 +400,8 @@ private:
     void sync_out_tab();
     size_t alloc_cursor_[2] = {0, 0};   // [for_batch] last buffer handed out
     std::vector<RawBuf> raws_;
+    bool raw_pool_primed_ = false;   // the stream-ordered pool was grown for the staging buffers
+    std::unordered_set<uintptr_t> pinned_pages_;   // 4 KB pages of validated pinned payloads
     std::vector<int64_t> free_raws_;
     SmallMap<int> open_buf_;                 // chain -> open slot buffer
     std::vector<int64_t> deferred_;          // full groups awaiting launch (timing mode)
@@ -413,7 +417,7 @@ private:
     bool chain_alive(const Chain* c) const;
     bool buf_reusable(SlotBuf& b);
     void assign_slot(Ticket& t, const Chain* c);
-    int64_t get_raw(int64_t bytes);
+    int64_t get_raw(int64_t bytes, cudaStream_t st);
     void launch_group(Group& g);
     char* slot_ptr(const Ticket& t, int plane) const;
     int64_t stage_raw_bytes(const Chain& c, const Ticket& t) const;
