@@ -10,9 +10,10 @@ within <= 1e-5 relative in fp32 for interpolation, normalization and spectrogram
   * image values: |gpu - oracle| <= 1e-5 * |oracle| + atol, atol 1e-6 (3D, unit
     variance voxels) or 1e-5 (normalised 2D, O(1) values) -- the absolute floor only
     matters where relative error is undefined (values near 0);
-  * speech: see speech_error() -- per-bin relative error 1e-5 in the mel-energy
-    domain for bins within 20 dB of their frame's peak, and below that the fp32
-    round-off floor measured for an fp32 CPU STFT (tests/test_oracle.py).
+  * speech: see speech_error() -- relative error 1e-5 in the mel-energy domain, with
+    an absolute floor of 1e-8 x the frame's peak mel energy for near-empty bands (log
+    amplifies fp32 round-off there): measured, the FFT kernel needs 7.6e-10 and stays
+    within 1.2e-6 relative for every bin within 20 dB of its frame's peak.
 Each function returns the worst err / bound ratio (<= 1 passes) and raises
 AssertionError on an integer mismatch.
 """
@@ -27,7 +28,7 @@ ATOL_2D = 1e-5
 # proportional to the frame's peak mel energy (fp32 round-off of the 320-tap DFT
 # sums is relative to the frame's scale, not to a quiet band's own energy).
 SPEECH_REL = 1e-5
-SPEECH_FLOOR = 1.0e-6     # x frame peak energy
+SPEECH_FLOOR = 1.0e-8     # x frame peak energy (measured need of the default FFT kernel: <= 7.6e-10)
 
 
 def ratio_close(got: np.ndarray, want: np.ndarray, atol: float) -> float:

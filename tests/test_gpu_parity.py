@@ -752,10 +752,12 @@ def test_speech_pinned_host_source_matches_device(lfgpu, oracle):
 
 
 def test_speech_matches_oracle(lfgpu, oracle):
-    """STFT power on tcgen05 (3xTF32) -> mel -> log -> SpecAugment -> splicing.
-    Tolerance (stated): compared in the mel-energy domain, |e^g - e^o| <= 1e-5 e^o +
-    1e-6 * (frame's peak mel energy) -- relative 1e-5 with an energy floor, because
-    log amplifies fp32 round-off in near-empty bands; masked entries exactly 0."""
+    """STFT power (the FFT kernel; LFG_SPEECH_KERNEL=tc: tcgen05 3xTF32) -> mel -> log ->
+    SpecAugment -> splicing.  Tolerance (stated): compared in the mel-energy domain,
+    |e^g - e^o| <= 1e-5 e^o + 1e-8 * (frame's peak mel energy) -- relative 1e-5 with an
+    energy floor for near-empty bands, where log amplifies fp32 round-off (measured need:
+    7.6e-10 for the FFT kernel; the tcgen05 A/B kernel needs up to 1.2e-8 on 170 k-sample
+    utterances and is not held to this bar); masked entries exactly 0."""
     ctx = lfgpu.Context(batch_size=8, n_workers=4, max_group=8, max_slot_buffers=8, seed=SEED)
     ch = ctx.chain(lfgpu.speech_ops(max_len=40000))
     ocfg = oracle.cfgsp()
@@ -790,7 +792,7 @@ def test_speech_matches_oracle(lfgpu, oracle):
         ge, oe = np.exp(got[~zero].astype(np.float64)), np.exp(e[~zero])
         frame_peak = np.exp(e.reshape(e.shape[0], 3, 80).max(axis=2)).repeat(80, axis=1)[~zero]
         err = np.abs(ge - oe)
-        bound = 1e-5 * oe + 1e-6 * frame_peak
+        bound = 1e-5 * oe + 1e-8 * frame_peak
         worst = max(worst, float((err / bound).max()))
         assert (err <= bound).all(), f"max err/bound {(err / bound).max():.3f}"
     print("speech worst err/bound", worst)
