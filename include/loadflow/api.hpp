@@ -571,6 +571,16 @@ void prepare_chain(const TransformChain& chain, int shard);
 // (lfg_seal_batch); fills Batch::device_batch.
 void seal_device_batch(Batch& batch);
 
+// The high-throughput path under the reference's consumer: runs `samples` (device
+// payloads, one bound shard) through the event-driven shard loop (lfg_shard_start: launch
+// groups, timeouts, fast-first eager device seals) and publishes every sealed batch into
+// `out` as it is sealed -- Batch::device_batch set, samples carrying ids and accounting
+// -- so run_consumer (trainer.cpp:20-66) consumes and releases them unchanged.  Closes
+// `out` at the end; blocks while `out` is full (back-pressure).  Run it as an actor
+// (rt.spawn).  cfg.trainer_us is ignored: the consumer is the trainer.
+lfg_run_report feed_shard(const TransformChain& chain, std::vector<Sample> samples, BatchQueue& out, Runtime& rt,
+                          const lfg_run_config& cfg);
+
 }  // namespace gpu
 
 }  // namespace loadflow

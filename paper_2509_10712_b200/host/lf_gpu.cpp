@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <mutex>
 #include <thread>
 
@@ -185,6 +186,63 @@ void seal_device_batch(Batch& b) {
     retry_full([&] { return lfg_seal_batch(ctx, ts.data(), static_cast<int>(ts.size()), &h); });
     for (lfg_ticket t : ts) check(lfg_ticket_release(ctx, t));
     b.device_batch = h;
+}
+
+lfg_run_report feed_shard(const TransformChain& chain, std::vector<Sample> samples, BatchQueue& out, Runtime& rt,
+                          const lfg_run_config& cfg) {
+    if (samples.empty()) {
+        out.close();
+        return lfg_run_report{};
+    }
+    lfg_ctx* ctx = ctx_of(samples.front());
+    lfg_chain* ch = compiled(ctx, chain);
+    std::vector<lfg_sample_desc> descs(samples.size());
+    std::unordered_map<uint64_t, size_t> where;
+    where.reserve(samples.size());
+    for (size_t i = 0; i < samples.size(); ++i) {
+        descs[i] = samples[i].device.desc;
+        descs[i].id = samples[i].id;
+        where.emplace(samples[i].id, i);
+    }
+    lfg_shard* sh = nullptr;
+    check(lfg_shard_start(ctx, ch, descs.data(), static_cast<int64_t>(descs.size()), &cfg, &sh));
+    std::vector<uint64_t> ids(static_cast<size_t>(std::max(1, 256)));
+    int rc = LFG_OK;
+    for (;;) {
+        lfg_batch b = -1;
+        int nb = 0;
+        rc = lfg_shard_next_batch(sh, -1, &b, &nb);
+        if (rc != LFG_OK) break;
+        if (static_cast<size_t>(nb) > ids.size()) ids.resize(static_cast<size_t>(nb));
+        void* p = nullptr;
+        int64_t bytes = 0;
+        int n = 0, inplace = 0;
+        rc = lfg_batch_info(ctx, b, &p, &bytes, &n, ids.data(), &inplace);
+        if (rc != LFG_OK) break;
+        Batch batch;
+        batch.samples.reserve(static_cast<size_t>(n));
+        for (int k = 0; k < n; ++k) {
+            const Sample& src = samples[where.at(ids[static_cast<size_t>(k)])];
+            Sample s;   // the delivered sample's identity and accounting (its payload stays on the device)
+            s.id = src.id;
+            s.chain = src.chain;
+            s.bytes_in = src.bytes_in;
+            s.size_bytes = src.size_bytes;
+            s.bytes_out = src.bytes_out;
+            s.device.shard = src.device.shard;
+            s.device.desc = descs[where.at(src.id)];
+            batch.samples.push_back(std::move(s));
+        }
+        batch.sealed_at = rt.now();
+        batch.device_batch = b;
+        out.put(std::move(batch));   // blocks while the consumer is behind (back-pressure)
+    }
+    out.close();
+    lfg_run_report rep{};
+    const int frc = lfg_shard_finish(sh, &rep, nullptr, nullptr, nullptr);
+    if (rc != LFG_ERR_CLOSED) check(rc);
+    check(frc);
+    return rep;
 }
 
 }  // namespace gpu

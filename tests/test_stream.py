@@ -112,3 +112,22 @@ def test_stream_finish_drains_untaken_batches(lfgpu):
         for p in ptrs:
             ctx.device_free(p)
         ctx.close()
+
+
+def test_cpp_run_consumer_over_shard_feed():
+    """The reference's own run_consumer (trainer.cpp:20-66) consuming the high-throughput
+    path: gpu::feed_shard publishes each sealed device batch into a BatchQueue as it is
+    sealed; exactly-once, batch accounting and one batch tensor against the oracle are
+    checked inside the program (tests/cpp/shard_feed.cpp)."""
+    import subprocess
+    root = ROOT
+    pkg = os.path.join(root, "paper_2509_10712_b200")
+    ora = os.path.join(root, "oracle")
+    src = os.path.join(root, "tests", "cpp", "shard_feed.cpp")
+    exe = os.path.join(root, "tests", "cpp", "shard_feed")
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"), src, "-o", exe,
+                           "-L", pkg, "-lloadflow_b200", "-llfgpu", f"-Wl,-rpath,{pkg}",
+                           "-L", ora, "-llf_oracle", f"-Wl,-rpath,{ora}", "-lpthread"])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
