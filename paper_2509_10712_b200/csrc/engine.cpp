@@ -303,6 +303,8 @@ Context::Context(const lfg_config& c) : cfg(c) {
     cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     cuda_check(cudaStreamCreateWithPriority(&seal_stream, cudaStreamNonBlocking, hi), "seal stream");
     cuda_check(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking), "aux stream");
+    side_streams_.resize(4);
+    for (auto& ss : side_streams_) cuda_check(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking), "side stream");
     // Nothing that can implicitly synchronise the device (stream / event /
     // buffer creation) may run inside the shard loop: a blocked host loop
     // would push in-flight samples past t_out.  Pools are created up front.
@@ -387,6 +389,7 @@ Context::~Context() {
     for (auto s : streams_) cudaStreamDestroy(s);
     cudaStreamDestroy(seal_stream);
     cudaStreamDestroy(aux_stream);
+    for (auto ss : side_streams_) cudaStreamDestroy(ss);
     speech_tables_destroy(speech_);
 }
 
@@ -1335,13 +1338,6 @@ void Context::launch_group(Group& g) {
                     }
                     return X;
                 };
-                if (!plain.empty()) {
-                    auto Lp = subset(plain);
-                    contrast_and_transform(*Lp);
-                    g.part_ev = get_event(g.timed);
-                    cuda_check(cudaEventRecord(g.part_ev, st), "record plain part");
-                    g.part_idx = plain;
-                }
                 auto Lf = subset(fgi);
                 FgLaunch F{};
                 for (size_t j = 0; j < fgi.size(); ++j) {
@@ -1356,13 +1352,32 @@ void Context::launch_group(Group& g) {
                 int32_t* box = fg_box_ + size_t(slot) * kMax3D * 48;
                 int4* offs = fg_offs_ + size_t(slot) * kMax3D;
                 start();
+                // The label scans (K2) fork onto a side stream and run concurrently with
+                // the plain samples' K1 on the group's stream; the group's stream joins
+                // them before the foreground crops.
+                cudaStream_t side = side_streams_[static_cast<size_t>(side_next_++) % side_streams_.size()];
+                cudaEvent_t fork = get_event();
+                cuda_check(cudaEventRecord(fork, st), "record fork");
+                cuda_check(cudaStreamWaitEvent(side, fork, 0), "fork");
+                put_event(fork);   // (the wait captured the record; the event may be reused)
                 // mins ([kMax3D][8][3]) preset large, maxs (the next block) to -1
-                cuda_check(cudaMemsetAsync(box, 0x7f, kMax3D * 24 * sizeof(int32_t), st), "fg box reset");
-                cuda_check(cudaMemsetAsync(box + kMax3D * 24, 0xff, kMax3D * 24 * sizeof(int32_t), st),
+                cuda_check(cudaMemsetAsync(box, 0x7f, kMax3D * 24 * sizeof(int32_t), side), "fg box reset");
+                cuda_check(cudaMemsetAsync(box + kMax3D * 24, 0xff, kMax3D * 24 * sizeof(int32_t), side),
                            "fg box reset");
-                cuda_check(launch_fg_scan(*Lf, F, box, st), "fg scan launch");
-                cuda_check(launch_fg_offsets(*Lf, F, box, offs, st), "fg offsets launch");
+                cuda_check(launch_fg_scan(*Lf, F, box, side), "fg scan launch");
+                cuda_check(launch_fg_offsets(*Lf, F, box, offs, side), "fg offsets launch");
                 counters.launches += 2;
+                cudaEvent_t join = get_event();
+                cuda_check(cudaEventRecord(join, side), "record join");
+                if (!plain.empty()) {   // the plain samples complete at a sub-launch event
+                    auto Lp = subset(plain);
+                    contrast_and_transform(*Lp);
+                    g.part_ev = get_event(g.timed);
+                    cuda_check(cudaEventRecord(g.part_ev, st), "record plain part");
+                    g.part_idx = plain;
+                }
+                cuda_check(cudaStreamWaitEvent(st, join, 0), "join");
+                put_event(join);
                 if (staged) {
                     // K0w: the windows at the resolved origins, from pinned host memory
                     // (image) and the staged label volume (label), into compact windows

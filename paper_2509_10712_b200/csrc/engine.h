@@ -393,6 +393,8 @@ private:
     int4* fg_offs_ = nullptr;              // [kFgSlots][kMax3D]
     int fg_next_ = 0;
     std::vector<cudaStream_t> streams_;
+    std::vector<cudaStream_t> side_streams_;   // forked work of a group (the K2 label scans)
+    int64_t side_next_ = 0;
     std::vector<int> free_streams_;
     std::vector<cudaEvent_t> free_events_, free_tevents_;   // untimed / timed
     std::vector<SlotBuf> bufs_;
