@@ -19,6 +19,20 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kIlp = 4;   // 16-B chunks in flight per lane (all loads issued before the stores)
 
+// The aligned 16-B chunk at `a` (chunk address) of a row spanning [lo, hi): only the
+// bytes inside the range are read (byte loads), the rest of the chunk is zero.  Used
+// for the box's first and last chunk, which may extend past the caller's allocation
+// (aligned chunks never cross a page, but the bytes outside belong to no allocation).
+__device__ __forceinline__ int4 load_chunk_exact(uintptr_t a, uintptr_t lo, uintptr_t hi) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        const uintptr_t x = a + b;
+        if (x >= lo && x < hi) w[b >> 2] |= uint32_t(*reinterpret_cast<const volatile uint8_t*>(x)) << (8 * (b & 3));
+    }
+    return make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+}
+
 // The box's 16-B chunks are one flat index space (row-major, nch_max chunks per
 // row, the padded staging pitch): consecutive lanes take consecutive chunks, so
 // short rows (the 144-B label rows of a crop window) do not idle most of a warp,
@@ -44,7 +58,10 @@ __global__ void __launch_bounds__(32 * kWarps) stage_kernel(const __grid_constan
             const uintptr_t a = s & ~uintptr_t(15);
             const int nch = (int)((((s + d.row_bytes + 15) & ~uintptr_t(15)) - a) >> 4);
             if (c >= nch) continue;
-            v[k] = reinterpret_cast<const int4*>(a)[c];
+            // the box's first and last chunk: only the box's own bytes are read
+            const bool edge = (r == 0 && c == 0) || (r == rows - 1 && c == nch - 1);
+            v[k] = edge ? load_chunk_exact(a + 16 * (uintptr_t)c, s, s + d.row_bytes)
+                        : reinterpret_cast<const int4*>(a)[c];
             dst[k] = reinterpret_cast<int4*>(d.dst + z * d.dst_pz + y * d.dst_py) + c;
         }
 #pragma unroll
@@ -64,22 +81,41 @@ __global__ void __launch_bounds__(32 * kWarps) stage_bulk_kernel(const __grid_co
     __shared__ __align__(8) uint64_t bars[kWarps][kBulkDepth];
     const StageDesc& d = L.d[blockIdx.y];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t rows = (int64_t)d.ny * d.nz;
+    if (blockIdx.x == 0 && warp == 0) {
+        // the box's first and last row by lanes, their end chunks read exactly (a bulk
+        // copy of the aligned superset could read bytes outside the caller's buffer)
+        for (int e = 0; e < (rows > 1 ? 2 : 1); ++e) {
+            const int64_t r = e == 0 ? 0 : rows - 1;
+            const int64_t z = r / d.ny, y = r - z * d.ny;
+            const uintptr_t s = reinterpret_cast<uintptr_t>(d.src) + z * d.src_pz + y * d.src_py;
+            const uintptr_t a = s & ~uintptr_t(15);
+            const int nch = (int)((((s + d.row_bytes + 15) & ~uintptr_t(15)) - a) >> 4);
+            int4* out = reinterpret_cast<int4*>(d.dst + z * d.dst_pz + y * d.dst_py);
+            for (int c = lane; c < nch; c += 32)
+                out[c] = (c == 0 || c == nch - 1) ? load_chunk_exact(a + 16 * (uintptr_t)c, s, s + d.row_bytes)
+                                                  : reinterpret_cast<const int4*>(a)[c];
+        }
+    }
     if (lane != 0) return;
     uint8_t* ring = sbuf + warp * kBulkDepth * kBulkBuf;
     for (int k = 0; k < kBulkDepth; ++k) mbar_init(&bars[warp][k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int64_t rows = (int64_t)d.ny * d.nz;
+    // bulk rows: 1 .. rows - 2 (row index 1 + i)
+    const int64_t nbulk = rows > 2 ? rows - 2 : 0;
     const int64_t first = (int64_t)blockIdx.x * kWarps + warp, step = (int64_t)gridDim.x * kWarps;
-    const int64_t mine = first < rows ? (rows - first + step - 1) / step : 0;
+    const int64_t mine = first < nbulk ? (nbulk - first + step - 1) / step : 0;
     int64_t use[kBulkDepth] = {};
-    auto row_src = [&](int64_t r, uint32_t& nb) {
+    auto row_src = [&](int64_t i, uint32_t& nb) {
+        const int64_t r = 1 + i;
         const int64_t z = r / d.ny, y = r - z * d.ny;
         const uintptr_t s = reinterpret_cast<uintptr_t>(d.src) + z * d.src_pz + y * d.src_py;
         const uintptr_t a = s & ~uintptr_t(15);
         nb = (uint32_t)(((s + d.row_bytes + 15) & ~uintptr_t(15)) - a);
         return a;
     };
-    auto row_dst = [&](int64_t r) {
+    auto row_dst = [&](int64_t i) {
+        const int64_t r = 1 + i;
         const int64_t z = r / d.ny, y = r - z * d.ny;
         return d.dst + z * d.dst_pz + y * d.dst_py;
     };
@@ -148,13 +184,26 @@ __global__ void __launch_bounds__(32 * kWarps) stage_window_kernel(const __grid_
         const int m = (int)((ab & 15) >> 2);                               // warp-uniform
         const float4* c0 = reinterpret_cast<const float4*>(ab & ~uintptr_t(15));
         const int nch = (m + vw + 3) >> 2;                                 // chunks holding window data
+        // the volume's first and last rows: end chunks read exactly (the aligned chunk
+        // may reach outside the caller's buffer); other rows' overreads stay inside it
+        const bool vol_edge = (sz == 0 && sy == 0) || (sz == D - 1 && sy == H - 1);
+        const uintptr_t row_lo = reinterpret_cast<uintptr_t>(d.img_host + ((int64_t)sz * H + sy) * W);
+        const uintptr_t row_hi = row_lo + uintptr_t(4) * W;
+        auto chunk = [&](int c) {
+            const uintptr_t ca = reinterpret_cast<uintptr_t>(c0 + c);
+            if (vol_edge && (ca < row_lo || ca + 16 > row_hi)) {
+                const int4 w = load_chunk_exact(ca, row_lo, row_hi);
+                return make_float4(__int_as_float(w.x), __int_as_float(w.y), __int_as_float(w.z), __int_as_float(w.w));
+            }
+            return c0[c];
+        };
         for (int q0 = 0; q0 < nq; q0 += 32) {
             const int c = q0 + lane;
             const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 v = c < nch ? c0[c] : zero;
+            const float4 v = c < nch ? chunk(c) : zero;
             float4 nx = make_float4(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1),
                                     __shfl_down_sync(0xffffffffu, v.z, 1), __shfl_down_sync(0xffffffffu, v.w, 1));
-            if (lane == 31) nx = (q0 + 32 < nch) ? c0[q0 + 32] : zero;
+            if (lane == 31) nx = (q0 + 32 < nch) ? chunk(q0 + 32) : zero;
             if (c < nq) {
                 float4 x = shift4w(v, nx, m);
                 const int keep = vw - 4 * c;                                // valid floats of this quad
