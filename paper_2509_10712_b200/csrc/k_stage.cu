@@ -24,11 +24,21 @@ constexpr int kIlp = 4;   // 16-B chunks in flight per lane (all loads issued be
 // for the box's first and last chunk, which may extend past the caller's allocation
 // (aligned chunks never cross a page, but the bytes outside belong to no allocation).
 __device__ __forceinline__ int4 load_chunk_exact(uintptr_t a, uintptr_t lo, uintptr_t hi) {
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    // whole 4-B words inside the range by word loads, the rest byte by byte; all loads
+    // independent, so a PCIe round trip is paid once, not per byte
+    uint32_t w[4];
 #pragma unroll
-    for (int b = 0; b < 16; ++b) {
-        const uintptr_t x = a + b;
-        if (x >= lo && x < hi) w[b >> 2] |= uint32_t(*reinterpret_cast<const volatile uint8_t*>(x)) << (8 * (b & 3));
+    for (int q = 0; q < 4; ++q) {
+        const uintptr_t x = a + 4 * q;
+        if (x >= lo && x + 4 <= hi) {
+            w[q] = *reinterpret_cast<const uint32_t*>(x);
+        } else {
+            uint32_t v = 0u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (x + b >= lo && x + b < hi) v |= uint32_t(*reinterpret_cast<const uint8_t*>(x + b)) << (8 * b);
+            w[q] = v;
+        }
     }
     return make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
 }
