@@ -362,7 +362,9 @@ int lfg_shard_start(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* sampl
  * LFG_ERR_CLOSED: end of stream (every sample delivered; QueueClosedError,
  * queue.hpp:29-33); another code: the run failed (lfg_last_error). */
 int lfg_shard_next_batch(lfg_shard* sh, int64_t timeout_us, lfg_batch* out, int* n);
-/* Waits for the run to end, releasing batches the consumer did not take, fills
+/* Waits for the run to end, releasing batches the consumer did not take (release every
+ * batch you took first: batches you hold keep their buffers, and a loop waiting for a
+ * buffer cannot end), fills
  * the report (consumer_busy/span/idle from the caller's time blocked in
  * lfg_shard_next_batch, as ConsumerStats, trainer.hpp:30-47) and the optional
  * arrays as lfg_run_shard does, and frees the handle (also on error). */

@@ -380,6 +380,7 @@ Context::~Context() {
         cudaFree(b.base);
     }
     for (auto& r : raws_) cudaFree(r.ptr);
+    if (raw_pool_ != nullptr) cudaMemPoolDestroy(raw_pool_);
     if (stamp_host_) cudaFreeHost(stamp_host_);
     if (stamp_cnt_) cudaFree(stamp_cnt_);
     if (csum_) cudaFree(csum_);
@@ -771,23 +772,26 @@ int64_t Context::get_raw(int64_t bytes, cudaStream_t st) {
     r.cap = (std::max<int64_t>(bytes + bytes / 4, int64_t(8) << 20) + kRound - 1) / kRound * kRound;
     static const bool trace = std::getenv("LFG_SHARD_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    if (!raw_pool_primed_) {
-        // Growing the stream-ordered pool maps physical memory (~1 ms per 64 MB): at the
-        // first staged group, grow it once for every launch-group stream and keep it
-        // (release threshold: never), so later groups -- inside a timed run -- carve their
-        // buffers from memory the pool already holds
-        cudaMemPool_t pool;
-        cuda_check(cudaDeviceGetDefaultMemPool(&pool, cfg.device), "default mem pool");
+    if (raw_pool_ == nullptr) {
+        // The context's own stream-ordered pool (the device's default pool and its
+        // settings stay untouched).  Growing a pool maps physical memory (~1 ms per
+        // 64 MB): at the first staged group it is grown once for every launch-group
+        // stream and kept (release threshold: never), so later groups -- inside a timed
+        // run -- carve their buffers from memory the pool already holds.
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = cfg.device;
+        cuda_check(cudaMemPoolCreate(&raw_pool_, &props), "raw staging pool");
         uint64_t keep = UINT64_MAX;
-        cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool threshold");
+        cuda_check(cudaMemPoolSetAttribute(raw_pool_, cudaMemPoolAttrReleaseThreshold, &keep), "pool threshold");
         void* prime = nullptr;
         const size_t total = static_cast<size_t>(r.cap) * static_cast<size_t>(std::min(stream_pool, 32));
-        if (cudaMallocAsync(&prime, total, st) == cudaSuccess) cudaFreeAsync(prime, st);
+        if (cudaMallocFromPoolAsync(&prime, total, raw_pool_, st) == cudaSuccess) cudaFreeAsync(prime, st);
         else cudaGetLastError();   // (not enough free HBM to hold it all: grow on demand)
-        raw_pool_primed_ = true;
     }
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&r.ptr), static_cast<size_t>(r.cap), st),
-               "cudaMallocAsync(raw staging)");
+    cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&r.ptr), static_cast<size_t>(r.cap), raw_pool_, st),
+               "cudaMallocFromPoolAsync(raw staging)");
     if (trace)
         std::fprintf(stderr, "[lfg trace] raw staging +%lld MB (pool %zu) in %.0f us\n",
                      static_cast<long long>(r.cap >> 20), raws_.size() + 1,

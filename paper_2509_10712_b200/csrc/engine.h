@@ -402,7 +402,7 @@ private:
     void sync_out_tab();
     size_t alloc_cursor_[2] = {0, 0};   // [for_batch] last buffer handed out
     std::vector<RawBuf> raws_;
-    bool raw_pool_primed_ = false;   // the stream-ordered pool was grown for the staging buffers
+    cudaMemPool_t raw_pool_ = nullptr;   // the context's stream-ordered pool for the staging buffers
     std::unordered_set<uintptr_t> pinned_pages_;   // 4 KB pages of validated pinned payloads
     std::vector<int64_t> free_raws_;
     SmallMap<int> open_buf_;                 // chain -> open slot buffer

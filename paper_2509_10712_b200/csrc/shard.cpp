@@ -783,6 +783,7 @@ int run_shard(Context& ctx, Chain* chain, const lfg_sample_desc* samples, int64_
                      (ctx.prof_final_ns - f_ns0) / double(std::max<size_t>(1, ctx.groups.size() - groups0)),
                      double(iters) / double(std::max<size_t>(1, ctx.groups.size() - groups0)));
     chain->est_group_us = est_group_us;
+    ctx.forget_pinned();   // payload pages are re-validated by the next run (the caller may free them now)
     if (trace_on) {
         static const char* kinds[3] = {"fed", "done", "sealed"};
         std::fprintf(stderr, "[lfg trace] n=%lld:", static_cast<long long>(n));

@@ -526,7 +526,8 @@ class ShardStream:
     """A streaming shard run (lfg_shard_start / lfg_shard_next_batch / lfg_shard_finish):
     ``next_batch()`` returns ``(batch, n)``, ``None`` at the end of the stream; the batch
     is the caller's until ``ctx.batch_release(batch, stream)``.  ``finish()`` returns
-    ``(report, consumed ids, batch sizes, sample classes)`` as ``Context.run_shard``."""
+    ``(report, consumed ids, batch sizes, sample classes)`` as ``Context.run_shard``;
+    release every batch taken before calling it (held batches keep their buffers)."""
 
     def __init__(self, ctx: Context, ch: Chain, descs: Sequence[SampleDesc], rc: RunConfig, capture=None):
         self.ctx = ctx
