@@ -814,7 +814,7 @@ def dropin_arm():
     (`loadflow_b200 dropin`, host/lf_dropin.cpp).  Host clock over the whole run."""
     exe = os.path.join(ROOT, "paper_2509_10712_b200", "loadflow_b200")
     try:
-        r = subprocess.run([exe, "dropin", "--workers", "16", "--coalesce-us", "60", "--samples", "20480",
+        r = subprocess.run([exe, "dropin", "--workers", "32", "--coalesce-us", "150", "--samples", "20480",
                             "--batch", "256", "--group", "64", "--max-seconds", "60"],
                            capture_output=True, text=True, timeout=90)
         d = json.loads(r.stdout.strip().splitlines()[-1])

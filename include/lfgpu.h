@@ -183,6 +183,12 @@ int lfg_flush(lfg_ctx* ctx);
 int lfg_progress(lfg_ctx* ctx, lfg_ticket t, int* ops_done, int* complete, int64_t* elapsed_us);
 /* Blocks until the ticket's chain completes (resume_slow's wait, balancer.cpp:96-113). */
 int lfg_wait(lfg_ctx* ctx, lfg_ticket t);
+/* Waits up to timeout_us for the ticket's sample to finish, without holding the
+ * context lock: *complete = 1 when it did.  A coalescing group still open is launched
+ * once due; with coalesce_us > 0 launched groups wake their waiters by a completion
+ * notice (host function after the group's last stage), so per-sample workers block
+ * instead of polling (ABI 5).  The process_sample budget check: balancer.cpp:55. */
+int lfg_wait_for(lfg_ctx* ctx, lfg_ticket t, int64_t timeout_us, int* complete);
 /* Device-timed per-op costs in microseconds (one per op; ops fused into one
  * stage share the stage's time, attributed to the stage's last op). */
 int lfg_exec_costs(lfg_ctx* ctx, lfg_ticket t, double* costs_us, int cap, int* n_out);

@@ -365,6 +365,48 @@ int lfg_wait(lfg_ctx* ctx, lfg_ticket t) {
     });
 }
 
+int lfg_wait_for(lfg_ctx* ctx, lfg_ticket t, int64_t timeout_us, int* complete) {
+    // Blocks (without the context lock) until the ticket's sample finished or the
+    // timeout passed.  A coalescing group still open is launched once due; launched
+    // groups wake their waiters through the completion notice (coalesce_us > 0),
+    // otherwise the wait polls.
+    return guarded([&] {
+        Context& c = C(ctx);
+        if (!complete) fail(LFG_ERR_INVALID, "null out");
+        *complete = 0;
+        const int64_t deadline = host_now_us() + std::max<int64_t>(0, timeout_us);
+        for (;;) {
+            int64_t serial = 0, due = 0;
+            {
+                std::lock_guard<std::mutex> g(c.mu);
+                Group& gr = c.group_of(t);
+                const int64_t now = host_now_us();
+                if (!gr.launched && !gr.complete && c.cfg.coalesce_us > 0 && now - gr.t_open_us >= c.cfg.coalesce_us)
+                    c.launch_if_pending(t);
+                if (gr.launched && c.group_done_notified(gr.serial)) c.poll_group(gr);
+                if (c.sample_ready(t)) {
+                    *complete = 1;
+                    return;
+                }
+                serial = gr.launched ? gr.serial : 0;
+                due = gr.launched ? 0 : gr.t_open_us + std::max(1, c.cfg.coalesce_us);
+            }
+            const int64_t now = host_now_us();
+            if (now >= deadline) return;
+            int64_t until = deadline;
+            if (serial == 0) until = std::min(until, std::max(due, now + 1));   // wake to launch it when due
+            if (serial > 0 && c.cfg.coalesce_us > 0) {
+                const int w = static_cast<int>(serial & (Context::kDoneWaits - 1));
+                std::unique_lock<std::mutex> lk(c.done_mu_[w]);
+                c.done_cv_[w].wait_for(lk, std::chrono::microseconds(until - now),
+                                       [&] { return c.group_done_notified(serial); });
+            } else {
+                std::this_thread::sleep_for(std::chrono::microseconds(std::min<int64_t>(until - now, 20)));
+            }
+        }
+    });
+}
+
 int lfg_exec_costs(lfg_ctx* ctx, lfg_ticket t, double* costs_us, int cap, int* n_out) {
     return guarded([&] {
         Context& c = C(ctx);

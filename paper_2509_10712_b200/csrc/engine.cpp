@@ -363,6 +363,8 @@ Context::Context(const lfg_config& c) : cfg(c) {
         std::memset(static_cast<void*>(pre_store.data()), 0, kPrefault * sizeof(PreDraw));
         groups.reserve(kPrefault / 8);
     }
+    done_ring_.reset(new std::atomic<int64_t>[kDoneSlots]);
+    for (int i = 0; i < kDoneSlots; ++i) done_ring_[i].store(0, std::memory_order_relaxed);
     // draw workers: half the host threads (the shard loop and the trainer keep theirs), <= 16
     workers = std::make_unique<WorkerThreads>(
         static_cast<int>(std::clamp(std::thread::hardware_concurrency() / 2, 1u, 16u)));
@@ -1513,6 +1515,29 @@ void Context::launch_group(Group& g) {
     }
     g.launched = true;
     g.t_launch_us = host_now_us();
+    g.serial = ++launch_serial_;
+    if (cfg.coalesce_us > 0) {
+        struct DoneMsg {
+            Context* ctx;
+            int64_t serial;
+        };
+        auto* msg = new DoneMsg{this, g.serial};
+        cuda_check(cudaLaunchHostFunc(
+                       st,
+                       [](void* p) {
+                           auto* m = static_cast<DoneMsg*>(p);
+                           Context* cx = m->ctx;
+                           const int w = static_cast<int>(m->serial & (kDoneWaits - 1));
+                           {
+                               std::lock_guard<std::mutex> lk(cx->done_mu_[w]);
+                               cx->done_ring_[m->serial & (kDoneSlots - 1)].store(m->serial, std::memory_order_release);
+                           }
+                           cx->done_cv_[w].notify_all();
+                           delete m;
+                       },
+                       msg),
+                   "group completion notice");
+    }
     prof_group_ns += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t_enter).count();
 }
 
@@ -1573,10 +1598,17 @@ void Context::finalize_group_timing(Group& g) {
 
 void Context::progress(int64_t t, int* ops_done, int* complete, int64_t* elapsed_us) {
     Group& g = group_of(t);
+    const int64_t now = host_now_us();
     // a coalescing group still open launches once its deadline passed
-    if (!g.launched && !g.complete && cfg.coalesce_us > 0 && host_now_us() - g.t_open_us >= cfg.coalesce_us)
+    if (!g.launched && !g.complete && cfg.coalesce_us > 0 && now - g.t_open_us >= cfg.coalesce_us)
         launch_if_pending(t);
-    poll_group(g);
+    // Per-sample pollers (process_sample workers) share launch groups: the group's
+    // events are queried at most once per 2 us however many of its samples' workers
+    // poll (an event query costs ~1.5 us under the context lock)
+    if (!g.complete && now - g.t_query_us >= 2) {
+        g.t_query_us = now;
+        poll_group(g);
+    }
     const bool done = sample_ready(t);   // its own stamp, or the whole group
     const auto& st = g.chain->stages;
     const int od = g.stages_done > 0 ? st[g.stages_done - 1].last_op : 0;

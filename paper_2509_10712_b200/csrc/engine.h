@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <functional>
@@ -180,6 +181,8 @@ struct Group {
     int stages_done = 0;
     int64_t t_launch_us = 0;
     int64_t t_open_us = 0;       // first submit (coalescing deadline, lfg_config.coalesce_us)
+    int64_t t_query_us = 0;      // last event query from lfg_progress (poll throttle)
+    int64_t serial = 0;          // launch serial (> 0 once launched; the completion ring's key)
     int64_t raw_idx = -1;
     int refs = 0;
     bool timed = true;             // stage events carry timing (Context::time_groups at launch)
@@ -325,7 +328,22 @@ public:
         return poll_group(g);
     }
     cudaEvent_t make_ready_event() { return get_event(); }
-    void forget_pinned() { pinned_pages_.clear(); }   // (a pinned buffer was freed)   // a batch's pooled ready event
+    void forget_pinned() { pinned_pages_.clear(); }   // (a pinned buffer was freed)
+    // Completion notices for per-sample waiters (lfg_wait_for; enabled with coalesce_us > 0):
+    // each launched group enqueues a host function after its last stage that records the
+    // group's launch serial in a ring and wakes the waiters, so process_sample workers
+    // block until their group finishes instead of polling events.
+    static constexpr int kDoneSlots = 1 << 16;
+    std::unique_ptr<std::atomic<int64_t>[]> done_ring_;
+    // waiters of a group sleep on one of kDoneWaits condition variables (by launch serial),
+    // so a group's completion wakes its own waiters, not every blocked worker
+    static constexpr int kDoneWaits = 64;
+    std::mutex done_mu_[kDoneWaits];
+    std::condition_variable done_cv_[kDoneWaits];
+    int64_t launch_serial_ = 0;
+    bool group_done_notified(int64_t serial) const {
+        return serial > 0 && done_ring_[serial & (kDoneSlots - 1)].load(std::memory_order_acquire) >= serial;
+    }   // a batch's pooled ready event
     bool poll_group(Group& g);          // updates stages_done/complete; true if complete
     void finalize_group_timing(Group& g);
     int64_t open_group_count() const;

@@ -46,7 +46,7 @@ void ck(int rc, const char* what) {
 
 int cmd_dropin(int argc, char** argv) {
     int workers = 32, batch = 256, group = 64, pool_n = 256;
-    int64_t samples = 20480, coalesce_us = 30, t_out_us = 0, max_seconds = 120;
+    int64_t samples = 20480, coalesce_us = 150, t_out_us = 0, max_seconds = 120;
     uint64_t seed = 1;
     for (int i = 2; i + 1 < argc; i += 2) {
         const std::string k = argv[i];

@@ -20,7 +20,6 @@
 #include <mutex>
 #include <thread>
 
-#include <sys/prctl.h>
 
 #include "loadflow/api.hpp"
 
@@ -61,15 +60,6 @@ void retry_full(F&& call) {
         if (k < 64) std::this_thread::yield();
         else std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
-}
-
-void poll_pause() {
-    thread_local bool slack = [] {
-        prctl(PR_SET_TIMERSLACK, 1000UL, 0, 0, 0);   // 1 us: short sleeps stay short
-        return true;
-    }();
-    (void)slack;
-    std::this_thread::sleep_for(std::chrono::microseconds(4));
 }
 
 lfg_ctx* ctx_of(const Sample& s) {
@@ -285,9 +275,15 @@ RouteResult process_on_device(Sample s, DurationMs t_out, SampleQueue& fast_q, T
         }
         res.foreground_ms = spent;
     } else {
+        const double tick_us = static_cast<double>(rt.tick_ns()) / 1000.0;
         for (;;) {
             int ops_done = 0, complete = 0;
             std::int64_t el_us = 0;
+            // block (no polling) until the sample's group finishes or its budget runs out
+            const DurationMs left = t_out >= kNoTimeout ? kNoTimeout : t_out - (rt.now() - t0);
+            const std::int64_t wait_us =
+                left >= kNoTimeout ? 1000000 : std::max<std::int64_t>(1, static_cast<std::int64_t>(left * tick_us) + 1);
+            check(lfg_wait_for(ctx, s.device.ticket, std::min<std::int64_t>(wait_us, 1000000), &complete));
             check(lfg_progress(ctx, s.device.ticket, &ops_done, &complete, &el_us));
             const DurationMs el = rt.now() - t0;
             if (complete) {
@@ -301,10 +297,6 @@ RouteResult process_on_device(Sample s, DurationMs t_out, SampleQueue& fast_q, T
                 break;
             }
             if (el > t_out) return park(static_cast<std::size_t>(ops_done), el);
-            // every worker thread polls its own sample: sleep between polls (1 us timer
-            // slack) rather than spin, so the pollers do not keep the context lock and
-            // the host cores busy that the submitting workers need
-            poll_pause();
         }
     }
     advance_to(s, n);

@@ -129,6 +129,7 @@ _sig = {
     "lfg_flush": ([_vp], C.c_int),
     "lfg_progress": ([_vp, C.c_int64, _P(C.c_int), _P(C.c_int), _P(C.c_int64)], C.c_int),
     "lfg_wait": ([_vp, C.c_int64], C.c_int),
+    "lfg_wait_for": ([_vp, C.c_int64, C.c_int64, _P(C.c_int)], C.c_int),
     "lfg_exec_costs": ([_vp, C.c_int64, _P(C.c_double), C.c_int, _P(C.c_int)], C.c_int),
     "lfg_ticket_output": ([_vp, C.c_int64, _vp, C.c_size_t], C.c_int),
     "lfg_ticket_release": ([_vp, C.c_int64], C.c_int),
@@ -375,6 +376,12 @@ class Context:
         od, cp, el = C.c_int(), C.c_int(), C.c_int64()
         _check(_lib.lfg_progress(self.h, t, C.byref(od), C.byref(cp), C.byref(el)))
         return od.value, bool(cp.value), el.value
+
+    def wait_for(self, t: int, timeout_us: int) -> bool:
+        """lfg_wait_for: True once the sample finished, False at the timeout."""
+        done = C.c_int(0)
+        _check(_lib.lfg_wait_for(self.h, t, timeout_us, C.byref(done)))
+        return bool(done.value)
 
     def wait(self, t: int):
         _check(_lib.lfg_wait(self.h, t))
