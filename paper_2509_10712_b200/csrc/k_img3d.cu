@@ -89,11 +89,30 @@ img3d_kernel(const __grid_constant__ Img3dLaunch L) {
             const uint32_t* la = reinterpret_cast<const uint32_t*>(lrow - mb) + qs;
             const bool second_i = mi != 0 && 4 * qs + 4 - mi < valid_w;       // next chunk has data
             const bool second_l = mb != 0 && 4 * qs + 4 - mb < valid_w;
-            const float4 a = __ldg(ia);
-            const float4 b = second_i ? __ldg(ia + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-            const uint32_t wa = __ldg(la), wb = second_l ? __ldg(la + 1) : 0u;
-            float4 x = shift4(a, b, mi);
-            uint32_t lb = __funnelshift_r(wa, wb, 8 * mb);
+            float4 x;
+            uint32_t lb;
+            // rows within a chunk of the end of the source (its last row; with tiny rows,
+            // the last few): element loads, as an aligned chunk could reach past the
+            // caller's buffer
+            const int64_t to_end_l = (int64_t)(d.sdim[0] - 1 - sz) * d.lbl_pz + (int64_t)(d.sdim[1] - 1 - sy) * d.lbl_py;
+            const int64_t to_end_i = (int64_t)(d.sdim[0] - 1 - sz) * d.img_pz + (int64_t)(d.sdim[1] - 1 - sy) * d.img_py;
+            if ((to_end_l < 16 || to_end_i < 4) && 4 * qs + 8 > valid_w) {
+                float e[4];
+                lb = 0u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int col = 4 * qs + k;
+                    e[k] = col < valid_w ? __ldg(irow + col) : 0.f;
+                    lb |= (col < valid_w ? uint32_t(__ldg(lrow + col)) : 0u) << (8 * k);
+                }
+                x = make_float4(e[0], e[1], e[2], e[3]);
+            } else {
+                const float4 a = __ldg(ia);
+                const float4 b = second_i ? __ldg(ia + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const uint32_t wa = __ldg(la), wb = second_l ? __ldg(la + 1) : 0u;
+                x = shift4(a, b, mi);
+                lb = __funnelshift_r(wa, wb, 8 * mb);
+            }
             if (4 * qs + 4 > valid_w) {                    // zero-pad past the source edge
                 const int keep = valid_w - 4 * qs;         // 1..3 valid voxels
                 if (keep < 4) x.w = 0.f;

@@ -189,21 +189,36 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
             }
             __syncwarp();
             // stage the touched source rows (aligned 16-byte superset of each row) with
-            // bulk async copies, one per row (a lane per row), all on one mbarrier
+            // bulk async copies, one per row (a lane per row), all on one mbarrier.  The
+            // window's first chunk and last chunk are copied byte by byte instead when they
+            // are partial: the superset there may reach past the caller's buffer.
+            auto span = [&](int r, uintptr_t& sa, uintptr_t& b0, uintptr_t& b1) {
+                sa = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
+                const uintptr_t al = sa & ~uintptr_t(15), ae = (sa + row_bytes + 15) & ~uintptr_t(15);
+                b0 = (r == 0 && (sa & 15) != 0) ? al + 16 : al;
+                b1 = (r == nrows - 1 && ((sa + row_bytes) & 15) != 0) ? ae - 16 : ae;
+                if (b1 < b0) b1 = b0;
+            };
             int bytes = 0;
             for (int r = lane; r < nrows; r += 32) {
-                const uintptr_t sa = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
-                bytes += (int)(((sa + row_bytes + 15) & ~uintptr_t(15)) - (sa & ~uintptr_t(15)));
+                uintptr_t sa, b0, b1;
+                span(r, sa, b0, b1);
+                bytes += (int)(b1 - b0);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
             if (lane == 0) mbar_expect_tx(&stage_bar, (uint32_t)bytes);
             __syncwarp();
             for (int r = lane; r < nrows; r += 32) {
-                const uintptr_t sa = reinterpret_cast<uintptr_t>(row_ptr(d, ylo + r));
+                uintptr_t sa, b0, b1;
+                span(r, sa, b0, b1);
                 const uintptr_t al = sa & ~uintptr_t(15);
-                const uint32_t nb = (uint32_t)(((sa + row_bytes + 15) & ~uintptr_t(15)) - al);
-                bulk_g2s(smem + r * spitch, reinterpret_cast<const void*>(al), nb, &stage_bar);
+                uint8_t* srow = smem + r * spitch;
+                if (b1 > b0) bulk_g2s(srow + (b0 - al), reinterpret_cast<const void*>(b0), (uint32_t)(b1 - b0), &stage_bar);
+                // the exact parts: [sa, b0) and [b1, sa + row_bytes) (visible to the other
+                // warps after the CTA barrier below)
+                for (uintptr_t x = sa; x < b0 && x < sa + row_bytes; ++x) srow[x - al] = *reinterpret_cast<const uint8_t*>(x);
+                for (uintptr_t x = b1 > sa ? b1 : sa; x < sa + row_bytes; ++x) srow[x - al] = *reinterpret_cast<const uint8_t*>(x);
             }
         }
         // the previous output row's taps (row j - 1 is lane j - 1)
