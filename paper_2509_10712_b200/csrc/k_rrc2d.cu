@@ -215,10 +215,18 @@ rrc2d_kernel(const __grid_constant__ RrcLaunch L, int smem_bytes) {
                 const uintptr_t al = sa & ~uintptr_t(15);
                 uint8_t* srow = smem + r * spitch;
                 if (b1 > b0) bulk_g2s(srow + (b0 - al), reinterpret_cast<const void*>(b0), (uint32_t)(b1 - b0), &stage_bar);
-                // the exact parts: [sa, b0) and [b1, sa + row_bytes) (visible to the other
-                // warps after the CTA barrier below)
-                for (uintptr_t x = sa; x < b0 && x < sa + row_bytes; ++x) srow[x - al] = *reinterpret_cast<const uint8_t*>(x);
-                for (uintptr_t x = b1 > sa ? b1 : sa; x < sa + row_bytes; ++x) srow[x - al] = *reinterpret_cast<const uint8_t*>(x);
+            }
+            {
+                // the exact parts, one byte per lane (one round trip): lanes 0-15 the
+                // window's first chunk [sa, b0), lanes 16-31 its last chunk [b1, end)
+                // (visible to the other warps after the CTA barrier below)
+                const int r = lane < 16 ? 0 : nrows - 1;
+                uintptr_t sa, b0, b1;
+                span(r, sa, b0, b1);
+                const uintptr_t al = sa & ~uintptr_t(15), end = sa + row_bytes;
+                const uintptr_t x = lane < 16 ? al + lane : (((end - 1) & ~uintptr_t(15)) + (lane - 16));
+                const bool in = x >= sa && x < end && (lane < 16 ? x < b0 : x >= b1);
+                if (in) smem[r * spitch + (x - al)] = *reinterpret_cast<const uint8_t*>(x);
             }
         }
         // the previous output row's taps (row j - 1 is lane j - 1)
