@@ -60,6 +60,7 @@ METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform H
 # workload -> (batch size, samples per launch group, default timed steps)
 BATCH = {"rrc": (256, 256, 1000), "img3d": (2, 16, 4000), "img3d_fg": (2, 16, 2000),
          "img3d_heavy": (2, 16, 400),
+         "img3d_zoom": (2, 16, 2000),
          "speech": (64, 64, 500)}
 
 
@@ -312,7 +313,7 @@ class Img3dWorkload:
     B = 2
 
     def __init__(self, L, ctx, pool: int, host: bool, seed: int, heavy_frac: float = 0.0,
-                 time_scale_us_per_ms: float = 0.0, p_fg: float = 0.0, depths=None):
+                 time_scale_us_per_ms: float = 0.0, p_fg: float = 0.0, depths=None, zoom=None):
         self.L, self.ctx, self.seed, self.host = L, ctx, seed, host
         self.D, self.cost_ms = img_seg_dims(pool, seed)
         if depths is not None:                    # explicit volume depths (parity tests)
@@ -330,7 +331,8 @@ class Img3dWorkload:
         self.heavy_frac = heavy_frac
         self.scale = time_scale_us_per_ms
         self.p_fg = p_fg
-        self.chain = ctx.chain(L.img_seg_ops(spin_first=heavy_frac > 0, p_fg=p_fg))
+        self.zoom = zoom
+        self.chain = ctx.chain(L.img_seg_ops(spin_first=heavy_frac > 0, p_fg=p_fg, zoom=zoom))
         self.roof_chain = ctx.chain(L.img_seg_ops()) if heavy_frac > 0 else self.chain
 
     def descs(self, ids):
@@ -442,6 +444,8 @@ def make_workload(name, L, ctx, host, seed, args):
         return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed)
     if name == "img3d_fg":   # MLPerf RandBalancedCrop: 40% of crops scan the label volume (K2)
         return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed, p_fg=0.4)
+    if name == "img3d_zoom":    # north_star "trilinear resize": RandomZoom3D on every crop (K4)
+        return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed, zoom=(1.0, 0.8, 1.2))
     if name == "img3d_heavy":   # the real tail (foreground oversampling); optional spin tail on top
         return Img3dWorkload(L, ctx, pool=pool, host=host, seed=seed, p_fg=args.fg,
                              heavy_frac=args.heavy_frac, time_scale_us_per_ms=args.time_scale)
@@ -452,6 +456,7 @@ WORKLOAD_NAMES = {
     "rrc": "C2 ImageNet-shaped u8 3x(256..512)^2 -> RRC224+hflip+normalize",
     "img3d": "C1 KiTS19-shaped 3D crop128^3+flip+brightness+noise+cast",
     "img3d_fg": "C1 shapes, RandomCrop with MLPerf foreground oversampling 0.4 (K2 label scan + K1)",
+    "img3d_zoom": "C1 shapes with RandomZoom3D (p 1, f in [0.8, 1.2]: window round(128 f), trilinear back to 128^3)",
     "img3d_heavy": "C3 heavy-tailed 3D (MLPerf foreground oversampling 0.4 as the tail) + synthetic "
                    "trainer at 90% of loader capacity",
     "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT + log-mel (tcgen05 3xTF32) + SpecAugment + splice, batch 64",
@@ -546,7 +551,10 @@ def oracle_check(wl, ids_timed, cap) -> dict:
         elif wl.name == "speech":
             r = checks.check_speech(O, O.cfgsp(), seed, sid, src[0], raw)
         else:
-            ocfg = O.cfg3d(has_fg=1 if wl.p_fg > 0 else 0, p_fg=wl.p_fg)
+            zk = {}
+            if getattr(wl, "zoom", None) is not None:
+                zk = dict(has_zoom=1, p_zoom=wl.zoom[0], zoom_lo=wl.zoom[1], zoom_hi=wl.zoom[2])
+            ocfg = O.cfg3d(has_fg=1 if wl.p_fg > 0 else 0, p_fg=wl.p_fg, **zk)
             r = checks.check_img3d(O, ocfg, seed, sid, src[0], src[1], raw, (128, 128, 128))
         worst = max(worst, r)
         n += 1
@@ -577,8 +585,11 @@ def kernel_roofline(L, ctx, wl, ids, hbm_peak, tf32_peak):
         wl.name.split("_")[0]]
     if getattr(wl, "p_fg", 0) > 0:
         kernel = "fg_scan_kernel + img3d_tma_kernel (one stage)"
+    if getattr(wl, "zoom", None) is not None:
+        kernel = "img3d_zoom_kernel"
     out = {"kernel": kernel, "launches": int(launches), "mean_launch_us": round(1e3 * t["mean_ms"], 2),
-           "traffic": traffic_of(wl.name), "algo_bytes_per_launch": int(t["bytes"] / max(launches, 1))}
+           "traffic": traffic_of("zoom" if getattr(wl, "zoom", None) is not None else wl.name),
+           "algo_bytes_per_launch": int(t["bytes"] / max(launches, 1))}
     if wl.name == "speech" and os.environ.get("LFG_SPEECH_KERNEL") == "tc":
         # the tcgen05 3xTF32 DFT-GEMM kernel (A/B switch): tensor-bound
         tf = t["flops"] / (ms / 1e3) / 1e12 if ms > 0 else 0.0
@@ -613,7 +624,7 @@ def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: i
     cores = os.cpu_count() or 1
     h = ref_harness()
     wl = {"rrc": "rrc", "speech": "speech"}.get(workload, "img3d")
-    if h and wl != "speech":
+    if h and wl != "speech" and workload != "img3d_zoom":   # (the reference harness has no zoom op)
         k = steps or (8 if wl == "rrc" else 10)
         fg = ["--fg", "0.4"] if workload == "img3d_fg" else []
         out = subprocess.run([h, "--workload", wl, "--steps", str(k), "--warmup", str(warmup),
@@ -635,14 +646,15 @@ def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: i
             O.chain2d(cfg, 1, i, imgs[i % len(imgs)])
         sample = "RandomResizedCrop224+flip+normalize on 3x(256..512)^2 u8 images"
     else:
-        cfg = O.cfg3d()
+        cfg = O.cfg3d(**(dict(has_zoom=1, p_zoom=1.0, zoom_lo=0.8, zoom_hi=1.2) if workload == "img3d_zoom" else {}))
         vols = [(rng.standard_normal((128, 384, 384)).astype(np.float32),
                  rng.integers(0, 3, (128, 384, 384), dtype=np.uint8)) for _ in range(2)]
 
         def one(i):
             v = vols[i % len(vols)]
             O.chain3d(cfg, 1, i, v[0], v[1])
-        sample = "crop128^3+flip+brightness+noise+cast on 128x384x384 volumes"
+        sample = ("crop128^3+" + ("zoom(0.8..1.2, trilinear)+" if workload == "img3d_zoom" else "") +
+                  "flip+brightness+noise+cast on 128x384x384 volumes")
     if wl == "speech":
         cfg = O.cfgsp()
         waves = [(0.3 * rng.standard_normal(int(n))).astype(np.float32)
