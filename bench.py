@@ -796,9 +796,9 @@ def fake_measure(args, rank: int, local: int, world: int, dist) -> dict:
 def other_workloads(args) -> dict:
     """The other SURVEY 8(d) configurations, each measured by this same script in its own
     process (default steps, oracle check of 8 delivered samples) after the headline run,
-    so the driver's N=1 record carries C1, C1-fg, C3 and C4 next to C2."""
+    so the driver's N=1 record carries C1, C1-fg, C3, C4 and C1 with RandomZoom3D next to C2."""
     out = {}
-    for wl in ("img3d", "img3d_fg", "img3d_heavy", "speech"):
+    for wl in ("img3d", "img3d_fg", "img3d_heavy", "speech", "img3d_zoom"):
         try:
             r = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload", wl, "--no-cpu-baseline",
                                 "--no-dropin", "--no-others", "--seed", str(args.seed)],
