@@ -459,7 +459,7 @@ WORKLOAD_NAMES = {
     "img3d_zoom": "C1 shapes with RandomZoom3D (p 1, f in [0.8, 1.2]: window round(128 f), trilinear back to 128^3)",
     "img3d_heavy": "C3 heavy-tailed 3D (MLPerf foreground oversampling 0.4 as the tail) + synthetic "
                    "trainer at 90% of loader capacity",
-    "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT + log-mel (tcgen05 3xTF32) + SpecAugment + splice, batch 64",
+    "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT (warp-per-frame fp32 real FFT) + log-mel + SpecAugment + splice, batch 64",
 }
 
 
