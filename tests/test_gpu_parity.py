@@ -123,6 +123,7 @@ CASES_ZC = [
     ((30, 34, 40), (16, 16, 32), (1.0, 0.7, 1.3), (1.0, 0.5, 1.5), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),
     ((12, 14, 20), (16, 16, 32), (1.0, 0.8, 1.2), (1.0, 0.75, 1.25), dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),  # zero pad
     ((140, 150, 160), (128, 128, 128), (0.5, 0.8, 1.2), (0.5, 0.75, 1.25), dict()),
+    ((14, 12, 260), (8, 8, 200), (1.0, 0.8, 1.2), None, dict(p_flip=0.5, p_bright=1.0, p_noise=1.0)),  # W > 128, ragged
 ]
 
 
