@@ -406,7 +406,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
 //   one shuffle per c fetches Z[256 - k]; X_k = E_k + W512^k O_k (E, O the even / odd
 //   sample spectra), P_k = |X_k|^2 for k = 0..256 (X_256 = E_0 - O_0).
 // Mel: each lane sums its filters' (bin, weight) lists from the warp's power row in
-// shared memory; then log(x + 2^-24), SpecAugment masks and the stack-3 splice layout
+// shared memory (bank-spread, pw_at; the 16 widest filters two lanes apiece); then log(x + 2^-24), SpecAugment masks and the stack-3 splice layout
 // (frame f's 80 values at out + 80 f) as the tensor-core kernel.  Index mapping and
 // pairing are checked against numpy in tests (test_speech_* vs the oracle).
 constexpr int kFftFrames = 96;                                   // per CTA (multiple of 3)
@@ -415,14 +415,21 @@ constexpr int kTrPitch = 36;                                     // transpose ro
 // mel filters as dense taps: filter m = lane + 32 g reads kMelW[g] consecutive bins from
 // mel_b0[m] (the slaney bank's widest filters per lane group: 3, 10, 18 bins)
 constexpr int kMelW0 = 3, kMelW1 = 10, kMelW2 = 18;
-constexpr int kPwPitch = 260;
+// The warp's power row in shared memory, bank-spread: bin k lives at pw_at(k) = k + 40 (k / 64),
+// so the split's stores (lanes (k1, b') write bins k1 + 8 c + 64 bitrev2(b'), 64 apart across
+// b') fall in distinct banks; the 40-word gap after each 64-bin block repeats the next
+// block's first 40 bins, so a filter's taps stay contiguous from pw_at(b0) (mel_b0 holds
+// pw_at(b0); filters are at most 18 bins wide).  The Nyquist bin lives in block 3's gap.
+constexpr int kPwGap = 40;
+constexpr int kPwPitch = 4 * (64 + kPwGap);
+__device__ __host__ __forceinline__ int pw_at(int k) { return k + kPwGap * (k >> 6); }
 
 struct __align__(16) FftTables {
     float win[kTaps];                 // periodic Hann(320)
     float2 tw256[8 * 32];             // [k1][l] W256^(l k1)
-    float2 tw32[4 * 8];               // [b][c] W32^(b c)
-    float2 tw512[kBins];              // W512^k
-    int32_t mel_b0[kMels];            // filter m's first bin
+    float2 tw32[8 * 4];               // [c][b] W32^(b c)
+    float2 tw512[8 * 32];             // [c][lane (k1, b')] W512^k, k = k1 + 8 c + 64 bitrev2(b')
+    int32_t mel_b0[kMels];            // pw_at(filter m's first bin)
     float mel_wd[kMelW2 * kMels];     // [tap][filter] weights (0 past the filter's span)
 };
 
@@ -489,13 +496,13 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
         rtw256[k] = tb->tw256[k * 32 + lane];
-        rtw32[k] = tb->tw32[qb * 8 + k];
+        rtw32[k] = tb->tw32[k * 4 + qb];
     }
 #define TW256(k1) rtw256[k1]
 #define TW32(c) rtw32[c]
 #else
 #define TW256(k1) tb->tw256[(k1) * 32 + lane]
-#define TW32(c) tb->tw32[qb * 8 + (c)]
+#define TW32(c) tb->tw32[(c) * 4 + qb]
 #endif
     const int total = L.tile_start[L.n];
     const int stride = gridDim.x * kFftWarps;
@@ -533,7 +540,7 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
         const int T = d.T;
         float* out = d.out + (int64_t)f * kMels;
         bool tmask = f >= T;                            // splice padding frames are zero
-        for (int q = 0; q < L.n_tmask; ++q) tmask |= f >= d.t_lo[q] && f < d.t_lo[q] + d.t_w[q];
+        for (int q = 0; q < L.n_tmask; ++q) tmask |= (unsigned)(f - d.t_lo[q]) < (unsigned)d.t_w[q];
         if (tmask) {
             for (int m = lane; m < kMels; m += 32) out[m] = 0.0f;
         } else {
@@ -561,14 +568,16 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             dft8(v);
 #pragma unroll
             for (int c = 1; c < 8; ++c) v[c] = cmul(v[c], TW32(c));
-            // stage 3: 4-point DFT across the lane quad (decimation in frequency)
+            // stage 3: 4-point DFT across the lane quad (decimation in frequency); the
+            // butterflies' p -/+ v as fmaf(-/+1, v, p): exact, one FFMA per component
+            const float s2 = (qb & 2) ? -1.0f : 1.0f, s1 = (qb & 1) ? -1.0f : 1.0f;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const float2 p2 = shfl2(v[c], lane ^ 2);
-                v[c] = (qb & 2) ? csub(p2, v[c]) : cadd(v[c], p2);
-                if ((qb & 2) && (qb & 1)) v[c] = mul_mi(v[c]);     // W4^1 on the upper half, j = 1
+                v[c] = make_float2(fmaf(s2, v[c].x, p2.x), fmaf(s2, v[c].y, p2.y));
+                if (qb == 3) v[c] = mul_mi(v[c]);                  // W4^1 on the upper half, j = 1
                 const float2 p1 = shfl2(v[c], lane ^ 1);
-                v[c] = (qb & 1) ? csub(p1, v[c]) : cadd(v[c], p1);
+                v[c] = make_float2(fmaf(s1, v[c].x, p1.x), fmaf(s1, v[c].y, p1.y));
             }
             // lane (k1, b') holds Z[k1 + 8 c + 64 d], d = bitrev2(b').  Real-FFT split:
             // Z[256 - k] lives at lane 4 (8 - k1) + 3 - b', element 7 - c (k1 >= 1), or in
@@ -585,11 +594,13 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
                 const float2 zk = v[c];
                 const float2 e = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
                 const float2 o = make_float2(0.5f * (zk.y + zp.y), -0.5f * (zk.x - zp.x));   // -i/2 (zk - conj zp)
-                const float2 xk = cadd(e, cmul(tb->tw512[k], o));
-                pw[k] = fmaf(xk.x, xk.x, xk.y * xk.y);
+                const float2 xk = cadd(e, cmul(tb->tw512[c * 32 + lane], o));
+                const float p = fmaf(xk.x, xk.x, xk.y * xk.y);
+                pw[pw_at(k)] = p;
+                if (c < kPwGap / 8 && qd != 0) pw[pw_at(k) - kPwGap] = p;   // the previous block's gap
                 if (k == 0) {
                     const float ny = e.x - o.x;              // X_256 = E_0 - O_0 (both real)
-                    pw[kBins] = ny * ny;
+                    pw[pw_at(kBins) - kPwGap] = ny * ny;
                 }
             }
             __syncwarp();
@@ -606,7 +617,17 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             };
             mel_out(std::integral_constant<int, kMelW0>{}, lane);
             mel_out(std::integral_constant<int, kMelW1>{}, lane + 32);
-            if (lane + 64 < kMels) mel_out(std::integral_constant<int, kMelW2>{}, lane + 64);
+            {   // filters 64..79 (the widest): two lanes per filter, 9 taps each
+                const int m = 64 + (lane & 15), h = lane >> 4;
+                const int b0 = tb->mel_b0[m] + (kMelW2 / 2) * h;
+                float acc = 0.0f;
+#pragma unroll
+                for (int q = 0; q < kMelW2 / 2; ++q)
+                    acc = fmaf(tb->mel_wd[((kMelW2 / 2) * h + q) * kMels + m], pw[b0 + q], acc);
+                acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 16);
+                const bool masked = (m >= fl0 && m < fh0) || (m >= fl1 && m < fh1);
+                if (h == 0) out[m] = masked ? 0.0f : logf(acc + 5.9604644775390625e-8f);
+            }
         }
         __syncwarp();   // (tr / pw are reused by the next frame; the frame's stores precede the count)
         if (L.st.cnt != nullptr && lane == 0)
@@ -738,8 +759,12 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     for (int k1 = 0; k1 < 8; ++k1)
         for (int l = 0; l < 32; ++l) ft.tw256[k1 * 32 + l] = tw(l * k1, 256);
     for (int b = 0; b < 4; ++b)
-        for (int c = 0; c < 8; ++c) ft.tw32[b * 8 + c] = tw(b * c, 32);
-    for (int k = 0; k < kBins; ++k) ft.tw512[k] = tw(k, 512);
+        for (int c = 0; c < 8; ++c) ft.tw32[c * 4 + b] = tw(b * c, 32);
+    for (int c = 0; c < 8; ++c)
+        for (int l = 0; l < 32; ++l) {
+            const int b = l & 3, d = ((b & 1) << 1) | ((b >> 1) & 1);
+            ft.tw512[c * 32 + l] = tw((l >> 2) + 8 * c + 64 * d, 512);
+        }
     for (int m = 0; m < kMels; ++m) {
         int lo = -1, hi = -1;
         for (int k = 0; k < nf; ++k)
@@ -750,7 +775,7 @@ cudaError_t speech_tables_create(SpeechTables** out) {
         const int width = m < 32 ? kMelW0 : (m < 64 ? kMelW1 : kMelW2);
         if (lo < 0) lo = hi = 0;
         if (hi - lo + 1 > width || lo + width > nf) return cudaErrorInvalidValue;   // bank wider than the taps
-        ft.mel_b0[m] = lo;
+        ft.mel_b0[m] = pw_at(lo);
         for (int q = 0; q < width; ++q) ft.mel_wd[q * kMels + m] = (float)fb[(size_t)m * nf + lo + q];
     }
     cudaError_t e;
