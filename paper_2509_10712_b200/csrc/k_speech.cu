@@ -428,9 +428,9 @@ struct __align__(16) FftTables {
     float win[kTaps];                 // periodic Hann(320)
     float2 tw256[8 * 32];             // [k1][l] W256^(l k1)
     float2 tw32[8 * 4];               // [c][b] W32^(b c)
-    float2 tw512[8 * 32];             // [c][lane (k1, b')] W512^k, k = k1 + 8 c + 64 bitrev2(b')
+    float2 tw512[8 * 32];             // [c][lane (k1, b')] -i W512^k, k = k1 + 8 c + 64 bitrev2(b')
     int32_t mel_b0[kMels];            // pw_at(filter m's first bin)
-    float mel_wd[kMelW2 * kMels];     // [tap][filter] weights (0 past the filter's span)
+    float mel_wd[kMelW2 * kMels];     // [tap][filter] weights / 4 (0 past the filter's span)
 };
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -540,7 +540,10 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
         const int T = d.T;
         float* out = d.out + (int64_t)f * kMels;
         bool tmask = f >= T;                            // splice padding frames are zero
-        for (int q = 0; q < L.n_tmask; ++q) tmask |= (unsigned)(f - d.t_lo[q]) < (unsigned)d.t_w[q];
+        {   // time masks: lane q tests mask q
+            const int qm = lane < 10 ? lane : 9;
+            tmask |= __any_sync(0xFFFFFFFFu, lane < L.n_tmask && (unsigned)(f - d.t_lo[qm]) < (unsigned)d.t_w[qm]);
+        }
         if (tmask) {
             for (int m = lane; m < kMels; m += 32) out[m] = 0.0f;
         } else {
@@ -592,14 +595,19 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
                 const float2 zp = shfl2(give, src);
                 const int k = qk1 + 8 * c + 64 * qd;
                 const float2 zk = v[c];
-                const float2 e = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
-                const float2 o = make_float2(0.5f * (zk.y + zp.y), -0.5f * (zk.x - zp.x));   // -i/2 (zk - conj zp)
-                const float2 xk = cadd(e, cmul(tb->tw512[c * 32 + lane], o));
-                const float p = fmaf(xk.x, xk.x, xk.y * xk.y);
+                // 2 X_k = A + (-i W512^k) B with A = zk + conj zp (= 2 E_k), B = zk - conj zp
+                // (= 2i O_k): the table holds -i W512^k and the mel weights carry the 1/4 of
+                // |X_k|^2 = |2 X_k|^2 / 4
+                const float2 A = make_float2(zk.x + zp.x, zk.y - zp.y);
+                const float2 Bv = make_float2(zk.x - zp.x, zk.y + zp.y);
+                const float2 t = tb->tw512[c * 32 + lane];
+                const float yx = fmaf(t.x, Bv.x, fmaf(-t.y, Bv.y, A.x));
+                const float yy = fmaf(t.x, Bv.y, fmaf(t.y, Bv.x, A.y));
+                const float p = fmaf(yx, yx, yy * yy);
                 pw[pw_at(k)] = p;
                 if (c < kPwGap / 8 && qd != 0) pw[pw_at(k) - kPwGap] = p;   // the previous block's gap
                 if (k == 0) {
-                    const float ny = e.x - o.x;              // X_256 = E_0 - O_0 (both real)
+                    const float ny = A.x - Bv.y;             // 2 X_256 = 2 E_0 - 2 O_0 (both real)
                     pw[pw_at(kBins) - kPwGap] = ny * ny;
                 }
             }
@@ -763,7 +771,8 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     for (int c = 0; c < 8; ++c)
         for (int l = 0; l < 32; ++l) {
             const int b = l & 3, d = ((b & 1) << 1) | ((b >> 1) & 1);
-            ft.tw512[c * 32 + l] = tw((l >> 2) + 8 * c + 64 * d, 512);
+            const float2 w = tw((l >> 2) + 8 * c + 64 * d, 512);
+            ft.tw512[c * 32 + l] = make_float2(w.y, -w.x);            // -i W512^k
         }
     for (int m = 0; m < kMels; ++m) {
         int lo = -1, hi = -1;
@@ -776,7 +785,7 @@ cudaError_t speech_tables_create(SpeechTables** out) {
         if (lo < 0) lo = hi = 0;
         if (hi - lo + 1 > width || lo + width > nf) return cudaErrorInvalidValue;   // bank wider than the taps
         ft.mel_b0[m] = pw_at(lo);
-        for (int q = 0; q < width; ++q) ft.mel_wd[q * kMels + m] = (float)fb[(size_t)m * nf + lo + q];
+        for (int q = 0; q < width; ++q) ft.mel_wd[q * kMels + m] = (float)fb[(size_t)m * nf + lo + q] * 0.25f;
     }
     cudaError_t e;
     if ((e = cudaMemcpyToSymbol(c_win_nyq, nyq, sizeof(nyq))) != cudaSuccess) return e;
