@@ -476,6 +476,7 @@ __device__ __forceinline__ int bitrev2(int x) { return ((x & 1) << 1) | ((x >> 1
 __global__ void __launch_bounds__(32 * kFftWarps, LFG_FFT_REG_TW ? 2 : 3)
 speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restrict__ g) {
     extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int ts[kMaxSp + 1];                      // the launch's frame prefix sums
     FftTables* tb = reinterpret_cast<FftTables*>(smem);
     float2* tr_all = reinterpret_cast<float2*>(smem + sizeof(FftTables));
     float* pw_all = reinterpret_cast<float*>(tr_all + kFftWarps * 8 * kTrPitch);
@@ -485,6 +486,7 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
         float4* dst = reinterpret_cast<float4*>(tb);
 #pragma unroll 4
         for (int q = tid; q < (int)(sizeof(FftTables) / 16); q += blockDim.x) dst[q] = __ldg(src + q);
+        for (int q = tid; q <= L.n; q += blockDim.x) ts[q] = L.tile_start[q];
     }
     __syncthreads();
     float2* tr = tr_all + warp * 8 * kTrPitch;
@@ -509,9 +511,19 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
     // the raw taps x[(f - 1) * 160 + 2 n .. + 1], n = 32 n1 + lane (n1 < 5), of frame gf,
     // loaded one frame ahead so their latency hides behind the current frame's FFT
     auto load_taps = [&](int gfx, int& ux, float2 xv[5]) {
-        while (gfx >= L.tile_start[ux + 1]) ++ux;      // warp-uniform, monotone
+        // the utterance holding frame gfx: warp-uniform and monotone; the lanes test 32
+        // utterances per step (a warp's next frame is ~stride / 600 utterances further on)
+        for (;;) {
+            const int idx = ux + 1 + lane;
+            const unsigned past = __ballot_sync(0xFFFFFFFFu, idx > L.n ? true : ts[idx] > gfx);
+            if (past != 0u) {
+                ux += __ffs(past) - 1;
+                break;
+            }
+            ux += 32;
+        }
         const SpDesc& dx = L.d[ux];
-        const int f = gfx - L.tile_start[ux];
+        const int f = gfx - ts[ux];
         const int base = (f - 1) * kHop, Lw = dx.L;
         if (f >= dx.T) return;                          // splice padding: no taps
         const bool interior = base >= 0 && base + kTaps <= Lw && ((reinterpret_cast<uintptr_t>(dx.wav) & 7) == 0);
@@ -536,7 +548,7 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
         u = un;
         if (gf + stride < total) load_taps(gf + stride, un, nxt);
         const SpDesc& d = L.d[u];
-        const int f = gf - L.tile_start[u];
+        const int f = gf - ts[u];
         const int T = d.T;
         float* out = d.out + (int64_t)f * kMels;
         bool tmask = f >= T;                            // splice padding frames are zero
@@ -613,15 +625,15 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             }
             __syncwarp();
             // mel filters m = lane, lane + 32, lane + 64, log, frequency masks, store
-            const int fl0 = L.n_fmask > 0 ? d.f_lo[0] : 0, fh0 = L.n_fmask > 0 ? d.f_lo[0] + d.f_w[0] : 0;
-            const int fl1 = L.n_fmask > 1 ? d.f_lo[1] : 0, fh1 = L.n_fmask > 1 ? d.f_lo[1] + d.f_w[1] : 0;
+            const int fl0 = d.f_lo[0], fw0 = L.n_fmask > 0 ? d.f_w[0] : 0;
+            const int fl1 = d.f_lo[1], fw1 = L.n_fmask > 1 ? d.f_w[1] : 0;
             auto mel_out = [&](auto W, int m) {
                 const int b0 = tb->mel_b0[m];
                 float acc = 0.0f;
 #pragma unroll
                 for (int q = 0; q < decltype(W)::value; ++q) acc = fmaf(tb->mel_wd[q * kMels + m], pw[b0 + q], acc);
-                const bool masked = (m >= fl0 && m < fh0) || (m >= fl1 && m < fh1);
-                out[m] = masked ? 0.0f : logf(acc + 5.9604644775390625e-8f);   // + 2^-24
+                const bool masked = (unsigned)(m - fl0) < (unsigned)fw0 || (unsigned)(m - fl1) < (unsigned)fw1;
+                out[m] = masked ? 0.0f : __logf(acc + 5.9604644775390625e-8f);   // + 2^-24
             };
             mel_out(std::integral_constant<int, kMelW0>{}, lane);
             mel_out(std::integral_constant<int, kMelW1>{}, lane + 32);
@@ -633,13 +645,13 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
                 for (int q = 0; q < kMelW2 / 2; ++q)
                     acc = fmaf(tb->mel_wd[((kMelW2 / 2) * h + q) * kMels + m], pw[b0 + q], acc);
                 acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 16);
-                const bool masked = (m >= fl0 && m < fh0) || (m >= fl1 && m < fh1);
-                if (h == 0) out[m] = masked ? 0.0f : logf(acc + 5.9604644775390625e-8f);
+                const bool masked = (unsigned)(m - fl0) < (unsigned)fw0 || (unsigned)(m - fl1) < (unsigned)fw1;
+                if (h == 0) out[m] = masked ? 0.0f : __logf(acc + 5.9604644775390625e-8f);
             }
         }
         __syncwarp();   // (tr / pw are reused by the next frame; the frame's stores precede the count)
         if (L.st.cnt != nullptr && lane == 0)
-            sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, (uint32_t)(L.tile_start[u + 1] - L.tile_start[u]));
+            sample_part_done(L.st.cnt + d.slot, L.st.stamp + d.slot, (uint32_t)(ts[u + 1] - ts[u]));
 #pragma unroll
         for (int n1 = 0; n1 < 5; ++n1) cur[n1] = nxt[n1];
     }
