@@ -702,6 +702,15 @@ int lfg_shard_start(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* sampl
             if (c.streaming) fail(LFG_ERR_STATE, "a streaming shard run is already active on this context");
             c.streaming = true;
         }
+        struct Unclaim {   // until the run's thread owns the flag, a throw hands it back
+            Context* c;
+            ~Unclaim() {
+                if (c) {
+                    std::lock_guard<std::mutex> g(c->mu);
+                    c->streaming = false;
+                }
+            }
+        } unclaim{&c};
         auto sh = std::make_unique<lfg_shard>();
         sh->ctx = ctx;
         sh->samples.assign(samples, samples + n);
@@ -743,6 +752,7 @@ int lfg_shard_start(lfg_ctx* ctx, lfg_chain* chain, const lfg_sample_desc* sampl
             }
             p->cv.notify_all();
         });
+        unclaim.c = nullptr;
         *out = sh.release();
     });
 }
