@@ -61,7 +61,8 @@ METRIC = "samples/sec/GPU delivered to trainer; consumer GPU idle %; transform H
 BATCH = {"rrc": (256, 256, 1000), "img3d": (2, 16, 4000), "img3d_fg": (2, 16, 2000),
          "img3d_heavy": (2, 16, 400),
          "img3d_zoom": (2, 16, 2000),
-         "speech": (64, 64, 500)}
+         "speech": (64, 64, 500),
+         "speech_f32": (64, 64, 500)}
 
 
 def peaks():
@@ -370,26 +371,48 @@ class Img3dWorkload:
 
 
 class SpeechWorkload:
-    """C4: 16 kHz utterances, L ~ U{30000..170000} (the reference's speech bytes_in of
-    60k-340k B as int16, workloads.cpp:115); three sines + N(0, 0.01) noise."""
+    """C4: 16 kHz utterances, L ~ U{30000..170000}; three sines + N(0, 0.01) noise.
+    pcm16 (the default C4 input): int16 PCM -- the reference's speech bytes_in of
+    60k-340k B (2 B per sample, workloads.cpp:115) -- quantised from the f32 synth as
+    round(20000 x) and read by the kernel as s / 32768; else f32 samples."""
     name = "speech"
     B = 64
+    PCM_SCALE = 20000.0
 
-    def __init__(self, L, ctx, pool: int, host: bool, seed: int, lens=None):
-        self.L, self.ctx, self.host = L, ctx, host
+    def __init__(self, L, ctx, pool: int, host: bool, seed: int, lens=None, pcm16: bool = True):
+        self.L, self.ctx, self.host, self.pcm16 = L, ctx, host, pcm16
         rng = np.random.default_rng(seed)
         self.lens = rng.integers(30000, 170001, size=pool)
         if lens is not None:                      # explicit lengths (parity tests)
             self.lens = np.asarray(lens, dtype=int)[:pool]
-        offs = np.concatenate([[0], np.cumsum([(int(n) * 4 + 255) // 256 * 256 for n in self.lens])])
+        self.esize = 2 if pcm16 else 4
+        offs = np.concatenate([[0], np.cumsum([(int(n) * self.esize + 255) // 256 * 256 for n in self.lens])])
         self.offs = offs
         total = int(offs[-1])
         self.base = ctx.host_alloc(total) if host else ctx.device_alloc(total)
-        for i, n in enumerate(self.lens):
-            ctx.synth_waveform(seed, i, int(n), self.base + int(offs[i]), on_device=not host)
+        if pcm16:
+            tmp = ctx.device_alloc(4 * int(max(self.lens)))
+            try:
+                for i, n in enumerate(self.lens):
+                    ctx.synth_waveform(seed, i, int(n), tmp, on_device=True)
+                    x = _read(ctx, tmp, int(n), np.float32, False)
+                    pcm = np.clip(np.rint(x.astype(np.float64) * self.PCM_SCALE), -32768, 32767).astype(np.int16)
+                    self._write(self.base + int(offs[i]), pcm)
+            finally:
+                ctx.device_free(tmp)
+        else:
+            for i, n in enumerate(self.lens):
+                ctx.synth_waveform(seed, i, int(n), self.base + int(offs[i]), on_device=not host)
         self.pool = pool
         self.pool_bytes = total
-        self.chain = ctx.chain(L.speech_ops())
+        self.chain = ctx.chain(L.speech_ops(pcm16=pcm16))
+
+    def _write(self, ptr: int, arr: np.ndarray):
+        if self.host:
+            import ctypes
+            ctypes.memmove(ptr, arr.ctypes.data, arr.nbytes)
+        else:
+            self.ctx.h2d(ptr, arr)
 
     def descs(self, ids):
         L = self.L
@@ -397,14 +420,17 @@ class SpeechWorkload:
                               src_kind=L.SRC_HOST_PINNED if self.host else L.SRC_DEVICE) for i in ids]
 
     def source(self, i):
-        """f32 waveform of sample id i (for the oracle check)."""
+        """f32 waveform of sample id i (for the oracle check; PCM as its exact f32 image s / 32768)."""
         k = i % self.pool
+        if self.pcm16:
+            pcm = _read(self.ctx, self.base + int(self.offs[k]), int(self.lens[k]), np.int16, self.host)
+            return (pcm.astype(np.float32) / np.float32(32768.0),)
         return (_read(self.ctx, self.base + int(self.offs[k]), int(self.lens[k]), np.float32, self.host),)
 
     @staticmethod
-    def pool_bytes_of(pool: int, seed: int) -> int:
+    def pool_bytes_of(pool: int, seed: int, esize: int = 2) -> int:
         lens = np.random.default_rng(seed).integers(30000, 170001, size=pool)
-        return int(sum((int(n) * 4 + 255) // 256 * 256 for n in lens))
+        return int(sum((int(n) * esize + 255) // 256 * 256 for n in lens))
 
     def close(self):
         (self.ctx.host_free if self.host else self.ctx.device_free)(self.base)
@@ -413,7 +439,7 @@ class SpeechWorkload:
 def pool_size(workload: str, host: bool, pool_arg: int = 0) -> int:
     if pool_arg:
         return pool_arg
-    if workload == "speech":
+    if workload.startswith("speech"):
         return 512
     if workload == "rrc":
         return 1024
@@ -436,8 +462,10 @@ def make_context(L, workload: str, device: int = 0, workers: int = 16, group: in
 
 def make_workload(name, L, ctx, host, seed, args):
     pool = pool_size(name, host, args.pool)
-    if name == "speech":
-        return SpeechWorkload(L, ctx, pool=pool, host=host, seed=seed)
+    if name == "speech":        # int16 PCM input, the reference's speech bytes_in
+        return SpeechWorkload(L, ctx, pool=pool, host=host, seed=seed, pcm16=True)
+    if name == "speech_f32":    # the same utterances as f32 samples
+        return SpeechWorkload(L, ctx, pool=pool, host=host, seed=seed, pcm16=False)
     if name == "rrc":
         return RrcWorkload(L, ctx, pool=pool, host=host, seed=seed)
     if name == "img3d":
@@ -459,7 +487,8 @@ WORKLOAD_NAMES = {
     "img3d_zoom": "C1 shapes with RandomZoom3D (p 1, f in [0.8, 1.2]: window round(128 f), trilinear back to 128^3)",
     "img3d_heavy": "C3 heavy-tailed 3D (MLPerf foreground oversampling 0.4 as the tail) + synthetic "
                    "trainer at 90% of loader capacity",
-    "speech": "C4 speech 16 kHz L~U{30k..170k} -> STFT (warp-per-frame fp32 real FFT) + log-mel + SpecAugment + splice, batch 64",
+    "speech": "C4 speech 16 kHz int16 PCM L~U{30k..170k} -> STFT (warp-per-frame fp32 real FFT) + log-mel + SpecAugment + splice, batch 64",
+    "speech_f32": "C4 speech 16 kHz f32 samples L~U{30k..170k} -> STFT (warp-per-frame fp32 real FFT) + log-mel + SpecAugment + splice, batch 64",
 }
 
 
@@ -472,10 +501,11 @@ def workers_of(args) -> int:
 def bench_config(args, world: int) -> dict:
     """The `config` object of the JSON line -- identical for both arms (--impl)."""
     wl = args.workload
-    cls = {"rrc": RrcWorkload, "speech": SpeechWorkload}.get(wl, Img3dWorkload)
+    cls = {"rrc": RrcWorkload, "speech": SpeechWorkload, "speech_f32": SpeechWorkload}.get(wl, Img3dWorkload)
+    extra = {"esize": 4} if wl == "speech_f32" else {}
     return {"workload": WORKLOAD_NAMES[wl], "batch": BATCH[wl][0],
             "launch_group": args.group or BATCH[wl][1], "workers": workers_of(args),
-            "raw_pool_bytes": cls.pool_bytes_of(pool_size(wl, False, args.pool), args.seed),
+            "raw_pool_bytes": cls.pool_bytes_of(pool_size(wl, False, args.pool), args.seed, **extra),
             "l2": "inputs > L2 (pool larger than 126 MB)",
             "parallelism": f"dp{world} independent loader shards",
             **({"trainer": "synthetic step per batch calibrated to 90% of the loader capacity measured "
@@ -623,7 +653,7 @@ def cpu_baseline(workload: str, seconds: float = 12.0, steps: int = 0, warmup: i
     was built, else the oracle port alone on a thread pool.  Bounded sample."""
     cores = os.cpu_count() or 1
     h = ref_harness()
-    wl = {"rrc": "rrc", "speech": "speech"}.get(workload, "img3d")
+    wl = {"rrc": "rrc", "speech": "speech", "speech_f32": "speech"}.get(workload, "img3d")
     if h and wl != "speech" and workload != "img3d_zoom":   # (the reference harness has no zoom op)
         k = steps or (8 if wl == "rrc" else 10)
         fg = ["--fg", "0.4"] if workload == "img3d_fg" else []
@@ -798,7 +828,7 @@ def other_workloads(args) -> dict:
     process (default steps, oracle check of 8 delivered samples) after the headline run,
     so the driver's N=1 record carries C1, C1-fg, C3, C4 and C1 with RandomZoom3D next to C2."""
     out = {}
-    for wl in ("img3d", "img3d_fg", "img3d_heavy", "speech", "img3d_zoom"):
+    for wl in ("img3d", "img3d_fg", "img3d_heavy", "speech", "speech_f32", "img3d_zoom"):
         try:
             r = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload", wl, "--no-cpu-baseline",
                                 "--no-dropin", "--no-others", "--seed", str(args.seed)],

@@ -67,7 +67,8 @@ enum {
     /* speech chain, proj/src/workloads.cpp:103-111 */
     LFG_OP_PAD = 20,
     LFG_OP_SPEC_AUGMENT = 21,     /* param: n_freq, freq_max, n_time, time_frac */
-    LFG_OP_FILTER_BANK = 22,      /* param: n_fft, win, hop, n_mels, sr, f_min, f_max */
+    LFG_OP_FILTER_BANK = 22,      /* param: n_fft, win, hop, n_mels, max_len, input type (LFG_DT_F32 /
+                                     0, or LFG_DT_I16: 16-bit PCM read as s / 32768) */
     LFG_OP_FRAME_SPLICING = 23,   /* param: stack (=subsample)              */
     LFG_OP_PERMUTE_AUDIO = 24,
     /* synthetic cost steps (LightStep/HeavyStep, workloads.cpp:109-110; and the

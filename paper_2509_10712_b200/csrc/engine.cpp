@@ -232,7 +232,7 @@ int64_t Chain::algo_bytes_per_sample(const lfg_sample_desc& s) const {
             return out_bytes;  // write side; the read side is added per sample by the caller
         }
         case FAM_SPEECH:
-            return 4 * s.dims[0] + out_bytes;
+            return wav_bytes * s.dims[0] + out_bytes;
         default:
             return 0;
     }
@@ -544,6 +544,12 @@ Chain* Context::chain_create(const lfg_op* ops, int n) {
                     (p[2] != 0 && p[2] != 160) || (p[3] != 0 && p[3] != 80))
                     fail(LFG_ERR_UNSUPPORTED, "FilterBank kernel is built for n_fft 512, win 320, hop 160, 80 mels");
                 if (p[4] > 0) c->max_L = static_cast<int64_t>(p[4]);
+                // param[5]: the waveform's sample type, LFG_DT_F32 (0 = default) or LFG_DT_I16
+                // (16-bit PCM, the reference's speech bytes_in = 2 B per sample,
+                // workloads.cpp:115; converted on the device as s / 32768, exactly)
+                if (p[5] != 0 && p[5] != LFG_DT_F32 && p[5] != LFG_DT_I16)
+                    fail(LFG_ERR_UNSUPPORTED, "FilterBank input type must be LFG_DT_F32 or LFG_DT_I16");
+                c->wav_bytes = p[5] == LFG_DT_I16 ? 2 : 4;
                 has_anchor = true;
                 break;
             case LFG_OP_FRAME_SPLICING:
@@ -854,7 +860,7 @@ static int boxes_of(const Chain& c, const Ticket& t, Box out[2], int64_t wd[3]) 
                      static_cast<int32_t>(t.p2().w * 3), static_cast<int32_t>(t.p2().h), 1, 0};
         return 1;
     }
-    out[0] = Box{static_cast<const char*>(s.data), 0, 0, static_cast<int32_t>(s.dims[0] * 4), 1, 1, 0};
+    out[0] = Box{static_cast<const char*>(s.data), 0, 0, static_cast<int32_t>(s.dims[0] * c.wav_bytes), 1, 1, 0};
     return 1;
 }
 
@@ -906,6 +912,8 @@ int64_t Context::submit(Chain* c, const lfg_sample_desc& s, const PreDraw* pre) 
         // reflect padding by n_fft/2 needs L > n_fft/2 (torch.stft center=True has the same rule)
         if (s.ndim != 1 || s.dims[0] < c->n_fft / 2 + 1 || s.dims[0] > c->max_L)
             fail(LFG_ERR_INVALID, "speech sample needs a waveform of length in [n_fft/2 + 1, max_L]");
+        if (reinterpret_cast<uintptr_t>(s.data) % static_cast<uintptr_t>(c->wav_bytes) != 0)
+            fail(LFG_ERR_INVALID, "waveform pointer is not aligned to its sample type");
     }
     if (s.src_kind == LFG_SRC_HOST_PINNED) {
         // K0 reads the payload over PCIe through its UVA mapping: it must be pinned
@@ -1483,12 +1491,13 @@ void Context::launch_group(Group& g) {
             L.n_fmask = c.n_fmask;
             L.n_tmask = c.n_tmask;
             L.stack = c.stack;
+            L.pcm16 = c.wav_bytes == 2;
             if (stamp_here) L.st = stamps;
             for (int i = 0; i < n; ++i) {
                 Ticket& t = tickets[g.tickets[i]];
                 SpDesc& d = L.d[i];
                 d.slot = slot_of(i);
-                d.wav = reinterpret_cast<const float*>(views[i].p[0]);
+                d.wav = views[i].p[0];
                 d.out = reinterpret_cast<float*>(slot_ptr(t, 0));
                 d.L = static_cast<int32_t>(t.desc().dims[0]);
                 d.T = t.ps().T;
@@ -1500,7 +1509,7 @@ void Context::launch_group(Group& g) {
                     d.t_lo[k] = t.ps().t_lo[k];
                     d.t_w[k] = t.ps().t_w[k];
                 }
-                counters.kernel_bytes += 4 * t.desc().dims[0] +
+                counters.kernel_bytes += c.wav_bytes * t.desc().dims[0] +
                                          4 * int64_t((t.ps().T + c.stack - 1) / c.stack) * c.stack * c.n_mels;
                 counters.reserved[1] += int64_t(t.ps().T) * 2 * kTapsDft * 512 * 3;   // tensor FLOPs
             }

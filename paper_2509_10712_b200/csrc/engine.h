@@ -104,6 +104,7 @@ struct Chain {
     int n_fmask = 0, fmask_max = 0, n_tmask = 0;
     double tmask_frac = 0;
     int64_t max_L = 170000;
+    int wav_bytes = 4;             // waveform element: 4 = f32, 2 = int16 PCM (full scale 32768)
     // output slot layout (planar)
     bool spin_last = false;        // the last stage ends in a synthetic-cost spin (stamps)
     int nplanes = 1;

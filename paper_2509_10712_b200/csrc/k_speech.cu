@@ -223,7 +223,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
         const bool row_live = r < kFramesPerCta && f < T;
         const int64_t n0 = (int64_t)(f - 1) * kHop;       // first tap's sample index
         const bool interior = row_live && n0 >= 0 && n0 + kTaps <= d.L &&
-                              ((reinterpret_cast<uintptr_t>(d.wav + n0) & 15) == 0);
+                              ((reinterpret_cast<uintptr_t>(static_cast<const float*>(d.wav) + n0) & 15) == 0);
         float nyq = 0.0f;
         // All 8 warps build A: warps 2-5 taps 0-3 of every K step (16-B chunk 0 of
         // the row), warps 6-9 taps 4-7 (chunk 1), each into its own half of the
@@ -231,7 +231,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
         const int half = warp >= 6 ? 1 : 0;
         auto load = [&](int it, float x[4]) {
             if (interior) {
-                const float4 a = __ldg(reinterpret_cast<const float4*>(d.wav + n0 + it * kKChunk + 4 * half));
+                const float4 a = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(d.wav) + n0 + it * kKChunk + 4 * half));
                 x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
             } else {
 #pragma unroll
@@ -241,7 +241,7 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
                         int64_t n = n0 + it * kKChunk + 4 * half + j;     // reflect padding
                         if (n < 0) n = -n;
                         if (n >= d.L) n = 2 * ((int64_t)d.L - 1) - n;
-                        v = __ldg(d.wav + n);
+                        v = __ldg(static_cast<const float*>(d.wav) + n);
                     }
                     x[j] = v;
                 }
@@ -463,6 +463,16 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
     return make_float2(__shfl_sync(0xFFFFFFFFu, v.x, src), __shfl_sync(0xFFFFFFFFu, v.y, src));
 }
 __device__ __forceinline__ int bitrev2(int x) { return ((x & 1) << 1) | ((x >> 1) & 1); }
+// two int16 PCM samples (low half first) -> (s0, s1) / 32768, exactly: flipping each sign
+// bit maps s to s + 32768 in [0, 65535]; PRMT places it under 0x4B00'0000 (the float
+// 2^23 + s + 32768); one paired FFMA removes the offset and scales by 2^-15
+__device__ __forceinline__ float2 pcm_pair(uint32_t w) {
+    w ^= 0x80008000u;
+    const float2 m = make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7410u)),
+                                 __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7432u)));
+    constexpr float k = 1.0f / 32768.0f, off = -(8388608.0f + 32768.0f) / 32768.0f;
+    return __ffma2_rn(m, make_float2(k, k), make_float2(off, off));
+}
 
 // Frames are dealt to warps round-robin over the launch's flattened frame space
 // (L.tile_start holds per-utterance frame prefix sums for this kernel), so every SM
@@ -526,17 +536,26 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
         const int f = gfx - ts[ux];
         const int base = (f - 1) * kHop, Lw = dx.L;
         if (f >= dx.T) return;                          // splice padding: no taps
-        const bool interior = base >= 0 && base + kTaps <= Lw && ((reinterpret_cast<uintptr_t>(dx.wav) & 7) == 0);
+        // taps come in pairs (2 n, 2 n + 1): one 8-B load of f32, or one 4-B load of int16
+        // PCM kept as the raw word in .x until the frame's stage 1 (pcm_pair) -- converting
+        // here would wait on the load one frame early; reflect padding at the utterance ends
+        const int esh = L.pcm16 ? 1 : 2;                  // log2 bytes per sample
+        const bool interior = base >= 0 && base + kTaps <= Lw &&
+                              ((reinterpret_cast<uintptr_t>(dx.wav) & ((2u << esh) - 1)) == 0);
+        const float* wf = static_cast<const float*>(dx.wav);
+        const unsigned short* ws = static_cast<const unsigned short*>(dx.wav);
 #pragma unroll
         for (int n1 = 0; n1 < 5; ++n1) {
             const int j = 2 * (32 * n1 + lane);
             if (interior) {
-                xv[n1] = __ldg(reinterpret_cast<const float2*>(dx.wav + base + j));
+                xv[n1] = L.pcm16 ? make_float2(__uint_as_float(__ldg(reinterpret_cast<const unsigned int*>(ws + base + j))), 0.f)
+                                 : __ldg(reinterpret_cast<const float2*>(wf + base + j));
             } else {
                 int i0 = base + j, i1 = base + j + 1;
                 i0 = i0 < 0 ? -i0 : (i0 >= Lw ? 2 * (Lw - 1) - i0 : i0);
                 i1 = i1 < 0 ? -i1 : (i1 >= Lw ? 2 * (Lw - 1) - i1 : i1);
-                xv[n1] = make_float2(__ldg(dx.wav + i0), __ldg(dx.wav + i1));
+                xv[n1] = L.pcm16 ? make_float2(__uint_as_float((uint32_t)__ldg(ws + i0) | ((uint32_t)__ldg(ws + i1) << 16)), 0.f)
+                                 : make_float2(__ldg(wf + i0), __ldg(wf + i1));
             }
         }
     };
@@ -566,7 +585,8 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
                 if (n1 < 5) {
                     const int j = 2 * (32 * n1 + lane);
                     const float2 ww = *reinterpret_cast<const float2*>(tb->win + j);
-                    v[n1] = make_float2(cur[n1].x * ww.x, cur[n1].y * ww.y);
+                    const float2 x = L.pcm16 ? pcm_pair(__float_as_uint(cur[n1].x)) : cur[n1];
+                    v[n1] = make_float2(x.x * ww.x, x.y * ww.y);
                 } else {
                     v[n1] = make_float2(0.f, 0.f);
                 }
@@ -842,6 +862,7 @@ cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, cudaStream_
     L.debug = dbg;
     L.tile_start[0] = 0;
     if (speech_use_tc()) {   // CTA tiles of kFramesPerCta frames
+        if (L.pcm16) return cudaErrorNotSupported;   // (the A/B tensor-core kernel reads f32 only)
         for (int i = 0; i < L.n; ++i)
             L.tile_start[i + 1] = L.tile_start[i] + (L.d[i].T + kFramesPerCta - 1) / kFramesPerCta;
         speech_kernel<<<L.tile_start[L.n], kThreads, kSmemBytes, s>>>(L, t->basis);

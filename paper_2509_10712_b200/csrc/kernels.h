@@ -200,7 +200,7 @@ struct RrcLaunch {
 
 // ---- K8-K11 (speech): STFT power -> mel -> log -> SpecAugment -> FrameSplicing
 struct SpDesc {
-    const float* wav;
+    const void* wav;         // f32 samples, or int16 PCM (SpLaunch.pcm16)
     float* out;              // spliced log-mel [T', stack*n_mels]  (time-major)
     int32_t L;
     int32_t T;               // frames
@@ -214,6 +214,7 @@ struct SpLaunch {
     int32_t n_fmask, n_tmask;
     int32_t stack;
     int32_t debug;            // profiling switch: 1 builders skip loads, 2 skip MMAs
+    int32_t pcm16;            // waveforms are int16 PCM (x = s / 32768), else f32
     StampRef st;
     int32_t tile_start[kMaxSp + 1];   // CTA prefix sums (flattened grid), filled by the launcher
     SpDesc d[kMaxSp];

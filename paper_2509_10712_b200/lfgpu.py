@@ -240,13 +240,15 @@ def obj_det_ops(out=(224, 224), scale=(0.08, 1.0), ratio=(3 / 4, 4 / 3), p_hflip
 
 
 def speech_ops(max_len=170_000, freq_masks=2, freq_mask_max=27, time_masks=10,
-               time_mask_frac=0.05, stack=3) -> list[Op]:
+               time_mask_frac=0.05, stack=3, pcm16=False) -> list[Op]:
     """speech chain, proj/src/workloads.cpp:103-108: Pad, SpecAugment, FilterBank
-    (STFT 512/320/160 -> 80 slaney mels -> log), FrameSplicing, PermuteAudio."""
+    (STFT 512/320/160 -> 80 slaney mels -> log), FrameSplicing, PermuteAudio.
+    pcm16: the waveforms are int16 PCM (the reference's speech bytes_in, 2 B per
+    sample, workloads.cpp:115), read as s / 32768; else f32."""
     ops = [
         op(OP_PAD, "Pad", 1.12),
         op(OP_SPEC_AUGMENT, "SpecAugment", 1.0, [freq_masks, freq_mask_max, time_masks, time_mask_frac]),
-        op(OP_FILTER_BANK, "FilterBank", 1.0, [512, 320, 160, 80, max_len]),
+        op(OP_FILTER_BANK, "FilterBank", 1.0, [512, 320, 160, 80, max_len, DT_I16 if pcm16 else DT_F32]),
     ]
     if stack > 1:
         ops.append(op(OP_FRAME_SPLICING, "FrameSplicing", 0.9, [stack]))

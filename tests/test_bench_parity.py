@@ -7,7 +7,8 @@ oracle (oracle/checks.py bars: labels / windows / masks / padding bit-exact, val
 within 1e-5 relative).
 
   C2  rrc     batch 256, launch groups of 256, 1,024-image 256..512 px pool, 640 ids
-  C4  speech  batch 64, groups of 64, max_len 170,000, L in {30k, 100k, 170k} + random
+  C4  speech  batch 64, groups of 64, max_len 170,000, L in {30k, 100k, 170k} + random;
+              int16 PCM (the bench default) and f32 samples
   C1  img3d   batch 2, groups of 16, D x 384 x 384 volumes with D in {128, 300, 512};
               also with RandomCrop's foreground oversampling (K2) on
 Both input sources: HBM-resident (bench "value") and pinned host (bench "e2e").
@@ -74,20 +75,22 @@ def test_c2_rrc_bench_config(lfgpu, oracle, host):
         ctx.close()
 
 
+@pytest.mark.parametrize("pcm16", [True, False], ids=["pcm16", "f32"])
 @pytest.mark.parametrize("host", [False, True], ids=["hbm", "pinned"])
-def test_c4_speech_bench_config(lfgpu, oracle, host):
+def test_c4_speech_bench_config(lfgpu, oracle, host, pcm16):
     ctx, B, group = bench.make_context(lfgpu, "speech", seed=SEED)
     assert (B, group) == (64, 64)
     lens = np.random.default_rng(5).integers(30000, 170001, size=64)
     lens[:6] = [30000, 100000, 170000, 170000, 30001, 99999]
-    wl = bench.SpeechWorkload(lfgpu, ctx, pool=64, host=host, seed=SEED, lens=lens)
+    wl = bench.SpeechWorkload(lfgpu, ctx, pool=64, host=host, seed=SEED, lens=lens, pcm16=pcm16)
     ocfg = oracle.cfgsp()
     try:
         ids = list(range(0, 160))                    # 2.5 batches of 64
         rep, worst = _run_and_check(
             lfgpu, oracle, ctx, wl, ids,
             lambda sid, raw: checks.check_speech(oracle, ocfg, SEED, sid, wl.source(sid)[0], raw))
-        print(f"C4 {'pinned' if host else 'hbm'}: 160 utterances, worst err/bound {worst:.3f}")
+        print(f"C4 {'pinned' if host else 'hbm'} {'pcm16' if pcm16 else 'f32'}: 160 utterances, "
+              f"worst err/bound {worst:.3f}")
     finally:
         wl.close()
         ctx.close()

@@ -752,6 +752,65 @@ def test_speech_pinned_host_source_matches_device(lfgpu, oracle):
     ctx.close()
 
 
+def test_speech_pcm16_equals_its_f32_image(lfgpu, oracle):
+    """int16 PCM input (FilterBank param 5 = LFG_DT_I16; the reference's speech bytes_in
+    are 2 B per sample, workloads.cpp:115): the kernel reads s / 32768, which is exact in
+    fp32, so every output equals the f32 path's on the waveform s / 32768 bit for bit --
+    HBM-resident and pinned, 4-B-aligned (paired loads) and 2-B-aligned (scalar loads)
+    waveforms, reflect-padded ends, full-scale samples; plus the oracle bar on the PCM run."""
+    ctx = lfgpu.Context(batch_size=8, n_workers=4, max_group=8, max_slot_buffers=8, seed=SEED)
+    ch16 = ctx.chain(lfgpu.speech_ops(max_len=40000, pcm16=True))
+    ch32 = ctx.chain(lfgpu.speech_ops(max_len=40000))
+    ocfg = oracle.cfgsp()
+    rng = np.random.default_rng(23)
+    lens = [4000, 4321, 20000, 39999, 257, 300, 16000, 12345]
+    keep, runs = [], []
+    for k, L in enumerate(lens):
+        t = np.arange(L) / 16000.0
+        x = 0.6 * np.sin(2 * np.pi * (150 + 70 * k) * t) + 0.05 * rng.standard_normal(L)
+        pcm = np.clip(np.rint(x * 32768), -32768, 32767).astype(np.int16)
+        pcm[:3] = [32767, -32768, 0]                     # full scale inside the reflected edge
+        f32 = pcm.astype(np.float32) / np.float32(32768.0)
+        assert np.array_equal((f32 * 32768).astype(np.int16), pcm)
+        mis = k % 2                                      # odd samples start 2 B past a 4-B boundary
+        raw16 = np.zeros(L + 1, dtype=np.int16)
+        raw16[mis:mis + L] = pcm
+        pd, ph, p32 = _upload(ctx, raw16), _pinned(ctx, raw16), _upload(ctx, f32)
+        keep += [("d", pd), ("h", ph), ("d", p32)]
+        sid = 700 + k
+        a = ctx.submit(ch16, lfgpu.sample_desc(sid, (L,), pd + 2 * mis))
+        b = ctx.submit(ch16, lfgpu.sample_desc(sid, (L,), ph + 2 * mis, src_kind=lfgpu.SRC_HOST_PINNED))
+        c = ctx.submit(ch32, lfgpu.sample_desc(sid, (L,), p32))
+        runs.append((L, sid, f32, a, b, c))
+    ctx.flush()
+    _, out_bytes, _ = ch16.info()
+    assert ch32.info()[1] == out_bytes
+    for L, sid, f32, a, b, c in runs:
+        rows = -(-(1 + L // 160) // 3)
+        outs = []
+        for tk in (a, b, c):
+            ctx.wait(tk)
+            outs.append(ctx.ticket_output(tk, out_bytes).view(np.float32)[: rows * 240].copy())
+            ctx.release(tk)
+        for got in outs[:2]:
+            bad = np.flatnonzero(got != outs[2])
+            assert bad.size == 0, f"L={L}: {bad.size} outputs differ from the f32 path; first {bad[:5]}"
+        (lm, _), _ = oracle.chainsp(ocfg, SEED, sid, f32)
+        e = _splice(lm)
+        got = outs[0].reshape(-1, 240)[: e.shape[0]]
+        zero = e == 0.0
+        assert np.array_equal(got[zero], e[zero])
+        ge, oe = np.exp(got[~zero].astype(np.float64)), np.exp(e[~zero])
+        frame_peak = np.exp(e.reshape(e.shape[0], 3, 80).max(axis=2)).repeat(80, axis=1)[~zero]
+        assert (np.abs(ge - oe) <= 1e-5 * oe + 1e-8 * frame_peak).all()
+    # a PCM waveform must be 2-B aligned
+    with pytest.raises(lfgpu.LfgError):
+        ctx.submit(ch16, lfgpu.sample_desc(799, (4000,), keep[0][1] + 1))
+    for kind, p in keep:
+        (ctx.device_free if kind == "d" else ctx.host_free)(p)
+    ctx.close()
+
+
 def test_speech_matches_oracle(lfgpu, oracle):
     """STFT power (the FFT kernel; LFG_SPEECH_KERNEL=tc: tcgen05 3xTF32) -> mel -> log ->
     SpecAugment -> splicing.  Tolerance (stated): compared in the mel-energy domain,

@@ -45,7 +45,7 @@ if __name__ == "__main__":
         print(json.dumps(one(sys.argv[2], int(sys.argv[3]))))
         sys.exit(0)
     wl = sys.argv[1]
-    group = int(os.environ.get("GROUP", "0")) or {"img3d": 16, "img3d_fg": 16, "img3d_zoom": 16, "rrc": 256, "speech": 64}[wl]
+    group = int(os.environ.get("GROUP", "0")) or {"img3d": 16, "img3d_fg": 16, "img3d_zoom": 16, "rrc": 256, "speech": 64, "speech_f32": 64}[wl]
     for var in sys.argv[2:] or [""]:
         env = dict(os.environ)
         for kv in var.split():
