@@ -32,6 +32,7 @@
 // bank is 2.4% dense, so it stays on the CUDA cores instead of a mostly-zero
 // GEMM) -> shared memory -> log(x + eps), SpecAugment masks, stack-3 splice,
 // coalesced time-major stores into the sample's output slot.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -411,6 +412,10 @@ speech_kernel(const __grid_constant__ SpLaunch L, const char* __restrict__ basis
 // pairing are checked against numpy in tests (test_speech_* vs the oracle).
 constexpr int kFftFrames = 96;                                   // per CTA (multiple of 3)
 constexpr int kFftWarps = 8;
+#ifndef LFG_FFT_DYN_ROUNDS
+#define LFG_FFT_DYN_ROUNDS 4   // (build-time A/B) frame-deal rounds left to the dynamic tail (1..8 measured)
+#endif
+constexpr int kFftDynRounds = LFG_FFT_DYN_ROUNDS;
 constexpr int kTrPitch = 36;                                     // transpose row pitch (float2)
 // mel filters as dense taps: filter m = lane + 32 g reads kMelW[g] consecutive bins from
 // mel_b0[m] (the slaney bank's widest filters per lane group: 3, 10, 18 bins)
@@ -559,13 +564,33 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             }
         }
     };
+    // Frame deal: round-robin for all but the last rounds (warp w of CTA b takes frames
+    // b * 8 + w + k * stride: neighbouring frames, which share half their taps, sit on
+    // neighbouring warps of one CTA), then -- with L.work -- the tail from the launch's
+    // counter, so no SM idles while others finish (masked and padding frames are cheap, so
+    // equal frame counts are not equal work: ncu showed sm__cycles_active min 57 k / avg
+    // 69 k / max 82 k of 86 k with the pure round-robin deal).  Lane 0's atomic runs one
+    // take ahead.  A warp's frames increase (load_taps' utterance search relies on it).
+    const bool dyn = L.work != nullptr;
+    const int n_rr = dyn ? max(0, total / stride - kFftDynRounds) : (total + stride - 1) / stride;
+    const int rr_end = n_rr * stride;
+    uint32_t pend = 0;
+    int k_rr = 0;
+    auto take = [&]() -> int {
+        if (k_rr < n_rr) return blockIdx.x * kFftWarps + warp + (k_rr++) * stride;
+        if (!dyn) return total;
+        const int g = rr_end + __shfl_sync(0xFFFFFFFFu, (int)pend, 0);
+        if (lane == 0) pend = atomicAdd(L.work, 1u);
+        return g;
+    };
+    if (dyn && lane == 0) pend = atomicAdd(L.work, 1u);
     int u = 0, un = 0;
     float2 cur[5], nxt[5];
-    const int gf0 = blockIdx.x * kFftWarps + warp;
-    if (gf0 < total) load_taps(gf0, un, cur);
-    for (int gf = gf0; gf < total; gf += stride) {
+    int gf = take(), gn = take();
+    if (gf < total) load_taps(gf, un, cur);
+    for (; gf < total; gf = gn, gn = take()) {
         u = un;
-        if (gf + stride < total) load_taps(gf + stride, un, nxt);
+        if (gn < total) load_taps(gn, un, nxt);
         const SpDesc& d = L.d[u];
         const int f = gf - ts[u];
         const int T = d.T;
@@ -675,6 +700,20 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
 #pragma unroll
         for (int n1 = 0; n1 < 5; ++n1) cur[n1] = nxt[n1];
     }
+    if (dyn) {
+        // Hand the counter back zeroed: every warp's last grab must have landed (reading
+        // pend waits for the atomic's return), then each CTA counts itself out and the
+        // last one zeroes both words for the next launch on this pair.
+        if (lane == 0 && pend == 0xFFFFFFFFu) __trap();   // (never: a counter value; waits on pend)
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            if (atomicAdd(L.work + 1, 1u) == gridDim.x - 1) {
+                L.work[0] = 0u;
+                L.work[1] = 0u;
+            }
+        }
+    }
 }
 constexpr int kFftSmem = (int)sizeof(FftTables) + kFftWarps * 8 * kTrPitch * 8 + kFftWarps * kPwPitch * 4;
 
@@ -710,9 +749,16 @@ float as_f(uint32_t u) {
 
 }  // namespace
 
+// FFT-kernel tail counters: one {next frame, CTAs done} pair per launch, taken
+// round-robin; the last CTA of a launch zeroes its pair, so a pair is free again once
+// that launch has finished -- far fewer than kWorkSlots launches are in flight at once.
+constexpr int kWorkSlots = 4096;
+
 struct SpeechTables {
     char* basis = nullptr;   // kChunks x 64 KB, the per-stage smem image of B (tensor-core kernel)
     FftTables* fft = nullptr;   // window, twiddles and mel (bin, weight) lists (FFT kernel)
+    uint32_t* work = nullptr;   // kWorkSlots x {next frame, CTAs done}
+    mutable std::atomic<uint32_t> seq{0};   // next pair (launches take pairs through a const table)
 };
 
 namespace {
@@ -842,6 +888,8 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     if ((e = cudaFuncSetAttribute(speech_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kFftSmem)) != cudaSuccess)
         return e;
+    if ((e = cudaMalloc(&t->work, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess) return e;
+    if ((e = cudaMemset(t->work, 0, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess) return e;
     *out = t;
     return cudaSuccess;
 }
@@ -850,6 +898,7 @@ void speech_tables_destroy(SpeechTables* t) {
     if (!t) return;
     cudaFree(t->basis);
     cudaFree(t->fft);
+    cudaFree(t->work);
     delete t;
 }
 
@@ -879,6 +928,9 @@ cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, cudaStream_
     }();
     const int need = (L.tile_start[L.n] + kFftWarps - 1) / kFftWarps;
     const int grid = need < 3 * sms ? need : 3 * sms;
+    // LFG_SPEECH_DEAL=static: round-robin deal of every frame (A/B switch)
+    static const bool stat = getenv("LFG_SPEECH_DEAL") && std::strcmp(getenv("LFG_SPEECH_DEAL"), "static") == 0;
+    L.work = stat ? nullptr : t->work + 2 * (t->seq.fetch_add(1, std::memory_order_relaxed) & (kWorkSlots - 1));
     speech_fft_kernel<<<grid > 0 ? grid : 1, 32 * kFftWarps, kFftSmem, s>>>(L, t->fft);
     return cudaGetLastError();
 }

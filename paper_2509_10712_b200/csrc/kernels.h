@@ -215,6 +215,7 @@ struct SpLaunch {
     int32_t stack;
     int32_t debug;            // profiling switch: 1 builders skip loads, 2 skip MMAs
     int32_t pcm16;            // waveforms are int16 PCM (x = s / 32768), else f32
+    uint32_t* work;           // FFT kernel: this launch's {next tail frame, CTAs done} (null: no tail deal)
     StampRef st;
     int32_t tile_start[kMaxSp + 1];   // CTA prefix sums (flattened grid), filled by the launcher
     SpDesc d[kMaxSp];
