@@ -1045,8 +1045,8 @@ void Context::flush_due() {
 
 // Roofline timing of a chain's transform kernels: all samples are submitted
 // first (launches deferred), then every launch group is issued back to back on
-// one stream, so the per-stage CUDA events bracket kernel time only -- no host
-// submission gaps.  Returns the mean device time of one transform-stage launch.
+// one stream behind a device-side gate, so the per-stage CUDA events bracket kernel
+// time only -- no host submission gaps or launch-call time.  Returns the mean device time of one transform-stage launch.
 void Context::time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* mean_ms,
                            int64_t* launches, int64_t* bytes, int64_t* flops) {
     if (n < 1) fail(LFG_ERR_INVALID, "no samples to time");
@@ -1067,6 +1067,14 @@ void Context::time_kernels(Chain* c, const lfg_sample_desc* s, int n, double* me
             og.erase(c);
         }
         defer_launch = false;
+        // Hold stream 0 with a device spin while the host issues the groups: each stage's
+        // start event then fires when the previous launch ends instead of when the host
+        // gets to it, so the events bracket the kernel and not the host's launch call
+        // (the 256-image K3 launch prepares ~20-40 us of descriptors on the host and its
+        // launch call costs ~8 us with the large parameter block).  The spin is sized well
+        // above the host's issue time; it sits outside every stage's events.
+        const int64_t gate_ns = 500'000 + 250'000 * static_cast<int64_t>(deferred_.size());
+        cuda_check(launch_trainer_spin(std::min<int64_t>(gate_ns, 50'000'000), 1, streams_[0]), "timing gate");
         flush();
     } catch (...) {
         serial = defer_launch = false;
