@@ -803,9 +803,15 @@ def test_speech_pcm16_equals_its_f32_image(lfgpu, oracle):
         ge, oe = np.exp(got[~zero].astype(np.float64)), np.exp(e[~zero])
         frame_peak = np.exp(e.reshape(e.shape[0], 3, 80).max(axis=2)).repeat(80, axis=1)[~zero]
         assert (np.abs(ge - oe) <= 1e-5 * oe + 1e-8 * frame_peak).all()
-    # a PCM waveform must be 2-B aligned
-    with pytest.raises(lfgpu.LfgError):
+    # a PCM waveform must be 2-B aligned; FilterBank takes f32 or int16 input only
+    with pytest.raises(lfgpu.LfgError) as ei:
         ctx.submit(ch16, lfgpu.sample_desc(799, (4000,), keep[0][1] + 1))
+    assert ei.value.code == lfgpu.ERR_INVALID
+    bad = lfgpu.speech_ops(max_len=40000)
+    bad[2].param[5] = lfgpu.DT_U8
+    with pytest.raises(lfgpu.LfgError) as ei:
+        ctx.chain(bad)
+    assert ei.value.code == lfgpu.ERR_UNSUPPORTED
     for kind, p in keep:
         (ctx.device_free if kind == "d" else ctx.host_free)(p)
     ctx.close()
