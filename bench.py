@@ -550,11 +550,24 @@ def run_timed(L, ctx, wl, ids_warm, ids_timed, args, dist, local, trainer_us=0, 
 def calibrated_trainer_us(L, ctx, wl, ids, args, util: float = 0.9) -> int:
     """C3's consumer: the loader's capacity R (samples/s) from a drain run (no trainer
     step, no timeout) over `ids`; the synthetic step per batch of B is B / (util * R),
-    so the loader runs at `util` of its capacity (trainer.hpp:14-21 consumer model)."""
+    so the loader runs at `util` of its capacity (trainer.hpp:14-21 consumer model),
+    refined with the trainer running beside the loader (below)."""
     rc = L.run_config(batch_size=wl.B, n_workers=workers_of(args))
     rep, *_ = ctx.run_shard(wl.chain, wl.descs(ids), rc, want_ids=False)
     ctx.synchronize()
-    return max(1, int(round(wl.B / (util * rep.samples_per_s) * 1e6)))
+    t = max(1, int(round(wl.B / (util * rep.samples_per_s) * 1e6)))
+    # The trainer's step is a kernel on the same GPU, so the loader's capacity while it
+    # runs is lower than the drain run's: re-measure with the trainer in place and re-aim
+    # at `util` of what the loader then delivers (two fixed-point steps; the trainer only
+    # ever slows down, so the pipeline stays loader-bound at most at that utilisation).
+    for _ in range(2):
+        rc_t = L.run_config(batch_size=wl.B, n_workers=workers_of(args), trainer_us=t)
+        rep, *_ = ctx.run_shard(wl.chain, wl.descs(ids), rc_t, want_ids=False)
+        ctx.synchronize()
+        if rep.consumer_idle_frac < 0.02:
+            break
+        t = max(t, int(round(wl.B / (util * rep.samples_per_s) * 1e6)))
+    return t
 
 
 def capture_positions(n_timed: int, k: int, seed: int) -> list[int]:
