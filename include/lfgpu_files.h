@@ -4,7 +4,9 @@
  *
  * File format (little endian): "LFGS" | u32 version = 1 | i32 kind | i32 ndim |
  * i64 dims[4] | payload.  kind 1: img_seg volume, payload = f32 image [D,H,W] then
- * u8 label [D,H,W]; kind 2: obj_det image, u8 [H,W,3]; kind 3: waveform, f32 [L].
+ * u8 label [D,H,W]; kind 2: obj_det image, u8 [H,W,3]; kind 3: waveform, f32 [L];
+ * kind 4: waveform, int16 PCM [L] (the reference's 2-B speech samples; chains with
+ * FilterBank param 5 = LFG_DT_I16).
  *
  * The source reads files with `readers` threads into `slots` pinned host buffers
  * (sized for the largest file), in feed order, ahead of the shard; a buffer is
@@ -19,7 +21,7 @@
 extern "C" {
 #endif
 
-enum { LFG_FILE_VOLUME = 1, LFG_FILE_IMAGE = 2, LFG_FILE_WAVEFORM = 3 };
+enum { LFG_FILE_VOLUME = 1, LFG_FILE_IMAGE = 2, LFG_FILE_WAVEFORM = 3, LFG_FILE_PCM16 = 4 };
 
 int lfg_write_sample_file(const char* path, int kind, int ndim, const int64_t dims[4], const void* data,
                           const void* aux);

@@ -37,6 +37,7 @@ int64_t payload_bytes(int kind, const int64_t dims[4], int64_t* first) {
     }
     if (kind == LFG_FILE_IMAGE) return *first = dims[0] * dims[1] * 3;
     if (kind == LFG_FILE_WAVEFORM) return *first = 4 * dims[0];
+    if (kind == LFG_FILE_PCM16) return *first = 2 * dims[0];
     return *first = -1;
 }
 
@@ -124,7 +125,7 @@ struct lfg_file_source {
         std::memset(out, 0, sizeof(*out));
         out->id = ids[i];
         out->src_kind = LFG_SRC_HOST_PINNED;
-        out->ndim = h.kind == LFG_FILE_WAVEFORM ? 1 : 3;
+        out->ndim = (h.kind == LFG_FILE_WAVEFORM || h.kind == LFG_FILE_PCM16) ? 1 : 3;
         for (int a = 0; a < 4; ++a) out->dims[a] = h.dims[a];
         if (h.kind == LFG_FILE_IMAGE) out->dims[2] = 3;
         char* base = slots[slot_of[i]];

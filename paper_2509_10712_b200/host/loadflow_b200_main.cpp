@@ -123,7 +123,8 @@ std::vector<lfg_op> chain_ops(loadflow::WorkloadKind k) {
     } else {
         ops.push_back(mk(LFG_OP_PAD, "Pad", 1.12));
         ops.push_back(mk(LFG_OP_SPEC_AUGMENT, "SpecAugment", 1.0, {2, 27, 10, 0.05}));
-        ops.push_back(mk(LFG_OP_FILTER_BANK, "FilterBank", 1.0, {512, 320, 160, 80, 170000}));
+        // waveforms as int16 PCM: the reference's speech bytes_in is 2 B per sample (workloads.cpp:115)
+        ops.push_back(mk(LFG_OP_FILTER_BANK, "FilterBank", 1.0, {512, 320, 160, 80, 170000, LFG_DT_I16}));
         ops.push_back(mk(LFG_OP_FRAME_SPLICING, "FrameSplicing", 0.9, {3}));
         ops.push_back(mk(LFG_OP_PERMUTE_AUDIO, "PermuteAudio", 1.0));
     }
@@ -207,8 +208,14 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
             const int64_t L = std::clamp<int64_t>(std::llround(bytes / 2.0), 30000, 170000);
             p.ndim = 1;
             p.dims[0] = L;
-            p.data = alloc(L * 4);
-            check(lfg_synth_waveform(ctx, seed, i, L, p.data, pinned ? 0 : 1), "synth waveform");
+            p.data = alloc(L * 2);
+            std::vector<float> wav(static_cast<size_t>(L));
+            check(lfg_synth_waveform(ctx, seed, i, L, wav.data(), 0), "synth waveform");
+            std::vector<int16_t> pcm(static_cast<size_t>(L));
+            for (size_t v = 0; v < pcm.size(); ++v)
+                pcm[v] = static_cast<int16_t>(std::clamp<long>(std::lrint(wav[v] * 20000.0f), -32768, 32767));
+            if (pinned) std::memcpy(p.data, pcm.data(), pcm.size() * 2);
+            else check(lfg_memcpy_h2d(ctx, p.data, pcm.data(), pcm.size() * 2), "upload waveform");
         }
     }
     check(lfg_synchronize(ctx), "sync");
@@ -261,7 +268,7 @@ int cmd_run(const std::string& cfg_path, const std::string& loader_arg, int64_t 
         std::vector<std::string> files;
         const int fkind = kind == loadflow::WorkloadKind::img_seg
                               ? LFG_FILE_VOLUME
-                              : (kind == loadflow::WorkloadKind::obj_det ? LFG_FILE_IMAGE : LFG_FILE_WAVEFORM);
+                              : (kind == loadflow::WorkloadKind::obj_det ? LFG_FILE_IMAGE : LFG_FILE_PCM16);
         for (size_t i = 0; i < pay.size(); ++i) {
             files.push_back(dir + "/sample_" + std::to_string(i) + ".lfgs");
             check(lfg_write_sample_file(files.back().c_str(), fkind, pay[i].ndim, pay[i].dims, pay[i].data, pay[i].aux),

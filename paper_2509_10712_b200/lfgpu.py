@@ -586,7 +586,7 @@ class ShardStream:
 
 
 # ---- raw sample files + reader-thread source (include/lfgpu_files.h, host library) ----
-FILE_VOLUME, FILE_IMAGE, FILE_WAVEFORM = 1, 2, 3
+FILE_VOLUME, FILE_IMAGE, FILE_WAVEFORM, FILE_PCM16 = 1, 2, 3, 4
 HOST_LIB_PATH = os.path.join(_PKG, "libloadflow_b200.so")
 _host = None
 

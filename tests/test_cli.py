@@ -75,3 +75,19 @@ def test_cli_dropin_coalesces_per_sample_submissions(cli):
     assert res[0]["samples_per_launch"] < 1.5
     assert res[40]["samples_per_launch"] > 2.0
     print(res)
+
+
+@pytest.mark.gpu
+def test_cli_speech_from_pcm_files(cli, tmp_path):
+    """The reference speech stream from int16 PCM sample files (LFG_FILE_PCM16, the
+    reference's 2-B samples, workloads.cpp:115) through reader threads, pinned slots,
+    K0 and the speech kernel: exactly once, every sample delivered."""
+    cfg = tmp_path / "speech_file.ini"
+    text = open(os.path.join(ROOT, "configs", "speech_file.ini")).read()
+    cfg.write_text(text.replace("[gpu]\n", f"[gpu]\ndata_dir = {tmp_path / 'data'}\n"))
+    out = tmp_path / "speech"
+    r = subprocess.run([cli, "run", str(cfg), "--out", str(out)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert "exactly_once=yes" in r.stdout
+    rep = json.loads((out / "report.json").read_text())
+    assert rep["samples"] == 4096

@@ -23,6 +23,13 @@ def test_sample_file_layout(lfgpu, tmp_path):
     assert np.array_equal(np.frombuffer(raw[48 + 96:], np.uint8).reshape(2, 3, 4), lbl)
     with pytest.raises(lfgpu.LfgError):
         lfgpu.write_sample_file(p, 9, (1,), img)
+    # int16 PCM waveform (the reference's 2-B speech samples): 2 B per sample
+    pcm = np.array([0, 1, -1, 32767, -32768, 12345, -222], dtype=np.int16)
+    lfgpu.write_sample_file(p, lfgpu.FILE_PCM16, (pcm.size,), pcm)
+    raw = open(p, "rb").read()
+    hdr = np.frombuffer(raw[:48], dtype=np.int32)
+    assert len(raw) == 48 + 2 * pcm.size and hdr[2] == lfgpu.FILE_PCM16 and hdr[3] == 1
+    assert np.array_equal(np.frombuffer(raw[48:], np.int16), pcm)
 
 
 @pytest.mark.gpu
