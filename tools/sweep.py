@@ -12,7 +12,9 @@ brightness + noise + cast) on KiTS19-shaped D x 384 x 384 volumes.
 
 Consumer: a synthetic trainer step per batch of 2 (trainer.hpp:14-21), calibrated on
 each side to 90% of that side's own measured loader capacity at that p_fg (a drain
-run: no trainer step, no timeout) -- the same relative time scale on both sides.
+run: no trainer step, no timeout; on the GPU re-measured with the trainer's kernel
+running beside the loader, bench.calibrated_trainer_us) -- the same relative time
+scale on both sides.
 
 Policies (lfg_run_config.policy on the GPU, minato_cpu --pct / --loader on the CPU):
   minato  the Profiler's adaptive p75 -> p90 timeout (profiler.cpp:47-72)
@@ -141,7 +143,7 @@ def main():
              "",
              "Tail: MLPerf foreground oversampling p_fg (an oversampled crop scans its whole label volume; "
              "GPU: from pinned host memory the volume crosses PCIe, then K2). Trainer step per batch of 2 "
-             f"calibrated on each side to {UTIL:.0%} of that side's drain-run loader capacity at that p_fg. "
+             f"calibrated on each side to {UTIL:.0%} of that side's loader capacity at that p_fg (drain run; GPU: re-measured with the trainer kernel beside the loader). "
              f"GPU: launch groups of {GROUP}, W in-flight groups, pinned-host inputs. "
              f"CPU: reference libloadflow realtime Minato / sync loader + oracle transforms, {cores} host cores.",
              "minato = adaptive p75 -> p90 timeout; p50 / p90 = fixed percentile; none = no timeout; "
