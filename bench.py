@@ -933,8 +933,9 @@ def main():
     exactly_once = dig[:4] == want and dig[4:] == want and cnt[5] == 0
     value = cnt[0] / (el_max / 1e3)
     e2e = cnt[1] / (el_h / 1e3)
-    cpu = None if (args.no_cpu_baseline or fake) else cpu_baseline(args.workload)
-    dropin = dropin_arm() if (args.workload == "rrc" and not fake and not args.no_dropin) else None
+    # the CPU baseline and the drop-in arm: rank 0 at N = 1 only (the scaling runs report GPU shards)
+    cpu = None if (args.no_cpu_baseline or fake or world > 1) else cpu_baseline(args.workload)
+    dropin = dropin_arm() if (args.workload == "rrc" and world == 1 and not fake and not args.no_dropin) else None
     steps = args.steps
     checks = [c for c in (r["check_value"], r["check_e2e"]) if c is not None]
     line = {
