@@ -564,13 +564,13 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             }
         }
     };
-    // Frame deal: round-robin for all but the last rounds (warp w of CTA b takes frames
-    // b * 8 + w + k * stride: neighbouring frames, which share half their taps, sit on
-    // neighbouring warps of one CTA), then -- with L.work -- the tail from the launch's
-    // counter, so no SM idles while others finish (masked and padding frames are cheap, so
-    // equal frame counts are not equal work: ncu showed sm__cycles_active min 57 k / avg
-    // 69 k / max 82 k of 86 k with the pure round-robin deal).  Lane 0's atomic runs one
-    // take ahead.  A warp's frames increase (load_taps' utterance search relies on it).
+    // Frame deal: round robin -- warp w of CTA b takes frames b * 8 + w + k * stride, so
+    // neighbouring frames, which share half their taps, sit on neighbouring warps of one
+    // CTA.  With L.work (A/B switch LFG_SPEECH_DEAL=tail) the last kFftDynRounds rounds come
+    // from the launch's counter instead, so no SM of a lone launch idles while others
+    // finish (masked and padding frames are cheap: ncu showed sm__cycles_active min 57 k /
+    // avg 69 k / max 82 k of 86 k); lane 0's atomic runs one take ahead.  A warp's frames
+    // increase either way (load_taps' utterance search relies on it).
     const bool dyn = L.work != nullptr;
     const int n_rr = dyn ? max(0, total / stride - kFftDynRounds) : (total + stride - 1) / stride;
     const int rr_end = n_rr * stride;
@@ -883,13 +883,15 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     if ((e = cudaFuncSetAttribute(speech_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBytes)) != cudaSuccess)
         return e;
-    if ((e = cudaMalloc(&t->fft, sizeof(FftTables))) != cudaSuccess) return e;
-    if ((e = cudaMemcpy(t->fft, &ft, sizeof(FftTables), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(speech_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kFftSmem)) != cudaSuccess)
+    if ((e = cudaMalloc(&t->fft, sizeof(FftTables))) != cudaSuccess ||
+        (e = cudaMemcpy(t->fft, &ft, sizeof(FftTables), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(speech_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem)) !=
+            cudaSuccess ||
+        (e = cudaMalloc(&t->work, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess ||
+        (e = cudaMemset(t->work, 0, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess) {
+        speech_tables_destroy(t);
         return e;
-    if ((e = cudaMalloc(&t->work, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess) return e;
-    if ((e = cudaMemset(t->work, 0, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess) return e;
+    }
     *out = t;
     return cudaSuccess;
 }
