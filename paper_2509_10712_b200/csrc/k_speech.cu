@@ -434,8 +434,10 @@ struct __align__(16) FftTables {
     float2 tw256[8 * 32];             // [k1][l] W256^(l k1)
     float2 tw32[8 * 4];               // [c][b] W32^(b c)
     float2 tw512[8 * 32];             // [c][lane (k1, b')] -i W512^k, k = k1 + 8 c + 64 bitrev2(b')
-    int32_t mel_b0[kMels];            // pw_at(filter m's first bin)
-    float mel_wd[kMelW2 * kMels];     // [tap][filter] weights / 4 (0 past the filter's span)
+    int32_t mel_b0[kMels];            // pw_at(first bin of filter m's tap window): lo_m - s_m
+    float mel_wd[kMelW2 * kMels];     // [tap][filter] weights / 4 over the window (0 outside the filter's span)
+    int32_t mel_b2[32];               // the 16 widest filters per lane (filter 64 + (l & 15), half l >> 4):
+                                      // mel_b0 + 9 * half
 };
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -672,11 +674,15 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             // mel filters m = lane, lane + 32, lane + 64, log, frequency masks, store
             const int fl0 = d.f_lo[0], fw0 = L.n_fmask > 0 ? d.f_w[0] : 0;
             const int fl1 = d.f_lo[1], fw1 = L.n_fmask > 1 ? d.f_w[1] : 0;
+            // Each filter's W-tap window starts s_m bins before its first bin (zero weights there;
+            // s_m within the filter's slack W - span, chosen on the host so that a warp's
+            // power-row loads of one tap step fall in distinct banks -- unshifted, the filters'
+            // first bins collide 2-4 ways).
             auto mel_out = [&](auto W, int m) {
-                const int b0 = tb->mel_b0[m];
+                const int a0 = tb->mel_b0[m];
                 float acc = 0.0f;
 #pragma unroll
-                for (int q = 0; q < decltype(W)::value; ++q) acc = fmaf(tb->mel_wd[q * kMels + m], pw[b0 + q], acc);
+                for (int q = 0; q < decltype(W)::value; ++q) acc = fmaf(tb->mel_wd[q * kMels + m], pw[a0 + q], acc);
                 const bool masked = (unsigned)(m - fl0) < (unsigned)fw0 || (unsigned)(m - fl1) < (unsigned)fw1;
                 out[m] = masked ? 0.0f : __logf(acc + 5.9604644775390625e-8f);   // + 2^-24
             };
@@ -684,11 +690,11 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
             mel_out(std::integral_constant<int, kMelW1>{}, lane + 32);
             {   // filters 64..79 (the widest): two lanes per filter, 9 taps each
                 const int m = 64 + (lane & 15), h = lane >> 4;
-                const int b0 = tb->mel_b0[m] + (kMelW2 / 2) * h;
+                const int a0 = tb->mel_b2[lane];
                 float acc = 0.0f;
 #pragma unroll
                 for (int q = 0; q < kMelW2 / 2; ++q)
-                    acc = fmaf(tb->mel_wd[((kMelW2 / 2) * h + q) * kMels + m], pw[b0 + q], acc);
+                    acc = fmaf(tb->mel_wd[((kMelW2 / 2) * h + q) * kMels + m], pw[a0 + q], acc);
                 acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 16);
                 const bool masked = (unsigned)(m - fl0) < (unsigned)fw0 || (unsigned)(m - fl1) < (unsigned)fw1;
                 if (h == 0) out[m] = masked ? 0.0f : __logf(acc + 5.9604644775390625e-8f);
@@ -852,6 +858,7 @@ cudaError_t speech_tables_create(SpeechTables** out) {
             const float2 w = tw((l >> 2) + 8 * c + 64 * d, 512);
             ft.tw512[c * 32 + l] = make_float2(w.y, -w.x);            // -i W512^k
         }
+    int mel_lo[kMels];
     for (int m = 0; m < kMels; ++m) {
         int lo = -1, hi = -1;
         for (int k = 0; k < nf; ++k)
@@ -862,8 +869,85 @@ cudaError_t speech_tables_create(SpeechTables** out) {
         const int width = m < 32 ? kMelW0 : (m < 64 ? kMelW1 : kMelW2);
         if (lo < 0) lo = hi = 0;
         if (hi - lo + 1 > width || lo + width > nf) return cudaErrorInvalidValue;   // bank wider than the taps
-        ft.mel_b0[m] = pw_at(lo);
-        for (int q = 0; q < width; ++q) ft.mel_wd[q * kMels + m] = (float)fb[(size_t)m * nf + lo + q] * 0.25f;
+        mel_lo[m] = lo;
+    }
+    int mel_hi[kMels];
+    for (int m = 0; m < kMels; ++m) {
+        mel_hi[m] = mel_lo[m];
+        for (int k = mel_lo[m]; k < nf; ++k)
+            if (fb[(size_t)m * nf + k] != 0.0) mel_hi[m] = k;
+    }
+    // Window shifts: filter m's W-tap window starts s_m bins before its first bin, 0 <= s_m <=
+    // min(W - span_m, lo_m) (the extra taps carry zero weights).  The 32 lanes of a group read
+    // pw_at(lo - s) + q at tap step q; s is chosen by coordinate descent to minimise the summed
+    // shared-memory wavefronts of the W steps (distinct addresses per bank; the row's bank is
+    // its word offset mod 32: the per-warp pitch is 13 x 32 words).  For the slaney bank:
+    // 30 -> 10 wavefronts for the 10-tap group (one per step), 27 -> 18 for the 18-tap group
+    // (both halves share a filter's shift), 6 for the 3-tap group (no slack).
+    // LFG_MEL_SHIFT=0 keeps every s = 0 (A/B switch).
+    static const bool shift_on = !(getenv("LFG_MEL_SHIFT") && std::strcmp(getenv("LFG_MEL_SHIFT"), "0") == 0);
+    // f(l) = the filter of lane l, off(l) = the lane's tap offset inside the window
+    auto shifts = [&](int W, int nf_group, auto filt, auto off, int sh[32]) {
+        auto cost = [&]() {
+            int total = 0;
+            for (int q = 0; q < W; ++q) {
+                int addr[32];
+                for (int l = 0; l < 32; ++l) {
+                    const int m = filt(l);
+                    addr[l] = pw_at(mel_lo[m] - sh[l % nf_group]) + off(l) + q;
+                }
+                int worst = 0, sq = 0;
+                for (int b = 0; b < 32; ++b) {
+                    int seen[32], ns = 0;
+                    for (int l = 0; l < 32; ++l) {
+                        if ((addr[l] & 31) != b) continue;
+                        bool dup = false;
+                        for (int i = 0; i < ns; ++i) dup |= seen[i] == addr[l];
+                        if (!dup) seen[ns++] = addr[l];
+                    }
+                    worst = std::max(worst, ns);
+                    sq += ns * ns;
+                }
+                total += 1000 * worst + sq;   // wavefronts; the squares break the descent's ties
+            }
+            return total;
+        };
+        for (int l = 0; l < 32; ++l) sh[l] = 0;
+        if (!shift_on) return;
+        for (int pass = 0; pass < 8; ++pass)
+            for (int f = 0; f < nf_group; ++f) {
+                const int m = filt(f), Wf = nf_group == 32 ? W : 2 * W;
+                const int slack = std::min(Wf - (mel_hi[m] - mel_lo[m] + 1), mel_lo[m]);
+                int best = sh[f], best_c = cost();
+                for (int r = 0; r <= slack; ++r) {
+                    sh[f] = r;
+                    const int c = cost();
+                    if (c < best_c) best = r, best_c = c;
+                }
+                sh[f] = best;
+            }
+    };
+    auto wgt = [&](int m, int k) { return (float)fb[(size_t)m * nf + k] * 0.25f; };
+    for (int g = 0; g < 2; ++g) {   // filters 0..31 (3 taps), 32..63 (10 taps): lane l = filter 32 g + l
+        const int W = g == 0 ? kMelW0 : kMelW1;
+        int sh[32];
+        shifts(W, 32, [&](int l) { return 32 * g + l; }, [](int) { return 0; }, sh);
+        for (int l = 0; l < 32; ++l) {
+            const int m = 32 * g + l, k0 = mel_lo[m] - sh[l];
+            ft.mel_b0[m] = pw_at(k0);
+            for (int q = 0; q < W; ++q) ft.mel_wd[q * kMels + m] = wgt(m, k0 + q);
+        }
+    }
+    {   // filters 64..79 (18 taps): lane l = filter 64 + (l & 15), taps 9 (l >> 4) .. + 8
+        constexpr int W = kMelW2 / 2;
+        int sh[32];
+        shifts(W, 16, [](int l) { return 64 + (l & 15); }, [](int l) { return W * (l >> 4); }, sh);
+        for (int f = 0; f < 16; ++f) {
+            const int m = 64 + f, k0 = mel_lo[m] - sh[f];
+            ft.mel_b0[m] = pw_at(k0);
+            for (int q = 0; q < kMelW2; ++q) ft.mel_wd[q * kMels + m] = wgt(m, k0 + q);
+        }
+        for (int l = 0; l < 32; ++l) ft.mel_b2[l] = ft.mel_b0[64 + (l & 15)] + W * (l >> 4);
     }
     cudaError_t e;
     if ((e = cudaMemcpyToSymbol(c_win_nyq, nyq, sizeof(nyq))) != cudaSuccess) return e;
