@@ -437,7 +437,7 @@ struct __align__(16) FftTables {
     int32_t mel_b0[kMels];            // pw_at(first bin of filter m's tap window): lo_m - s_m
     float mel_wd[kMelW2 * kMels];     // [tap][filter] weights / 4 over the window (0 outside the filter's span)
     int32_t mel_b2[32];               // the 16 widest filters per lane (filter 64 + (l & 15), half l >> 4):
-                                      // mel_b0 + 9 * half
+                                      // half 0 at mel_b0, half 1 at mel_b0 + 9 - t (see the tables)
 };
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -882,8 +882,8 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     // pw_at(lo - s) + q at tap step q; s is chosen by coordinate descent to minimise the summed
     // shared-memory wavefronts of the W steps (distinct addresses per bank; the row's bank is
     // its word offset mod 32: the per-warp pitch is 13 x 32 words).  For the slaney bank:
-    // 30 -> 10 wavefronts for the 10-tap group (one per step), 27 -> 18 for the 18-tap group
-    // (both halves share a filter's shift), 6 for the 3-tap group (no slack).
+    // 30 -> 10 wavefronts for the 10-tap group (one per step), 6 for the 3-tap group (no
+    // slack); the 18-tap group below.
     // LFG_MEL_SHIFT=0 keeps every s = 0 (A/B switch).
     static const bool shift_on = !(getenv("LFG_MEL_SHIFT") && std::strcmp(getenv("LFG_MEL_SHIFT"), "0") == 0);
     // f(l) = the filter of lane l, off(l) = the lane's tap offset inside the window
@@ -938,16 +938,76 @@ cudaError_t speech_tables_create(SpeechTables** out) {
             for (int q = 0; q < W; ++q) ft.mel_wd[q * kMels + m] = wgt(m, k0 + q);
         }
     }
-    {   // filters 64..79 (18 taps): lane l = filter 64 + (l & 15), taps 9 (l >> 4) .. + 8
+    {   // filters 64..79 (18 taps): lane l = filter 64 + (l & 15), half h = l >> 4.  Half 0
+        // reads bins k0 .. k0 + 8 (k0 = lo - s), half 1 bins k0 + 9 - t .. k0 + 17 - t; bins both
+        // halves read carry their weight in half 0 only.  Coverage of [lo, hi] needs
+        // s + t <= 18 - span.  (s, t) per filter by a fixed-seed annealing (coordinate descent
+        // stalls here; model: 27 -> 9 wavefronts per frame), computed once per process.
         constexpr int W = kMelW2 / 2;
-        int sh[32];
-        shifts(W, 16, [](int l) { return 64 + (l & 15); }, [](int l) { return W * (l >> 4); }, sh);
+        struct G2 {
+            int s[16], t[16];
+        };
+        static const G2 g2 = [&] {
+            G2 g{};
+            if (!shift_on) return g;
+            int span[16];
+            for (int f = 0; f < 16; ++f) span[f] = mel_hi[64 + f] - mel_lo[64 + f] + 1;
+            auto cost = [&](const G2& x) {
+                int total = 0;
+                for (int q = 0; q < W; ++q) {
+                    int addr[32];
+                    for (int l = 0; l < 32; ++l) {
+                        const int f = l & 15;
+                        addr[l] = pw_at(mel_lo[64 + f] - x.s[f]) + (l >> 4) * (W - x.t[f]) + q;
+                    }
+                    int worst = 0, sq = 0;
+                    for (int b = 0; b < 32; ++b) {
+                        int seen[32], ns = 0;
+                        for (int l = 0; l < 32; ++l) {
+                            if ((addr[l] & 31) != b) continue;
+                            bool dup = false;
+                            for (int i = 0; i < ns; ++i) dup |= seen[i] == addr[l];
+                            if (!dup) seen[ns++] = addr[l];
+                        }
+                        worst = std::max(worst, ns);
+                        sq += ns * ns;
+                    }
+                    total += 1000 * worst + sq;
+                }
+                return total;
+            };
+            uint64_t rng = 0x9E3779B97F4A7C15ull;
+            auto next = [&](int n) {   // uniform in [0, n)
+                rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+                return static_cast<int>((rng >> 33) % static_cast<uint64_t>(n));
+            };
+            G2 cur = g, best = g;
+            int c_cur = cost(cur), c_best = c_cur;
+            double T = 200.0;
+            for (int it = 0; it < 30000; ++it) {
+                const int f = next(16);
+                const int smax = std::min(kMelW2 - span[f], mel_lo[64 + f]);
+                G2 cand = cur;
+                cand.s[f] = next(smax + 1);
+                cand.t[f] = next(kMelW2 - span[f] - cand.s[f] + 1);
+                const int c = cost(cand);
+                const double u = static_cast<double>(next(1 << 30)) / static_cast<double>(1 << 30);
+                if (c <= c_cur || u < std::exp((c_cur - c) / T)) cur = cand, c_cur = c;
+                if (c_cur < c_best) best = cur, c_best = c_cur;
+                T = std::max(0.5, T * 0.9997);
+            }
+            return best;
+        }();
         for (int f = 0; f < 16; ++f) {
-            const int m = 64 + f, k0 = mel_lo[m] - sh[f];
+            const int m = 64 + f, k0 = mel_lo[m] - g2.s[f], k1 = k0 + W - g2.t[f];
             ft.mel_b0[m] = pw_at(k0);
-            for (int q = 0; q < kMelW2; ++q) ft.mel_wd[q * kMels + m] = wgt(m, k0 + q);
+            for (int q = 0; q < W; ++q) {
+                ft.mel_wd[q * kMels + m] = wgt(m, k0 + q);
+                ft.mel_wd[(W + q) * kMels + m] = k1 + q < k0 + W ? 0.0f : wgt(m, k1 + q);
+            }
+            ft.mel_b2[f] = pw_at(k0);
+            ft.mel_b2[16 + f] = pw_at(k0) + W - g2.t[f];
         }
-        for (int l = 0; l < 32; ++l) ft.mel_b2[l] = ft.mel_b0[64 + (l & 15)] + W * (l >> 4);
     }
     cudaError_t e;
     if ((e = cudaMemcpyToSymbol(c_win_nyq, nyq, sizeof(nyq))) != cudaSuccess) return e;
