@@ -886,16 +886,13 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     // slack); the 18-tap group below.
     // LFG_MEL_SHIFT=0 keeps every s = 0 (A/B switch).
     static const bool shift_on = !(getenv("LFG_MEL_SHIFT") && std::strcmp(getenv("LFG_MEL_SHIFT"), "0") == 0);
-    // f(l) = the filter of lane l, off(l) = the lane's tap offset inside the window
-    auto shifts = [&](int W, int nf_group, auto filt, auto off, int sh[32]) {
+    // group of 32 lanes, lane l = filter m0 + l, W taps each
+    auto shifts = [&](int W, int m0, int sh[32]) {
         auto cost = [&]() {
             int total = 0;
             for (int q = 0; q < W; ++q) {
                 int addr[32];
-                for (int l = 0; l < 32; ++l) {
-                    const int m = filt(l);
-                    addr[l] = pw_at(mel_lo[m] - sh[l % nf_group]) + off(l) + q;
-                }
+                for (int l = 0; l < 32; ++l) addr[l] = pw_at(mel_lo[m0 + l] - sh[l]) + q;
                 int worst = 0, sq = 0;
                 for (int b = 0; b < 32; ++b) {
                     int seen[32], ns = 0;
@@ -915,9 +912,9 @@ cudaError_t speech_tables_create(SpeechTables** out) {
         for (int l = 0; l < 32; ++l) sh[l] = 0;
         if (!shift_on) return;
         for (int pass = 0; pass < 8; ++pass)
-            for (int f = 0; f < nf_group; ++f) {
-                const int m = filt(f), Wf = nf_group == 32 ? W : 2 * W;
-                const int slack = std::min(Wf - (mel_hi[m] - mel_lo[m] + 1), mel_lo[m]);
+            for (int f = 0; f < 32; ++f) {
+                const int m = m0 + f;
+                const int slack = std::min(W - (mel_hi[m] - mel_lo[m] + 1), mel_lo[m]);
                 int best = sh[f], best_c = cost();
                 for (int r = 0; r <= slack; ++r) {
                     sh[f] = r;
@@ -931,7 +928,7 @@ cudaError_t speech_tables_create(SpeechTables** out) {
     for (int g = 0; g < 2; ++g) {   // filters 0..31 (3 taps), 32..63 (10 taps): lane l = filter 32 g + l
         const int W = g == 0 ? kMelW0 : kMelW1;
         int sh[32];
-        shifts(W, 32, [&](int l) { return 32 * g + l; }, [](int) { return 0; }, sh);
+        shifts(W, 32 * g, sh);
         for (int l = 0; l < 32; ++l) {
             const int m = 32 * g + l, k0 = mel_lo[m] - sh[l];
             ft.mel_b0[m] = pw_at(k0);
