@@ -490,6 +490,7 @@ __device__ __forceinline__ float2 pcm_pair(uint32_t w) {
 #ifndef LFG_FFT_REG_TW
 #define LFG_FFT_REG_TW 0   // (build-time A/B) lane twiddles held in registers, 2 CTAs / SM
 #endif
+template <bool kPcm>   // int16 PCM waveforms (else f32): one instantiation each, no per-tap selects
 __global__ void __launch_bounds__(32 * kFftWarps, LFG_FFT_REG_TW ? 2 : 3)
 speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restrict__ g) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -546,7 +547,7 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
         // taps come in pairs (2 n, 2 n + 1): one 8-B load of f32, or one 4-B load of int16
         // PCM kept as the raw word in .x until the frame's stage 1 (pcm_pair) -- converting
         // here would wait on the load one frame early; reflect padding at the utterance ends
-        const int esh = L.pcm16 ? 1 : 2;                  // log2 bytes per sample
+        const int esh = kPcm ? 1 : 2;                     // log2 bytes per sample
         const bool interior = base >= 0 && base + kTaps <= Lw &&
                               ((reinterpret_cast<uintptr_t>(dx.wav) & ((2u << esh) - 1)) == 0);
         const float* wf = static_cast<const float*>(dx.wav);
@@ -555,14 +556,14 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
         for (int n1 = 0; n1 < 5; ++n1) {
             const int j = 2 * (32 * n1 + lane);
             if (interior) {
-                xv[n1] = L.pcm16 ? make_float2(__uint_as_float(__ldg(reinterpret_cast<const unsigned int*>(ws + base + j))), 0.f)
-                                 : __ldg(reinterpret_cast<const float2*>(wf + base + j));
+                if constexpr (kPcm) xv[n1] = make_float2(__uint_as_float(__ldg(reinterpret_cast<const unsigned int*>(ws + base + j))), 0.f);
+                else xv[n1] = __ldg(reinterpret_cast<const float2*>(wf + base + j));
             } else {
                 int i0 = base + j, i1 = base + j + 1;
                 i0 = i0 < 0 ? -i0 : (i0 >= Lw ? 2 * (Lw - 1) - i0 : i0);
                 i1 = i1 < 0 ? -i1 : (i1 >= Lw ? 2 * (Lw - 1) - i1 : i1);
-                xv[n1] = L.pcm16 ? make_float2(__uint_as_float((uint32_t)__ldg(ws + i0) | ((uint32_t)__ldg(ws + i1) << 16)), 0.f)
-                                 : make_float2(__ldg(wf + i0), __ldg(wf + i1));
+                if constexpr (kPcm) xv[n1] = make_float2(__uint_as_float((uint32_t)__ldg(ws + i0) | ((uint32_t)__ldg(ws + i1) << 16)), 0.f);
+                else xv[n1] = make_float2(__ldg(wf + i0), __ldg(wf + i1));
             }
         }
     };
@@ -612,7 +613,8 @@ speech_fft_kernel(const __grid_constant__ SpLaunch L, const FftTables* __restric
                 if (n1 < 5) {
                     const int j = 2 * (32 * n1 + lane);
                     const float2 ww = *reinterpret_cast<const float2*>(tb->win + j);
-                    const float2 x = L.pcm16 ? pcm_pair(__float_as_uint(cur[n1].x)) : cur[n1];
+                    float2 x = cur[n1];
+                    if constexpr (kPcm) x = pcm_pair(__float_as_uint(cur[n1].x));
                     v[n1] = make_float2(x.x * ww.x, x.y * ww.y);
                 } else {
                     v[n1] = make_float2(0.f, 0.f);
@@ -1026,7 +1028,9 @@ cudaError_t speech_tables_create(SpeechTables** out) {
         return e;
     if ((e = cudaMalloc(&t->fft, sizeof(FftTables))) != cudaSuccess ||
         (e = cudaMemcpy(t->fft, &ft, sizeof(FftTables), cudaMemcpyHostToDevice)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(speech_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem)) !=
+        (e = cudaFuncSetAttribute(speech_fft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem)) !=
+            cudaSuccess ||
+        (e = cudaFuncSetAttribute(speech_fft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem)) !=
             cudaSuccess ||
         (e = cudaMalloc(&t->work, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess ||
         (e = cudaMemset(t->work, 0, sizeof(uint32_t) * 2 * kWorkSlots)) != cudaSuccess) {
@@ -1079,7 +1083,8 @@ cudaError_t launch_speech(const SpLaunch& L0, const SpeechTables* t, cudaStream_
     // pure round-robin deal.
     static const bool tail = getenv("LFG_SPEECH_DEAL") && std::strcmp(getenv("LFG_SPEECH_DEAL"), "tail") == 0;
     L.work = tail ? t->work + 2 * (t->seq.fetch_add(1, std::memory_order_relaxed) & (kWorkSlots - 1)) : nullptr;
-    speech_fft_kernel<<<grid > 0 ? grid : 1, 32 * kFftWarps, kFftSmem, s>>>(L, t->fft);
+    if (L.pcm16) speech_fft_kernel<true><<<grid > 0 ? grid : 1, 32 * kFftWarps, kFftSmem, s>>>(L, t->fft);
+    else speech_fft_kernel<false><<<grid > 0 ? grid : 1, 32 * kFftWarps, kFftSmem, s>>>(L, t->fft);
     return cudaGetLastError();
 }
 
@@ -1092,7 +1097,8 @@ cudaError_t launch_speech_collate(const SpCollate& C, cudaStream_t s) {
 cudaError_t warm_speech() {
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, speech_kernel);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, speech_fft_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, speech_fft_kernel<false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, speech_fft_kernel<true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, speech_collate_kernel);
     return e;
 }
